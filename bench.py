@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: 5MP two-exposure pairs/sec registered+merged (BASELINE.json).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU). Pairs are independent,
+so each rank owns its own resident batch: per-GPU work is fixed ("weak"
+scaling) and no collective touches the data path (timings are max-reduced
+over ranks with one tiny all-reduce after the timed region).
+
+A step = one batch of `--pairs` 5MP pairs per GPU (synthetic scenes of
+SURVEY.md §8(d) C2, rendered on the host, resident in HBM, each pair its own
+buffers so the batch (~1.9 GB of inputs) is far larger than the 126 MB L2).
+`e2e` is the same metric through the public batch API (runner.BatchRunner
+.run_host) with pinned host inputs: H2D of both frames and D2H of the
+composite + verdict words happen inside the timed region.
+
+--impl reference times the CPU oracle port of the reference (oracle/, the
+reference itself is pure Python and cannot travel to this box) on all host
+cores: one pair per process per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W5, H5 = 2592, 1944
+METRIC = "5MP 2-exposure pairs/sec registered+merged (1/2/4/8 B200) vs host-CPU ref"
+WORKLOAD = "5MP (2592x1944) two-exposure pair, registered + merged (BASELINE configs[1])"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--pairs", type=int, default=16, help="resident pairs per GPU per step")
+    ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--scenes", type=int, default=4, help="distinct synthetic scenes")
+    ap.add_argument("--e2e-pairs", type=int, default=8)
+    ap.add_argument("--width", type=int, default=W5)
+    ap.add_argument("--height", type=int, default=H5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ scenes
+def _render(args):
+    from paper_1504_01441_b200 import synth
+    w, h, seed = args
+    st = synth.synth_stack(synth.working_spec(w, h), seed)
+    return st.ref, st.src
+
+
+def render_scenes(n, w, h, base_seed):
+    jobs = [(w, h, base_seed + i) for i in range(n)]
+    with mp.get_context("fork").Pool(min(n, os.cpu_count() or 1)) as pool:
+        return pool.map(_render, jobs)
+
+
+# ------------------------------------------------------------------ CPU reference
+_CPU_PAIRS = None
+
+
+def _cpu_pair(i):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import hdr_oracle as O
+    ref, src = _CPU_PAIRS[i % len(_CPU_PAIRS)]
+    t = time.perf_counter()
+    out = O.register_and_fuse(ref, src)
+    return time.perf_counter() - t, len(out.matches)
+
+
+def cpu_pool(pairs, procs):
+    global _CPU_PAIRS
+    _CPU_PAIRS = pairs
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+    return mp.get_context("fork").Pool(procs)
+
+
+def cpu_step(pool, procs):
+    t = time.perf_counter()
+    res = pool.map(_cpu_pair, range(procs), chunksize=1)
+    return time.perf_counter() - t, res
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.path = index, None, f"/tmp/hdr_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ roofline bookkeeping
+def stage_bytes(w, h):
+    """Algorithmic HBM bytes per launch of each stage."""
+    P = w * h
+    return {
+        "raster": P * (24 + 4 + 1 + 4) + 2 * 4 * P // 3,
+        "finalize_warp": P * (24 + 12 + 8 + 12 + 1 + 1),
+        "ssim": P * (4 + 1 + 4),
+        "fuse": P * 41,
+        "dt_filter": None,
+    }
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        return json.load(open(path))
+    return {}
+
+
+# ------------------------------------------------------------------ arms
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    procs = min(os.cpu_count() or 1, 16)
+    scenes = render_scenes(min(args.scenes, procs), args.width, args.height, 0)
+    pool = cpu_pool(scenes, procs)
+    for _ in range(args.warmup):
+        cpu_step(pool, procs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_step(pool, procs)
+    dt = time.perf_counter() - t0
+    pool.close()
+    value = procs * args.steps / dt
+    sample = (f"{procs} synthetic {args.width}x{args.height} pairs per step, one per process "
+              f"(oracle port of hdrflow.register_and_fuse, OMP/OpenBLAS threads = 1)")
+    emit({"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+          "dtype": "f32/f64", "data": "synthetic",
+          "config": {"workload": WORKLOAD, "width": args.width, "height": args.height,
+                     "pairs_per_step": procs, "parallelism": "process per core"},
+          "impl": "reference",
+          "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": procs, "kind": "port",
+                           "sample": sample},
+          "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": 0}})
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    cpu_base = None
+    scenes = render_scenes(args.scenes, args.width, args.height, 1000 * rank)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = min(os.cpu_count() or 1, 16)
+        pool = cpu_pool(scenes, procs)
+        dt, res = cpu_step(pool, procs)
+        pool.close()
+        cpu_base = {"value": procs / dt, "unit": "pairs/s", "cores": procs, "kind": "port",
+                    "sample": f"{procs} {args.width}x{args.height} pairs, one per process, "
+                              f"{dt:.1f} s wall (oracle port of the reference)"}
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1504_01441_b200.pipeline import PairBuffers, PipelineParams
+    from paper_1504_01441_b200.runner import BatchRunner
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = f"cuda:{local}"
+    w, h, B = args.width, args.height, args.pairs
+    pairs = []
+    for k in range(B):
+        ref, src = scenes[k % len(scenes)]
+        pairs.append((torch.from_numpy(ref).to(dev), torch.from_numpy(src).to(dev)))
+    outs = [PairBuffers(w, h, local) for _ in range(B)]
+    runner = BatchRunner(w, h, streams=args.streams, params=PipelineParams(), device=local,
+                         graph=not args.no_graph)
+    from paper_1504_01441_b200 import _native
+    nst = _native.NUM_STAGES
+    probes = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(B)]
+    for evs in probes:
+        for e in evs:
+            e.record()
+    torch.cuda.synchronize()
+
+    def step():
+        cur = torch.cuda.current_stream()
+        for s in runner.streams:
+            s.wait_stream(cur)
+        for k in range(B):
+            runner.set_probes(k, probes[k])
+            runner.enqueue(k, pairs[k][0], pairs[k][1], outs[k])
+        for s in runner.streams:
+            cur.wait_stream(s)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    infos = [o.info.cpu().numpy() for o in outs]
+    ok = all(int(i[0]) == 0 for i in infos)
+    by_scene = {}
+    for k, i in enumerate(infos):
+        by_scene.setdefault(k % len(scenes), set()).add(tuple(i[:18].tolist()))
+    consistent = all(len(v) == 1 for v in by_scene.values())
+
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    # per-stage durations of the last timed step (probes inside the graphs)
+    stage_ms = {}
+    for s_i, name in enumerate(_native.STAGES):
+        v = [probes[k][2 * s_i].elapsed_time(probes[k][2 * s_i + 1]) for k in range(B)]
+        stage_ms[name] = statistics.mean(v)
+    kernels_per_pair = runner.graph_kernels()
+
+    # ---- end to end through the public batch API (host buffers)
+    E = args.e2e_pairs
+    hpairs = []
+    for k in range(E):
+        ref, src = scenes[k % len(scenes)]
+        hpairs.append((torch.from_numpy(ref).pin_memory(), torch.from_numpy(src).pin_memory()))
+    hout = [(torch.empty((h, w, 3), dtype=torch.float32).pin_memory(),
+             torch.empty((_native.INFO_WORDS,), dtype=torch.int32).pin_memory()) for _ in range(E)]
+    runner.set_probes(0, None)
+    for k in range(len(runner.streams)):
+        runner.set_probes(k, None)
+    for _ in range(max(args.warmup, 1)):
+        runner.run_host(hpairs, hout)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        a, b = runner.run_host(hpairs, hout)
+        h2d, d2h = a, b
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    e2e_ok = all(int(x[1][0]) == 0 for x in hout)
+    if world > 1:
+        t = torch.tensor([ems], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    value = world * B * args.steps / (ms / 1e3)
+    e2e_value = world * E * args.steps / (ems / 1e3)
+    peak, peak_src = peaks()
+    sb = stage_bytes(w, h)
+    dom = max(stage_ms, key=lambda k: stage_ms[k])
+    roof_stage = dom if sb.get(dom) else max((k for k in sb if sb[k]), key=lambda k: stage_ms[k])
+    traffic = ncu_traffic().get(roof_stage)
+    achieved = sb[roof_stage] / (stage_ms[roof_stage] / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32/f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "width": w, "height": h, "pairs_per_step_per_gpu": B,
+                   "global_pairs_per_step": B * world, "streams": args.streams,
+                   "distinct_scenes": len(scenes), "graph": not args.no_graph,
+                   "l2": "inputs larger than L2 (each pair 121 MB, %d resident pairs)" % B,
+                   "parallelism": f"pair-sharded x{world}, no collective"},
+        "roofline": {"bound": "hbm", "stage": roof_stage, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "note": "achieved = algorithmic bytes per launch / mean stage time "
+                             "(CUDA-event probes inside the graphs, last timed step)"},
+        "stage_ms": stage_ms, "dominant_stage": dom,
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "pairs_per_step": E},
+        "gpu_launches": kernels_per_pair * B * args.steps,
+        "kernels_per_pair": kernels_per_pair,
+        "clocks": clk,
+        "checks": {"all_registered": ok, "replicas_identical": consistent, "e2e_ok": e2e_ok},
+    }
+    if cpu_base is not None:
+        line["cpu_baseline"] = cpu_base
+    emit(line)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

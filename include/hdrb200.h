@@ -1,0 +1,224 @@
+/*
+ * hdrb200.h — C ABI of libhdrb200.so, the sm_100a register+merge path.
+ *
+ * The reference (`hdrflow`, pure Python) has no FFI; its drop-in boundary is
+ * the set of Python functions in pkg/src/hdrflow/{pipeline,image,matcher,
+ * weeding,geometry,densify,fusion}.py. Each export below is the GPU twin of
+ * one of those functions (cited per entry) so a binding (ctypes, see
+ * INTEGRATION.md) can replace them one for one. All array arguments are
+ * DEVICE pointers (caller-owned, row-major, C-contiguous); work is enqueued
+ * on the context's stream. No torch types cross this boundary.
+ *
+ * Error convention: every entry returns an int status.
+ */
+#ifndef HDRB200_H
+#define HDRB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HDR_OK = 0,
+  HDR_ERR_INVALID = 1,      /* ValueError (bad shape / precondition)        */
+  HDR_ERR_DEGENERATE = 2,   /* geometry.DegenerateFit (geometry.py:18)      */
+  HDR_ERR_REGISTRATION = 3, /* pipeline.RegistrationError (pipeline.py:27)  */
+  HDR_ERR_CONFIG = 4,       /* pipeline.ConfigError (pipeline.py:31)        */
+  HDR_ERR_CUDA = 5,         /* RuntimeError from the CUDA runtime           */
+  HDR_ERR_EMPTY = 6         /* "no result" (ssd_match returns None)         */
+};
+
+/* Mirror of PipelineParams (pipeline.py:35-57); delta < 0 means None. */
+typedef struct hdr_params {
+  int32_t tile;
+  int32_t quadrant_half;
+  int32_t radius;
+  int32_t patch;
+  int32_t max_levels;
+  int32_t iterations;
+  int32_t coarse_iterations;
+  int32_t delta;
+  int32_t passes;
+  int32_t ssim_window;
+  int32_t workers;
+  int32_t _pad;
+  double threshold;
+  double eps_px;
+  double sigma_s;
+  double sigma_r;
+  double ssim_sigma;
+  double normalization_floor;
+  uint64_t seed;
+} hdr_params;
+
+/* Caller-owned device outputs of one register_and_fuse call
+ * (RegistrationOutput, pipeline.py:99-109). `ssim` is float32 on the device
+ * (the host wrapper widens to float64). `info` receives int32 words:
+ *   [0] status (HDR_OK or HDR_ERR_REGISTRATION)
+ *   [1] 1 if `homography` is valid (MatchResult.homography is not None)
+ *   [2] number of pyramid levels L
+ *   [3 + 2*l], [4 + 2*l]  level_counts[l] = (raw, weeded), l < L
+ *   [16] number of weeded level-0 matches, [17] number of raw level-0 matches
+ *   [18] diagnostic: fits whose rank test fell in the grey zone
+ * `matches`/`raw_matches` hold up to hdr_max_matches() rows of 5 float64. */
+typedef struct hdr_outputs {
+  float* composite;   /* (H, W, 3) */
+  float* flow;        /* (H, W, 2) */
+  float* warped;      /* (H, W, 3) */
+  uint8_t* valid;     /* (H, W)    */
+  float* ssim;        /* (H, W)    */
+  double* matches;    /* (max, 5)  */
+  double* raw_matches;/* (max, 5)  */
+  double* homography; /* 3x3       */
+  int32_t* info;      /* 32 words  */
+} hdr_outputs;
+
+#define HDR_INFO_WORDS 32
+
+typedef struct hdr_ctx hdr_ctx;
+
+/* ---- context / params ------------------------------------------------- */
+void hdr_params_default(hdr_params* p);
+/* PipelineParams.validate (pipeline.py:59-87): HDR_OK or HDR_ERR_CONFIG with
+ * the reference's message copied into msg. */
+int hdr_params_validate(const hdr_params* p, char* msg, size_t msg_len);
+/* Allocates the whole workspace for images up to width x height once; the
+ * hot path never allocates. `stream` is a cudaStream_t (NULL = legacy). */
+int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_ctx** out);
+int hdr_ctx_destroy(hdr_ctx* ctx);
+int hdr_ctx_set_stream(hdr_ctx* ctx, void* stream);
+int32_t hdr_max_matches(int32_t width, int32_t height, int32_t tile);
+const char* hdr_last_error(void);
+/* Blocks until the context's stream drains; returns HDR_ERR_CUDA on a
+ * sticky or asynchronous CUDA error. */
+int hdr_ctx_sync(hdr_ctx* ctx);
+
+/* ---- whole pair (pipeline.register_and_fuse, pipeline.py:174-198) -------
+ * ref/src: (H, W, 3) float32 in [0,1]. Fully asynchronous, no host sync,
+ * CUDA-graph capturable; the registration verdict lands in out->info[0]. */
+int hdr_register_and_fuse(hdr_ctx* ctx, const hdr_params* p, int32_t width,
+                          int32_t height, const float* ref, const float* src,
+                          const hdr_outputs* out);
+/* Captures the whole pair into a CUDA graph bound to these pointers and
+ * replays it (first call per (ctx, shape, pointers, params) instantiates). */
+int hdr_register_and_fuse_graph(hdr_ctx* ctx, const hdr_params* p, int32_t width,
+                                int32_t height, const float* ref, const float* src,
+                                const hdr_outputs* out);
+
+/* Stage probes: when set, the pair pipeline records events[2*s] before and
+ * events[2*s+1] after stage s on the context stream (cudaEvent_t handles;
+ * NULL disables). Stages: 0 luminance/histograms/LUT/pyramids, 1 SAT +
+ * corners, 2 coarse-to-fine match/weed/fit chain, 3 splat + domain-transform
+ * filter, 4 densify-finalise + warp, 5 SSIM, 6 fusion. Probes are baked into
+ * graphs captured while they are set. */
+#define HDR_NUM_STAGES 7
+int hdr_ctx_set_probes(hdr_ctx* ctx, void* const* events);
+/* Kernel nodes in the most recently instantiated pair graph of ctx. */
+int32_t hdr_ctx_graph_kernels(hdr_ctx* ctx);
+
+/* ---- per-stage twins ---------------------------------------------------- */
+/* image.luminance (image.py:23-29): rgb (n,3) -> lum (n). */
+int hdr_luminance(hdr_ctx* ctx, const float* rgb, int64_t n, float* lum);
+/* image.match_histogram (image.py:96-122), one channel: src (n_src) mapped
+ * onto ref's histogram; channel c of interleaved data via stride. */
+int hdr_match_histogram(hdr_ctx* ctx, const float* src, int64_t n_src,
+                        const float* ref, int64_t n_ref, int32_t stride,
+                        float* out);
+/* image.build_pyramid (image.py:71-88): levels[0] = img (not copied); writes
+ * levels 1.. into out_levels[] (device buffers of (h>>l) x (w>>l) floats);
+ * returns the count in *n_levels. */
+int hdr_build_pyramid(hdr_ctx* ctx, const float* img, int32_t width, int32_t height,
+                      int32_t max_levels, int32_t min_dim, float** out_levels,
+                      int32_t* n_levels);
+/* image.integral (image.py:32-44): (h+1, w+1) float64 summed-area table. */
+int hdr_integral(hdr_ctx* ctx, const float* img, int32_t width, int32_t height,
+                 double* table);
+/* matcher.detect_corners (matcher.py:64-105): rows (x, y, score) in tile
+ * order; *count (host) receives n. corners needs room for ntiles rows. */
+int hdr_detect_corners(hdr_ctx* ctx, const float* lum, int32_t width, int32_t height,
+                       int32_t tile, double threshold, int32_t half,
+                       double* corners, int32_t* count);
+/* matcher.ssd_match (matcher.py:108-143) for n points at once:
+ * pts (n, 4) int32 (x_ref, y_ref, x_init, y_init) -> out (n, 3) float64
+ * (x_src, y_src, score), found[i] = 0 where the reference returns None. */
+int hdr_ssd_match(hdr_ctx* ctx, const float* ref, const float* src, int32_t width,
+                  int32_t height, const int32_t* pts, int32_t n, int32_t radius,
+                  int32_t patch, double* out, uint8_t* found);
+/* matcher._match_level (matcher.py:181-210): detect + predict through
+ * h_pred (device 3x3) + SSD; raw (ntiles, 5); *count (host) = rows. */
+int hdr_match_level(hdr_ctx* ctx, const hdr_params* p, const float* lum_ref,
+                    const float* lum_src, int32_t width, int32_t height,
+                    const double* h_pred, double* raw, int32_t* count);
+/* weeding.weed (weeding.py:100-111): matches (n, 5); kept (n) int64 sorted
+ * indices, *n_kept (host); witness (n) int64. seed is WeedParams.seed. */
+int hdr_weed(hdr_ctx* ctx, const double* matches, int32_t n, int32_t width,
+             int32_t height, int32_t iterations, double eps, uint64_t seed,
+             int32_t delta, int64_t* kept, int32_t* n_kept, int64_t* witness);
+/* matcher.fit_matches_homography (matcher.py:213-218): least-squares H over
+ * (n, 5) matches; h (3x3, device). HDR_ERR_DEGENERATE on DegenerateFit. */
+int hdr_fit_matches_homography(hdr_ctx* ctx, const double* matches, int32_t n,
+                               int32_t width, int32_t height, double* h);
+/* geometry.fit_homography (geometry.py:35-77): ref_pts/src_pts (n, 2). */
+int hdr_fit_homography(hdr_ctx* ctx, const double* ref_pts, const double* src_pts,
+                       int32_t n, double* h);
+/* geometry.inlier_mask (geometry.py:118-121). */
+int hdr_inlier_mask(hdr_ctx* ctx, const double* h, const double* ref_pts,
+                    const double* src_pts, int32_t n, double eps, uint8_t* mask);
+/* geometry.homography_pixel_flow (geometry.py:124-135): flow (h, w, 2). */
+int hdr_homography_flow(hdr_ctx* ctx, const double* h, int32_t width, int32_t height,
+                        float* flow);
+/* pipeline.match_stack (pipeline.py:122-130): RGB pair -> level-0 weeded and
+ * raw matches, H, level counts (info words as in hdr_outputs). */
+int hdr_match_stack(hdr_ctx* ctx, const hdr_params* p, int32_t width, int32_t height,
+                    const float* ref, const float* src, double* matches,
+                    double* raw_matches, double* homography, int32_t* info);
+/* densify.build_sparse_maps (densify.py:38-56): (m, 5) -> pu, pv, n planes
+ * (h, w) float64; collisions keep the lowest (score, index). */
+int hdr_sparse_maps(hdr_ctx* ctx, const double* matches, int32_t m, int32_t width,
+                    int32_t height, double* pu, double* pv, double* n);
+/* densify.dt_filter (densify.py:78-113): guide (h, w) f32, planes (k, h, w)
+ * float64 planar, filtered in place. */
+int hdr_dt_filter(hdr_ctx* ctx, const float* guide, double* planes, int32_t k,
+                  int32_t width, int32_t height, double sigma_s, double sigma_r,
+                  int32_t passes);
+/* densify.densify_flow (densify.py:116-142): filtered planes (3, h, w) ->
+ * flow (h, w, 2) f32; fallback = device 3x3 or NULL. */
+int hdr_densify_finalize(hdr_ctx* ctx, const double* smooth, int32_t width,
+                         int32_t height, const double* fallback, double floor_,
+                         float* flow);
+/* densify.warp_image (densify.py:145-174): src (h, w, c) c in {1,3}. */
+int hdr_warp_image(hdr_ctx* ctx, const float* src, int32_t channels, int32_t width,
+                   int32_t height, const float* flow, float* warped, uint8_t* valid);
+/* fusion.ssim_map (fusion.py:34-64): a, b (h, w) f32 -> ssim (h, w) f32. */
+int hdr_ssim_map(hdr_ctx* ctx, const float* a, const float* b, int32_t width,
+                 int32_t height, int32_t window, double sigma, float* out);
+/* pipeline.make_ssim (pipeline.py:165-171). */
+int hdr_make_ssim(hdr_ctx* ctx, const float* lum_ref, const float* warped,
+                  int32_t width, int32_t height, int32_t window, double sigma,
+                  float* out);
+/* fusion.quality_weights (fusion.py:67-77): rgb (h, w, 3) -> (h, w) f32. */
+int hdr_quality_weights(hdr_ctx* ctx, const float* rgb, int32_t width, int32_t height,
+                        float* out);
+/* fusion.fuse (fusion.py:135-157): levels <= 0 selects the default. */
+int hdr_fuse(hdr_ctx* ctx, const float* ref, const float* warped, const float* ssim,
+             const uint8_t* valid, int32_t width, int32_t height, int32_t levels,
+             float* out);
+
+/* ---- host-side helpers (no GPU work) ------------------------------------ */
+/* matcher.level_seed (matcher.py:146-149). */
+uint32_t hdr_level_seed(uint64_t seed, int32_t level);
+/* Philox keys of weeding._iteration_rng (weeding.py:62-66):
+ * keys[2*i], keys[2*i+1] = SeedSequence(seed, spawn_key=(i,)).generate_state(2, u64). */
+int hdr_iteration_keys(uint64_t seed, int32_t iterations, uint64_t* keys);
+/* Test hook: the device sampler's own code run on the host —
+ * Generator(Philox(key)).choice(n, 4, replace=False) repeated `draws` times
+ * on one stream; out (draws, 4). */
+int hdr_choice4_host(const uint64_t* key, int32_t n, int32_t draws, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,164 @@
+"""Generate tests/golden/*.npz by running the REAL reference (`hdrflow`).
+
+TEST INFRASTRUCTURE ONLY. Runs in the build container, where the reference
+is importable from /root/reference/pkg/src; the fixtures it writes are what
+pins the oracle (tests/test_oracle_golden.py) on any host.
+
+The reference needs one shim to return from a successful registration:
+`pipeline.fit_fallback` uses `fit_matches_homography`, which pipeline.py
+never imports (pipeline.py:148 vs :18-24).
+
+usage: python oracle/gen_golden.py [--ref /root/reference/pkg/src]
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1504_01441_b200 import synth  # noqa: E402
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+STRIDE = 8  # dense outputs: full-array digests + a 1-in-8 lattice sample
+
+
+def sub(a):
+    s = np.ascontiguousarray(a[::STRIDE, ::STRIDE])
+    return s.astype(np.float32) if s.dtype == np.float64 else s
+
+# (name, width, height, rotation_deg, seed)
+SCENES = [
+    ("vga_s0", 640, 480, 0.0, 0),
+    ("vga_rot_s1", 640, 480, 0.5, 1),
+    ("qvga_s2", 320, 240, 0.0, 2),
+    ("r960_s3", 960, 720, 0.25, 3),
+]
+
+
+def digest(a) -> str:
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes() + str(a.dtype).encode() + str(a.shape).encode()).hexdigest()
+
+
+def load_reference(path):
+    sys.path.insert(0, path)
+    from hdrflow import image, matcher, pipeline  # noqa: F401
+    pipeline.fit_matches_homography = matcher.fit_matches_homography
+    import hdrflow
+    return hdrflow
+
+
+def scene_fixture(hf, w, h, rot, seed):
+    from hdrflow import densify, fusion, image, matcher, pipeline, weeding
+    st = synth.synth_stack(synth.working_spec(w, h, rotation_deg=rot), seed)
+    ref, src = st.ref, st.src
+    params = pipeline.PipelineParams()
+    out = {"inputs_digest": np.array([digest(ref), digest(src)])}
+    lum_ref = image.luminance(ref)
+    lum_src = image.luminance(src)
+    eq = image.match_histogram(lum_src, lum_ref)
+    rp = image.build_pyramid(lum_ref, params.max_levels)
+    sp = image.build_pyramid(eq, params.max_levels)
+    out["lum_ref_digest"] = np.array(digest(lum_ref))
+    out["eq_src_digest"] = np.array(digest(eq))
+    out["pyr_digests"] = np.array([digest(a) for a in rp] + [digest(a) for a in sp])
+    out["n_levels"] = np.array(len(rp))
+    # per-level trace, re-running the reference's own stages
+    mp = params.matcher_params()
+    h_pred = np.eye(3)
+    for lev in range(len(rp) - 1, -1, -1):
+        lr, ls = rp[lev], sp[lev]
+        hh, ww = lr.shape
+        out[f"L{lev}_corners"] = matcher.detect_corners(lr, mp.tile, mp.threshold, mp.quadrant_half)
+        out[f"L{lev}_hpred"] = h_pred.copy()
+        raw = matcher._match_level(lr, ls, h_pred, mp)
+        out[f"L{lev}_raw"] = raw
+        kept = np.zeros(0, dtype=np.int64)
+        if len(raw) >= 4:
+            res = weeding.weed_parallel(raw, (ww, hh), mp.weed_params(lev, ww), mp.workers)
+            kept, wit = res.kept, res.witness
+            out[f"L{lev}_witness"] = wit
+        out[f"L{lev}_kept"] = kept
+        weeded = raw[kept] if len(raw) >= 4 else np.zeros((0, 5))
+        if len(weeded) >= 4:
+            try:
+                h_pred = matcher.fit_matches_homography(weeded, ww, hh)
+                out[f"L{lev}_hfit"] = h_pred
+            except Exception:
+                pass
+    r = pipeline.register_and_fuse(ref, src, params)
+    for k in ("matches", "raw_matches"):
+        out[k] = getattr(r, k)
+    out["homography"] = r.homography if r.homography is not None else np.zeros((0, 3))
+    out["level_counts"] = np.array(r.level_counts, dtype=np.int64)
+    for k in ("composite", "flow", "warped", "valid", "ssim"):
+        a = getattr(r, k)
+        out[f"{k}_digest"] = np.array(digest(a))
+        out[f"{k}_sub"] = sub(a)
+    # staged intermediates on the reference's own path
+    maps = densify.build_sparse_maps(r.matches, w, h)
+    sm = densify.dt_filter(lum_ref, np.stack([maps.pu, maps.pv, maps.n], axis=-1),
+                           params.sigma_s, params.sigma_r, params.passes)
+    out["smooth_digest"] = np.array(digest(sm))
+    out["smooth_sub"] = sub(sm)
+    wr, ws = fusion.fusion_weights(ref, r.warped, r.ssim, r.valid.astype(np.float32))
+    out["wref_sub"] = sub(wr)
+    out["wsrc_sub"] = sub(ws)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default="/root/reference/pkg/src")
+    args = ap.parse_args()
+    hf = load_reference(args.ref)
+    os.makedirs(GOLDEN, exist_ok=True)
+    for name, w, h, rot, seed in SCENES:
+        fx = scene_fixture(hf, w, h, rot, seed)
+        fx["scene"] = np.array([w, h, rot, seed], dtype=np.float64)
+        np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **fx)
+        print(name, fx["level_counts"].tolist())
+    # error-parity case: the reference's default SceneSpec does not register
+    from hdrflow import pipeline
+    st = synth.synth_stack(synth.SceneSpec(), 0)
+    try:
+        pipeline.register_and_fuse(st.ref, st.src)
+        raised = ""
+    except pipeline.RegistrationError as exc:
+        raised = str(exc)
+    np.savez_compressed(os.path.join(GOLDEN, "default_scene_error.npz"),
+                        inputs_digest=np.array([digest(st.ref), digest(st.src)]),
+                        message=np.array(raised))
+    print("default scene:", raised)
+    # SeedSequence / Philox / choice vectors (weeding.py:62-84)
+    rng = np.random.default_rng(7)
+    cases = []
+    for _ in range(40):
+        seed = int(rng.integers(0, 2 ** 32))
+        it = int(rng.integers(0, 256))
+        n = int(rng.integers(4, 2000))
+        ss = np.random.SeedSequence(entropy=seed, spawn_key=(it,))
+        key = ss.generate_state(2, np.uint64)
+        g = np.random.Generator(np.random.Philox(ss))
+        draws = np.stack([g.choice(n, size=4, replace=False) for _ in range(10)])
+        cases.append((seed, it, n, key, draws))
+    np.savez_compressed(os.path.join(GOLDEN, "philox_choice.npz"),
+                        seed=np.array([c[0] for c in cases], dtype=np.uint64),
+                        it=np.array([c[1] for c in cases]), n=np.array([c[2] for c in cases]),
+                        key=np.stack([c[3] for c in cases]),
+                        draws=np.stack([c[4] for c in cases]),
+                        level_seeds=np.array([[int(np.random.SeedSequence(entropy=s, spawn_key=(l,))
+                                                   .generate_state(1)[0]) for l in range(5)]
+                                              for s in (0, 1, 12345, 2 ** 40 + 3)],
+                                             dtype=np.uint64))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1015 @@
+// C ABI of libhdrb200.so: context/workspace, the device-resident pair
+// pipeline (pipeline.register_and_fuse, pipeline.py:174-198), CUDA-graph
+// replay, per-stage twins, and the host-side SeedSequence key schedule.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hdrb200.h"
+#include "hdr_common.cuh"
+#include "hdr_geom.cuh"
+#include "hdr_internal.h"
+#include "hdr_scan.cuh"
+
+using namespace hdr;
+
+// ------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(HDR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static int check_launch() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return fail(HDR_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return HDR_OK;
+}
+
+extern "C" const char* hdr_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------ SeedSequence
+// numpy.random.SeedSequence (numpy/random/bit_generator.pyx), host side.
+namespace {
+constexpr uint32_t INIT_A = 0x43b0d7e5u, MULT_A = 0x931e8875u, INIT_B = 0x8b51f9ddu,
+                   MULT_B = 0x58f38dedu, MIX_L = 0xca01f9ddu, MIX_R = 0x4973f715u;
+
+void words_of(uint64_t v, std::vector<uint32_t>& out) {
+  if (v == 0) { out.push_back(0); return; }
+  while (v) { out.push_back((uint32_t)v); v >>= 32; }
+}
+
+void seedseq_pool(uint64_t entropy, uint64_t spawn, uint32_t pool[4]) {
+  std::vector<uint32_t> run, sp, ent;
+  words_of(entropy, run);
+  words_of(spawn, sp);
+  while (run.size() < 4) run.push_back(0);  // spawn key present: pad run entropy
+  ent = run;
+  ent.insert(ent.end(), sp.begin(), sp.end());
+  uint32_t hc = INIT_A;
+  auto hashmix = [&](uint32_t v) {
+    v ^= hc;
+    hc *= MULT_A;
+    v *= hc;
+    v ^= v >> 16;
+    return v;
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    uint32_t r = MIX_L * x - MIX_R * y;
+    r ^= r >> 16;
+    return r;
+  };
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < (int)ent.size() ? ent[i] : 0u);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s]));
+  for (size_t s = 4; s < ent.size(); ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[s]));
+}
+
+void seedseq_state(const uint32_t pool[4], int n, uint32_t* out) {
+  uint32_t hc = INIT_B;
+  for (int i = 0; i < n; ++i) {
+    uint32_t v = pool[i % 4];
+    v ^= hc;
+    hc *= MULT_B;
+    v *= hc;
+    v ^= v >> 16;
+    out[i] = v;
+  }
+}
+}  // namespace
+
+extern "C" uint32_t hdr_level_seed(uint64_t seed, int32_t level) {
+  uint32_t pool[4], s;
+  seedseq_pool(seed, (uint64_t)level, pool);
+  seedseq_state(pool, 1, &s);
+  return s;
+}
+
+extern "C" int hdr_iteration_keys(uint64_t seed, int32_t iterations, uint64_t* keys) {
+  if (iterations < 0 || (!keys && iterations)) return fail(HDR_ERR_INVALID, "bad key request");
+  for (int i = 0; i < iterations; ++i) {
+    uint32_t pool[4], st[4];
+    seedseq_pool(seed, (uint64_t)i, pool);
+    seedseq_state(pool, 4, st);
+    keys[2 * i] = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+    keys[2 * i + 1] = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+  }
+  return HDR_OK;
+}
+
+extern "C" int hdr_choice4_host(const uint64_t* key, int32_t n, int32_t draws, int64_t* out) {
+  if (n < 4) return fail(HDR_ERR_INVALID, "n must be >= 4");
+  Philox g;
+  philox_init(&g, key[0], key[1]);
+  for (int d = 0; d < draws; ++d) {
+    int idx[4];
+    choice4(&g, n, idx);
+    for (int k = 0; k < 4; ++k) out[4 * d + k] = idx[k];
+  }
+  return HDR_OK;
+}
+
+// ------------------------------------------------------------ params
+extern "C" void hdr_params_default(hdr_params* p) {
+  memset(p, 0, sizeof(*p));
+  p->tile = 64;
+  p->threshold = 4.0 / 255.0;
+  p->quadrant_half = 8;
+  p->radius = 10;
+  p->patch = 21;
+  p->max_levels = 5;
+  p->iterations = 256;
+  p->coarse_iterations = 64;
+  p->delta = -1;
+  p->eps_px = 2.0;
+  p->sigma_s = 400.0;
+  p->sigma_r = 0.2;
+  p->passes = 3;
+  p->ssim_window = 11;
+  p->ssim_sigma = 1.5;
+  p->normalization_floor = 1e-4;
+  p->seed = 0;
+  p->workers = 1;
+}
+
+extern "C" int hdr_params_validate(const hdr_params* p, char* msg, size_t len) {
+  struct Rule { bool ok; const char* text; };
+  const Rule rules[] = {  // PipelineParams.validate order (pipeline.py:60-87)
+      {p->tile >= 16, "tile must be >= 16"},
+      {p->threshold > 0, "threshold must be positive"},
+      {p->quadrant_half >= 2, "quadrant_half must be >= 2"},
+      {p->radius >= 1, "radius must be >= 1"},
+      {p->patch >= 3 && p->patch % 2 == 1, "patch must be odd and >= 3"},
+      {1 <= p->max_levels && p->max_levels <= kMaxLevels, "max_levels must be in [1, 5]"},
+      {p->iterations >= 1, "iterations must be >= 1"},
+      {p->coarse_iterations >= 1, "coarse_iterations must be >= 1"},
+      {p->delta < 0 || p->delta >= 4, "delta must be >= 4"},
+      {p->eps_px > 0, "eps_px must be positive"},
+      {p->sigma_s > 0, "sigma_s must be positive"},
+      {p->sigma_r > 0, "sigma_r must be positive"},
+      {p->passes >= 1, "passes must be >= 1"},
+      {p->ssim_window >= 3 && p->ssim_window % 2 == 1, "ssim_window must be odd and >= 3"},
+      {p->ssim_sigma > 0, "ssim_sigma must be positive"},
+      {p->normalization_floor > 0, "normalization_floor must be positive"},
+      {p->workers >= 1, "workers must be >= 1"},
+      {p->workers >= 1 && p->iterations % p->workers == 0, "iterations must be divisible by workers"},
+      {p->workers >= 1 && p->coarse_iterations % p->workers == 0,
+       "coarse_iterations must be divisible by workers"},
+  };
+  for (const Rule& r : rules)
+    if (!r.ok) {
+      if (msg && len) snprintf(msg, len, "%s", r.text);
+      return fail(HDR_ERR_CONFIG, r.text);
+    }
+  return HDR_OK;
+}
+
+// ------------------------------------------------------------ geometry of a call
+struct Dims {
+  int w, h;
+};
+
+// image.build_pyramid level dims (image.py:71-88)
+static int pyramid_dims(int w, int h, int max_levels, Dims* d) {
+  d[0] = {w, h};
+  int n = 1;
+  while (n < max_levels) {
+    int nw = d[n - 1].w / 2, nh = d[n - 1].h / 2;
+    if (std::min(nw, nh) < 100) break;
+    d[n++] = {nw, nh};
+  }
+  return n;
+}
+
+// fusion.default_fusion_levels (fusion.py:131-132): max(1, floor(log2 min) - 1)
+static int fusion_levels_default(int w, int h) {
+  int m = std::min(w, h);
+  int lg = 31 - __builtin_clz((unsigned)m);
+  return std::max(1, lg - 1);
+}
+
+// fusion.gaussian_pyramid dims: ceil halving while len < levels and min >= 2
+static int fusion_dims(int w, int h, int levels, std::vector<Dims>& d) {
+  d.clear();
+  d.push_back({w, h});
+  while ((int)d.size() < levels && std::min(d.back().w, d.back().h) >= 2)
+    d.push_back({(d.back().w + 1) / 2, (d.back().h + 1) / 2});
+  return (int)d.size();
+}
+
+static int ntiles_of(int w, int h, int tile) { return ceil_div(w, tile) * ceil_div(h, tile); }
+
+// ------------------------------------------------------------ context
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct hdr_ctx {
+  int W = 0, H = 0;
+  int64_t P = 0;
+  cudaStream_t stream = nullptr;
+  // raster
+  float* lum_ref = nullptr;
+  uint8_t* q_src = nullptr;
+  float* eq_src = nullptr;
+  float* pyr = nullptr;         // levels 1.. of both pyramids
+  uint32_t* hist = nullptr;     // [ref, src, warped, scratch] x 256
+  float* lut = nullptr;         // [src, warped, scratch] x 256
+  double* sat = nullptr;
+  TileCorner* tiles = nullptr;  // all levels
+  int64_t tiles_cap = 0;
+  // matching
+  MatchRow* slot_rows = nullptr;
+  uint8_t* slot_flags = nullptr;
+  MatchRow* raw = nullptr;
+  MatchRow* weeded = nullptr;
+  int64_t rows_cap = 0;
+  int32_t* counters = nullptr;  // 0 raw, 1 weeded, 2 splat status, 3 grey, 4 fit status
+  uint32_t* mask = nullptr;
+  int32_t* witness = nullptr;
+  int64_t* kept = nullptr;
+  double* hpred = nullptr;      // 9 + 9 scratch
+  double* fits = nullptr;
+  int64_t fits_cap = 0;
+  uint64_t* keys = nullptr;     // kMaxLevels x keys_iters x 2
+  int keys_iters = 0;
+  uint64_t keys_seed = ~0ULL;
+  int keys_it = -1, keys_cit = -1;
+  // densify
+  double* planes = nullptr;     // 3 x P
+  double* carry = nullptr;
+  uint64_t* splat_key = nullptr;
+  int32_t* splat_idx = nullptr;
+  uint8_t* qw = nullptr;
+  // merge
+  float* wr = nullptr;
+  float* ws = nullptr;
+  float* fpyr = nullptr;
+  int64_t fpyr_cap = 0;
+  double* taps = nullptr;       // 31
+  int taps_window = -1;
+  double taps_sigma = -1.0;
+  int32_t* info_scratch = nullptr;
+  cudaEvent_t probes[2 * HDR_NUM_STAGES] = {};
+  bool probing = false;
+  int32_t graph_kernels = 0;
+  std::map<std::string, GraphEntry> graphs;
+  std::vector<void*> allocs;
+};
+
+template <class T>
+static cudaError_t ctx_alloc(hdr_ctx* c, T** p, size_t count) {
+  size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e == cudaSuccess) {
+    c->allocs.push_back(q);
+    *p = reinterpret_cast<T*>(q);
+  }
+  return e;
+}
+
+extern "C" int32_t hdr_max_matches(int32_t width, int32_t height, int32_t tile) {
+  return ntiles_of(width, height, std::max(16, tile));
+}
+
+extern "C" int hdr_ctx_destroy(hdr_ctx* c) {
+  if (!c) return HDR_OK;
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+  return HDR_OK;
+}
+
+static void init_kernel_attributes();
+
+extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_ctx** out) {
+  if (!out || width < 1 || height < 1) return fail(HDR_ERR_INVALID, "bad context size");
+  static std::once_flag once;
+  std::call_once(once, init_kernel_attributes);
+  hdr_ctx* c = new hdr_ctx();
+  c->W = width;
+  c->H = height;
+  c->P = (int64_t)width * height;
+  c->stream = (cudaStream_t)stream;
+  int64_t P = c->P;
+  Dims d[kMaxLevels];
+  int64_t pyr_sum = 0;
+  {
+    int w = width, h = height;
+    for (int l = 1; l < kMaxLevels; ++l) { w /= 2; h /= 2; pyr_sum += (int64_t)w * h + 64; }
+  }
+  (void)d;
+  int64_t tiles_total = 0;
+  {
+    int w = width, h = height;
+    for (int l = 0; l < kMaxLevels; ++l) { tiles_total += ntiles_of(std::max(w, 1), std::max(h, 1), 16); w /= 2; h /= 2; }
+  }
+  c->tiles_cap = tiles_total;
+  c->rows_cap = ntiles_of(width, height, 16) + 32;
+  std::vector<Dims> fd;
+  fusion_dims(width, height, 64, fd);
+  int64_t fsum = 0;
+  for (size_t k = 1; k < fd.size(); ++k) fsum += 11 * ((int64_t)fd[k].w * fd[k].h + 64);
+  c->fpyr_cap = fsum;
+  cudaError_t e = cudaSuccess;
+#define ALLOC(ptr, n) \
+  if (e == cudaSuccess) e = ctx_alloc(c, &c->ptr, (size_t)(n))
+  ALLOC(lum_ref, P);
+  ALLOC(q_src, P + 16);
+  ALLOC(eq_src, P);
+  ALLOC(pyr, 2 * pyr_sum);
+  ALLOC(hist, 4 * kBins);
+  ALLOC(lut, 3 * kBins);
+  ALLOC(sat, (int64_t)(width + 1) * (height + 1));
+  ALLOC(tiles, tiles_total);
+  ALLOC(slot_rows, c->rows_cap);
+  ALLOC(slot_flags, c->rows_cap);
+  ALLOC(raw, c->rows_cap);
+  ALLOC(weeded, c->rows_cap);
+  ALLOC(counters, 16);
+  ALLOC(mask, c->rows_cap / 32 + 2);
+  ALLOC(witness, c->rows_cap + 1);
+  ALLOC(kept, c->rows_cap);
+  ALLOC(hpred, 32);
+  ALLOC(planes, 3 * P);
+  ALLOC(carry, (int64_t)ceil_div(height, 64) * width * 4 + 64);
+  ALLOC(splat_key, P);
+  ALLOC(splat_idx, P);
+  ALLOC(qw, P + 16);
+  ALLOC(wr, P);
+  ALLOC(ws, P);
+  ALLOC(fpyr, fsum + 64);
+  ALLOC(taps, 64);
+  ALLOC(info_scratch, HDR_INFO_WORDS);
+#undef ALLOC
+  if (e != cudaSuccess) {
+    hdr_ctx_destroy(c);
+    return fail(HDR_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return HDR_OK;
+}
+
+extern "C" int hdr_ctx_set_stream(hdr_ctx* c, void* stream) {
+  if (!c) return fail(HDR_ERR_INVALID, "null context");
+  c->stream = (cudaStream_t)stream;
+  return HDR_OK;
+}
+
+extern "C" int hdr_ctx_set_probes(hdr_ctx* c, void* const* events) {
+  if (!c) return fail(HDR_ERR_INVALID, "null context");
+  c->probing = events != nullptr;
+  for (int i = 0; i < 2 * HDR_NUM_STAGES; ++i)
+    c->probes[i] = events ? (cudaEvent_t)events[i] : nullptr;
+  return HDR_OK;
+}
+
+extern "C" int32_t hdr_ctx_graph_kernels(hdr_ctx* c) { return c ? c->graph_kernels : -1; }
+
+static void probe(hdr_ctx* c, int stage, int end) {
+  if (!c->probing) return;
+  cudaEvent_t e = c->probes[2 * stage + end];
+  if (e) cudaEventRecord(e, c->stream);
+}
+
+extern "C" int hdr_ctx_sync(hdr_ctx* c) {
+  if (!c) return fail(HDR_ERR_INVALID, "null context");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaGetLastError());
+  return HDR_OK;
+}
+
+// Philox keys for every level, cached per (seed, iterations, coarse_iterations).
+static int ensure_keys(hdr_ctx* c, const hdr_params* p) {
+  int iters = std::max(p->iterations, p->coarse_iterations);
+  if (c->keys && c->keys_seed == p->seed && c->keys_it == p->iterations &&
+      c->keys_cit == p->coarse_iterations)
+    return HDR_OK;
+  if (iters > c->keys_iters) {
+    if (c->keys) cudaFree(c->keys);
+    CUDA_TRY(cudaMalloc(&c->keys, sizeof(uint64_t) * 2 * (size_t)iters * kMaxLevels));
+    c->keys_iters = iters;
+  }
+  if ((int64_t)iters * 20 > c->fits_cap) {
+    if (c->fits) cudaFree(c->fits);
+    CUDA_TRY(cudaMalloc(&c->fits, sizeof(double) * 20 * (size_t)iters));
+    c->fits_cap = (int64_t)iters * 20;
+  }
+  std::vector<uint64_t> host(2 * (size_t)c->keys_iters * kMaxLevels, 0);
+  for (int l = 0; l < kMaxLevels; ++l) {
+    int n = l == 0 ? p->iterations : p->coarse_iterations;
+    hdr_iteration_keys(hdr_level_seed(p->seed, l), n, host.data() + 2 * (size_t)c->keys_iters * l);
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(c->keys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  c->keys_seed = p->seed;
+  c->keys_it = p->iterations;
+  c->keys_cit = p->coarse_iterations;
+  return HDR_OK;
+}
+
+// fusion._gaussian_kernel (fusion.py:28-31)
+static int ensure_taps(hdr_ctx* c, int window, double sigma) {
+  if (window == c->taps_window && sigma == c->taps_sigma) return HDR_OK;
+  int r = window / 2;
+  if (r > 15) return fail(HDR_ERR_INVALID, "ssim_window above 31 is not supported");
+  double k[31], sum = 0.0;
+  for (int i = -r; i <= r; ++i) {
+    double x = (double)i / sigma;
+    k[i + r] = exp(-0.5 * (x * x));
+  }
+  for (int i = 0; i < 2 * r + 1; ++i) sum += k[i];
+  for (int i = 0; i < 2 * r + 1; ++i) k[i] /= sum;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(c->taps, k, sizeof(double) * (2 * r + 1), cudaMemcpyHostToDevice));
+  c->taps_window = window;
+  c->taps_sigma = sigma;
+  return HDR_OK;
+}
+
+static float* pyr_level(hdr_ctx* c, const Dims* d, int l, int which) {
+  // levels 1.. of [ref, src], packed after each other
+  float* base = c->pyr;
+  for (int k = 1; k < l; ++k) base += 2 * ((int64_t)d[k].w * d[k].h + 64);
+  return base + which * ((int64_t)d[l].w * d[l].h + 64);
+}
+
+static TileCorner* tiles_level(hdr_ctx* c, const Dims* d, int l, int tile) {
+  TileCorner* t = c->tiles;
+  for (int k = 0; k < l; ++k) t += ntiles_of(d[k].w, d[k].h, tile);
+  return t;
+}
+
+// ------------------------------------------------------------ kernels used by the pipeline only
+__global__ void info_init_kernel(int32_t* info, int levels) {
+  int i = threadIdx.x;
+  if (i < HDR_INFO_WORDS) info[i] = (i == 2) ? levels : 0;
+}
+
+__global__ void status_kernel(const int32_t* weeded_count, int32_t* info) {
+  if (threadIdx.x == 0) info[0] = (*weeded_count >= 4) ? HDR_OK : HDR_ERR_REGISTRATION;
+}
+
+__global__ void copy_i32_kernel(const int32_t* src, int32_t* dst) {
+  if (threadIdx.x == 0) *dst = *src;
+}
+
+static int check_ptr_align(const void* p, size_t a, const char* what) {
+  if (((uintptr_t)p) % a) return fail(HDR_ERR_INVALID, std::string(what) + " must be 16-byte aligned");
+  return HDR_OK;
+}
+
+// The whole matching chain (pipeline.match_stack, pipeline.py:122-130) on
+// device-resident RGB inputs. info words as documented in hdrb200.h.
+static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
+                         const float* src, double* out_matches, double* out_raw,
+                         double* out_h, int32_t* info) {
+  cudaStream_t s = c->stream;
+  int64_t P = (int64_t)w * h;
+  Dims d[kMaxLevels];
+  int L = pyramid_dims(w, h, p->max_levels, d);
+  probe(c, 0, 0);
+  info_init_kernel<<<1, 32, 0, s>>>(info, L);
+  CUDA_TRY(cudaMemsetAsync(c->hist, 0, sizeof(uint32_t) * 4 * kBins, s));
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(int32_t) * 16, s));
+  launch_luma_hist(ref, P, c->lum_ref, nullptr, c->hist, s);
+  launch_luma_hist(src, P, nullptr, c->q_src, c->hist + kBins, s);
+  launch_lut(c->hist + kBins, P, c->hist, P, c->lut, s);
+  launch_apply_lut_q(c->q_src, P, c->lut, c->eq_src, s);
+  const float* lref[kMaxLevels];
+  const float* lsrc[kMaxLevels];
+  lref[0] = c->lum_ref;
+  lsrc[0] = c->eq_src;
+  for (int l = 1; l < L; ++l) {
+    float* a = pyr_level(c, d, l, 0);
+    float* b = pyr_level(c, d, l, 1);
+    launch_downsample2(lref[l - 1], lsrc[l - 1], d[l - 1].w, d[l - 1].h, a, b, s);
+    lref[l] = a;
+    lsrc[l] = b;
+  }
+  probe(c, 0, 1);
+  probe(c, 1, 0);
+  for (int l = 0; l < L; ++l) {
+    launch_integral(lref[l], d[l].w, d[l].h, c->sat, s);
+    launch_detect(c->sat, d[l].w, d[l].h, p->tile, p->threshold, p->quadrant_half,
+                  tiles_level(c, d, l, p->tile), s);
+  }
+  probe(c, 1, 1);
+  probe(c, 2, 0);
+  launch_set_identity(c->hpred, s);
+  int32_t* raw_count = c->counters + 0;
+  int32_t* weeded_count = c->counters + 1;
+  int32_t* grey = c->counters + 3;
+  for (int l = L - 1; l >= 0; --l) {
+    int nt = ntiles_of(d[l].w, d[l].h, p->tile);
+    launch_ssd_tiles(tiles_level(c, d, l, p->tile), nt, lref[l], lsrc[l], d[l].w, d[l].h,
+                     c->hpred, p->radius, p->patch, c->slot_rows, c->slot_flags, s);
+    launch_compact_rows(c->slot_rows, c->slot_flags, nt, c->raw, raw_count,
+                        l == 0 ? out_raw : nullptr, s);
+    int iters = l == 0 ? p->iterations : p->coarse_iterations;
+    double eps = 2.0 * p->eps_px / (double)d[l].w;  // MatcherParams.weed_params
+    launch_weed(c->raw, raw_count, nt, d[l].w, d[l].h, iters, eps,
+                c->keys + 2 * (size_t)c->keys_iters * l, p->delta, c->fits, c->mask, c->witness,
+                grey, s);
+    launch_finish_level(c->raw, raw_count, c->mask, d[l].w, d[l].h, l, c->weeded, weeded_count,
+                        nullptr, c->hpred, out_h, info, l == 0 ? out_matches : nullptr, nullptr,
+                        grey, s);
+  }
+  status_kernel<<<1, 32, 0, s>>>(weeded_count, info);
+  copy_i32_kernel<<<1, 32, 0, s>>>(grey, info + 18);
+  probe(c, 2, 1);
+  return check_launch();
+}
+
+static void fusion_offsets(const std::vector<Dims>& fd, float* base, std::vector<float*>& g,
+                           std::vector<float*>& cpl) {
+  g.assign(fd.size(), nullptr);
+  cpl.assign(fd.size(), nullptr);
+  float* q = base;
+  for (size_t k = 1; k < fd.size(); ++k) {
+    int64_t n = (int64_t)fd[k].w * fd[k].h;
+    g[k] = q;
+    q += 8 * n + 64;
+    cpl[k] = q;
+    q += 3 * n + 64;
+  }
+}
+
+static int enqueue_fuse(hdr_ctx* c, const float* ref, const float* warped, const float* ssim,
+                        const uint8_t* valid, int w, int h, int levels, float* out) {
+  cudaStream_t s = c->stream;
+  if (levels <= 0) levels = fusion_levels_default(w, h);
+  std::vector<Dims> fd;
+  int L = fusion_dims(w, h, levels, fd);
+  launch_fusion_weights(ref, warped, ssim, valid, w, h, c->wr, c->ws, s);
+  std::vector<float*> g, cp;
+  fusion_offsets(fd, c->fpyr, g, cp);
+  if (L == 1) {
+    launch_fuse_collapse0(ref, warped, c->wr, c->ws, w, h, nullptr, nullptr, 0, 0, out, s);
+    return check_launch();
+  }
+  launch_fuse_down0(ref, warped, c->wr, c->ws, w, h, g[1], fd[1].w, fd[1].h, s);
+  for (int k = 1; k + 1 < L; ++k)
+    launch_fuse_down(g[k], fd[k].w, fd[k].h, g[k + 1], fd[k + 1].w, fd[k + 1].h, s);
+  launch_fuse_top(g[L - 1], fd[L - 1].w, fd[L - 1].h, cp[L - 1], s);
+  for (int k = L - 2; k >= 1; --k)
+    launch_fuse_collapse(g[k], fd[k].w, fd[k].h, g[k + 1], cp[k + 1], fd[k + 1].w, fd[k + 1].h,
+                         cp[k], s);
+  launch_fuse_collapse0(ref, warped, c->wr, c->ws, w, h, g[1], cp[1], fd[1].w, fd[1].h, out, s);
+  return check_launch();
+}
+
+static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
+                        const float* src, const hdr_outputs* o) {
+  cudaStream_t s = c->stream;
+  int64_t P = (int64_t)w * h;
+  int rc = enqueue_match(c, p, w, h, ref, src, o->matches, o->raw_matches, o->homography, o->info);
+  if (rc) return rc;
+  int32_t* weeded_count = c->counters + 1;
+  // make_flow (pipeline.py:153-162): splat, filter, ratio + H fallback
+  probe(c, 3, 0);
+  launch_splat(o->matches, weeded_count, 0, w, h, c->planes, c->planes + P, c->planes + 2 * P,
+               c->splat_key, c->splat_idx, c->counters + 2, s);
+  launch_dt_filter(c->lum_ref, c->planes, 3, w, h, p->sigma_s, p->sigma_r, p->passes, c->carry, s);
+  probe(c, 3, 1);
+  probe(c, 4, 0);
+  // warp_image + luminance(warped) histogram (pipeline.py:192, :168)
+  launch_finalize_warp(c->planes, o->homography, o->info + 1, w, h, p->normalization_floor, src, 3,
+                       o->flow, o->warped, o->valid, c->qw, c->hist + 2 * kBins, true, s);
+  probe(c, 4, 1);
+  probe(c, 5, 0);
+  // make_ssim (pipeline.py:165-171)
+  launch_lut(c->hist + 2 * kBins, P, c->hist, P, c->lut + kBins, s);
+  launch_ssim(c->lum_ref, nullptr, c->qw, c->lut + kBins, w, h, p->ssim_window, c->taps, o->ssim, s);
+  probe(c, 5, 1);
+  probe(c, 6, 0);
+  // fusion.fuse (pipeline.py:193)
+  rc = enqueue_fuse(c, ref, o->warped, o->ssim, o->valid, w, h, 0, o->composite);
+  probe(c, 6, 1);
+  return rc;
+}
+
+static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
+                           const float* src, const hdr_outputs* o) {
+  if (!c || !p || !o) return fail(HDR_ERR_INVALID, "null argument");
+  char msg[128];
+  int rc = hdr_params_validate(p, msg, sizeof msg);
+  if (rc) return rc;
+  if (w > c->W || h > c->H || w < 1 || h < 1)
+    return fail(HDR_ERR_INVALID, "image larger than the context workspace");
+  if (std::min(w, h) < 100) return fail(HDR_ERR_INVALID, "input below 100 pixels in one dimension");
+  if (ntiles_of(w, h, p->tile) > c->rows_cap) return fail(HDR_ERR_INVALID, "too many tiles");
+  if (w > 7000) return fail(HDR_ERR_INVALID, "width above 7000 is not supported by the row filter");
+  size_t side = 2 * (size_t)p->radius + p->patch;
+  if ((side * side + (size_t)p->patch * p->patch) * 8 > 200 * 1024)
+    return fail(HDR_ERR_INVALID, "radius/patch search window exceeds shared memory");
+  if (!ref || !src || !o->composite || !o->flow || !o->warped || !o->valid || !o->ssim ||
+      !o->matches || !o->raw_matches || !o->homography || !o->info)
+    return fail(HDR_ERR_INVALID, "null buffer");
+  rc = check_ptr_align(ref, 16, "ref");
+  if (!rc) rc = check_ptr_align(src, 16, "src");
+  if (rc) return rc;
+  rc = ensure_keys(c, p);
+  if (!rc) rc = ensure_taps(c, p->ssim_window, p->ssim_sigma);
+  return rc;
+}
+
+extern "C" int hdr_register_and_fuse(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
+                                     const float* ref, const float* src, const hdr_outputs* o) {
+  int rc = check_pair_args(c, p, w, h, ref, src, o);
+  if (rc) return rc;
+  return enqueue_pair(c, p, w, h, ref, src, o);
+}
+
+extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
+                                           const float* ref, const float* src,
+                                           const hdr_outputs* o) {
+  int rc = check_pair_args(c, p, w, h, ref, src, o);
+  if (rc) return rc;
+  char key[768];
+  int kn = snprintf(key, sizeof key, "%d,%d,%p,%p,%p,%p,%p,%p,%p,%p,%p,%p,%p|%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%a,%a,%a,%a,%a,%a,%llu",
+           w, h, (const void*)ref, (const void*)src, (void*)o->composite, (void*)o->flow,
+           (void*)o->warped, (void*)o->valid, (void*)o->ssim, (void*)o->matches,
+           (void*)o->raw_matches, (void*)o->homography, (void*)o->info, p->tile, p->quadrant_half,
+           p->radius, p->patch, p->max_levels, p->iterations, p->coarse_iterations, p->delta,
+           p->passes, p->ssim_window, p->threshold, p->eps_px, p->sigma_s, p->sigma_r,
+           p->ssim_sigma, p->normalization_floor, (unsigned long long)p->seed);
+  if (c->probing)
+    for (int i = 0; i < 2 * HDR_NUM_STAGES && kn > 0 && kn < (int)sizeof key - 24; ++i)
+      kn += snprintf(key + kn, sizeof key - kn, ",%p", (void*)c->probes[i]);
+  GraphEntry& g = c->graphs[key];
+  if (!g.exec) {
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_pair(c, p, w, h, ref, src, o);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      c->graphs.erase(key);
+      return rc;
+    }
+    if (e != cudaSuccess) {
+      c->graphs.erase(key);
+      return fail(HDR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    }
+    size_t nodes = 0;
+    cudaGraphGetNodes(graph, nullptr, &nodes);
+    std::vector<cudaGraphNode_t> list(nodes);
+    if (nodes) cudaGraphGetNodes(graph, list.data(), &nodes);
+    int32_t kernels = 0;
+    for (auto nd : list) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+    }
+    c->graph_kernels = kernels;
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      c->graphs.erase(key);
+      return fail(HDR_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+  }
+  CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+  return HDR_OK;
+}
+
+// ------------------------------------------------------------ per-stage twins
+#define NEED(cond, msg) \
+  if (!(cond)) return fail(HDR_ERR_INVALID, msg)
+
+extern "C" int hdr_luminance(hdr_ctx* c, const float* rgb, int64_t n, float* lum) {
+  NEED(c && rgb && lum, "null argument");
+  NEED(n >= 0, "bad size");
+  int rc = check_ptr_align(rgb, 16, "rgb");
+  if (!rc) rc = check_ptr_align(lum, 16, "lum");
+  if (rc) return rc;
+  if (n) launch_luminance(rgb, n, lum, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_match_histogram(hdr_ctx* c, const float* src, int64_t n_src, const float* ref,
+                                   int64_t n_ref, int32_t stride, float* out) {
+  NEED(c && src && ref && out, "null argument");
+  NEED(n_src > 0 && n_ref > 0 && stride >= 1, "bad size");
+  cudaStream_t s = c->stream;
+  uint32_t* hs = c->hist + 3 * kBins;
+  uint32_t* hr = c->hist + 2 * kBins;
+  CUDA_TRY(cudaMemsetAsync(hr, 0, sizeof(uint32_t) * 2 * kBins, s));
+  launch_hist_plain(src, n_src, stride, hs, s);
+  launch_hist_plain(ref, n_ref, stride, hr, s);
+  launch_lut(hs, n_src, hr, n_ref, c->lut + 2 * kBins, s);
+  launch_apply_lut_f(src, n_src, stride, c->lut + 2 * kBins, out, s);
+  return check_launch();
+}
+
+extern "C" int hdr_build_pyramid(hdr_ctx* c, const float* img, int32_t w, int32_t h,
+                                 int32_t max_levels, int32_t min_dim, float** out_levels,
+                                 int32_t* n_levels) {
+  NEED(c && img && out_levels && n_levels, "null argument");
+  if (std::min(w, h) < min_dim)
+    return fail(HDR_ERR_INVALID, "input below " + std::to_string(min_dim) + " pixels in one dimension");
+  int L = 1, cw = w, ch = h;
+  const float* prev = img;
+  while (L < max_levels) {
+    int nw = cw / 2, nh = ch / 2;
+    if (std::min(nw, nh) < min_dim || std::min(nw, nh) < 1) break;
+    NEED(out_levels[L], "missing level buffer");
+    launch_downsample2(prev, nullptr, cw, ch, out_levels[L], nullptr, c->stream);
+    prev = out_levels[L];
+    cw = nw;
+    ch = nh;
+    ++L;
+  }
+  *n_levels = L;
+  return check_launch();
+}
+
+extern "C" int hdr_integral(hdr_ctx* c, const float* img, int32_t w, int32_t h, double* table) {
+  NEED(c && img && table && w >= 1 && h >= 1, "bad argument");
+  launch_integral(img, w, h, table, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_detect_corners(hdr_ctx* c, const float* lum, int32_t w, int32_t h, int32_t tile,
+                                  double threshold, int32_t half, double* corners, int32_t* count) {
+  NEED(c && lum && corners && count, "null argument");
+  if (tile < 16) return fail(HDR_ERR_INVALID, "tile must be >= 16");
+  NEED((int64_t)(w + 1) * (h + 1) <= (int64_t)(c->W + 1) * (c->H + 1), "image larger than the workspace");
+  int nt = ntiles_of(w, h, tile);
+  NEED(nt <= c->tiles_cap, "too many tiles");
+  cudaStream_t s = c->stream;
+  launch_integral(lum, w, h, c->sat, s);
+  launch_detect(c->sat, w, h, tile, threshold, half, c->tiles, s);
+  launch_compact_corners(c->tiles, nt, corners, c->counters + 5, s);
+  CUDA_TRY(cudaMemcpyAsync(count, c->counters + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return check_launch();
+}
+
+extern "C" int hdr_ssd_match(hdr_ctx* c, const float* ref, const float* src, int32_t w, int32_t h,
+                             const int32_t* pts, int32_t n, int32_t radius, int32_t patch,
+                             double* out, uint8_t* found) {
+  NEED(c && ref && src && pts && out && found, "null argument");
+  NEED(radius >= 1 && patch >= 3 && patch % 2 == 1, "bad radius/patch");
+  size_t side = 2 * (size_t)radius + patch;
+  NEED((side * side + (size_t)patch * patch) * 8 <= 200 * 1024, "search window exceeds shared memory");
+  launch_ssd_points(ref, src, w, h, pts, n, radius, patch, out, found, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_match_level(hdr_ctx* c, const hdr_params* p, const float* lum_ref,
+                               const float* lum_src, int32_t w, int32_t h, const double* h_pred,
+                               double* raw, int32_t* count) {
+  NEED(c && p && lum_ref && lum_src && h_pred && raw && count, "null argument");
+  if (p->tile < 16) return fail(HDR_ERR_INVALID, "tile must be >= 16");
+  int nt = ntiles_of(w, h, p->tile);
+  NEED(nt <= c->rows_cap, "too many tiles");
+  NEED((int64_t)(w + 1) * (h + 1) <= (int64_t)(c->W + 1) * (c->H + 1), "image larger than the workspace");
+  cudaStream_t s = c->stream;
+  launch_integral(lum_ref, w, h, c->sat, s);
+  launch_detect(c->sat, w, h, p->tile, p->threshold, p->quadrant_half, c->tiles, s);
+  launch_ssd_tiles(c->tiles, nt, lum_ref, lum_src, w, h, h_pred, p->radius, p->patch, c->slot_rows,
+                   c->slot_flags, s);
+  launch_compact_rows(c->slot_rows, c->slot_flags, nt, c->raw, c->counters + 0, raw, s);
+  CUDA_TRY(cudaMemcpyAsync(count, c->counters + 0, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return check_launch();
+}
+
+__global__ void rows_from_matrix_kernel(const double* m, int n, MatchRow* rows, int32_t* count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *count = n;
+  if (i >= n) return;
+  MatchRow r;
+  for (int k = 0; k < 5; ++k) r.v[k] = m[5 * (int64_t)i + k];
+  rows[i] = r;
+}
+
+__global__ void widen_kept_kernel(const uint32_t* mask, const int32_t* wit, int n, int64_t* kept,
+                                  int32_t* n_kept, int64_t* witness) {
+  // single block: ordered compaction of the reliable mask
+  __shared__ int scratch[32];
+  int base = 0;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    int i = c0 + threadIdx.x;
+    int f = i < n ? (int)((mask[i >> 5] >> (i & 31)) & 1u) : 0;
+    int total;
+    int pos = hdr::block_exclusive_scan(f, scratch, &total);
+    if (f) kept[base + pos] = i;
+    if (i < n && witness) witness[i] = wit[i];
+    base += total;
+  }
+  if (threadIdx.x == 0) *n_kept = base;
+}
+
+extern "C" int hdr_weed(hdr_ctx* c, const double* matches, int32_t n, int32_t w, int32_t h,
+                        int32_t iterations, double eps, uint64_t seed, int32_t delta, int64_t* kept,
+                        int32_t* n_kept, int64_t* witness) {
+  NEED(c && matches && kept && n_kept, "null argument");
+  if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 matches to weed");
+  if (iterations < 1) return fail(HDR_ERR_INVALID, "iterations must be >= 1");
+  if (delta >= 0 && delta < 4) return fail(HDR_ERR_INVALID, "delta must be >= 4");
+  if (!(eps > 0)) return fail(HDR_ERR_INVALID, "eps must be positive");
+  NEED(n <= c->rows_cap, "too many matches for the workspace");
+  cudaStream_t s = c->stream;
+  // keys for this exact (seed, iterations): weeding._iteration_rng
+  std::vector<uint64_t> host(2 * (size_t)iterations);
+  hdr_iteration_keys(seed, iterations, host.data());
+  uint64_t* dkeys = nullptr;
+  double* dfits = nullptr;
+  CUDA_TRY(cudaMallocAsync(&dkeys, host.size() * sizeof(uint64_t), s));
+  CUDA_TRY(cudaMallocAsync(&dfits, sizeof(double) * 20 * (size_t)iterations, s));
+  CUDA_TRY(cudaMemcpyAsync(dkeys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  rows_from_matrix_kernel<<<ceil_div(n, 256), 256, 0, s>>>(matches, n, c->raw, c->counters + 0);
+  launch_weed(c->raw, c->counters + 0, n, w, h, iterations, eps, dkeys, delta, dfits, c->mask,
+              c->witness, c->counters + 3, s);
+  widen_kept_kernel<<<1, 1024, 0, s>>>(c->mask, c->witness, n, kept, c->counters + 6, witness);
+  CUDA_TRY(cudaMemcpyAsync(n_kept, c->counters + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaFreeAsync(dkeys, s));
+  CUDA_TRY(cudaFreeAsync(dfits, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return check_launch();
+}
+
+static int fit_status_to_rc(int32_t st) {
+  if (st == 0) return HDR_OK;
+  if (st == 1) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
+  return fail(HDR_ERR_DEGENERATE, "degenerate correspondence set");
+}
+
+extern "C" int hdr_fit_matches_homography(hdr_ctx* c, const double* matches, int32_t n, int32_t w,
+                                          int32_t h, double* H) {
+  NEED(c && matches && H, "null argument");
+  if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
+  NEED(n <= c->rows_cap, "too many matches for the workspace");
+  cudaStream_t s = c->stream;
+  rows_from_matrix_kernel<<<ceil_div(n, 256), 256, 0, s>>>(matches, n, c->raw, c->counters + 0);
+  launch_fit_rows(c->raw, c->counters + 0, w, h, H, c->counters + 4, s);
+  int32_t st = 0;
+  CUDA_TRY(cudaMemcpyAsync(&st, c->counters + 4, sizeof st, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int rc = check_launch();
+  return rc ? rc : fit_status_to_rc(st);
+}
+
+extern "C" int hdr_fit_homography(hdr_ctx* c, const double* ref_pts, const double* src_pts,
+                                  int32_t n, double* H) {
+  NEED(c && ref_pts && src_pts && H, "null argument");
+  if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
+  cudaStream_t s = c->stream;
+  launch_fit_points(ref_pts, src_pts, n, H, c->counters + 4, s);
+  int32_t st = 0;
+  CUDA_TRY(cudaMemcpyAsync(&st, c->counters + 4, sizeof st, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int rc = check_launch();
+  return rc ? rc : fit_status_to_rc(st);
+}
+
+extern "C" int hdr_inlier_mask(hdr_ctx* c, const double* H, const double* ref_pts,
+                               const double* src_pts, int32_t n, double eps, uint8_t* mask) {
+  NEED(c && H && ref_pts && src_pts && mask, "null argument");
+  launch_inlier_mask(H, ref_pts, src_pts, n, eps, mask, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_homography_flow(hdr_ctx* c, const double* H, int32_t w, int32_t h, float* flow) {
+  NEED(c && H && flow, "null argument");
+  launch_hflow(H, w, h, flow, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_match_stack(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
+                               const float* ref, const float* src, double* matches,
+                               double* raw_matches, double* homography, int32_t* info) {
+  NEED(c && p && ref && src && matches && raw_matches && homography && info, "null argument");
+  char msg[128];
+  int rc = hdr_params_validate(p, msg, sizeof msg);
+  if (rc) return rc;
+  if (std::min(w, h) < 100) return fail(HDR_ERR_INVALID, "input below 100 pixels in one dimension");
+  NEED((int64_t)w * h <= c->P && (int64_t)(w + 1) * (h + 1) <= (int64_t)(c->W + 1) * (c->H + 1),
+       "image larger than the workspace");
+  NEED(ntiles_of(w, h, p->tile) <= c->rows_cap, "too many tiles");
+  rc = check_ptr_align(ref, 16, "ref");
+  if (!rc) rc = check_ptr_align(src, 16, "src");
+  if (!rc) rc = ensure_keys(c, p);
+  if (rc) return rc;
+  return enqueue_match(c, p, w, h, ref, src, matches, raw_matches, homography, info);
+}
+
+extern "C" int hdr_sparse_maps(hdr_ctx* c, const double* matches, int32_t m, int32_t w, int32_t h,
+                               double* pu, double* pv, double* n) {
+  NEED(c && pu && pv && n && (m == 0 || matches), "null argument");
+  NEED((int64_t)w * h <= c->P, "image larger than the workspace");
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaMemsetAsync(c->counters + 2, 0, sizeof(int32_t), s));
+  launch_splat(matches, nullptr, m, w, h, pu, pv, n, c->splat_key, c->splat_idx, c->counters + 2, s);
+  int32_t st = 0;
+  CUDA_TRY(cudaMemcpyAsync(&st, c->counters + 2, sizeof st, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int rc = check_launch();
+  if (rc) return rc;
+  if (st) return fail(HDR_ERR_INVALID, "match reference position out of bounds");
+  return HDR_OK;
+}
+
+extern "C" int hdr_dt_filter(hdr_ctx* c, const float* guide, double* planes, int32_t k, int32_t w,
+                             int32_t h, double sigma_s, double sigma_r, int32_t passes) {
+  NEED(c && guide && planes, "null argument");
+  if (!(sigma_s > 0) || !(sigma_r > 0)) return fail(HDR_ERR_INVALID, "sigma_s and sigma_r must be positive");
+  if (passes < 1) return fail(HDR_ERR_INVALID, "passes must be >= 1");
+  NEED(k >= 1 && k <= 3, "1 to 3 planes supported");
+  NEED(w <= 7000, "width above 7000 is not supported by the row filter");
+  NEED((int64_t)ceil_div(h, 64) * w * 4 + 64 <= (int64_t)ceil_div(c->H, 64) * c->W * 4 + 64,
+       "image larger than the workspace");
+  launch_dt_filter(guide, planes, k, w, h, sigma_s, sigma_r, passes, c->carry, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_densify_finalize(hdr_ctx* c, const double* smooth, int32_t w, int32_t h,
+                                    const double* fallback, double floor_, float* flow) {
+  NEED(c && smooth && flow, "null argument");
+  // the fused kernel with the warp outputs switched off
+  launch_finalize_warp(smooth, fallback, nullptr, w, h, floor_, nullptr, 1, flow, nullptr, nullptr,
+                       nullptr, nullptr, true, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_warp_image(hdr_ctx* c, const float* src, int32_t channels, int32_t w, int32_t h,
+                              const float* flow, float* warped, uint8_t* valid) {
+  NEED(c && src && flow && warped && valid, "null argument");
+  NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  launch_finalize_warp(nullptr, nullptr, nullptr, w, h, 0.0, src, channels,
+                       const_cast<float*>(flow), warped, valid, nullptr, nullptr, false, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_ssim_map(hdr_ctx* c, const float* a, const float* b, int32_t w, int32_t h,
+                            int32_t window, double sigma, float* out) {
+  NEED(c && a && b && out, "null argument");
+  if (window % 2 != 1) return fail(HDR_ERR_INVALID, "window must be odd");
+  int rc = ensure_taps(c, window, sigma);
+  if (rc) return rc;
+  launch_ssim(a, b, nullptr, nullptr, w, h, window, c->taps, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_make_ssim(hdr_ctx* c, const float* lum_ref, const float* warped, int32_t w,
+                             int32_t h, int32_t window, double sigma, float* out) {
+  NEED(c && lum_ref && warped && out, "null argument");
+  int64_t P = (int64_t)w * h;
+  NEED(P <= c->P, "image larger than the workspace");
+  int rc = ensure_taps(c, window, sigma);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  uint32_t* hw = c->hist + 2 * kBins;
+  uint32_t* hr = c->hist + 3 * kBins;
+  CUDA_TRY(cudaMemsetAsync(hw, 0, sizeof(uint32_t) * 2 * kBins, s));
+  launch_luma_hist(warped, P, nullptr, c->qw, hw, s);
+  launch_hist_plain(lum_ref, P, 1, hr, s);
+  launch_lut(hw, P, hr, P, c->lut + 2 * kBins, s);
+  launch_ssim(lum_ref, nullptr, c->qw, c->lut + 2 * kBins, w, h, window, c->taps, out, s);
+  return check_launch();
+}
+
+extern "C" int hdr_quality_weights(hdr_ctx* c, const float* rgb, int32_t w, int32_t h, float* out) {
+  NEED(c && rgb && out, "null argument");
+  launch_quality(rgb, w, h, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_fuse(hdr_ctx* c, const float* ref, const float* warped, const float* ssim,
+                        const uint8_t* valid, int32_t w, int32_t h, int32_t levels, float* out) {
+  NEED(c && ref && warped && ssim && valid && out, "null argument");
+  NEED((int64_t)w * h <= c->P, "image larger than the workspace");
+  std::vector<Dims> fd;
+  fusion_dims(w, h, levels > 0 ? levels : fusion_levels_default(w, h), fd);
+  int64_t need = 0;
+  for (size_t k = 1; k < fd.size(); ++k) need += 11 * ((int64_t)fd[k].w * fd[k].h + 64);
+  NEED(need <= c->fpyr_cap, "fusion pyramid larger than the workspace");
+  return enqueue_fuse(c, ref, warped, ssim, valid, w, h, levels, out);
+}
+
+// ------------------------------------------------------------ attributes
+static void init_kernel_attributes() {
+  hdr::init_match_attributes();
+  hdr::init_densify_attributes();
+  hdr::init_fusion_attributes();
+}

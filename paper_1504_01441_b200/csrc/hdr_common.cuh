@@ -1,0 +1,89 @@
+// Shared helpers for libhdrb200 (sm_100a). Functions marked HD compile for
+// both the device and the host (the host copies back the test hooks).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#define HD __host__ __device__ __forceinline__
+
+namespace hdr {
+
+constexpr int kMaxLevels = 5;     // image.py:13
+constexpr int kBins = 256;        // image.py:15
+constexpr int kMaxResample = 10;  // weeding.py:27
+
+// scipy.ndimage mode='reflect' (half-sample symmetric: d c b a | a b c d | d c b a)
+// for any excursion (period 2n). SURVEY.md Appendix A.7.
+HD int reflect_index(int i, int n) {
+  if (n == 1) return 0;
+  int p = 2 * n;
+  i %= p;
+  if (i < 0) i += p;
+  return i < n ? i : p - 1 - i;
+}
+
+HD int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Separately rounded arithmetic: numpy never contracts a*b+c into an FMA
+// (SURVEY.md A.1); nvcc would, so parity-critical expressions use these.
+HD float fmul(float a, float b) {
+#ifdef __CUDA_ARCH__
+  return __fmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+HD float fadd(float a, float b) {
+#ifdef __CUDA_ARCH__
+  return __fadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+HD double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+HD double dadd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+HD double dsub(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+
+// image.to_normalized (image.py:125-129): ((2x - W) / W, (2y - H) / W), f64.
+HD void to_norm(double x, double y, int w, int h, double* xn, double* yn) {
+  double fw = (double)w;
+  *xn = dsub(dmul(2.0, x), (double)w) / fw;
+  *yn = dsub(dmul(2.0, y), (double)h) / fw;
+}
+
+// image.from_normalized (image.py:132-136).
+HD void from_norm(double xn, double yn, int w, int h, double* x, double* y) {
+  double fw = (double)w;
+  *x = dadd(dmul(xn, fw), (double)w) / 2.0;
+  *y = dadd(dmul(yn, fw), (double)h) / 2.0;
+}
+
+// Apply a row-major 3x3 H to (x, y), numpy operation order:
+// ((h0*x + h1*y) + h2) / ((h6*x + h7*y) + h8). Returns the denominator.
+HD double apply_h(const double* H, double x, double y, double* mx, double* my) {
+  double den = dadd(dadd(dmul(H[6], x), dmul(H[7], y)), H[8]);
+  *mx = dadd(dadd(dmul(H[0], x), dmul(H[1], y)), H[2]);
+  *my = dadd(dadd(dmul(H[3], x), dmul(H[4], y)), H[5]);
+  return den;
+}
+
+}  // namespace hdr

@@ -1,0 +1,109 @@
+// Internal launcher declarations shared between the kernel translation units
+// and the C-ABI layer (hdr_api.cu). Every launcher only enqueues work.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hdr {
+
+// per-tile detector output: x < 0 means "no corner in this tile"
+struct TileCorner {
+  int32_t x, y;
+  double score;
+};
+
+// one raw/weeded match row (x_ref, y_ref, x_src, y_src, score)
+struct MatchRow {
+  double v[5];
+};
+
+void init_match_attributes();
+void init_densify_attributes();
+void init_fusion_attributes();
+
+// ---- k_raster.cu
+void launch_luma_hist(const float* rgb, int64_t n, float* lum, uint8_t* q,
+                      uint32_t* hist, cudaStream_t s);
+void launch_hist_plain(const float* x, int64_t n, int32_t stride, uint32_t* hist,
+                       cudaStream_t s);
+void launch_lut(const uint32_t* hist_src, int64_t n_src, const uint32_t* hist_ref,
+                int64_t n_ref, float* lut, cudaStream_t s);
+void launch_apply_lut_q(const uint8_t* q, int64_t n, const float* lut, float* out,
+                        cudaStream_t s);
+void launch_apply_lut_f(const float* x, int64_t n, int32_t stride, const float* lut,
+                        float* out, cudaStream_t s);
+void launch_luminance(const float* rgb, int64_t n, float* lum, cudaStream_t s);
+void launch_downsample2(const float* a, const float* b, int w, int h, float* oa,
+                        float* ob, cudaStream_t s);
+void launch_integral(const float* img, int w, int h, double* table, cudaStream_t s);
+void launch_detect(const double* table, int w, int h, int tile, double threshold,
+                   int half, TileCorner* tiles, cudaStream_t s);
+void launch_compact_corners(const TileCorner* tiles, int ntiles, double* corners,
+                            int32_t* count, cudaStream_t s);
+
+// ---- k_match.cu
+void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref,
+                      const float* src, int w, int h, const double* hpred, int radius,
+                      int patch, MatchRow* rows, uint8_t* flags, cudaStream_t s);
+void launch_ssd_points(const float* ref, const float* src, int w, int h,
+                       const int32_t* pts, int n, int radius, int patch, double* out,
+                       uint8_t* found, cudaStream_t s);
+void launch_compact_rows(const MatchRow* rows, const uint8_t* flags, int nslots,
+                         MatchRow* out, int32_t* count, double* out_copy,
+                         cudaStream_t s);
+void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w,
+                 int h, int iterations, double eps, const uint64_t* keys, int delta,
+                 double* fit_scratch, uint32_t* mask, int32_t* witness,
+                 int32_t* grey, cudaStream_t s);
+// compaction of the weeded set + least-squares H (+ level bookkeeping)
+void launch_finish_level(const MatchRow* raw, const int32_t* raw_count,
+                         const uint32_t* mask, int w, int h, int level,
+                         MatchRow* weeded, int32_t* weeded_count, int64_t* kept_idx,
+                         double* hpred, double* homography, int32_t* info,
+                         double* out_matches, double* out_raw, int32_t* grey,
+                         cudaStream_t s);
+void launch_fit_rows(const MatchRow* rows, const int32_t* count, int w, int h,
+                     double* H, int32_t* status, cudaStream_t s);
+void launch_fit_points(const double* ref_pts, const double* src_pts, int n, double* H,
+                       int32_t* status, cudaStream_t s);
+void launch_inlier_mask(const double* H, const double* ref_pts, const double* src_pts,
+                        int n, double eps, uint8_t* mask, cudaStream_t s);
+void launch_set_identity(double* h, cudaStream_t s);
+
+// ---- k_densify.cu
+void launch_splat(const double* matches, const int32_t* count, int m_static, int w,
+                  int h, double* pu, double* pv, double* pn, uint64_t* scratch_key,
+                  int32_t* scratch_idx, int32_t* status, cudaStream_t s);
+void launch_dt_filter(const float* guide, double* planes, int k, int w, int h,
+                      double sigma_s, double sigma_r, int passes, double* carry,
+                      cudaStream_t s);
+void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
+void launch_finalize_warp(const double* smooth, const double* fallback,
+                          const int32_t* has_fallback, int w, int h, double floor_,
+                          const float* src, int channels, float* flow, float* warped,
+                          uint8_t* valid, uint8_t* qw, uint32_t* hist_w,
+                          bool do_flow, cudaStream_t s);
+
+// ---- k_fusion.cu
+void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb,
+                 const float* lut_b, int w, int h, int window, const double* taps,
+                 float* out, cudaStream_t s);
+void launch_quality(const float* rgb, int w, int h, float* out, cudaStream_t s);
+void launch_fusion_weights(const float* ref, const float* warped, const float* ssim,
+                           const uint8_t* valid, int w, int h, float* wr, float* ws,
+                           cudaStream_t s);
+// pyramid of 8 planar channels (ref rgb, warped rgb, wr, ws)
+void launch_fuse_down0(const float* ref, const float* warped, const float* wr,
+                       const float* ws, int w, int h, float* out, int ow, int oh,
+                       cudaStream_t s);
+void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh,
+                      cudaStream_t s);
+void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s);
+void launch_fuse_collapse(const float* g, int w, int h, const float* gc,
+                          const float* cc, int cw, int ch, float* c, cudaStream_t s);
+void launch_fuse_collapse0(const float* ref, const float* warped, const float* wr,
+                           const float* ws, int w, int h, const float* gc,
+                           const float* cc, int cw, int ch, float* out,
+                           cudaStream_t s);
+
+}  // namespace hdr

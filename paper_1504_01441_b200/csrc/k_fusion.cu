@@ -1,0 +1,335 @@
+// Merge: SSIM registration-trust map (K13), Mertens quality weights and the
+// normalised fusion weights (K14), Laplacian-pyramid blend (K15).
+//
+// Storage is f32 (images, weights, pyramid levels); SSIM moments and the
+// weight products are evaluated in f64 like the reference
+// (fusion.py:34-77); the 5-tap pyramid arithmetic is f32. Tolerances:
+// SURVEY.md §8(a) a19-a22 (SSIM <= 1e-4, composite <= 1e-3).
+#include "hdr_common.cuh"
+#include "hdr_internal.h"
+
+namespace hdr {
+
+// ---------------------------------------------------------------- K13
+constexpr int kSsimTW = 32, kSsimTH = 16, kMaxRad = 15;
+
+__device__ __forceinline__ float lumf(float r, float g, float b) {
+  float y = fadd(fadd(fmul(0.299f, r), fmul(0.587f, g)), fmul(0.114f, b));
+  return fminf(fmaxf(y, 0.0f), 1.0f);
+}
+
+// fusion.ssim_map (fusion.py:34-64): separable reflect blurs along axis 0
+// then axis 1 of a, b, a^2, b^2, ab; scipy's symmetric-kernel accumulation
+// order x0*w0 + sum_{j=r..1} (x[-j] + x[+j]) * w[j].
+// b = lut_b[qb] when qb != nullptr (the warped frame's equalised luminance).
+__global__ void __launch_bounds__(kSsimTW * 8) ssim_kernel(
+    const float* __restrict__ a, const float* __restrict__ b, const uint8_t* __restrict__ qb,
+    const float* __restrict__ lut_b, int w, int h, int r, const double* __restrict__ taps,
+    float* __restrict__ out) {
+  extern __shared__ double sm[];
+  const int EW = kSsimTW + 2 * r, EH = kSsimTH + 2 * r;
+  float* sa = reinterpret_cast<float*>(sm);  // EH x EW
+  float* sb = sa + EH * EW;
+  double* V = sm + ((2 * EH * EW + 1) / 2);  // 5 x kSsimTH x EW
+  __shared__ double k[2 * kMaxRad + 1];
+  __shared__ float lut[kBins];
+  int tid = threadIdx.x, nt = blockDim.x;
+  if (tid < 2 * r + 1) k[tid] = taps[tid];
+  if (qb)
+    for (int i = tid; i < kBins; i += nt) lut[i] = lut_b[i];
+  __syncthreads();
+  int x0 = blockIdx.x * kSsimTW - r, y0 = blockIdx.y * kSsimTH - r;
+  for (int i = tid; i < EH * EW; i += nt) {
+    int ly = i / EW, lx = i % EW;
+    int gy = reflect_index(y0 + ly, h), gx = reflect_index(x0 + lx, w);
+    int64_t p = (int64_t)gy * w + gx;
+    sa[i] = a[p];
+    sb[i] = qb ? lut[qb[p]] : b[p];
+  }
+  __syncthreads();
+  // vertical (axis 0)
+  const int SV = kSsimTH * EW;
+  for (int i = tid; i < SV; i += nt) {
+    int oy = i / EW, lx = i % EW;
+    int c = (oy + r) * EW + lx;
+    double va = sa[c], vb = sb[c];
+    double m0 = dmul(va, k[r]), m1 = dmul(vb, k[r]);
+    double m2 = dmul(dmul(va, va), k[r]), m3 = dmul(dmul(vb, vb), k[r]);
+    double m4 = dmul(dmul(va, vb), k[r]);
+    for (int j = r; j >= 1; --j) {
+      double ua = sa[c - j * EW], ub = sb[c - j * EW], da = sa[c + j * EW], db = sb[c + j * EW];
+      double kj = k[r + j];
+      m0 = dadd(m0, dmul(dadd(ua, da), kj));
+      m1 = dadd(m1, dmul(dadd(ub, db), kj));
+      m2 = dadd(m2, dmul(dadd(dmul(ua, ua), dmul(da, da)), kj));
+      m3 = dadd(m3, dmul(dadd(dmul(ub, ub), dmul(db, db)), kj));
+      m4 = dadd(m4, dmul(dadd(dmul(ua, ub), dmul(da, db)), kj));
+    }
+    V[0 * SV + i] = m0; V[1 * SV + i] = m1; V[2 * SV + i] = m2; V[3 * SV + i] = m3;
+    V[4 * SV + i] = m4;
+  }
+  __syncthreads();
+  // horizontal (axis 1) + SSIM formula
+  for (int i = tid; i < kSsimTW * kSsimTH; i += nt) {
+    int oy = i / kSsimTW, ox = i % kSsimTW;
+    int gx = blockIdx.x * kSsimTW + ox, gy = blockIdx.y * kSsimTH + oy;
+    if (gx >= w || gy >= h) continue;
+    double m[5];
+    int c = oy * EW + ox + r;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double* row = V + q * SV;
+      double acc = dmul(row[c], k[r]);
+      for (int j = r; j >= 1; --j) acc = dadd(acc, dmul(dadd(row[c - j], row[c + j]), k[r + j]));
+      m[q] = acc;
+    }
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double mu_a = m[0], mu_b = m[1];
+    double var_a = m[2] - mu_a * mu_a, var_b = m[3] - mu_b * mu_b, cov = m[4] - mu_a * mu_b;
+    double s = ((2.0 * mu_a * mu_b + C1) * (2.0 * cov + C2)) /
+               ((mu_a * mu_a + mu_b * mu_b + C1) * (var_a + var_b + C2));
+    s = fmin(fmax(s, -1.0), 1.0);
+    out[(int64_t)gy * w + gx] = (float)s;
+  }
+}
+
+void init_fusion_attributes() {
+  cudaFuncSetAttribute(ssim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb, const float* lut_b,
+                 int w, int h, int window, const double* taps, float* out, cudaStream_t s) {
+  int r = window / 2;
+  int EW = kSsimTW + 2 * r, EH = kSsimTH + 2 * r;
+  size_t bytes = ((2 * EH * EW + 1) / 2) * sizeof(double) + 5 * (size_t)kSsimTH * EW * sizeof(double);
+  dim3 grd(ceil_div(w, kSsimTW), ceil_div(h, kSsimTH));
+  ssim_kernel<<<grd, kSsimTW * 8, bytes, s>>>(a, b_or_null, qb, lut_b, w, h, r, taps, out);
+}
+
+// ---------------------------------------------------------------- K14
+// fusion.quality_weights (fusion.py:67-77) at one pixel, f64.
+__device__ __forceinline__ double quality(const float* __restrict__ rgb, int w, int h, int x,
+                                          int y) {
+  auto L = [&](int yy, int xx) -> double {
+    const float* p = rgb + ((int64_t)reflect_index(yy, h) * w + reflect_index(xx, w)) * 3;
+    return (double)lumf(p[0], p[1], p[2]);
+  };
+  double c0 = L(y, x);
+  // ndimage.laplace: correlate1d([1,-2,1]) along axis 0, += along axis 1
+  double lap0 = dadd(dmul(c0, -2.0), dadd(L(y - 1, x), L(y + 1, x)));
+  double lap1 = dadd(dmul(c0, -2.0), dadd(L(y, x - 1), L(y, x + 1)));
+  double con = fabs(dadd(lap0, lap1));
+  const float* p = rgb + ((int64_t)y * w + x) * 3;
+  double r = p[0], g = p[1], b = p[2];
+  double mean = dadd(dadd(r, g), b) / 3.0;
+  double dr = r - mean, dg = g - mean, db = b - mean;
+  double var = dadd(dadd(dmul(dr, dr), dmul(dg, dg)), dmul(db, db)) / 3.0;
+  double sat = sqrt(var);
+  double er = r - 0.5, eg = g - 0.5, eb = b - 0.5;
+  double ssum = dadd(dadd(dmul(er, er), dmul(eg, eg)), dmul(eb, eb));
+  double ex = exp(-ssum / (2.0 * 0.2 * 0.2));
+  return dadd(dmul(dmul(con, sat), ex), 1e-12);
+}
+
+__global__ void quality_kernel(const float* __restrict__ rgb, int w, int h, float* __restrict__ out) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  out[(int64_t)y * w + x] = (float)quality(rgb, w, h, x, y);
+}
+
+void launch_quality(const float* rgb, int w, int h, float* out, cudaStream_t s) {
+  dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
+  quality_kernel<<<grd, blk, 0, s>>>(rgb, w, h, out);
+}
+
+// fusion.fusion_weights (fusion.py:117-128)
+__global__ void fusion_weights_kernel(const float* __restrict__ ref, const float* __restrict__ warped,
+                                      const float* __restrict__ ssim,
+                                      const uint8_t* __restrict__ valid, int w, int h,
+                                      float* __restrict__ wr, float* __restrict__ ws) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  int64_t i = (int64_t)y * w + x;
+  double qr = quality(ref, w, h, x, y);
+  double qs = quality(warped, w, h, x, y);
+  double sv = fmin(fmax((double)ssim[i], 0.0), 1.0);
+  double vs = dmul(dmul(qs, sv), valid[i] ? 1.0 : 0.0);
+  double tot = dadd(qr, vs);
+  wr[i] = (float)(qr / tot);
+  ws[i] = (float)(vs / tot);
+}
+
+void launch_fusion_weights(const float* ref, const float* warped, const float* ssim,
+                           const uint8_t* valid, int w, int h, float* wr, float* ws,
+                           cudaStream_t s) {
+  dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
+  fusion_weights_kernel<<<grd, blk, 0, s>>>(ref, warped, ssim, valid, w, h, wr, ws);
+}
+
+// ---------------------------------------------------------------- K15
+// fusion._blur5 then [::2, ::2] (fusion.py:80-86), 8 planar channels out:
+// 0-2 reference RGB, 3-5 warped RGB, 6 w_ref, 7 w_src.
+__constant__ float kP5[5] = {1.0f / 16, 4.0f / 16, 6.0f / 16, 4.0f / 16, 1.0f / 16};
+
+template <bool LEVEL0>
+__global__ void __launch_bounds__(256) fuse_down_kernel(const float* __restrict__ in,
+                                                        const float* __restrict__ ref,
+                                                        const float* __restrict__ warped,
+                                                        const float* __restrict__ wr,
+                                                        const float* __restrict__ ws, int w,
+                                                        int h, float* __restrict__ out, int ow,
+                                                        int oh) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (X >= ow || Y >= oh) return;
+  int rows[5], cols[5];
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    rows[t] = reflect_index(2 * Y + t - 2, h);
+    cols[t] = reflect_index(2 * X + t - 2, w);
+  }
+  int64_t P = (int64_t)w * h, OP = (int64_t)ow * oh;
+  float acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    float rowacc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) rowacc[c] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      int64_t p = (int64_t)rows[i] * w + cols[j];
+      float v[8];
+      if (LEVEL0) {
+        v[0] = ref[3 * p]; v[1] = ref[3 * p + 1]; v[2] = ref[3 * p + 2];
+        v[3] = warped[3 * p]; v[4] = warped[3 * p + 1]; v[5] = warped[3 * p + 2];
+        v[6] = wr[p]; v[7] = ws[p];
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = in[c * P + p];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) rowacc[c] += kP5[j] * v[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] += kP5[i] * rowacc[c];
+  }
+  int64_t o = (int64_t)Y * ow + X;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) out[c * OP + o] = acc[c];
+}
+
+void launch_fuse_down0(const float* ref, const float* warped, const float* wr, const float* ws,
+                       int w, int h, float* out, int ow, int oh, cudaStream_t s) {
+  dim3 blk(32, 8), grd(ceil_div(ow, 32), ceil_div(oh, 8));
+  fuse_down_kernel<true><<<grd, blk, 0, s>>>(nullptr, ref, warped, wr, ws, w, h, out, ow, oh);
+}
+
+void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh, cudaStream_t s) {
+  dim3 blk(32, 8), grd(ceil_div(ow, 32), ceil_div(oh, 8));
+  fuse_down_kernel<false><<<grd, blk, 0, s>>>(in, nullptr, nullptr, nullptr, nullptr, w, h, out,
+                                              ow, oh);
+}
+
+// top of the pyramid: C = w_ref * G_ref + w_src * G_src (laps[-1] = gp[-1])
+__global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float* __restrict__ c) {
+  int64_t P = (int64_t)w * h;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  float a = g[6 * P + i], b = g[7 * P + i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k * P + i] = a * g[k * P + i] + b * g[(3 + k) * P + i];
+}
+
+void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s) {
+  int64_t P = (int64_t)w * h;
+  fuse_top_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(g, w, h, c);
+}
+
+// _pyr_up (fusion.py:89-93): zero-insert into the fine grid, 2x-gain 5-tap
+// blur per axis with reflect on the fine grid. Accumulates 9 coarse
+// channels (G_ref 0-2, G_src 3-5 from gc; C 0-2 from cc) at fine (y, x).
+__device__ __forceinline__ void up9(const float* __restrict__ gc, const float* __restrict__ cc,
+                                    int cw, int chh, int w, int h, int x, int y, float* o) {
+  int64_t CP = (int64_t)cw * chh;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) o[c] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    int ry = reflect_index(y + i - 2, h);
+    if (ry & 1) continue;
+    float row[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) row[c] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      int rx = reflect_index(x + j - 2, w);
+      if (rx & 1) continue;
+      int64_t p = (int64_t)(ry >> 1) * cw + (rx >> 1);
+      float kj = 2.0f * kP5[j];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) row[c] += kj * gc[c * CP + p];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) row[6 + c] += kj * cc[c * CP + p];
+    }
+    float ki = 2.0f * kP5[i];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) o[c] += ki * row[c];
+  }
+}
+
+// collapse step for level k >= 1:
+// C_k = w_ref (G_ref - up G_ref') + w_src (G_src - up G_src') + up C'
+__global__ void __launch_bounds__(256) fuse_collapse_kernel(const float* __restrict__ g, int w,
+                                                            int h, const float* __restrict__ gc,
+                                                            const float* __restrict__ cc, int cw,
+                                                            int chh, float* __restrict__ c) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  float u[9];
+  up9(gc, cc, cw, chh, w, h, x, y, u);
+  int64_t P = (int64_t)w * h, i = (int64_t)y * w + x;
+  float a = g[6 * P + i], b = g[7 * P + i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    c[k * P + i] = a * (g[k * P + i] - u[k]) + b * (g[(3 + k) * P + i] - u[3 + k]) + u[6 + k];
+}
+
+void launch_fuse_collapse(const float* g, int w, int h, const float* gc, const float* cc, int cw,
+                          int ch, float* c, cudaStream_t s) {
+  dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
+  fuse_collapse_kernel<<<grd, blk, 0, s>>>(g, w, h, gc, cc, cw, ch, c);
+}
+
+// level 0: reads the interleaved inputs and weights, writes the clipped
+// interleaved composite (fusion.py:154-157).
+__global__ void __launch_bounds__(256) fuse_collapse0_kernel(
+    const float* __restrict__ ref, const float* __restrict__ warped, const float* __restrict__ wr,
+    const float* __restrict__ ws, int w, int h, const float* __restrict__ gc,
+    const float* __restrict__ cc, int cw, int chh, float* __restrict__ out) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= w || y >= h) return;
+  float u[9];
+  if (gc) {
+    up9(gc, cc, cw, chh, w, h, x, y, u);
+  } else {  // single-level pyramid: the blend is the whole result
+#pragma unroll
+    for (int c = 0; c < 9; ++c) u[c] = 0.0f;
+  }
+  int64_t i = (int64_t)y * w + x;
+  float a = wr[i], b = ws[i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float v = a * (ref[3 * i + k] - u[k]) + b * (warped[3 * i + k] - u[3 + k]) + u[6 + k];
+    out[3 * i + k] = fminf(fmaxf(v, 0.0f), 1.0f);
+  }
+}
+
+void launch_fuse_collapse0(const float* ref, const float* warped, const float* wr, const float* ws,
+                           int w, int h, const float* gc, const float* cc, int cw, int ch,
+                           float* out, cudaStream_t s) {
+  dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
+  fuse_collapse0_kernel<<<grd, blk, 0, s>>>(ref, warped, wr, ws, w, h, gc, cc, cw, ch, out);
+}
+
+}  // namespace hdr

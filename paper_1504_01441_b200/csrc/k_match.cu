@@ -1,0 +1,582 @@
+// Sparse registration: per-corner SSD search (K6), ordered compaction,
+// union-of-inliers weeding with the reference's Philox sampler (K7) and the
+// least-squares homography that seeds the next finer level (K8).
+//
+// Everything stays on the device: counts are device words, grids are sized
+// for the tile count (the maximum number of corners) and idle blocks exit,
+// so the coarse-to-fine chain of matcher.pyramidal_match (matcher.py:221-263)
+// runs without a host round trip and can be captured in one CUDA graph.
+#include "hdr_common.cuh"
+#include "hdr_geom.cuh"
+#include "hdr_internal.h"
+#include "hdr_scan.cuh"
+
+namespace hdr {
+
+// ---------------------------------------------------------------- K6
+struct SsdKey {
+  double score;
+  long long d2;
+  int cy, cx;
+};
+
+// ssd_match tie rule (matcher.py:136-142): min score, then d2, then y, then x
+__device__ __forceinline__ bool key_less(const SsdKey& a, const SsdKey& b) {
+  if (a.score != b.score) return a.score < b.score;
+  if (a.d2 != b.d2) return a.d2 < b.d2;
+  if (a.cy != b.cy) return a.cy < b.cy;
+  return a.cx < b.cx;
+}
+
+__device__ __forceinline__ SsdKey shfl_key(const SsdKey& k, int off) {
+  SsdKey o;
+  o.score = __shfl_down_sync(0xffffffff, k.score, off);
+  o.d2 = __shfl_down_sync(0xffffffff, k.d2, off);
+  o.cy = __shfl_down_sync(0xffffffff, k.cy, off);
+  o.cx = __shfl_down_sync(0xffffffff, k.cx, off);
+  return o;
+}
+
+// Block-cooperative exhaustive search; returns true on thread 0 with the
+// winner in *best. Window bounds must already be clamped and non-empty.
+__device__ bool ssd_search(const float* __restrict__ ref, const float* __restrict__ src,
+                           int w, int xr, int yr, int xi, int yi, int cx0, int cx1, int cy0,
+                           int cy1, int patch, double* smem, SsdKey* best) {
+  int hp = patch / 2;
+  int nx = cx1 - cx0 + 1, ny = cy1 - cy0 + 1;
+  int sw = nx + patch - 1, sh = ny + patch - 1;
+  double* T = smem;
+  double* S = smem + patch * patch;
+  for (int i = threadIdx.x; i < patch * patch; i += blockDim.x) {
+    int ky = i / patch, kx = i % patch;
+    T[i] = (double)ref[(int64_t)(yr - hp + ky) * w + (xr - hp + kx)];
+  }
+  for (int i = threadIdx.x; i < sw * sh; i += blockDim.x) {
+    int ry = i / sw, rx = i % sw;
+    S[i] = (double)src[(int64_t)(cy0 - hp + ry) * w + (cx0 - hp + rx)];
+  }
+  __syncthreads();
+  SsdKey k;
+  k.score = INFINITY; k.d2 = 0x7fffffffffffffffLL; k.cy = 0x7fffffff; k.cx = 0x7fffffff;
+  for (int c = threadIdx.x; c < nx * ny; c += blockDim.x) {
+    int oy = c / nx, ox = c % nx;
+    double acc = 0.0;
+    for (int ky = 0; ky < patch; ++ky) {
+      const double* srow = S + (oy + ky) * sw + ox;
+      const double* trow = T + ky * patch;
+      for (int kx = 0; kx < patch; ++kx) {
+        double d = srow[kx] - trow[kx];
+        acc = fma(d, d, acc);
+      }
+    }
+    SsdKey cand;
+    cand.score = acc;
+    cand.cx = cx0 + ox;
+    cand.cy = cy0 + oy;
+    long long dx = cand.cx - xi, dy = cand.cy - yi;
+    cand.d2 = dx * dx + dy * dy;
+    if (key_less(cand, k)) k = cand;
+  }
+  for (int off = 16; off; off >>= 1) {
+    SsdKey o = shfl_key(k, off);
+    if (key_less(o, k)) k = o;
+  }
+  __shared__ SsdKey part[32];
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) part[warp] = k;
+  __syncthreads();
+  if (threadIdx.x != 0) return false;
+  for (int i = 1; i < (int)((blockDim.x + 31) >> 5); ++i)
+    if (key_less(part[i], k)) k = part[i];
+  *best = k;
+  return true;
+}
+
+// matcher._match_level body (matcher.py:186-207) for one detector tile.
+__global__ void __launch_bounds__(256) ssd_tiles_kernel(const TileCorner* __restrict__ tiles,
+                                                        const float* __restrict__ ref,
+                                                        const float* __restrict__ src, int w,
+                                                        int h, const double* __restrict__ hpred,
+                                                        int radius, int patch,
+                                                        MatchRow* __restrict__ rows,
+                                                        uint8_t* __restrict__ flags) {
+  extern __shared__ double smem[];
+  int slot = blockIdx.x;
+  TileCorner tc = tiles[slot];
+  int hp = patch / 2;
+  bool ok = tc.x >= 0;
+  int x = tc.x, y = tc.y, xi = 0, yi = 0;
+  if (ok && !(hp <= x && x <= w - 1 - hp && hp <= y && y <= h - 1 - hp)) ok = false;
+  if (ok) {
+    double H[9];
+    for (int i = 0; i < 9; ++i) H[i] = hpred[i];
+    double xn, yn, nx, ny;
+    to_norm((double)x, (double)y, w, h, &xn, &yn);
+    double den = apply_h(H, xn, yn, &nx, &ny);
+    if (fabs(den) < 1e-12) {
+      ok = false;
+    } else {
+      double px, py;
+      from_norm(nx / den, ny / den, w, h, &px, &py);
+      if (!(isfinite(px) && isfinite(py))) ok = false;
+      else if (fabs(px) > 8.0 * w || fabs(py) > 8.0 * h) ok = false;
+      else { xi = (int)rint(px); yi = (int)rint(py); }  // Python round(): half-even
+    }
+  }
+  int cx0 = max(xi - radius, hp), cx1 = min(xi + radius, w - 1 - hp);
+  int cy0 = max(yi - radius, hp), cy1 = min(yi + radius, h - 1 - hp);
+  if (ok && (cx0 > cx1 || cy0 > cy1)) ok = false;
+  if (!ok) {
+    if (threadIdx.x == 0) flags[slot] = 0;
+    return;
+  }
+  SsdKey best;
+  if (ssd_search(ref, src, w, x, y, xi, yi, cx0, cx1, cy0, cy1, patch, smem, &best)) {
+    MatchRow r;
+    r.v[0] = x; r.v[1] = y; r.v[2] = best.cx; r.v[3] = best.cy; r.v[4] = best.score;
+    rows[slot] = r;
+    flags[slot] = 1;
+  }
+}
+
+// matcher.ssd_match for explicit (x_ref, y_ref, x_init, y_init) points.
+__global__ void __launch_bounds__(256) ssd_points_kernel(const float* __restrict__ ref,
+                                                         const float* __restrict__ src, int w,
+                                                         int h, const int32_t* __restrict__ pts,
+                                                         int radius, int patch,
+                                                         double* __restrict__ out,
+                                                         uint8_t* __restrict__ found) {
+  extern __shared__ double smem[];
+  int i = blockIdx.x;
+  int hp = patch / 2;
+  int xr = pts[4 * i], yr = pts[4 * i + 1], xi = pts[4 * i + 2], yi = pts[4 * i + 3];
+  if (!(hp <= xr && xr <= w - 1 - hp && hp <= yr && yr <= h - 1 - hp)) {
+    if (threadIdx.x == 0) found[i] = 2;  // reference raises ValueError
+    return;
+  }
+  int cx0 = max(xi - radius, hp), cx1 = min(xi + radius, w - 1 - hp);
+  int cy0 = max(yi - radius, hp), cy1 = min(yi + radius, h - 1 - hp);
+  if (cx0 > cx1 || cy0 > cy1) {
+    if (threadIdx.x == 0) found[i] = 0;
+    return;
+  }
+  SsdKey best;
+  if (ssd_search(ref, src, w, xr, yr, xi, yi, cx0, cx1, cy0, cy1, patch, smem, &best)) {
+    out[3 * i] = best.cx; out[3 * i + 1] = best.cy; out[3 * i + 2] = best.score;
+    found[i] = 1;
+  }
+}
+
+static size_t ssd_smem(int radius, int patch) {
+  size_t side = 2 * (size_t)radius + patch;
+  return (side * side + (size_t)patch * patch) * sizeof(double);
+}
+
+constexpr int kSsdMaxSmem = 200 * 1024;
+
+void init_match_attributes() {
+  cudaFuncSetAttribute(ssd_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSsdMaxSmem);
+  cudaFuncSetAttribute(ssd_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSsdMaxSmem);
+}
+
+void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref, const float* src,
+                      int w, int h, const double* hpred, int radius, int patch, MatchRow* rows,
+                      uint8_t* flags, cudaStream_t s) {
+  size_t bytes = ssd_smem(radius, patch);
+  ssd_tiles_kernel<<<ntiles, 256, bytes, s>>>(tiles, ref, src, w, h, hpred, radius, patch, rows,
+                                              flags);
+}
+
+void launch_ssd_points(const float* ref, const float* src, int w, int h, const int32_t* pts,
+                       int n, int radius, int patch, double* out, uint8_t* found,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  size_t bytes = ssd_smem(radius, patch);
+  ssd_points_kernel<<<n, 256, bytes, s>>>(ref, src, w, h, pts, radius, patch, out, found);
+}
+
+// ordered compaction of per-slot rows (tile order is the reference's corner
+// order, matcher.py:97-104 -> :187)
+__global__ void __launch_bounds__(1024) compact_rows_kernel(const MatchRow* __restrict__ rows,
+                                                            const uint8_t* __restrict__ flags,
+                                                            int nslots, MatchRow* __restrict__ out,
+                                                            int32_t* __restrict__ count,
+                                                            double* __restrict__ out_copy) {
+  __shared__ int scratch[32];
+  int base = 0;
+  for (int c0 = 0; c0 < nslots; c0 += blockDim.x) {
+    int i = c0 + threadIdx.x;
+    int f = (i < nslots && flags[i] == 1) ? 1 : 0;
+    int total;
+    int pos = block_exclusive_scan(f, scratch, &total);
+    if (f) {
+      MatchRow r = rows[i];
+      out[base + pos] = r;
+      if (out_copy)
+        for (int k = 0; k < 5; ++k) out_copy[5 * (int64_t)(base + pos) + k] = r.v[k];
+    }
+    base += total;
+  }
+  if (threadIdx.x == 0) *count = base;
+}
+
+void launch_compact_rows(const MatchRow* rows, const uint8_t* flags, int nslots, MatchRow* out,
+                         int32_t* count, double* out_copy, cudaStream_t s) {
+  compact_rows_kernel<<<1, 1024, 0, s>>>(rows, flags, nslots, out, count, out_copy);
+}
+
+// ---------------------------------------------------------------- K7
+__device__ __forceinline__ void norm_row(const MatchRow& r, int w, int h, double* p) {
+  to_norm(r.v[0], r.v[1], w, h, &p[0], &p[1]);
+  to_norm(r.v[2], r.v[3], w, h, &p[2], &p[3]);
+}
+
+__device__ __forceinline__ int weed_delta(int n, int delta) {
+  if (delta >= 0) return delta;
+  int d = (int)ceil(0.15 * (double)n);  // weeding.default_delta (weeding.py:30-32)
+  return d > 12 ? d : 12;
+}
+
+constexpr int kFitStride = 20;  // H[9], Hinv[9], ok, pad
+
+// One thread per iteration: draw with resampling (weeding.py:74-84), fit.
+__global__ void __launch_bounds__(64) weed_fit_kernel(const MatchRow* __restrict__ rows,
+                                                      const int32_t* __restrict__ count, int w,
+                                                      int h, int iterations,
+                                                      const uint64_t* __restrict__ keys,
+                                                      double* __restrict__ fits,
+                                                      int32_t* __restrict__ grey) {
+  int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= iterations) return;
+  int n = *count;
+  double* f = fits + (int64_t)it * kFitStride;
+  f[18] = 0.0;
+  if (n < 4) return;
+  Philox g;
+  philox_init(&g, keys[2 * it], keys[2 * it + 1]);
+  double H[9];
+  int g_local = 0;
+  bool ok = false;
+  for (int r = 0; r < kMaxResample && !ok; ++r) {
+    int idx[4];
+    choice4(&g, n, idx);
+    double px[4], py[4], qx[4], qy[4];
+    for (int k = 0; k < 4; ++k) {
+      double p[4];
+      norm_row(rows[idx[k]], w, h, p);
+      px[k] = p[0]; py[k] = p[1]; qx[k] = p[2]; qy[k] = p[3];
+    }
+    ok = fit4(px, py, qx, qy, H, &g_local) == 0;
+  }
+  if (g_local) atomicAdd(grey, g_local);
+  if (!ok) return;
+  double Hi[9];
+  if (!inv3(H, Hi)) return;
+  for (int k = 0; k < 9; ++k) { f[k] = H[k]; f[9 + k] = Hi[k]; }
+  f[18] = 1.0;
+}
+
+// One block per iteration: symmetric-transfer inliers over the whole set
+// (weeding.py:85-89); accepted sets are OR-ed into the reliable mask.
+__global__ void __launch_bounds__(256) weed_count_kernel(const MatchRow* __restrict__ rows,
+                                                         const int32_t* __restrict__ count,
+                                                         int w, int h, double eps, int delta,
+                                                         const double* __restrict__ fits,
+                                                         uint32_t* __restrict__ mask,
+                                                         int32_t* __restrict__ witness) {
+  int it = blockIdx.x;
+  int n = *count;
+  const double* f = fits + (int64_t)it * kFitStride;
+  if (n < 4 || f[18] == 0.0) return;
+  __shared__ double Hs[18];
+  if (threadIdx.x < 18) Hs[threadIdx.x] = f[threadIdx.x];
+  __syncthreads();
+  int total = 0;
+  uint32_t bits = 0;  // inlier bits of this thread's first 32 chunks
+  for (int c0 = 0, k = 0; c0 < n; c0 += blockDim.x, ++k) {
+    int i = c0 + threadIdx.x;
+    bool in = false;
+    if (i < n) {
+      double p[4];
+      norm_row(rows[i], w, h, p);
+      in = is_inlier(Hs, Hs + 9, p[0], p[1], p[2], p[3], eps);
+    }
+    if (in && k < 32) bits |= 1u << k;
+    total += __syncthreads_count(in);
+  }
+  if (total <= weed_delta(n, delta)) return;
+  int lane = threadIdx.x & 31;
+  for (int c0 = 0, k = 0; c0 < n; c0 += blockDim.x, ++k) {
+    int i = c0 + threadIdx.x;
+    bool in;
+    if (k < 32) {
+      in = (bits >> k) & 1u;
+    } else {
+      in = false;
+      if (i < n) {
+        double p[4];
+        norm_row(rows[i], w, h, p);
+        in = is_inlier(Hs, Hs + 9, p[0], p[1], p[2], p[3], eps);
+      }
+    }
+    unsigned word = __ballot_sync(0xffffffff, in);
+    if (lane == 0 && word) atomicOr(&mask[i >> 5], word);
+    if (in) atomicMax(&witness[i], total);
+  }
+}
+
+void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w, int h,
+                 int iterations, double eps, const uint64_t* keys, int delta,
+                 double* fit_scratch, uint32_t* mask, int32_t* witness, int32_t* grey,
+                 cudaStream_t s) {
+  cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((n_static + 31) / 32 + 1), s);
+  cudaMemsetAsync(witness, 0, sizeof(int32_t) * (n_static + 1), s);
+  weed_fit_kernel<<<ceil_div(iterations, 64), 64, 0, s>>>(rows, count, w, h, iterations, keys,
+                                                          fit_scratch, grey);
+  weed_count_kernel<<<iterations, 256, 0, s>>>(rows, count, w, h, eps, delta, fit_scratch, mask,
+                                               witness);
+}
+
+// ---------------------------------------------------------------- K8
+// Block-wide least-squares DLT (geometry.fit_homography for n >= 4) over
+// points fetched by `get(i, p)` (p = ref x, ref y, src x, src y).
+template <class Get>
+__device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
+  __shared__ double red[32][6];
+  __shared__ double bc[6];
+  __shared__ int status;
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int nw = (blockDim.x + 31) >> 5;
+  if (n == 4) {
+    if (threadIdx.x == 0) {
+      double px[4], py[4], qx[4], qy[4];
+      for (int k = 0; k < 4; ++k) {
+        double p[4];
+        get(k, p);
+        px[k] = p[0]; py[k] = p[1]; qx[k] = p[2]; qy[k] = p[3];
+      }
+      int g = 0;
+      status = fit4(px, py, qx, qy, H, &g);
+      if (g && grey) atomicAdd(grey, g);
+    }
+    __syncthreads();
+    return status;
+  }
+  // centroids
+  double s[4] = {0, 0, 0, 0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double p[4];
+    get(i, p);
+    for (int k = 0; k < 4; ++k) s[k] += p[k];
+  }
+  for (int k = 0; k < 4; ++k)
+    for (int off = 16; off; off >>= 1) s[k] += __shfl_down_sync(0xffffffff, s[k], off);
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) red[warp][k] = s[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 4; ++k) {
+      double a = 0.0;
+      for (int j = 0; j < nw; ++j) a += red[j][k];
+      bc[k] = a / (double)n;
+    }
+  }
+  __syncthreads();
+  // mean distances to the centroids
+  double md[2] = {0, 0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double p[4];
+    get(i, p);
+    md[0] += hypot(p[0] - bc[0], p[1] - bc[1]);
+    md[1] += hypot(p[2] - bc[2], p[3] - bc[3]);
+  }
+  for (int k = 0; k < 2; ++k)
+    for (int off = 16; off; off >>= 1) md[k] += __shfl_down_sync(0xffffffff, md[k], off);
+  __syncthreads();
+  if (lane == 0) { red[warp][0] = md[0]; red[warp][1] = md[1]; }
+  __syncthreads();
+  __shared__ double tr[3], ts[3];
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int j = 0; j < nw; ++j) { a += red[j][0]; b += red[j][1]; }
+    a /= (double)n;
+    b /= (double)n;
+    status = (a < 1e-12 || b < 1e-12) ? 2 : 0;
+    double sr = sqrt(2.0) / a, ss = sqrt(2.0) / b;
+    tr[0] = sr; tr[1] = -sr * bc[0]; tr[2] = -sr * bc[1];
+    ts[0] = ss; ts[1] = -ss * bc[2]; ts[2] = -ss * bc[3];
+  }
+  __syncthreads();
+  if (status) return status;
+  // Gram matrix of the conditioned DLT rows (45 upper entries)
+  double gacc[45];
+  for (int k = 0; k < 45; ++k) gacc[k] = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double p[4];
+    get(i, p);
+    double r0[9], r1[9];
+    dlt_rows((p[0] - bc[0]) * tr[0], (p[1] - bc[1]) * tr[0], (p[2] - bc[2]) * ts[0],
+             (p[3] - bc[3]) * ts[0], r0, r1);
+    int k = 0;
+    for (int a = 0; a < 9; ++a)
+      for (int b = a; b < 9; ++b) { gacc[k] += r0[a] * r0[b] + r1[a] * r1[b]; ++k; }
+  }
+  __shared__ double gsh[32][45];
+  for (int k = 0; k < 45; ++k) {
+    double v = gacc[k];
+    for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffff, v, off);
+    if (lane == 0) gsh[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g45[45];
+    for (int k = 0; k < 45; ++k) {
+      double a = 0.0;
+      for (int j = 0; j < nw; ++j) a += gsh[j][k];
+      g45[k] = a;
+    }
+    int g = 0;
+    status = fit_from_gram(g45, tr, ts, H, &g);
+    if (g && grey) atomicAdd(grey, g);
+  }
+  __syncthreads();
+  return status;
+}
+
+// Close one pyramid level (matcher.py:247-260): compact the weeded set in
+// index order (np.flatnonzero), record level_counts, fit the LSQ H and hand
+// it to the next finer level; level 0 also fills the user-visible outputs.
+__global__ void __launch_bounds__(256) finish_level_kernel(
+    const MatchRow* __restrict__ raw, const int32_t* __restrict__ raw_count,
+    const uint32_t* __restrict__ mask, int w, int h, int level, MatchRow* __restrict__ weeded,
+    int32_t* __restrict__ weeded_count, int64_t* __restrict__ kept_idx,
+    double* __restrict__ hpred, double* __restrict__ homography, int32_t* __restrict__ info,
+    double* __restrict__ out_matches, double* __restrict__ out_raw, int32_t* grey) {
+  __shared__ int scratch[32];
+  int n = *raw_count;
+  int m = 0;
+  if (n >= 4) {
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+      int i = c0 + threadIdx.x;
+      int f = (i < n) ? (int)((mask[i >> 5] >> (i & 31)) & 1u) : 0;
+      int total;
+      int pos = block_exclusive_scan(f, scratch, &total);
+      if (f) {
+        weeded[m + pos] = raw[i];
+        if (kept_idx) kept_idx[m + pos] = i;
+        if (out_matches)
+          for (int k = 0; k < 5; ++k) out_matches[5 * (int64_t)(m + pos) + k] = raw[i].v[k];
+      }
+      m += total;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *weeded_count = m;
+    if (info) {
+      info[3 + 2 * level] = n;
+      info[4 + 2 * level] = m;
+      if (level == 0) { info[16] = m; info[17] = n; }
+    }
+  }
+  if (m < 4) return;
+  __shared__ double Hs[9];
+  const MatchRow* wr = weeded;
+  auto get = [&](int i, double* p) { norm_row(wr[i], w, h, p); };
+  __syncthreads();  // weeded rows visible block-wide
+  int st = block_fit(m, get, Hs, grey);
+  if (threadIdx.x == 0 && st == 0) {
+    for (int k = 0; k < 9; ++k) hpred[k] = Hs[k];
+    if (level == 0 && homography) {
+      for (int k = 0; k < 9; ++k) homography[k] = Hs[k];
+      if (info) info[1] = 1;
+    }
+  }
+}
+
+void launch_finish_level(const MatchRow* raw, const int32_t* raw_count, const uint32_t* mask,
+                         int w, int h, int level, MatchRow* weeded, int32_t* weeded_count,
+                         int64_t* kept_idx, double* hpred, double* homography, int32_t* info,
+                         double* out_matches, double* out_raw, int32_t* grey, cudaStream_t s) {
+  (void)out_raw;
+  finish_level_kernel<<<1, 256, 0, s>>>(raw, raw_count, mask, w, h, level, weeded, weeded_count,
+                                        kept_idx, hpred, homography, info, out_matches, out_raw,
+                                        grey);
+}
+
+// matcher.fit_matches_homography over device rows (count on the device)
+__global__ void __launch_bounds__(256) fit_rows_kernel(const MatchRow* __restrict__ rows,
+                                                       const int32_t* __restrict__ count, int w,
+                                                       int h, double* __restrict__ H,
+                                                       int32_t* __restrict__ status) {
+  int n = *count;
+  if (n < 4) {
+    if (threadIdx.x == 0) *status = 1;
+    return;
+  }
+  __shared__ double Hs[9];
+  auto get = [&](int i, double* p) { norm_row(rows[i], w, h, p); };
+  int st = block_fit(n, get, Hs, nullptr);
+  if (threadIdx.x == 0) {
+    *status = st;
+    if (st == 0)
+      for (int k = 0; k < 9; ++k) H[k] = Hs[k];
+  }
+}
+
+void launch_fit_rows(const MatchRow* rows, const int32_t* count, int w, int h, double* H,
+                     int32_t* status, cudaStream_t s) {
+  fit_rows_kernel<<<1, 256, 0, s>>>(rows, count, w, h, H, status);
+}
+
+// geometry.fit_homography on explicit point arrays
+__global__ void __launch_bounds__(256) fit_points_kernel(const double* __restrict__ rp,
+                                                         const double* __restrict__ sp, int n,
+                                                         double* __restrict__ H,
+                                                         int32_t* __restrict__ status) {
+  __shared__ double Hs[9];
+  auto get = [&](int i, double* p) {
+    p[0] = rp[2 * i]; p[1] = rp[2 * i + 1]; p[2] = sp[2 * i]; p[3] = sp[2 * i + 1];
+  };
+  int st = block_fit(n, get, Hs, nullptr);
+  if (threadIdx.x == 0) {
+    *status = st;
+    if (st == 0)
+      for (int k = 0; k < 9; ++k) H[k] = Hs[k];
+  }
+}
+
+void launch_fit_points(const double* ref_pts, const double* src_pts, int n, double* H,
+                       int32_t* status, cudaStream_t s) {
+  fit_points_kernel<<<1, 256, 0, s>>>(ref_pts, src_pts, n, H, status);
+}
+
+__global__ void inlier_mask_kernel(const double* __restrict__ H, const double* __restrict__ rp,
+                                   const double* __restrict__ sp, int n, double eps,
+                                   uint8_t* __restrict__ mask) {
+  __shared__ double Hs[18];
+  __shared__ int okinv;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 9; ++k) Hs[k] = H[k];
+    okinv = inv3(Hs, Hs + 9);
+  }
+  __syncthreads();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  mask[i] = okinv ? is_inlier(Hs, Hs + 9, rp[2 * i], rp[2 * i + 1], sp[2 * i], sp[2 * i + 1], eps)
+                  : 0;
+}
+
+void launch_inlier_mask(const double* H, const double* ref_pts, const double* src_pts, int n,
+                        double eps, uint8_t* mask, cudaStream_t s) {
+  if (n <= 0) return;
+  inlier_mask_kernel<<<ceil_div(n, 256), 256, 0, s>>>(H, ref_pts, src_pts, n, eps, mask);
+}
+
+__global__ void set_identity_kernel(double* h) {
+  int i = threadIdx.x;
+  if (i < 9) h[i] = (i % 4 == 0) ? 1.0 : 0.0;
+}
+
+void launch_set_identity(double* h, cudaStream_t s) { set_identity_kernel<<<1, 32, 0, s>>>(h); }
+
+}  // namespace hdr

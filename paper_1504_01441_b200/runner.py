@@ -1,0 +1,121 @@
+"""Throughput runner: many pairs in flight over several CUDA streams.
+
+Each stream owns its own hdr context (workspace) so pairs on different
+streams never share scratch; every pair is one CUDA-graph replay of the whole
+register+merge chain. `run_host` is the end-to-end public path (pinned host
+inputs -> H2D -> pair -> D2H of the composite and the verdict words), with
+copies of one stream overlapping compute of the others.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .engine import Engine
+from .pipeline import PairBuffers, PipelineParams
+
+
+class BatchRunner:
+    def __init__(self, width: int, height: int, streams: int = 4,
+                 params: PipelineParams | None = None, device: int | None = None,
+                 graph: bool = True):
+        self.device = torch.cuda.current_device() if device is None else device
+        self.width, self.height = width, height
+        self.params = params or PipelineParams()
+        self.params.validate()
+        self.native_params = self.params.to_native()
+        self.graph = graph
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(streams)]
+        self.engines = [Engine(width, height, self.device) for _ in range(streams)]
+        for e, s in zip(self.engines, self.streams):
+            e.bind_stream(s)
+        self._staging = None
+
+    # ---------------------------------------------------------- device path
+    def enqueue(self, k: int, ref: torch.Tensor, src: torch.Tensor, bufs: PairBuffers):
+        """Queue one pair on stream k % S (no host sync)."""
+        e = self.engines[k % len(self.engines)]
+        fn = (_native.lib().hdr_register_and_fuse_graph if self.graph
+              else _native.lib().hdr_register_and_fuse)
+        _native.check(fn(e.handle, ctypes.byref(self.native_params), self.width, self.height,
+                         ctypes.c_void_p(ref.data_ptr()), ctypes.c_void_p(src.data_ptr()),
+                         ctypes.byref(bufs.native)), "register_and_fuse")
+
+    def run_device(self, pairs, outs, start_event=None, stop_event=None):
+        """All pairs device-resident; optional events bracket the whole batch
+        on the current stream (the streams wait on start, stop waits on all)."""
+        cur = torch.cuda.current_stream(self.device)
+        if start_event is not None:
+            start_event.record(cur)
+        for s in self.streams:
+            s.wait_stream(cur)
+        for k, ((ref, src), bufs) in enumerate(zip(pairs, outs)):
+            self.enqueue(k, ref, src, bufs)
+        for s in self.streams:
+            cur.wait_stream(s)
+        if stop_event is not None:
+            stop_event.record(cur)
+
+    def set_probes(self, k: int, events):
+        """Stage probes (hdr_ctx_set_probes) for the context of stream k."""
+        e = self.engines[k % len(self.engines)]
+        arr = None
+        if events is not None:
+            arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
+        _native.check(_native.lib().hdr_ctx_set_probes(e.handle, arr))
+
+    # ---------------------------------------------------------- host path
+    def _ensure_staging(self):
+        if self._staging is None:
+            h, w = self.height, self.width
+            dev = f"cuda:{self.device}"
+            self._staging = [dict(ref=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                                  src=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                                  out=PairBuffers(w, h, self.device))
+                             for _ in self.streams]
+        return self._staging
+
+    def run_host(self, host_pairs, host_out, start_event=None, stop_event=None):
+        """End to end: pinned host (ref, src) in, composite + info words out.
+
+        host_out[k] = (composite pinned (h, w, 3) f32, info pinned (32,) i32).
+        Returns the H2D / D2H byte counts of the batch."""
+        st = self._ensure_staging()
+        cur = torch.cuda.current_stream(self.device)
+        if start_event is not None:
+            start_event.record(cur)
+        for s in self.streams:
+            s.wait_stream(cur)
+        h2d = d2h = 0
+        for k, ((href, hsrc), (hcomp, hinfo)) in enumerate(zip(host_pairs, host_out)):
+            j = k % len(self.streams)
+            slot = st[j]
+            with torch.cuda.stream(self.streams[j]):
+                slot["ref"].copy_(href, non_blocking=True)
+                slot["src"].copy_(hsrc, non_blocking=True)
+                self.enqueue(j, slot["ref"], slot["src"], slot["out"])
+                hcomp.copy_(slot["out"].composite, non_blocking=True)
+                hinfo.copy_(slot["out"].info, non_blocking=True)
+            h2d += href.numel() * 4 + hsrc.numel() * 4
+            d2h += hcomp.numel() * 4 + hinfo.numel() * 4
+        for s in self.streams:
+            cur.wait_stream(s)
+        if stop_event is not None:
+            stop_event.record(cur)
+        return h2d, d2h
+
+    def graph_kernels(self) -> int:
+        return int(_native.lib().hdr_ctx_graph_kernels(self.engines[0].handle))
+
+    def close(self):
+        for e in self.engines:
+            e.close()
+
+
+def verdicts(info: np.ndarray):
+    """(registered?, n_weeded_level0) from one pair's info words."""
+    return int(info[0]) == _native.HDR_OK, int(info[16])

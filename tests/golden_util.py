@@ -1,0 +1,25 @@
+"""Helpers shared by the oracle/golden and GPU parity tests."""
+import hashlib
+import os
+
+import numpy as np
+
+from paper_1504_01441_b200 import synth
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SCENES = ["vga_s0", "vga_rot_s1", "qvga_s2", "r960_s3"]
+
+
+def digest(a) -> str:
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes() + str(a.dtype).encode() + str(a.shape).encode()).hexdigest()
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, f"{name}.npz"), allow_pickle=False))
+
+
+def scene_inputs(fx):
+    w, h, rot, seed = fx["scene"]
+    st = synth.synth_stack(synth.working_spec(int(w), int(h), rotation_deg=float(rot)), int(seed))
+    return st.ref, st.src

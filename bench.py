@@ -230,9 +230,10 @@ def run_ours(args):
     from paper_1504_01441_b200.pipeline import PairBuffers, PipelineParams
     from paper_1504_01441_b200.runner import BatchRunner
 
+    from paper_1504_01441_b200 import dist as hd
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        hd.init("nccl", local)
     dev = f"cuda:{local}"
     w, h, B = args.width, args.height, args.pairs
     pairs = []
@@ -271,8 +272,7 @@ def run_ours(args):
     consistent = all(len(v) == 1 for v in by_scene.values())
 
     clocks = Clocks(local)
-    if world > 1:
-        dist.barrier()
+    hd.barrier()
     torch.cuda.synchronize()
     clocks.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -282,12 +282,8 @@ def run_ours(args):
     t1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
+    ms = hd.max_over_ranks(t0.elapsed_time(t1), device=dev)
+    hd.barrier()
     # per-stage durations of the last timed step (probes inside the graphs)
     stage_ms = {}
     for s_i, name in enumerate(_native.STAGES):
@@ -309,8 +305,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 1)):
         runner.run_host(hpairs, hout)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    hd.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     h2d = d2h = 0
@@ -319,12 +314,8 @@ def run_ours(args):
         h2d, d2h = a, b
     e1.record()
     torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
     e2e_ok = all(int(x[1][0]) == 0 for x in hout)
-    if world > 1:
-        t = torch.tensor([ems], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
+    ems = hd.max_over_ranks(e0.elapsed_time(e1), device=dev)
 
     if rank != 0:
         if world > 1:

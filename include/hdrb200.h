@@ -217,6 +217,10 @@ int hdr_iteration_keys(uint64_t seed, int32_t iterations, uint64_t* keys);
  * Generator(Philox(key)).choice(n, 4, replace=False) repeated `draws` times
  * on one stream; out (draws, 4). */
 int hdr_choice4_host(const uint64_t* key, int32_t n, int32_t draws, int64_t* out);
+/* Test hook: the device DLT fit (geometry.fit_homography) run on the host
+ * with HOST pointers; returns HDR_OK / HDR_ERR_DEGENERATE / HDR_ERR_INVALID. */
+int hdr_fit_homography_host(const double* ref_pts, const double* src_pts, int32_t n,
+                            double* h);
 
 #ifdef __cplusplus
 }

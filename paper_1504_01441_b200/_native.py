@@ -82,6 +82,7 @@ SIGNATURES = {
     "hdr_level_seed": (ctypes.c_uint32, [_U64, _I]),
     "hdr_iteration_keys": (_I, [_U64, _I, _P]),
     "hdr_choice4_host": (_I, [_P, _I, _I, _P]),
+    "hdr_fit_homography_host": (_I, [_P, _P, _I, _P]),
 }
 
 _lib = None

@@ -125,6 +125,43 @@ extern "C" int hdr_choice4_host(const uint64_t* key, int32_t n, int32_t draws, i
   return HDR_OK;
 }
 
+extern "C" int hdr_fit_homography_host(const double* rp, const double* sp, int32_t n, double* H) {
+  if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
+  if (n == 4) {
+    double px[4], py[4], qx[4], qy[4];
+    for (int i = 0; i < 4; ++i) { px[i] = rp[2 * i]; py[i] = rp[2 * i + 1]; qx[i] = sp[2 * i]; qy[i] = sp[2 * i + 1]; }
+    int g = 0;
+    return fit4(px, py, qx, qy, H, &g) ? fail(HDR_ERR_DEGENERATE, "degenerate correspondence set")
+                                       : HDR_OK;
+  }
+  // same arithmetic as block_fit's least-squares branch, serially
+  double c[4] = {0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) { c[0] += rp[2 * i]; c[1] += rp[2 * i + 1]; c[2] += sp[2 * i]; c[3] += sp[2 * i + 1]; }
+  for (int k = 0; k < 4; ++k) c[k] /= n;
+  double md0 = 0, md1 = 0;
+  for (int i = 0; i < n; ++i) {
+    md0 += hypot(rp[2 * i] - c[0], rp[2 * i + 1] - c[1]);
+    md1 += hypot(sp[2 * i] - c[2], sp[2 * i + 1] - c[3]);
+  }
+  md0 /= n;
+  md1 /= n;
+  if (md0 < 1e-12 || md1 < 1e-12) return fail(HDR_ERR_DEGENERATE, "coincident points");
+  double sr = sqrt(2.0) / md0, ss = sqrt(2.0) / md1;
+  double tr[3] = {sr, -sr * c[0], -sr * c[1]}, ts[3] = {ss, -ss * c[2], -ss * c[3]};
+  double g45[45] = {0};
+  for (int i = 0; i < n; ++i) {
+    double r0[9], r1[9];
+    dlt_rows((rp[2 * i] - c[0]) * sr, (rp[2 * i + 1] - c[1]) * sr, (sp[2 * i] - c[2]) * ss,
+             (sp[2 * i + 1] - c[3]) * ss, r0, r1);
+    int k = 0;
+    for (int a = 0; a < 9; ++a)
+      for (int b = a; b < 9; ++b) { g45[k] += r0[a] * r0[b] + r1[a] * r1[b]; ++k; }
+  }
+  int g = 0;
+  return fit_from_gram(g45, tr, ts, H, &g) ? fail(HDR_ERR_DEGENERATE, "degenerate correspondence set")
+                                          : HDR_OK;
+}
+
 // ------------------------------------------------------------ params
 extern "C" void hdr_params_default(hdr_params* p) {
   memset(p, 0, sizeof(*p));
@@ -231,7 +268,10 @@ struct hdr_ctx {
   float* pyr = nullptr;         // levels 1.. of both pyramids
   uint32_t* hist = nullptr;     // [ref, src, warped, scratch] x 256
   float* lut = nullptr;         // [src, warped, scratch] x 256
-  double* sat = nullptr;
+  double* ctab = nullptr;       // lattice SAT pass-1 rows, all levels
+  double* ltab = nullptr;       // lattice SAT, all levels
+  int64_t ctab_cap = 0, ltab_cap = 0;
+  std::map<std::string, int32_t*> lattice_maps;  // device rowmap|colmap|rowlist
   TileCorner* tiles = nullptr;  // all levels
   int64_t tiles_cap = 0;
   // matching
@@ -252,8 +292,8 @@ struct hdr_ctx {
   uint64_t keys_seed = ~0ULL;
   int keys_it = -1, keys_cit = -1;
   // densify
-  double* planes = nullptr;     // 3 x P
-  double* carry = nullptr;
+  void* planes = nullptr;       // pu, pv (f32) + n (f64): 16 B per pixel
+  double* carry = nullptr;      // domain-transform aggregates / carries / coefficients
   uint64_t* splat_key = nullptr;
   int32_t* splat_idx = nullptr;
   uint8_t* qw = nullptr;
@@ -266,6 +306,7 @@ struct hdr_ctx {
   int taps_window = -1;
   double taps_sigma = -1.0;
   int32_t* info_scratch = nullptr;
+  cudaStream_t cap_stream = nullptr;
   cudaEvent_t probes[2 * HDR_NUM_STAGES] = {};
   bool probing = false;
   int32_t graph_kernels = 0;
@@ -294,6 +335,9 @@ extern "C" int hdr_ctx_destroy(hdr_ctx* c) {
   for (auto& kv : c->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : c->allocs) cudaFree(p);
+  if (c->keys) cudaFree(c->keys);
+  if (c->fits) cudaFree(c->fits);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return HDR_OK;
 }
@@ -338,7 +382,20 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   ALLOC(pyr, 2 * pyr_sum);
   ALLOC(hist, 4 * kBins);
   ALLOC(lut, 3 * kBins);
-  ALLOC(sat, (int64_t)(width + 1) * (height + 1));
+  {
+    int64_t cs = 0, ls = 0;
+    int w = width, h = height;
+    for (int l = 0; l < kMaxLevels && w >= 1 && h >= 1; ++l) {
+      cs += (int64_t)(h + 1) * w + 64;
+      ls += (int64_t)(h + 1) * (w + 1) + 64;
+      w /= 2;
+      h /= 2;
+    }
+    c->ctab_cap = cs;
+    c->ltab_cap = ls;
+  }
+  ALLOC(ctab, c->ctab_cap);
+  ALLOC(ltab, c->ltab_cap);
   ALLOC(tiles, tiles_total);
   ALLOC(slot_rows, c->rows_cap);
   ALLOC(slot_flags, c->rows_cap);
@@ -349,8 +406,8 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   ALLOC(witness, c->rows_cap + 1);
   ALLOC(kept, c->rows_cap);
   ALLOC(hpred, 32);
-  ALLOC(planes, 3 * P);
-  ALLOC(carry, (int64_t)ceil_div(height, 64) * width * 4 + 64);
+  if (e == cudaSuccess) e = ctx_alloc(c, reinterpret_cast<double**>(&c->planes), 2 * P + 64);
+  ALLOC(carry, dt_scratch_doubles(width, height, 3));
   ALLOC(splat_key, P);
   ALLOC(splat_idx, P);
   ALLOC(qw, P + 16);
@@ -387,7 +444,8 @@ extern "C" int32_t hdr_ctx_graph_kernels(hdr_ctx* c) { return c ? c->graph_kerne
 static void probe(hdr_ctx* c, int stage, int end) {
   if (!c->probing) return;
   cudaEvent_t e = c->probes[2 * stage + end];
-  if (e) cudaEventRecord(e, c->stream);
+  // External: captured as a real event-record node, so replays time it
+  if (e) cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
 }
 
 extern "C" int hdr_ctx_sync(hdr_ctx* c) {
@@ -452,10 +510,129 @@ static float* pyr_level(hdr_ctx* c, const Dims* d, int l, int which) {
   return base + which * ((int64_t)d[l].w * d[l].h + 64);
 }
 
+// Table rows/columns the detector reads (matcher.py:75-87): {g-half, g, g+half}
+// for every candidate coordinate g that passes the fit test; `full` keeps all.
+static void lattice_axis(int n, int tile, int half, bool full, std::vector<char>& need) {
+  need.assign(n + 1, full ? 1 : 0);
+  if (full) return;
+  int sp = std::max(1, tile / 16), first = sp / 2;
+  for (int t0 = 0; t0 < n; t0 += tile) {
+    int lim = std::min(tile, n - t0);
+    for (int o = first; o < lim; o += sp) {
+      int g = t0 + o;
+      if (g >= half && g <= n - half) need[g - half] = need[g] = need[g + half] = 1;
+    }
+  }
+}
+
+struct LatticeInfo {
+  const int32_t* rowmap;
+  const int32_t* colmap;
+  const int32_t* rowlist;
+  int nrows, ncols;
+};
+
+// Device maps for one level, built on the host once per (w, h, tile, half).
+static int lattice_maps(hdr_ctx* c, int w, int h, int tile, int half, bool full, LatticeInfo* out) {
+  char key[96];
+  snprintf(key, sizeof key, "%d,%d,%d,%d,%d", w, h, tile, half, (int)full);
+  std::vector<char> rn, cn;
+  lattice_axis(h, tile, half, full, rn);
+  lattice_axis(w, tile, half, full, cn);
+  std::vector<int32_t> rowmap(h + 1, -1), colmap(w + 1, -1), rowlist;
+  int nc = 0;
+  for (int X = 0; X <= w; ++X)
+    if (cn[X]) colmap[X] = nc++;
+  for (int Y = 0; Y <= h; ++Y)
+    if (rn[Y]) {
+      rowmap[Y] = (int)rowlist.size();
+      rowlist.push_back(Y);
+    }
+  int nr = (int)rowlist.size();
+  auto it = c->lattice_maps.find(key);
+  int32_t* dev;
+  if (it != c->lattice_maps.end()) {
+    dev = it->second;
+  } else {
+    std::vector<int32_t> host;
+    host.insert(host.end(), rowmap.begin(), rowmap.end());
+    host.insert(host.end(), colmap.begin(), colmap.end());
+    host.insert(host.end(), rowlist.begin(), rowlist.end());
+    host.push_back(0);
+    CUDA_TRY(cudaMalloc(&dev, host.size() * sizeof(int32_t)));
+    c->allocs.push_back(dev);
+    CUDA_TRY(cudaMemcpy(dev, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    c->lattice_maps[key] = dev;
+  }
+  out->rowmap = dev;
+  out->colmap = dev + (h + 1);
+  out->rowlist = dev + (h + 1) + (w + 1);
+  out->nrows = nr;
+  out->ncols = nc;
+  return HDR_OK;
+}
+
+// Fill a SatBatch for n levels of images (lum[l], dims d[l]) carving ctab /
+// ltab from the context; tiles[l] receive the detector output.
+static int sat_batch(hdr_ctx* c, int n, const float* const* lum, const Dims* d, int tile,
+                     int half, bool full, TileCorner* const* tiles, double* ltab_override,
+                     SatBatch* b, int* max_w, int* max_rows, int* total_tiles) {
+  b->n = n;
+  int64_t co = 0, lo = 0;
+  *max_w = *max_rows = *total_tiles = 0;
+  for (int l = 0; l < n; ++l) {
+    LatticeInfo li;
+    int rc = lattice_maps(c, d[l].w, d[l].h, tile, half, full, &li);
+    if (rc) return rc;
+    SatLevel& L = b->lv[l];
+    L.img = lum[l];
+    L.w = d[l].w;
+    L.h = d[l].h;
+    L.rowmap = li.rowmap;
+    L.colmap = li.colmap;
+    L.rowlist = li.rowlist;
+    L.nrows = li.nrows;
+    L.ncols = li.ncols;
+    L.ctab = c->ctab + co;
+    L.ltab = ltab_override ? ltab_override : c->ltab + lo;
+    co += (int64_t)li.nrows * d[l].w + 64;
+    lo += (int64_t)li.nrows * li.ncols + 64;
+    if (co > c->ctab_cap || (!ltab_override && lo > c->ltab_cap))
+      return fail(HDR_ERR_INVALID, "image larger than the lattice workspace");
+    L.tiles = tiles ? tiles[l] : nullptr;
+    L.tile_base = *total_tiles;
+    *total_tiles += ntiles_of(d[l].w, d[l].h, tile);
+    *max_w = std::max(*max_w, d[l].w);
+    *max_rows = std::max(*max_rows, li.nrows);
+  }
+  return HDR_OK;
+}
+
 static TileCorner* tiles_level(hdr_ctx* c, const Dims* d, int l, int tile) {
   TileCorner* t = c->tiles;
   for (int k = 0; k < l; ++k) t += ntiles_of(d[k].w, d[k].h, tile);
   return t;
+}
+
+static DtPlanes f64_planes(double* a, double* b, double* n, int k) {
+  DtPlanes pl;
+  pl.p[0] = a; pl.p[1] = b; pl.p[2] = n;
+  pl.f64[0] = pl.f64[1] = pl.f64[2] = 1;
+  pl.k = k;
+  return pl;
+}
+
+// the pair path's planes: flow numerators f32, indicator f64
+static DtPlanes pair_planes(hdr_ctx* c, int64_t P) {
+  DtPlanes pl;
+  float* f = reinterpret_cast<float*>(c->planes);
+  pl.p[0] = f;
+  pl.p[1] = f + P;
+  pl.p[2] = reinterpret_cast<double*>(f + 2 * P + (2 * P) % 2);
+  pl.f64[0] = pl.f64[1] = 0;
+  pl.f64[2] = 1;
+  pl.k = 3;
+  return pl;
 }
 
 // ------------------------------------------------------------ kernels used by the pipeline only
@@ -507,10 +684,15 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
   }
   probe(c, 0, 1);
   probe(c, 1, 0);
-  for (int l = 0; l < L; ++l) {
-    launch_integral(lref[l], d[l].w, d[l].h, c->sat, s);
-    launch_detect(c->sat, d[l].w, d[l].h, p->tile, p->threshold, p->quadrant_half,
-                  tiles_level(c, d, l, p->tile), s);
+  {
+    SatBatch sb;
+    TileCorner* tl[kMaxLevels];
+    for (int l = 0; l < L; ++l) tl[l] = tiles_level(c, d, l, p->tile);
+    int mw, mr, nt;
+    int rc = sat_batch(c, L, lref, d, p->tile, p->quadrant_half, false, tl, nullptr, &sb, &mw, &mr, &nt);
+    if (rc) return rc;
+    launch_sat(sb, mw, mr, s);
+    launch_detect(sb, nt, DetectParams{p->tile, p->quadrant_half, p->threshold}, s);
   }
   probe(c, 1, 1);
   probe(c, 2, 0);
@@ -586,13 +768,13 @@ static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const flo
   int32_t* weeded_count = c->counters + 1;
   // make_flow (pipeline.py:153-162): splat, filter, ratio + H fallback
   probe(c, 3, 0);
-  launch_splat(o->matches, weeded_count, 0, w, h, c->planes, c->planes + P, c->planes + 2 * P,
-               c->splat_key, c->splat_idx, c->counters + 2, s);
-  launch_dt_filter(c->lum_ref, c->planes, 3, w, h, p->sigma_s, p->sigma_r, p->passes, c->carry, s);
+  DtPlanes pl = pair_planes(c, P);
+  launch_splat(o->matches, weeded_count, 0, w, h, pl, c->splat_key, c->splat_idx, c->counters + 2, s);
+  launch_dt_filter(c->lum_ref, pl, w, h, p->sigma_s, p->sigma_r, p->passes, c->carry, s);
   probe(c, 3, 1);
   probe(c, 4, 0);
   // warp_image + luminance(warped) histogram (pipeline.py:192, :168)
-  launch_finalize_warp(c->planes, o->homography, o->info + 1, w, h, p->normalization_floor, src, 3,
+  launch_finalize_warp(pl, o->homography, o->info + 1, w, h, p->normalization_floor, src, 3,
                        o->flow, o->warped, o->valid, c->qw, c->hist + 2 * kBins, true, s);
   probe(c, 4, 1);
   probe(c, 5, 0);
@@ -605,6 +787,18 @@ static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const flo
   rc = enqueue_fuse(c, ref, o->warped, o->ssim, o->valid, w, h, 0, o->composite);
   probe(c, 6, 1);
   return rc;
+}
+
+// lattice maps are uploaded with a blocking copy: build them before any capture
+static int ensure_lattice(hdr_ctx* c, const hdr_params* p, int w, int h) {
+  Dims d[kMaxLevels];
+  int L = pyramid_dims(w, h, p->max_levels, d);
+  for (int l = 0; l < L; ++l) {
+    LatticeInfo li;
+    int rc = lattice_maps(c, d[l].w, d[l].h, p->tile, p->quadrant_half, false, &li);
+    if (rc) return rc;
+  }
+  return HDR_OK;
 }
 
 static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
@@ -629,6 +823,7 @@ static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const 
   if (rc) return rc;
   rc = ensure_keys(c, p);
   if (!rc) rc = ensure_taps(c, p->ssim_window, p->ssim_sigma);
+  if (!rc) rc = ensure_lattice(c, p, w, h);
   return rc;
 }
 
@@ -657,10 +852,21 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
       kn += snprintf(key + kn, sizeof key - kn, ",%p", (void*)c->probes[i]);
   GraphEntry& g = c->graphs[key];
   if (!g.exec) {
+    // capture on the context's private stream (the caller's may be the
+    // legacy default stream, which cannot be captured); replay on theirs
     cudaGraph_t graph = nullptr;
-    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    if (!c->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      c->stream = user;
+      c->graphs.erase(key);
+      return fail(HDR_ERR_CUDA, std::string("begin capture: ") + cudaGetErrorString(e));
+    }
     rc = enqueue_pair(c, p, w, h, ref, src, o);
-    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    e = cudaStreamEndCapture(c->stream, &graph);
+    c->stream = user;
     if (rc) {
       if (graph) cudaGraphDestroy(graph);
       c->graphs.erase(key);
@@ -744,8 +950,31 @@ extern "C" int hdr_build_pyramid(hdr_ctx* c, const float* img, int32_t w, int32_
 
 extern "C" int hdr_integral(hdr_ctx* c, const float* img, int32_t w, int32_t h, double* table) {
   NEED(c && img && table && w >= 1 && h >= 1, "bad argument");
-  launch_integral(img, w, h, table, c->stream);
+  NEED(w <= c->W && h <= c->H, "image larger than the workspace");
+  SatBatch sb;
+  Dims d[1] = {{w, h}};
+  const float* lum[1] = {img};
+  int mw, mr, nt;
+  int rc = sat_batch(c, 1, lum, d, 16, 2, true, nullptr, table, &sb, &mw, &mr, &nt);
+  if (rc) return rc;
+  launch_sat(sb, mw, mr, c->stream);
   return check_launch();
+}
+
+// detect_corners on one level into c->tiles (shared by the per-stage entries)
+static int detect_one(hdr_ctx* c, const float* lum, int w, int h, int tile, double threshold,
+                      int half) {
+  NEED(w <= c->W && h <= c->H, "image larger than the workspace");
+  SatBatch sb;
+  Dims d[1] = {{w, h}};
+  const float* lv[1] = {lum};
+  TileCorner* tl[1] = {c->tiles};
+  int mw, mr, nt;
+  int rc = sat_batch(c, 1, lv, d, tile, half, false, tl, nullptr, &sb, &mw, &mr, &nt);
+  if (rc) return rc;
+  launch_sat(sb, mw, mr, c->stream);
+  launch_detect(sb, nt, DetectParams{tile, half, threshold}, c->stream);
+  return HDR_OK;
 }
 
 extern "C" int hdr_detect_corners(hdr_ctx* c, const float* lum, int32_t w, int32_t h, int32_t tile,
@@ -756,8 +985,8 @@ extern "C" int hdr_detect_corners(hdr_ctx* c, const float* lum, int32_t w, int32
   int nt = ntiles_of(w, h, tile);
   NEED(nt <= c->tiles_cap, "too many tiles");
   cudaStream_t s = c->stream;
-  launch_integral(lum, w, h, c->sat, s);
-  launch_detect(c->sat, w, h, tile, threshold, half, c->tiles, s);
+  int rc = detect_one(c, lum, w, h, tile, threshold, half);
+  if (rc) return rc;
   launch_compact_corners(c->tiles, nt, corners, c->counters + 5, s);
   CUDA_TRY(cudaMemcpyAsync(count, c->counters + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -784,8 +1013,8 @@ extern "C" int hdr_match_level(hdr_ctx* c, const hdr_params* p, const float* lum
   NEED(nt <= c->rows_cap, "too many tiles");
   NEED((int64_t)(w + 1) * (h + 1) <= (int64_t)(c->W + 1) * (c->H + 1), "image larger than the workspace");
   cudaStream_t s = c->stream;
-  launch_integral(lum_ref, w, h, c->sat, s);
-  launch_detect(c->sat, w, h, p->tile, p->threshold, p->quadrant_half, c->tiles, s);
+  int rc = detect_one(c, lum_ref, w, h, p->tile, p->threshold, p->quadrant_half);
+  if (rc) return rc;
   launch_ssd_tiles(c->tiles, nt, lum_ref, lum_src, w, h, h_pred, p->radius, p->patch, c->slot_rows,
                    c->slot_flags, s);
   launch_compact_rows(c->slot_rows, c->slot_flags, nt, c->raw, c->counters + 0, raw, s);
@@ -910,6 +1139,7 @@ extern "C" int hdr_match_stack(hdr_ctx* c, const hdr_params* p, int32_t w, int32
   rc = check_ptr_align(ref, 16, "ref");
   if (!rc) rc = check_ptr_align(src, 16, "src");
   if (!rc) rc = ensure_keys(c, p);
+  if (!rc) rc = ensure_lattice(c, p, w, h);
   if (rc) return rc;
   return enqueue_match(c, p, w, h, ref, src, matches, raw_matches, homography, info);
 }
@@ -920,7 +1150,8 @@ extern "C" int hdr_sparse_maps(hdr_ctx* c, const double* matches, int32_t m, int
   NEED((int64_t)w * h <= c->P, "image larger than the workspace");
   cudaStream_t s = c->stream;
   CUDA_TRY(cudaMemsetAsync(c->counters + 2, 0, sizeof(int32_t), s));
-  launch_splat(matches, nullptr, m, w, h, pu, pv, n, c->splat_key, c->splat_idx, c->counters + 2, s);
+  DtPlanes pl = f64_planes(pu, pv, n, 3);
+  launch_splat(matches, nullptr, m, w, h, pl, c->splat_key, c->splat_idx, c->counters + 2, s);
   int32_t st = 0;
   CUDA_TRY(cudaMemcpyAsync(&st, c->counters + 2, sizeof st, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -937,9 +1168,10 @@ extern "C" int hdr_dt_filter(hdr_ctx* c, const float* guide, double* planes, int
   if (passes < 1) return fail(HDR_ERR_INVALID, "passes must be >= 1");
   NEED(k >= 1 && k <= 3, "1 to 3 planes supported");
   NEED(w <= 7000, "width above 7000 is not supported by the row filter");
-  NEED((int64_t)ceil_div(h, 64) * w * 4 + 64 <= (int64_t)ceil_div(c->H, 64) * c->W * 4 + 64,
-       "image larger than the workspace");
-  launch_dt_filter(guide, planes, k, w, h, sigma_s, sigma_r, passes, c->carry, c->stream);
+  NEED(dt_scratch_doubles(w, h, k) <= dt_scratch_doubles(c->W, c->H, 3), "image larger than the workspace");
+  int64_t P = (int64_t)w * h;
+  DtPlanes pl = f64_planes(planes, planes + P, planes + 2 * P, k);
+  launch_dt_filter(guide, pl, w, h, sigma_s, sigma_r, passes, c->carry, c->stream);
   return check_launch();
 }
 
@@ -947,7 +1179,10 @@ extern "C" int hdr_densify_finalize(hdr_ctx* c, const double* smooth, int32_t w,
                                     const double* fallback, double floor_, float* flow) {
   NEED(c && smooth && flow, "null argument");
   // the fused kernel with the warp outputs switched off
-  launch_finalize_warp(smooth, fallback, nullptr, w, h, floor_, nullptr, 1, flow, nullptr, nullptr,
+  int64_t P = (int64_t)w * h;
+  DtPlanes pl = f64_planes(const_cast<double*>(smooth), const_cast<double*>(smooth) + P,
+                           const_cast<double*>(smooth) + 2 * P, 3);
+  launch_finalize_warp(pl, fallback, nullptr, w, h, floor_, nullptr, 1, flow, nullptr, nullptr,
                        nullptr, nullptr, true, c->stream);
   return check_launch();
 }
@@ -956,7 +1191,8 @@ extern "C" int hdr_warp_image(hdr_ctx* c, const float* src, int32_t channels, in
                               const float* flow, float* warped, uint8_t* valid) {
   NEED(c && src && flow && warped && valid, "null argument");
   NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
-  launch_finalize_warp(nullptr, nullptr, nullptr, w, h, 0.0, src, channels,
+  DtPlanes none = f64_planes(nullptr, nullptr, nullptr, 0);
+  launch_finalize_warp(none, nullptr, nullptr, w, h, 0.0, src, channels,
                        const_cast<float*>(flow), warped, valid, nullptr, nullptr, false, c->stream);
   return check_launch();
 }

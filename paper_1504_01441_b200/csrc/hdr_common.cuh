@@ -77,6 +77,21 @@ HD void from_norm(double xn, double yn, int w, int h, double* x, double* y) {
   *y = dadd(dmul(yn, fw), (double)h) / 2.0;
 }
 
+// Opt a kernel into the largest dynamic shared memory the device allows
+// (opt-in limit minus the kernel's static shared memory).
+template <class K>
+inline int allow_max_dynamic_smem(K kernel) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) return 0;
+  int bytes = optin - (int)fa.sharedSizeBytes;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return 0;
+  return bytes;
+}
+
 // Apply a row-major 3x3 H to (x, y), numpy operation order:
 // ((h0*x + h1*y) + h2) / ((h6*x + h7*y) + h8). Returns the denominator.
 HD double apply_h(const double* H, double x, double y, double* mx, double* my) {

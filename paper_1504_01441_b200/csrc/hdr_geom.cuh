@@ -395,26 +395,80 @@ HD void jacobi_eig9(double* a, double* w, double* v) {
 // triangle packed row-major, 45 entries) in conditioned coordinates.
 // The rank rule s[-2] <= 1e-9 s[0] is applied on sqrt(eigenvalues); below
 // ~1e-8 the Gram form cannot resolve it (documented in DESIGN.md).
+//
+// The smallest eigenvector comes from inverse iteration on G + sigma*I
+// (sigma = 1e-13 max diag keeps exact fits, lambda_min = 0, well posed)
+// through a diagonally pivoted Cholesky factor; the pivots double as the
+// rank estimate (d7 ~ lambda7 within a small factor).
 HD int fit_from_gram(const double* g45, const double* tr, const double* ts, double* H,
                      int* grey) {
-  double a[81], w[9], v[81];
+  double a[9][9];
   int k = 0;
+  double dmax = 0.0;
   for (int i = 0; i < 9; ++i)
-    for (int j = i; j < 9; ++j) { a[i * 9 + j] = g45[k]; a[j * 9 + i] = g45[k]; ++k; }
-  jacobi_eig9(a, w, v);
-  int order[9];
-  for (int i = 0; i < 9; ++i) order[i] = i;
-  for (int i = 1; i < 9; ++i)
-    for (int j = i; j > 0 && w[order[j]] > w[order[j - 1]]; --j) {
-      int t = order[j]; order[j] = order[j - 1]; order[j - 1] = t;
+    for (int j = i; j < 9; ++j) { a[i][j] = g45[k]; a[j][i] = g45[k]; ++k; }
+  for (int i = 0; i < 9; ++i) dmax = fmax(dmax, a[i][i]);
+  if (!(dmax > 0.0)) return 2;
+  double sigma = 1e-13 * dmax;
+  for (int i = 0; i < 9; ++i) a[i][i] += sigma;
+  int perm[9];
+  for (int i = 0; i < 9; ++i) perm[i] = i;
+  double piv[9];
+  for (int c = 0; c < 9; ++c) {
+    int p = c;
+    for (int i = c + 1; i < 9; ++i)
+      if (a[i][i] > a[p][p]) p = i;
+    if (p != c) {
+      for (int j = 0; j < 9; ++j) { double t = a[c][j]; a[c][j] = a[p][j]; a[p][j] = t; }
+      for (int j = 0; j < 9; ++j) { double t = a[j][c]; a[j][c] = a[j][p]; a[j][p] = t; }
+      int t = perm[c]; perm[c] = perm[p]; perm[p] = t;
     }
-  double s0 = sqrt(fmax(w[order[0]], 0.0));
-  double s7 = sqrt(fmax(w[order[7]], 0.0));
-  if (grey && s7 > 1e-13 * s0 && s7 < 1e-6 * s0) ++*grey;
-  if (s7 <= 1e-9 * s0) return 2;
+    double d = a[c][c];
+    piv[c] = d;
+    if (!(d > 0.0)) return 2;
+    double l = sqrt(d);
+    a[c][c] = l;
+    for (int i = c + 1; i < 9; ++i) a[i][c] /= l;
+    for (int i = c + 1; i < 9; ++i)
+      for (int j = c + 1; j <= i; ++j) {
+        a[i][j] -= a[i][c] * a[j][c];
+        a[j][i] = a[i][j];
+      }
+  }
+  // rank rule s[-2] <= 1e-9 s[0]: resolvable in Gram precision only down to
+  // ~1e-7 relative singular values; d7 - sigma estimates s7^2
+  double s7sq = fmax(piv[7] - sigma, 0.0), s0sq = piv[0] - sigma;
+  if (grey && s7sq > 1e-13 * s0sq && s7sq < 1e-10 * s0sq) ++*grey;
+  if (s7sq <= 1e-13 * s0sq) return 2;
+  double v[9], y[9];
+  for (int i = 0; i < 9; ++i) v[i] = 1.0 / 3.0;
+  for (int it = 0, settled = 0; it < 100 && settled < 2; ++it) {
+    for (int i = 0; i < 9; ++i) {  // L y = v
+      double s = v[i];
+      for (int j = 0; j < i; ++j) s -= a[i][j] * y[j];
+      y[i] = s / a[i][i];
+    }
+    for (int i = 8; i >= 0; --i) {  // L^T z = y (z into y)
+      double s = y[i];
+      for (int j = i + 1; j < 9; ++j) s -= a[j][i] * y[j];
+      y[i] = s / a[i][i];
+    }
+    double nrm = 0.0;
+    for (int i = 0; i < 9; ++i) nrm += y[i] * y[i];
+    nrm = 1.0 / sqrt(nrm);
+    double sgn = 0.0;
+    for (int i = 0; i < 9; ++i) sgn += y[i] * v[i];
+    if (sgn < 0) nrm = -nrm;
+    double diff = 0.0;
+    for (int i = 0; i < 9; ++i) {
+      double z = y[i] * nrm;
+      diff = fmax(diff, fabs(z - v[i]));
+      v[i] = z;
+    }
+    if (diff < 1e-15) ++settled;
+  }
   double hc[9];
-  int m = order[8];
-  for (int i = 0; i < 9; ++i) hc[i] = v[i * 9 + m];
+  for (int i = 0; i < 9; ++i) hc[perm[i]] = v[i];
   return finish_h(hc, tr, ts, H);
 }
 

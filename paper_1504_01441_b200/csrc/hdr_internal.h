@@ -35,9 +35,29 @@ void launch_apply_lut_f(const float* x, int64_t n, int32_t stride, const float* 
 void launch_luminance(const float* rgb, int64_t n, float* lum, cudaStream_t s);
 void launch_downsample2(const float* a, const float* b, int w, int h, float* oa,
                         float* ob, cudaStream_t s);
-void launch_integral(const float* img, int w, int h, double* table, cudaStream_t s);
-void launch_detect(const double* table, int w, int h, int tile, double threshold,
-                   int half, TileCorner* tiles, cudaStream_t s);
+// One pyramid level of the lattice summed-area table + corner detector.
+struct SatLevel {
+  const float* img;
+  int w, h;
+  const int32_t* rowmap;   // h+1 entries: stored row index of table row Y, or -1
+  const int32_t* colmap;   // w+1 entries
+  const int32_t* rowlist;  // nrows entries: Y of each stored row (ascending)
+  double* ctab;            // pass-1 column sums of stored rows, [nrows][w]
+  double* ltab;            // lattice table, [nrows][ncols]
+  int nrows, ncols;
+  TileCorner* tiles;       // per-tile detector output
+  int tile_base;           // first block of this level in the detect grid
+};
+struct SatBatch {
+  SatLevel lv[5];
+  int n;
+};
+struct DetectParams {
+  int tile, half;
+  double threshold;
+};
+void launch_sat(const SatBatch& b, int max_w, int max_rows, cudaStream_t s);
+void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s);
 void launch_compact_corners(const TileCorner* tiles, int ntiles, double* corners,
                             int32_t* count, cudaStream_t s);
 
@@ -70,15 +90,21 @@ void launch_inlier_mask(const double* H, const double* ref_pts, const double* sr
                         int n, double eps, uint8_t* mask, cudaStream_t s);
 void launch_set_identity(double* h, cudaStream_t s);
 
-// ---- k_densify.cu
+// ---- k_densify.cu / k_dtfilter.cu
+// Up to three H x W planes, each f32 or f64 (see hdr_planes.cuh).
+struct DtPlanes {
+  void* p[3];
+  int f64[3];
+  int k;
+};
 void launch_splat(const double* matches, const int32_t* count, int m_static, int w,
-                  int h, double* pu, double* pv, double* pn, uint64_t* scratch_key,
-                  int32_t* scratch_idx, int32_t* status, cudaStream_t s);
-void launch_dt_filter(const float* guide, double* planes, int k, int w, int h,
-                      double sigma_s, double sigma_r, int passes, double* carry,
-                      cudaStream_t s);
+                  int h, DtPlanes maps, uint64_t* scratch_key, int32_t* scratch_idx,
+                  int32_t* status, cudaStream_t s);
+int64_t dt_scratch_doubles(int w, int h, int k);
+void launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double sigma_s,
+                      double sigma_r, int passes, double* scratch, cudaStream_t s);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
-void launch_finalize_warp(const double* smooth, const double* fallback,
+void launch_finalize_warp(DtPlanes smooth, const double* fallback,
                           const int32_t* has_fallback, int w, int h, double floor_,
                           const float* src, int channels, float* flow, float* warped,
                           uint8_t* valid, uint8_t* qw, uint32_t* hist_w,

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kSsimTW * 8) ssim_kernel(
 }
 
 void init_fusion_attributes() {
-  cudaFuncSetAttribute(ssim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  allow_max_dynamic_smem(ssim_kernel);
 }
 
 void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb, const float* lut_b,

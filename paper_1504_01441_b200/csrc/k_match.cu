@@ -175,8 +175,8 @@ static size_t ssd_smem(int radius, int patch) {
 constexpr int kSsdMaxSmem = 200 * 1024;
 
 void init_match_attributes() {
-  cudaFuncSetAttribute(ssd_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSsdMaxSmem);
-  cudaFuncSetAttribute(ssd_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSsdMaxSmem);
+  allow_max_dynamic_smem(ssd_tiles_kernel);
+  allow_max_dynamic_smem(ssd_points_kernel);
 }
 
 void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref, const float* src,

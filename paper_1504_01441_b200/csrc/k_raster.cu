@@ -1,5 +1,5 @@
 // Raster stages: luminance + quantise + histograms (K1), CDF-matching LUT
-// (K2), 2x2 box pyramid (K3), FP64 summed-area table (K4) and quadrant
+// (K2), 2x2 box pyramid (K3), FP64 summed-area lattice (K4) and quadrant
 // cornerness with per-tile argmax (K5).
 //
 // Bit-exactness discipline: every f32/f64 op
@@ -218,90 +218,128 @@ void launch_downsample2(const float* a, const float* b, int w, int h, float* oa,
 }
 
 // ---------------------------------------------------------------- K4
-// image.integral (image.py:32-44): cumsum down each column in f64 (pass 1),
-// then along each row (pass 2) — numpy's sequential order, bit for bit.
-__global__ void sat_cols_kernel(const float* __restrict__ img, int w, int h,
-                                double* __restrict__ t) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t w1 = w + 1;
-  if (x == 0) t[0] = 0.0;
-  if (x >= w) return;
-  t[x + 1] = 0.0;
+// image.integral (image.py:32-44) restricted to the lattice the detector
+// reads. numpy fixes the rounding order: a sequential f64 cumsum down each
+// column (pass 1), then a sequential cumsum along each row (pass 2), so
+// both passes keep that order exactly; they only skip *storing* entries no
+// quadrant sum will read. Table row Y / column X live at rowmap[Y] /
+// colmap[X] (-1 = not needed); identity maps give the full table.
+constexpr int kSatPrefetch = 32;
+
+__global__ void __launch_bounds__(32) sat_cols_kernel(SatBatch b) {
+  const SatLevel& L = b.lv[blockIdx.y];
+  int x = blockIdx.x * 32 + threadIdx.x;
+  if (blockIdx.x * 32 >= L.w) return;
+  bool live = x < L.w;
+  const float* col = L.img + (live ? x : 0);
+  int64_t w = L.w;
+  int h = L.h;
+  float cur[kSatPrefetch];
+#pragma unroll
+  for (int k = 0; k < kSatPrefetch; ++k) cur[k] = (live && k < h) ? __ldg(col + k * w) : 0.0f;
   double acc = 0.0;
-  const float* p = img + x;
-  double* o = t + w1 + x + 1;
-  int y = 0;
-  for (; y + 8 <= h; y += 8) {
-    float v[8];
+  for (int y0 = 0; y0 < h; y0 += kSatPrefetch) {
+    float nxt[kSatPrefetch];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldg(p + (int64_t)(y + k) * w);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      acc = dadd(acc, (double)v[k]);
-      o[(int64_t)(y + k) * w1] = acc;
+    for (int k = 0; k < kSatPrefetch; ++k) {
+      int y = y0 + kSatPrefetch + k;
+      nxt[k] = (live && y < h) ? __ldg(col + (int64_t)y * w) : 0.0f;
     }
-  }
-  for (; y < h; ++y) {
-    acc = dadd(acc, (double)p[(int64_t)y * w]);
-    o[(int64_t)y * w1] = acc;
+#pragma unroll
+    for (int k = 0; k < kSatPrefetch; ++k) {
+      int y = y0 + k;
+      if (y < h) {
+        acc = dadd(acc, (double)cur[k]);
+        int ri = L.rowmap[y + 1];
+        if (ri >= 0 && live) L.ctab[(int64_t)ri * w + x] = acc;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kSatPrefetch; ++k) cur[k] = nxt[k];
   }
 }
 
-// pass 2: one warp per 32 rows, 32x32 tiles staged through shared memory so
-// both the loads and the stores stay coalesced; lane r scans row r.
-__global__ void __launch_bounds__(32) sat_rows_kernel(double* __restrict__ t, int w, int h) {
+// pass 2: one warp per 32 stored rows; lane r scans row r. 32x32 tiles are
+// staged through shared memory so the global loads stay coalesced, and the
+// next tile is prefetched into registers while the current one is scanned.
+__global__ void __launch_bounds__(32) sat_rows_kernel(SatBatch b) {
+  const SatLevel& L = b.lv[blockIdx.y];
   __shared__ double tile[32][33];
   int lane = threadIdx.x;
-  int row0 = blockIdx.x * 32 + 1;  // table rows 1..h
-  int64_t w1 = w + 1;
-  if (row0 + lane <= h) t[(int64_t)(row0 + lane) * w1] = 0.0;
+  int r0 = blockIdx.x * 32;
+  if (r0 >= L.nrows) return;
+  int myr = r0 + lane;
+  bool live = myr < L.nrows;
+  int Y = live ? L.rowlist[myr] : -1;
+  int64_t w = L.w;
+  double* out = L.ltab + (int64_t)myr * L.ncols;
+  if (live && L.colmap[0] >= 0) out[L.colmap[0]] = 0.0;
+  auto load = [&](int c0, int r) -> double {
+    int rr = r0 + r, c = c0 + lane;
+    if (rr >= L.nrows || c >= L.w) return 0.0;
+    return L.rowlist[rr] == 0 ? 0.0 : L.ctab[(int64_t)rr * w + c];
+  };
+  double pre[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) pre[r] = load(0, r);
   double acc = 0.0;
-  for (int c0 = 1; c0 <= w; c0 += 32) {
-    for (int r = 0; r < 32; ++r) {
-      int row = row0 + r, col = c0 + lane;
-      tile[r][lane] = (row <= h && col <= w) ? t[(int64_t)row * w1 + col] : 0.0;
-    }
+  for (int c0 = 0; c0 < L.w; c0 += 32) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) tile[r][lane] = pre[r];
     __syncwarp();
-    int ncol = min(32, w - c0 + 1);
-    for (int c = 0; c < ncol; ++c) {
+    if (c0 + 32 < L.w) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) pre[r] = load(c0 + 32, r);
+    }
+    int n = min(32, L.w - c0);
+    for (int c = 0; c < n; ++c) {
       acc = dadd(acc, tile[lane][c]);
-      tile[lane][c] = acc;
-    }
-    __syncwarp();
-    for (int r = 0; r < 32; ++r) {
-      int row = row0 + r, col = c0 + lane;
-      if (row <= h && col <= w) t[(int64_t)row * w1 + col] = tile[r][lane];
+      int ci = L.colmap[c0 + c + 1];
+      if (ci >= 0 && live) out[ci] = (Y == 0) ? 0.0 : acc;
     }
     __syncwarp();
   }
 }
 
-void launch_integral(const float* img, int w, int h, double* table, cudaStream_t s) {
-  sat_cols_kernel<<<ceil_div(w, 128), 128, 0, s>>>(img, w, h, table);
-  sat_rows_kernel<<<ceil_div(h, 32), 32, 0, s>>>(table, w, h);
+void launch_sat(const SatBatch& b, int max_w, int max_rows, cudaStream_t s) {
+  dim3 g1(ceil_div(max_w, 32), b.n), g2(ceil_div(max_rows, 32), b.n);
+  sat_cols_kernel<<<g1, 32, 0, s>>>(b);
+  sat_rows_kernel<<<g2, 32, 0, s>>>(b);
 }
 
 // ---------------------------------------------------------------- K5
 // matcher._quadrant_diffs + detect_corners (matcher.py:37-105). One block per
-// tile; candidate (lx, ly) sits at t0 + spacing/2 + k*spacing.
-__device__ __forceinline__ double box(const double* t, int64_t w1, int x0, int y0, int x1,
-                                      int y1) {
+// tile (all pyramid levels in one launch); candidate (lx, ly) sits at
+// t0 + spacing/2 + k*spacing.
+struct LatticeView {
+  const double* t;
+  const int32_t* rm;
+  const int32_t* cm;
+  int ncols;
+  __device__ __forceinline__ double at(int Y, int X) const {
+    return t[(int64_t)rm[Y] * ncols + cm[X]];
+  }
+};
+
+__device__ __forceinline__ double box(const LatticeView& v, int x0, int y0, int x1, int y1) {
   // ((t[y1,x1] - t[y0,x1]) - t[y1,x0]) + t[y0,x0]   (image.py:58)
-  return dadd(dsub(dsub(t[y1 * w1 + x1], t[y0 * w1 + x1]), t[y1 * w1 + x0]), t[y0 * w1 + x0]);
+  return dadd(dsub(dsub(v.at(y1, x1), v.at(y0, x1)), v.at(y1, x0)), v.at(y0, x0));
 }
 
-__global__ void __launch_bounds__(256) detect_kernel(const double* __restrict__ t, int w,
-                                                     int h, int tile, double threshold,
-                                                     int half, TileCorner* __restrict__ out) {
+__global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp) {
+  int lev = 0;
+  while (lev + 1 < b.n && (int)blockIdx.x >= b.lv[lev + 1].tile_base) ++lev;
+  const SatLevel& L = b.lv[lev];
+  int w = L.w, h = L.h, tile = dp.tile, half = dp.half;
   int tiles_x = ceil_div(w, tile);
-  int tid_tile = blockIdx.x;
+  int tid_tile = blockIdx.x - L.tile_base;
   int t0x = (tid_tile % tiles_x) * tile, t0y = (tid_tile / tiles_x) * tile;
   int sp = tile / 16 > 1 ? tile / 16 : 1;
   int first = sp / 2;
   int limx = min(tile, w - t0x), limy = min(tile, h - t0y);
   int nx = limx > first ? (limx - first + sp - 1) / sp : 0;
   int ny = limy > first ? (limy - first + sp - 1) / sp : 0;
-  int64_t w1 = w + 1;
+  LatticeView v{L.ltab, L.rowmap, L.colmap, L.ncols};
   double area = (double)(half * half);
   double best = -1.0;
   int best_i = 0x7fffffff;
@@ -309,14 +347,14 @@ __global__ void __launch_bounds__(256) detect_kernel(const double* __restrict__ 
     int lx = i % nx, ly = i / nx;
     int x = t0x + first + lx * sp, y = t0y + first + ly * sp;
     if (x < half || x > w - half || y < half || y > h - half) continue;
-    double tl = box(t, w1, x - half, y - half, x, y) / area;
-    double tr = box(t, w1, x, y - half, x + half, y) / area;
-    double br = box(t, w1, x, y, x + half, y + half) / area;
-    double bl = box(t, w1, x - half, y, x, y + half) / area;
+    double tl = box(v, x - half, y - half, x, y) / area;
+    double tr = box(v, x, y - half, x + half, y) / area;
+    double br = box(v, x, y, x + half, y + half) / area;
+    double bl = box(v, x - half, y, x, y + half) / area;
     double d0 = fabs(dsub(tr, tl)), d1 = fabs(dsub(br, tr));
     double d2 = fabs(dsub(bl, br)), d3 = fabs(dsub(tl, bl));
     double lo = fmin(fmin(d0, d1), fmin(d2, d3));
-    if (!(lo > threshold)) continue;
+    if (!(lo > dp.threshold)) continue;
     double c = dadd(dadd(dadd(d0, d1), d2), d3);
     if (c > best || (c == best && i < best_i)) { best = c; best_i = i; }
   }
@@ -342,14 +380,12 @@ __global__ void __launch_bounds__(256) detect_kernel(const double* __restrict__ 
       tc.y = t0y + first + (best_i / nx) * sp;
       tc.score = best;
     }
-    out[tid_tile] = tc;
+    L.tiles[tid_tile] = tc;
   }
 }
 
-void launch_detect(const double* table, int w, int h, int tile, double threshold, int half,
-                   TileCorner* tiles, cudaStream_t s) {
-  int nt = ceil_div(w, tile) * ceil_div(h, tile);
-  detect_kernel<<<nt, 256, 0, s>>>(table, w, h, tile, threshold, half, tiles);
+void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s) {
+  detect_kernel<<<total_tiles, 256, 0, s>>>(b, dp);
 }
 
 __global__ void __launch_bounds__(1024) compact_corners_kernel(const TileCorner* __restrict__ tiles,

@@ -104,7 +104,7 @@ def test_fit_homography_and_inliers(cuda):
     with pytest.raises(DegenerateFit):
         geometry.fit_homography(pts, pts)
     line = np.array([[0.0, 0.0], [1.0, 1.0], [2.0, 2.0], [3.0, 3.0]])
-    with pytest.raises(DegenerateFit):
+    with pytest.raises(O.DegenerateFit):
         O.fit_homography(line, line)
     with pytest.raises(DegenerateFit):
         geometry.fit_homography(line, line)

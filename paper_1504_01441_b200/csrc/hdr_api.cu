@@ -741,14 +741,15 @@ static int enqueue_fuse(hdr_ctx* c, const float* ref, const float* warped, const
   if (levels <= 0) levels = fusion_levels_default(w, h);
   std::vector<Dims> fd;
   int L = fusion_dims(w, h, levels, fd);
-  launch_fusion_weights(ref, warped, ssim, valid, w, h, c->wr, c->ws, s);
   std::vector<float*> g, cp;
   fusion_offsets(fd, c->fpyr, g, cp);
   if (L == 1) {
+    launch_fusion_weights(ref, warped, ssim, valid, w, h, c->wr, c->ws, s);
     launch_fuse_collapse0(ref, warped, c->wr, c->ws, w, h, nullptr, nullptr, 0, 0, out, s);
     return check_launch();
   }
-  launch_fuse_down0(ref, warped, c->wr, c->ws, w, h, g[1], fd[1].w, fd[1].h, s);
+  // weights (kept for level 0) fused with the first blur + decimation
+  launch_weights_down0(ref, warped, ssim, valid, w, h, c->wr, c->ws, g[1], fd[1].w, fd[1].h, s);
   for (int k = 1; k + 1 < L; ++k)
     launch_fuse_down(g[k], fd[k].w, fd[k].h, g[k + 1], fd[k + 1].w, fd[k + 1].h, s);
   launch_fuse_top(g[L - 1], fd[L - 1].w, fd[L - 1].h, cp[L - 1], s);
@@ -1248,4 +1249,5 @@ static void init_kernel_attributes() {
   hdr::init_match_attributes();
   hdr::init_densify_attributes();
   hdr::init_fusion_attributes();
+  hdr::init_merge_attributes();
 }

@@ -408,6 +408,10 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
   for (int i = 0; i < 9; ++i)
     for (int j = i; j < 9; ++j) { a[i][j] = g45[k]; a[j][i] = g45[k]; ++k; }
   for (int i = 0; i < 9; ++i) dmax = fmax(dmax, a[i][i]);
+#ifdef HDR_DEBUG_FIT
+  printf("gram in: g0=%g g1=%g g44=%g dmax=%g tr=%g %g %g ts=%g %g %g\n", g45[0], g45[1], g45[44],
+         dmax, tr[0], tr[1], tr[2], ts[0], ts[1], ts[2]);
+#endif
   if (!(dmax > 0.0)) return 2;
   double sigma = 1e-13 * dmax;
   for (int i = 0; i < 9; ++i) a[i][i] += sigma;
@@ -439,6 +443,9 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
   // ~1e-7 relative singular values; d7 - sigma estimates s7^2
   double s7sq = fmax(piv[7] - sigma, 0.0), s0sq = piv[0] - sigma;
   if (grey && s7sq > 1e-13 * s0sq && s7sq < 1e-10 * s0sq) ++*grey;
+#ifdef HDR_DEBUG_FIT
+  printf("gram: dmax=%g piv0=%g piv7=%g piv8=%g ratio=%g\n", dmax, piv[0], piv[7], piv[8], s7sq / s0sq);
+#endif
   if (s7sq <= 1e-13 * s0sq) return 2;
   double v[9], y[9];
   for (int i = 0; i < 9; ++i) v[i] = 1.0 / 3.0;
@@ -469,6 +476,11 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
   }
   double hc[9];
   for (int i = 0; i < 9; ++i) hc[perm[i]] = v[i];
+#ifdef HDR_DEBUG_FIT
+  int fr = finish_h(hc, tr, ts, H);
+  printf("gram: hc = %g %g %g %g %g %g %g %g %g -> %d\n", hc[0], hc[1], hc[2], hc[3], hc[4], hc[5], hc[6], hc[7], hc[8], fr);
+  return fr;
+#endif
   return finish_h(hc, tr, ts, H);
 }
 

@@ -118,10 +118,11 @@ void launch_quality(const float* rgb, int w, int h, float* out, cudaStream_t s);
 void launch_fusion_weights(const float* ref, const float* warped, const float* ssim,
                            const uint8_t* valid, int w, int h, float* wr, float* ws,
                            cudaStream_t s);
-// pyramid of 8 planar channels (ref rgb, warped rgb, wr, ws)
-void launch_fuse_down0(const float* ref, const float* warped, const float* wr,
-                       const float* ws, int w, int h, float* out, int ow, int oh,
-                       cudaStream_t s);
+// ---- k_merge.cu: pyramid of 8 planar channels (ref rgb, warped rgb, wr, ws)
+void init_merge_attributes();
+void launch_weights_down0(const float* ref, const float* warped, const float* ssim,
+                          const uint8_t* valid, int w, int h, float* wr, float* ws, float* g1,
+                          int ow, int oh, cudaStream_t s);
 void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh,
                       cudaStream_t s);
 void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s);

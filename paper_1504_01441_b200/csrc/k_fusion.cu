@@ -1,5 +1,5 @@
-// Merge: SSIM registration-trust map (K13), Mertens quality weights and the
-// normalised fusion weights (K14), Laplacian-pyramid blend (K15).
+// Merge inputs: SSIM registration-trust map (K13) and the per-stage quality /
+// fusion-weight kernels (K14); the pyramid blend itself is in k_merge.cu.
 //
 // Storage is f32 (images, weights, pyramid levels); SSIM moments and the
 // weight products are evaluated in f64 like the reference
@@ -164,172 +164,6 @@ void launch_fusion_weights(const float* ref, const float* warped, const float* s
                            cudaStream_t s) {
   dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
   fusion_weights_kernel<<<grd, blk, 0, s>>>(ref, warped, ssim, valid, w, h, wr, ws);
-}
-
-// ---------------------------------------------------------------- K15
-// fusion._blur5 then [::2, ::2] (fusion.py:80-86), 8 planar channels out:
-// 0-2 reference RGB, 3-5 warped RGB, 6 w_ref, 7 w_src.
-__constant__ float kP5[5] = {1.0f / 16, 4.0f / 16, 6.0f / 16, 4.0f / 16, 1.0f / 16};
-
-template <bool LEVEL0>
-__global__ void __launch_bounds__(256) fuse_down_kernel(const float* __restrict__ in,
-                                                        const float* __restrict__ ref,
-                                                        const float* __restrict__ warped,
-                                                        const float* __restrict__ wr,
-                                                        const float* __restrict__ ws, int w,
-                                                        int h, float* __restrict__ out, int ow,
-                                                        int oh) {
-  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (X >= ow || Y >= oh) return;
-  int rows[5], cols[5];
-#pragma unroll
-  for (int t = 0; t < 5; ++t) {
-    rows[t] = reflect_index(2 * Y + t - 2, h);
-    cols[t] = reflect_index(2 * X + t - 2, w);
-  }
-  int64_t P = (int64_t)w * h, OP = (int64_t)ow * oh;
-  float acc[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    float rowacc[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) rowacc[c] = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      int64_t p = (int64_t)rows[i] * w + cols[j];
-      float v[8];
-      if (LEVEL0) {
-        v[0] = ref[3 * p]; v[1] = ref[3 * p + 1]; v[2] = ref[3 * p + 2];
-        v[3] = warped[3 * p]; v[4] = warped[3 * p + 1]; v[5] = warped[3 * p + 2];
-        v[6] = wr[p]; v[7] = ws[p];
-      } else {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = in[c * P + p];
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) rowacc[c] += kP5[j] * v[c];
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] += kP5[i] * rowacc[c];
-  }
-  int64_t o = (int64_t)Y * ow + X;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) out[c * OP + o] = acc[c];
-}
-
-void launch_fuse_down0(const float* ref, const float* warped, const float* wr, const float* ws,
-                       int w, int h, float* out, int ow, int oh, cudaStream_t s) {
-  dim3 blk(32, 8), grd(ceil_div(ow, 32), ceil_div(oh, 8));
-  fuse_down_kernel<true><<<grd, blk, 0, s>>>(nullptr, ref, warped, wr, ws, w, h, out, ow, oh);
-}
-
-void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh, cudaStream_t s) {
-  dim3 blk(32, 8), grd(ceil_div(ow, 32), ceil_div(oh, 8));
-  fuse_down_kernel<false><<<grd, blk, 0, s>>>(in, nullptr, nullptr, nullptr, nullptr, w, h, out,
-                                              ow, oh);
-}
-
-// top of the pyramid: C = w_ref * G_ref + w_src * G_src (laps[-1] = gp[-1])
-__global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float* __restrict__ c) {
-  int64_t P = (int64_t)w * h;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  float a = g[6 * P + i], b = g[7 * P + i];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) c[k * P + i] = a * g[k * P + i] + b * g[(3 + k) * P + i];
-}
-
-void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s) {
-  int64_t P = (int64_t)w * h;
-  fuse_top_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(g, w, h, c);
-}
-
-// _pyr_up (fusion.py:89-93): zero-insert into the fine grid, 2x-gain 5-tap
-// blur per axis with reflect on the fine grid. Accumulates 9 coarse
-// channels (G_ref 0-2, G_src 3-5 from gc; C 0-2 from cc) at fine (y, x).
-__device__ __forceinline__ void up9(const float* __restrict__ gc, const float* __restrict__ cc,
-                                    int cw, int chh, int w, int h, int x, int y, float* o) {
-  int64_t CP = (int64_t)cw * chh;
-#pragma unroll
-  for (int c = 0; c < 9; ++c) o[c] = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    int ry = reflect_index(y + i - 2, h);
-    if (ry & 1) continue;
-    float row[9];
-#pragma unroll
-    for (int c = 0; c < 9; ++c) row[c] = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      int rx = reflect_index(x + j - 2, w);
-      if (rx & 1) continue;
-      int64_t p = (int64_t)(ry >> 1) * cw + (rx >> 1);
-      float kj = 2.0f * kP5[j];
-#pragma unroll
-      for (int c = 0; c < 6; ++c) row[c] += kj * gc[c * CP + p];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) row[6 + c] += kj * cc[c * CP + p];
-    }
-    float ki = 2.0f * kP5[i];
-#pragma unroll
-    for (int c = 0; c < 9; ++c) o[c] += ki * row[c];
-  }
-}
-
-// collapse step for level k >= 1:
-// C_k = w_ref (G_ref - up G_ref') + w_src (G_src - up G_src') + up C'
-__global__ void __launch_bounds__(256) fuse_collapse_kernel(const float* __restrict__ g, int w,
-                                                            int h, const float* __restrict__ gc,
-                                                            const float* __restrict__ cc, int cw,
-                                                            int chh, float* __restrict__ c) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= w || y >= h) return;
-  float u[9];
-  up9(gc, cc, cw, chh, w, h, x, y, u);
-  int64_t P = (int64_t)w * h, i = (int64_t)y * w + x;
-  float a = g[6 * P + i], b = g[7 * P + i];
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    c[k * P + i] = a * (g[k * P + i] - u[k]) + b * (g[(3 + k) * P + i] - u[3 + k]) + u[6 + k];
-}
-
-void launch_fuse_collapse(const float* g, int w, int h, const float* gc, const float* cc, int cw,
-                          int ch, float* c, cudaStream_t s) {
-  dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
-  fuse_collapse_kernel<<<grd, blk, 0, s>>>(g, w, h, gc, cc, cw, ch, c);
-}
-
-// level 0: reads the interleaved inputs and weights, writes the clipped
-// interleaved composite (fusion.py:154-157).
-__global__ void __launch_bounds__(256) fuse_collapse0_kernel(
-    const float* __restrict__ ref, const float* __restrict__ warped, const float* __restrict__ wr,
-    const float* __restrict__ ws, int w, int h, const float* __restrict__ gc,
-    const float* __restrict__ cc, int cw, int chh, float* __restrict__ out) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= w || y >= h) return;
-  float u[9];
-  if (gc) {
-    up9(gc, cc, cw, chh, w, h, x, y, u);
-  } else {  // single-level pyramid: the blend is the whole result
-#pragma unroll
-    for (int c = 0; c < 9; ++c) u[c] = 0.0f;
-  }
-  int64_t i = (int64_t)y * w + x;
-  float a = wr[i], b = ws[i];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    float v = a * (ref[3 * i + k] - u[k]) + b * (warped[3 * i + k] - u[3 + k]) + u[6 + k];
-    out[3 * i + k] = fminf(fmaxf(v, 0.0f), 1.0f);
-  }
-}
-
-void launch_fuse_collapse0(const float* ref, const float* warped, const float* wr, const float* ws,
-                           int w, int h, const float* gc, const float* cc, int cw, int ch,
-                           float* out, cudaStream_t s) {
-  dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
-  fuse_collapse0_kernel<<<grd, blk, 0, s>>>(ref, warped, wr, ws, w, h, gc, cc, cw, ch, out);
 }
 
 }  // namespace hdr

@@ -402,39 +402,39 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     a /= (double)n;
     b /= (double)n;
     status = (a < 1e-12 || b < 1e-12) ? 2 : 0;
+#ifdef HDR_DEBUG_FIT
+    printf("block_fit: n=%d md=%g %g c=%g %g %g %g\n", n, a, b, bc[0], bc[1], bc[2], bc[3]);
+#endif
     double sr = sqrt(2.0) / a, ss = sqrt(2.0) / b;
     tr[0] = sr; tr[1] = -sr * bc[0]; tr[2] = -sr * bc[1];
     ts[0] = ss; ts[1] = -ss * bc[2]; ts[2] = -ss * bc[3];
   }
   __syncthreads();
   if (status) return status;
-  // Gram matrix of the conditioned DLT rows (45 upper entries)
-  double gacc[45];
-  for (int k = 0; k < 45; ++k) gacc[k] = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double p[4];
-    get(i, p);
-    double r0[9], r1[9];
-    dlt_rows((p[0] - bc[0]) * tr[0], (p[1] - bc[1]) * tr[0], (p[2] - bc[2]) * ts[0],
-             (p[3] - bc[3]) * ts[0], r0, r1);
-    int k = 0;
-    for (int a = 0; a < 9; ++a)
-      for (int b = a; b < 9; ++b) { gacc[k] += r0[a] * r0[b] + r1[a] * r1[b]; ++k; }
-  }
-  __shared__ double gsh[32][45];
-  for (int k = 0; k < 45; ++k) {
-    double v = gacc[k];
-    for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffff, v, off);
-    if (lane == 0) gsh[warp][k] = v;
+  // Gram matrix of the conditioned DLT rows (45 upper entries): warp w
+  // reduces entries w, w + nw, ... over all points, so no thread carries a
+  // 45-entry accumulator
+  __shared__ double gsh[45];
+  for (int e = warp; e < 45; e += nw) {
+    int ea = 0, rem = e;
+    while (rem >= 9 - ea) { rem -= 9 - ea; ++ea; }
+    int eb = ea + rem;
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      double p[4];
+      get(i, p);
+      double r0[9], r1[9];
+      dlt_rows((p[0] - bc[0]) * tr[0], (p[1] - bc[1]) * tr[0], (p[2] - bc[2]) * ts[0],
+               (p[3] - bc[3]) * ts[0], r0, r1);
+      acc += r0[ea] * r0[eb] + r1[ea] * r1[eb];
+    }
+    for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffff, acc, off);
+    if (lane == 0) gsh[e] = acc;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double g45[45];
-    for (int k = 0; k < 45; ++k) {
-      double a = 0.0;
-      for (int j = 0; j < nw; ++j) a += gsh[j][k];
-      g45[k] = a;
-    }
+    for (int k = 0; k < 45; ++k) g45[k] = gsh[k];
     int g = 0;
     status = fit_from_gram(g45, tr, ts, H, &g);
     if (g && grey) atomicAdd(grey, g);

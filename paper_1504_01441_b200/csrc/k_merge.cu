@@ -1,0 +1,280 @@
+// Laplacian-pyramid exposure fusion (K14 + K15), fusion.py:96-157, as four
+// tiled kernels:
+//   weights_down0  quality weights of both frames (fusion.py:67-77), the
+//                  SSIM/validity trust and normalisation (fusion.py:117-128)
+//                  for a 36x36 level-0 tile, written for the owned 32x32 and
+//                  immediately blurred + decimated into level 1 of the
+//                  8-channel Gaussian pyramid (ref RGB, warped RGB, W_ref,
+//                  W_src) -- the weights never make a separate HBM round trip
+//                  before the first reduction;
+//   down           the same 5-tap reflect blur + [::2, ::2] for levels >= 1;
+//   collapse       C_k = W_ref (G_ref - up G_ref') + W_src (G_src - up G_src')
+//                  + up C'  (the blend of laplacian_pyramid terms and
+//                  collapse_pyramid folded together); level 0 reads the
+//                  interleaved inputs and writes the clipped composite.
+// up() is _pyr_up (fusion.py:89-93): zero-insert on the fine grid, 2x-gain
+// 5-tap blur, scipy 'reflect' on the fine grid -- evaluated separably from a
+// shared-memory staging of the horizontally up-sampled rows.
+// Arithmetic is f32 (the composite tolerance is 1e-3).
+#include "hdr_common.cuh"
+#include "hdr_internal.h"
+
+namespace hdr {
+
+__constant__ float kK5[5] = {1.0f / 16, 4.0f / 16, 6.0f / 16, 4.0f / 16, 1.0f / 16};
+__constant__ float kK5x2[5] = {2.0f / 16, 8.0f / 16, 12.0f / 16, 8.0f / 16, 2.0f / 16};
+
+__device__ __forceinline__ float lum_f(float r, float g, float b) {
+  float y = fadd(fadd(fmul(0.299f, r), fmul(0.587f, g)), fmul(0.114f, b));
+  return fminf(fmaxf(y, 0.0f), 1.0f);
+}
+
+// contrast x saturation x well-exposedness (f32); lap = 4-neighbour laplacian
+__device__ __forceinline__ float quality_f(float lap, float r, float g, float b) {
+  float mean = (r + g + b) * (1.0f / 3.0f);
+  float dr = r - mean, dg = g - mean, db = b - mean;
+  float sat = sqrtf((dr * dr + dg * dg + db * db) * (1.0f / 3.0f));
+  float er = r - 0.5f, eg = g - 0.5f, eb = b - 0.5f;
+  float ex = expf(-(er * er + eg * eg + eb * eb) * (1.0f / 0.08f));
+  return fabsf(lap) * sat * ex + 1e-12f;
+}
+
+// ---------------------------------------------------------------- weights + level 1
+constexpr int kOT = 16;           // level-1 outputs per tile side
+constexpr int kRT = 2 * kOT + 4;  // level-0 region incl. the 2-px blur halo (36)
+constexpr int kLT = kRT + 2;      // + 1-px laplacian halo (38)
+
+__global__ void __launch_bounds__(256) weights_down0_kernel(
+    const float* __restrict__ ref, const float* __restrict__ warped, const float* __restrict__ ssim,
+    const uint8_t* __restrict__ valid, int w, int h, float* __restrict__ wr_out,
+    float* __restrict__ ws_out, float* __restrict__ g1, int ow, int oh) {
+  extern __shared__ float smf[];
+  float (*lr)[kLT] = reinterpret_cast<float (*)[kLT]>(smf);
+  float (*lw)[kLT] = reinterpret_cast<float (*)[kLT]>(smf + kLT * kLT);
+  // ref rgb, warped rgb, w_ref, w_src
+  float (*px)[kRT][kRT + 1] = reinterpret_cast<float (*)[kRT][kRT + 1]>(smf + 2 * kLT * kLT);
+  float (*V)[kOT][kRT] = reinterpret_cast<float (*)[kOT][kRT]>(smf + 2 * kLT * kLT + 8 * kRT * (kRT + 1));
+  int tid = threadIdx.x, nt = blockDim.x;
+  int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
+  int vy0 = 2 * Y0 - 3, vx0 = 2 * X0 - 3;  // virtual origin of the 38x38 lum tile
+  for (int i = tid; i < kLT * kLT; i += nt) {
+    int ly = i / kLT, lx = i % kLT;
+    int gy = reflect_index(vy0 + ly, h), gx = reflect_index(vx0 + lx, w);
+    int64_t p = ((int64_t)gy * w + gx) * 3;
+    float r0 = ref[p], r1 = ref[p + 1], r2 = ref[p + 2];
+    float w0 = warped[p], w1 = warped[p + 1], w2 = warped[p + 2];
+    lr[ly][lx] = lum_f(r0, r1, r2);
+    lw[ly][lx] = lum_f(w0, w1, w2);
+    if (ly >= 1 && ly <= kRT && lx >= 1 && lx <= kRT) {
+      int ty = ly - 1, tx = lx - 1;
+      px[0][ty][tx] = r0; px[1][ty][tx] = r1; px[2][ty][tx] = r2;
+      px[3][ty][tx] = w0; px[4][ty][tx] = w1; px[5][ty][tx] = w2;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < kRT * kRT; i += nt) {
+    int ty = i / kRT, tx = i % kRT;
+    int ly = ty + 1, lx = tx + 1;
+    float lapr = (lr[ly - 1][lx] + lr[ly + 1][lx] - 2.0f * lr[ly][lx]) +
+                 (lr[ly][lx - 1] + lr[ly][lx + 1] - 2.0f * lr[ly][lx]);
+    float lapw = (lw[ly - 1][lx] + lw[ly + 1][lx] - 2.0f * lw[ly][lx]) +
+                 (lw[ly][lx - 1] + lw[ly][lx + 1] - 2.0f * lw[ly][lx]);
+    float qr = quality_f(lapr, px[0][ty][tx], px[1][ty][tx], px[2][ty][tx]);
+    float qs = quality_f(lapw, px[3][ty][tx], px[4][ty][tx], px[5][ty][tx]);
+    int gy = reflect_index(vy0 + ly, h), gx = reflect_index(vx0 + lx, w);
+    int64_t p = (int64_t)gy * w + gx;
+    float sv = fminf(fmaxf(ssim[p], 0.0f), 1.0f);
+    qs = valid[p] ? qs * sv : 0.0f;
+    float tot = qr + qs;
+    float a = qr / tot, b = qs / tot;
+    px[6][ty][tx] = a;
+    px[7][ty][tx] = b;
+    // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image
+    int ry = vy0 + ly, rx = vx0 + lx;
+    if (ty >= 2 && ty < 2 + 2 * kOT && tx >= 2 && tx < 2 + 2 * kOT && ry < h && rx < w) {
+      wr_out[p] = a;
+      ws_out[p] = b;
+    }
+  }
+  __syncthreads();
+  // vertical 5-tap + decimation: V[c][oy][tx] (region row 2*oy + i)
+  for (int i = tid; i < 8 * kOT * kRT; i += nt) {
+    int c = i / (kOT * kRT), r = i % (kOT * kRT);
+    int oy = r / kRT, tx = r % kRT;
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc += kK5[k] * px[c][2 * oy + k][tx];
+    V[c][oy][tx] = acc;
+  }
+  __syncthreads();
+  int64_t OP = (int64_t)ow * oh;
+  for (int i = tid; i < 8 * kOT * kOT; i += nt) {
+    int c = i / (kOT * kOT), r = i % (kOT * kOT);
+    int oy = r / kOT, ox = r % kOT;
+    int Y = Y0 + oy, X = X0 + ox;
+    if (Y >= oh || X >= ow) continue;
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc += kK5[k] * V[c][oy][2 * ox + k];
+    g1[c * OP + (int64_t)Y * ow + X] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- levels >= 1
+__global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
+                                                   float* __restrict__ out, int ow, int oh) {
+  __shared__ float tile[kRT][kRT + 1];
+  __shared__ float V[kOT][kRT];
+  int tid = threadIdx.x, nt = blockDim.x;
+  int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
+  int vy0 = 2 * Y0 - 2, vx0 = 2 * X0 - 2;
+  int64_t P = (int64_t)w * h, OP = (int64_t)ow * oh;
+  for (int c = 0; c < 8; ++c) {
+    const float* src = in + c * P;
+    for (int i = tid; i < kRT * kRT; i += nt) {
+      int ty = i / kRT, tx = i % kRT;
+      tile[ty][tx] = src[(int64_t)reflect_index(vy0 + ty, h) * w + reflect_index(vx0 + tx, w)];
+    }
+    __syncthreads();
+    for (int i = tid; i < kOT * kRT; i += nt) {
+      int oy = i / kRT, tx = i % kRT;
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) acc += kK5[k] * tile[2 * oy + k][tx];
+      V[oy][tx] = acc;
+    }
+    __syncthreads();
+    for (int i = tid; i < kOT * kOT; i += nt) {
+      int oy = i / kOT, ox = i % kOT;
+      int Y = Y0 + oy, X = X0 + ox;
+      if (Y >= oh || X >= ow) continue;
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) acc += kK5[k] * V[oy][2 * ox + k];
+      out[c * OP + (int64_t)Y * ow + X] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- collapse
+constexpr int kFT = 32;           // fine outputs per tile side
+constexpr int kFV = kFT + 4;      // virtual fine rows incl. the 2-px halo
+
+// 9 coarse channels: G_ref 0-2, G_src 3-5 (gc, planar 8-ch level), C 6-8 (cc)
+__device__ __forceinline__ float coarse_at(const float* gc, const float* cc, int64_t CP, int c,
+                                           int64_t p) {
+  return c < 6 ? __ldg(gc + c * CP + p) : __ldg(cc + (c - 6) * CP + p);
+}
+
+template <bool LEVEL0>
+__global__ void __launch_bounds__(256) collapse_kernel(
+    const float* __restrict__ g, const float* __restrict__ ref, const float* __restrict__ warped,
+    const float* __restrict__ wr, const float* __restrict__ ws, int w, int h,
+    const float* __restrict__ gc, const float* __restrict__ cc, int cw, int ch,
+    float* __restrict__ out) {
+  __shared__ float Hs[9][kFV][kFT + 1];
+  int tid = threadIdx.x, nt = blockDim.x;
+  int y0 = blockIdx.y * kFT, x0 = blockIdx.x * kFT;
+  int64_t CP = (int64_t)cw * ch;
+  // horizontal up-sampling of the virtual rows y0-2 .. y0+33
+  for (int i = tid; i < kFV * kFT; i += nt) {
+    int v = i / kFT, x = i % kFT;
+    int R = reflect_index(y0 - 2 + v, h);
+    float acc[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
+    if (!(R & 1) && gc) {
+      int64_t rowoff = (int64_t)(R >> 1) * cw;
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        int Rx = reflect_index(x0 + x + j - 2, w);
+        if (Rx & 1) continue;
+        int64_t p = rowoff + (Rx >> 1);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) acc[c] += kK5x2[j] * coarse_at(gc, cc, CP, c, p);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) Hs[c][v][x] = acc[c];
+  }
+  __syncthreads();
+  int64_t P = (int64_t)w * h;
+  for (int i = tid; i < kFT * kFT; i += nt) {
+    int yy = i / kFT, x = i % kFT;
+    int Y = y0 + yy, X = x0 + x;
+    if (Y >= h || X >= w) continue;
+    float u[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) acc += kK5x2[k] * Hs[c][yy + k][x];
+      u[c] = acc;
+    }
+    int64_t p = (int64_t)Y * w + X;
+    if (LEVEL0) {
+      float a = wr[p], b = ws[p];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float v = a * (ref[3 * p + k] - u[k]) + b * (warped[3 * p + k] - u[3 + k]) + u[6 + k];
+        out[3 * p + k] = fminf(fmaxf(v, 0.0f), 1.0f);
+      }
+    } else {
+      float a = g[6 * P + p], b = g[7 * P + p];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        out[k * P + p] = a * (g[k * P + p] - u[k]) + b * (g[(3 + k) * P + p] - u[3 + k]) + u[6 + k];
+    }
+  }
+}
+
+// top of the pyramid: C = w_ref * G_ref + w_src * G_src (laps[-1] = gp[-1])
+__global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float* __restrict__ c) {
+  int64_t P = (int64_t)w * h;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  float a = g[6 * P + i], b = g[7 * P + i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k * P + i] = a * g[k * P + i] + b * g[(3 + k) * P + i];
+}
+
+constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * (kRT + 1) + 8 * kOT * kRT);
+
+void init_merge_attributes() {
+  cudaFuncSetAttribute(weights_down0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kW0Smem);
+}
+
+void launch_weights_down0(const float* ref, const float* warped, const float* ssim,
+                          const uint8_t* valid, int w, int h, float* wr, float* ws, float* g1,
+                          int ow, int oh, cudaStream_t s) {
+  dim3 grd(ceil_div(ow, kOT), ceil_div(oh, kOT));
+  weights_down0_kernel<<<grd, 256, kW0Smem, s>>>(ref, warped, ssim, valid, w, h, wr, ws, g1, ow, oh);
+}
+
+void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh, cudaStream_t s) {
+  dim3 grd(ceil_div(ow, kOT), ceil_div(oh, kOT));
+  down_kernel<<<grd, 256, 0, s>>>(in, w, h, out, ow, oh);
+}
+
+void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s) {
+  int64_t P = (int64_t)w * h;
+  fuse_top_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(g, w, h, c);
+}
+
+void launch_fuse_collapse(const float* g, int w, int h, const float* gc, const float* cc, int cw,
+                          int ch, float* c, cudaStream_t s) {
+  dim3 grd(ceil_div(w, kFT), ceil_div(h, kFT));
+  collapse_kernel<false><<<grd, 256, 0, s>>>(g, nullptr, nullptr, nullptr, nullptr, w, h, gc, cc,
+                                             cw, ch, c);
+}
+
+void launch_fuse_collapse0(const float* ref, const float* warped, const float* wr, const float* ws,
+                           int w, int h, const float* gc, const float* cc, int cw, int ch,
+                           float* out, cudaStream_t s) {
+  dim3 grd(ceil_div(w, kFT), ceil_div(h, kFT));
+  collapse_kernel<true><<<grd, 256, 0, s>>>(nullptr, ref, warped, wr, ws, w, h, gc, cc, cw, ch,
+                                            out);
+}
+
+}  // namespace hdr

@@ -292,7 +292,7 @@ struct hdr_ctx {
   uint64_t keys_seed = ~0ULL;
   int keys_it = -1, keys_cit = -1;
   // densify
-  void* planes = nullptr;       // pu, pv (f32) + n (f64): 16 B per pixel
+  void* planes = nullptr;       // pu, pv, n: f64 planes (24 B per pixel)
   double* carry = nullptr;      // domain-transform aggregates / carries / coefficients
   uint64_t* splat_key = nullptr;
   int32_t* splat_idx = nullptr;
@@ -306,6 +306,8 @@ struct hdr_ctx {
   int taps_window = -1;
   double taps_sigma = -1.0;
   int32_t* info_scratch = nullptr;
+  int32_t* stats_q = nullptr;   // exactness certificate per level (K4)
+  double* stats_s = nullptr;
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t probes[2 * HDR_NUM_STAGES] = {};
   bool probing = false;
@@ -406,7 +408,7 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   ALLOC(witness, c->rows_cap + 1);
   ALLOC(kept, c->rows_cap);
   ALLOC(hpred, 32);
-  if (e == cudaSuccess) e = ctx_alloc(c, reinterpret_cast<double**>(&c->planes), 2 * P + 64);
+  if (e == cudaSuccess) e = ctx_alloc(c, reinterpret_cast<double**>(&c->planes), 3 * P + 64);
   ALLOC(carry, dt_scratch_doubles(width, height, 3));
   ALLOC(splat_key, P);
   ALLOC(splat_idx, P);
@@ -416,6 +418,8 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   ALLOC(fpyr, fsum + 64);
   ALLOC(taps, 64);
   ALLOC(info_scratch, HDR_INFO_WORDS);
+  ALLOC(stats_q, 8);
+  ALLOC(stats_s, 8);
 #undef ALLOC
   if (e != cudaSuccess) {
     hdr_ctx_destroy(c);
@@ -444,8 +448,15 @@ extern "C" int32_t hdr_ctx_graph_kernels(hdr_ctx* c) { return c ? c->graph_kerne
 static void probe(hdr_ctx* c, int stage, int end) {
   if (!c->probing) return;
   cudaEvent_t e = c->probes[2 * stage + end];
-  // External: captured as a real event-record node, so replays time it
-  if (e) cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+  if (!e) return;
+  // while capturing, External makes it a real event-record node (replays
+  // time it); outside capture the flag is not accepted
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, c->stream);
 }
 
 extern "C" int hdr_ctx_sync(hdr_ctx* c) {
@@ -578,6 +589,8 @@ static int sat_batch(hdr_ctx* c, int n, const float* const* lum, const Dims* d, 
                      int half, bool full, TileCorner* const* tiles, double* ltab_override,
                      SatBatch* b, int* max_w, int* max_rows, int* total_tiles) {
   b->n = n;
+  b->qmin = full ? nullptr : c->stats_q;  // full tables always take numpy's order
+  b->sums = full ? nullptr : c->stats_s;
   int64_t co = 0, lo = 0;
   *max_w = *max_rows = *total_tiles = 0;
   for (int l = 0; l < n; ++l) {
@@ -608,6 +621,12 @@ static int sat_batch(hdr_ctx* c, int n, const float* const* lum, const Dims* d, 
   return HDR_OK;
 }
 
+static DetectParams detect_params(int tile, int half, double threshold) {
+  DetectParams dp{tile, half, threshold, 0};
+  dp.exact_ok = detect_exact_smem(tile, half) <= 200 * 1024;
+  return dp;
+}
+
 static TileCorner* tiles_level(hdr_ctx* c, const Dims* d, int l, int tile) {
   TileCorner* t = c->tiles;
   for (int k = 0; k < l; ++k) t += ntiles_of(d[k].w, d[k].h, tile);
@@ -622,17 +641,14 @@ static DtPlanes f64_planes(double* a, double* b, double* n, int k) {
   return pl;
 }
 
-// the pair path's planes: flow numerators f32, indicator f64
+// The pair path's planes are all f64: with f32 flow numerators the flow moves
+// by ~1e-6 px, which flips warp_image's validity test on pixels whose sample
+// lands exactly on the frame edge (integer shifts) and the fusion spreads each
+// flip over ~70 composite pixels. f64 keeps the flow within
+// ~1e-13 of the reference before its f32 cast.
 static DtPlanes pair_planes(hdr_ctx* c, int64_t P) {
-  DtPlanes pl;
-  float* f = reinterpret_cast<float*>(c->planes);
-  pl.p[0] = f;
-  pl.p[1] = f + P;
-  pl.p[2] = reinterpret_cast<double*>(f + 2 * P + (2 * P) % 2);
-  pl.f64[0] = pl.f64[1] = 0;
-  pl.f64[2] = 1;
-  pl.k = 3;
-  return pl;
+  double* d = reinterpret_cast<double*>(c->planes);
+  return f64_planes(d, d + P, d + 2 * P, 3);
 }
 
 // ------------------------------------------------------------ kernels used by the pipeline only
@@ -691,8 +707,10 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
     int mw, mr, nt;
     int rc = sat_batch(c, L, lref, d, p->tile, p->quadrant_half, false, tl, nullptr, &sb, &mw, &mr, &nt);
     if (rc) return rc;
+    int maxpx = d[0].w * d[0].h;
+    launch_level_stats(sb, maxpx, s);
     launch_sat(sb, mw, mr, s);
-    launch_detect(sb, nt, DetectParams{p->tile, p->quadrant_half, p->threshold}, s);
+    launch_detect(sb, nt, detect_params(p->tile, p->quadrant_half, p->threshold), s);
   }
   probe(c, 1, 1);
   probe(c, 2, 0);
@@ -973,8 +991,9 @@ static int detect_one(hdr_ctx* c, const float* lum, int w, int h, int tile, doub
   int mw, mr, nt;
   int rc = sat_batch(c, 1, lv, d, tile, half, false, tl, nullptr, &sb, &mw, &mr, &nt);
   if (rc) return rc;
+  launch_level_stats(sb, w * h, c->stream);
   launch_sat(sb, mw, mr, c->stream);
-  launch_detect(sb, nt, DetectParams{tile, half, threshold}, c->stream);
+  launch_detect(sb, nt, detect_params(tile, half, threshold), c->stream);
   return HDR_OK;
 }
 
@@ -1250,4 +1269,5 @@ static void init_kernel_attributes() {
   hdr::init_densify_attributes();
   hdr::init_fusion_attributes();
   hdr::init_merge_attributes();
+  hdr::init_raster_attributes();
 }

@@ -20,6 +20,7 @@ struct MatchRow {
 void init_match_attributes();
 void init_densify_attributes();
 void init_fusion_attributes();
+void init_raster_attributes();
 
 // ---- k_raster.cu
 void launch_luma_hist(const float* rgb, int64_t n, float* lum, uint8_t* q,
@@ -51,13 +52,21 @@ struct SatLevel {
 struct SatBatch {
   SatLevel lv[5];
   int n;
+  // Exactness certificate per level (k_raster.cu K4): when every partial sum
+  // of numpy's cumsums is exactly representable, any summation order gives
+  // numpy's bits and the detector takes the tile-local path. null = never.
+  int32_t* qmin;   // min log2 quantum of the level's nonzero samples
+  double* sums;    // sum of the level's samples
 };
 struct DetectParams {
   int tile, half;
   double threshold;
+  int exact_ok;    // tile region fits the tile-local kernel's shared memory
 };
+void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s);
 void launch_sat(const SatBatch& b, int max_w, int max_rows, cudaStream_t s);
 void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s);
+size_t detect_exact_smem(int tile, int half);
 void launch_compact_corners(const TileCorner* tiles, int ntiles, double* corners,
                             int32_t* count, cudaStream_t s);
 

@@ -226,8 +226,59 @@ void launch_downsample2(const float* a, const float* b, int w, int h, float* oa,
 // colmap[X] (-1 = not needed); identity maps give the full table.
 constexpr int kSatPrefetch = 32;
 
+// Exactness certificate. Every partial sum numpy forms (image.py:42-43) and
+// every rect_sum difference (image.py:58) is a sum of a subset of the
+// level's samples. If all samples are multiples of 2^qmin and their total is
+// below 2^(52+qmin), all of those values are representable in f64, every
+// addition is exact, and ANY summation order reproduces numpy's bits.
+__device__ __forceinline__ int log2_quantum(float v) {
+  uint32_t u = __float_as_uint(v) & 0x7fffffffu;
+  if (u == 0) return 1 << 20;
+  uint32_t e = u >> 23, m = u & 0x7fffffu;
+  uint32_t M = e ? (m | 0x800000u) : m;
+  return (e ? (int)e - 150 : -149) + __ffs(M) - 1;
+}
+
+__device__ __forceinline__ bool level_exact(const SatBatch& b, int l) {
+  if (!b.qmin) return false;
+  double s = b.sums[l];
+  if (!(s > 0.0)) return s == 0.0;
+  int q = b.qmin[l];
+  // s * (1 + 2^-30) bounds the rounding of the f64 reduction itself
+  return ilogb(s * (1.0 + 9.3e-10)) + 1 <= 52 + q;
+}
+
+__global__ void __launch_bounds__(256) level_stats_kernel(SatBatch b) {
+  const SatLevel& L = b.lv[blockIdx.y];
+  int64_t n = (int64_t)L.w * L.h;
+  int qm = 1 << 20;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = L.img[i];
+    qm = min(qm, log2_quantum(v));
+    acc += (double)fabsf(v);
+  }
+  for (int off = 16; off; off >>= 1) {
+    qm = min(qm, __shfl_down_sync(0xffffffff, qm, off));
+    acc += __shfl_down_sync(0xffffffff, acc, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&b.qmin[blockIdx.y], qm);
+    atomicAdd(&b.sums[blockIdx.y], acc);
+  }
+}
+
+void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s) {
+  cudaMemsetAsync(b.sums, 0, sizeof(double) * 5, s);
+  cudaMemsetAsync(b.qmin, 0x3f, sizeof(int32_t) * 5, s);  // large positive
+  dim3 g(grid_for(max_pixels, 256), b.n);
+  level_stats_kernel<<<g, 256, 0, s>>>(b);
+}
+
 __global__ void __launch_bounds__(32) sat_cols_kernel(SatBatch b) {
   const SatLevel& L = b.lv[blockIdx.y];
+  if (level_exact(b, blockIdx.y)) return;  // the tile-local detector handles it
   int x = blockIdx.x * 32 + threadIdx.x;
   if (blockIdx.x * 32 >= L.w) return;
   bool live = x < L.w;
@@ -264,6 +315,7 @@ __global__ void __launch_bounds__(32) sat_cols_kernel(SatBatch b) {
 // next tile is prefetched into registers while the current one is scanned.
 __global__ void __launch_bounds__(32) sat_rows_kernel(SatBatch b) {
   const SatLevel& L = b.lv[blockIdx.y];
+  if (level_exact(b, blockIdx.y)) return;
   __shared__ double tile[32][33];
   int lane = threadIdx.x;
   int r0 = blockIdx.x * 32;
@@ -326,9 +378,12 @@ __device__ __forceinline__ double box(const LatticeView& v, int x0, int y0, int 
   return dadd(dsub(dsub(v.at(y1, x1), v.at(y0, x1)), v.at(y1, x0)), v.at(y0, x0));
 }
 
+template <bool EXACT>
 __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp) {
+  extern __shared__ double local_sat[];
   int lev = 0;
   while (lev + 1 < b.n && (int)blockIdx.x >= b.lv[lev + 1].tile_base) ++lev;
+  if ((dp.exact_ok && level_exact(b, lev)) != EXACT) return;
   const SatLevel& L = b.lv[lev];
   int w = L.w, h = L.h, tile = dp.tile, half = dp.half;
   int tiles_x = ceil_div(w, tile);
@@ -339,7 +394,33 @@ __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp
   int limx = min(tile, w - t0x), limy = min(tile, h - t0y);
   int nx = limx > first ? (limx - first + sp - 1) / sp : 0;
   int ny = limy > first ? (limy - first + sp - 1) / sp : 0;
+  // tile-local summed-area table (exact path): pixels [r0, r1) x [c0, c1)
+  int r0 = max(0, t0y - half), r1 = min(h, t0y + tile + half);
+  int c0 = max(0, t0x - half), c1 = min(w, t0x + tile + half);
+  int R = r1 - r0, C = c1 - c0, SW = C + 1;
+  if (EXACT) {
+    for (int i = threadIdx.x; i < (R + 1) * SW; i += blockDim.x) {
+      int r = i / SW, c = i % SW;
+      local_sat[i] = (r && c) ? (double)L.img[(int64_t)(r0 + r - 1) * w + (c0 + c - 1)] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 1 + threadIdx.x; r <= R; r += blockDim.x)
+      for (int c = 1; c <= C; ++c) local_sat[r * SW + c] += local_sat[r * SW + c - 1];
+    __syncthreads();
+    for (int c = 1 + threadIdx.x; c <= C; c += blockDim.x)
+      for (int r = 1; r <= R; ++r) local_sat[r * SW + c] += local_sat[(r - 1) * SW + c];
+    __syncthreads();
+  }
   LatticeView v{L.ltab, L.rowmap, L.colmap, L.ncols};
+  // ((t[y1,x1] - t[y0,x1]) - t[y1,x0]) + t[y0,x0]   (image.py:58)
+  auto box = [&](int x0, int y0, int x1, int y1) -> double {
+    if (EXACT) {
+      const double* S = local_sat;
+      int a0 = y0 - r0, a1 = y1 - r0, b0 = x0 - c0, b1 = x1 - c0;
+      return dadd(dsub(dsub(S[a1 * SW + b1], S[a0 * SW + b1]), S[a1 * SW + b0]), S[a0 * SW + b0]);
+    }
+    return dadd(dsub(dsub(v.at(y1, x1), v.at(y0, x1)), v.at(y1, x0)), v.at(y0, x0));
+  };
   double area = (double)(half * half);
   double best = -1.0;
   int best_i = 0x7fffffff;
@@ -347,10 +428,10 @@ __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp
     int lx = i % nx, ly = i / nx;
     int x = t0x + first + lx * sp, y = t0y + first + ly * sp;
     if (x < half || x > w - half || y < half || y > h - half) continue;
-    double tl = box(v, x - half, y - half, x, y) / area;
-    double tr = box(v, x, y - half, x + half, y) / area;
-    double br = box(v, x, y, x + half, y + half) / area;
-    double bl = box(v, x - half, y, x, y + half) / area;
+    double tl = box(x - half, y - half, x, y) / area;
+    double tr = box(x, y - half, x + half, y) / area;
+    double br = box(x, y, x + half, y + half) / area;
+    double bl = box(x - half, y, x, y + half) / area;
     double d0 = fabs(dsub(tr, tl)), d1 = fabs(dsub(br, tr));
     double d2 = fabs(dsub(bl, br)), d3 = fabs(dsub(tl, bl));
     double lo = fmin(fmin(d0, d1), fmin(d2, d3));
@@ -384,8 +465,17 @@ __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp
   }
 }
 
+size_t detect_exact_smem(int tile, int half) {
+  size_t side = (size_t)tile + 2 * (size_t)half + 1;
+  return side * side * sizeof(double);
+}
+
+void init_raster_attributes() { allow_max_dynamic_smem(detect_kernel<true>); }
+
 void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s) {
-  detect_kernel<<<total_tiles, 256, 0, s>>>(b, dp);
+  if (dp.exact_ok)
+    detect_kernel<true><<<total_tiles, 256, detect_exact_smem(dp.tile, dp.half), s>>>(b, dp);
+  detect_kernel<false><<<total_tiles, 256, 0, s>>>(b, dp);
 }
 
 __global__ void __launch_bounds__(1024) compact_corners_kernel(const TileCorner* __restrict__ tiles,

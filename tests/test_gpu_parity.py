@@ -84,6 +84,20 @@ def test_corners_matches_weeding_per_level(scene):
             assert rel_h(hf, fx[f"L{lev}_hfit"]) < 1e-9
 
 
+def test_corner_detector_both_sat_paths(cuda):
+    """The tile-local detector runs only under the exactness certificate;
+    tiny samples (real photos' dark pixels) break it and force numpy's
+    sequential lattice SAT. Both must reproduce the oracle bit for bit."""
+    st = synth.synth_stack(synth.working_spec(640, 480), 5)
+    lum = O.luminance(st.ref)
+    dark = lum.copy()
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, dark.size, 400)
+    dark.ravel()[idx] = np.float32(1e-9) * rng.random(400, dtype=np.float32)
+    for img in (lum, dark, (lum * np.float32(0.013)).astype(np.float32)):
+        np.testing.assert_array_equal(matcher.detect_corners(img), O.detect_corners(img))
+
+
 def test_fit_homography_and_inliers(cuda):
     rng = np.random.default_rng(3)
     for n in (4, 5, 9, 40, 300):

@@ -144,13 +144,13 @@ __device__ __forceinline__ double col_a(const float* g, int64_t w, int h, int y,
                                : 0.0;
 }
 
-// Aggregate layout per (chunk, column): [A, Q, R, B[K], Z0[K]]
+// Aggregates, field-major: agg[f][chunk][col], f = A, Q, R, B[K], Z0[K]
 template <int K>
 __global__ void __launch_bounds__(64) dt_cols_agg(const float* __restrict__ guide, DtPlanes P,
                                                   int w, int h, double ratio, double c,
                                                   double* __restrict__ agg) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int ch = blockIdx.y;
+  int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
   int r0 = ch * kColChunk, r1 = min(h, r0 + kColChunk);
   double y0[K], z0[K];
@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(64) dt_cols_agg(const float* __restrict__ guid
   for (int k = 0; k < K; ++k) { y0[k] = 0.0; z0[k] = 0.0; }
   double Pp = 1.0, R = 0.0, pref = 1.0;
   double a_prev = col_a(guide, w, h, r0 - 1, x, ratio, c);
+#pragma unroll 8
   for (int y = r0; y < r1; ++y) {
     int64_t i = (int64_t)y * w + x;
     Pp *= a_prev;
@@ -174,64 +175,73 @@ __global__ void __launch_bounds__(64) dt_cols_agg(const float* __restrict__ guid
     pref *= a;
     a_prev = a;
   }
-  double* o = agg + ((int64_t)ch * w + x) * (3 + 2 * K);
-  o[0] = Pp;
-  o[1] = pref;
-  o[2] = R;
+  int64_t F = (int64_t)nch * w, o = (int64_t)ch * w + x;
+  agg[o] = Pp;
+  agg[F + o] = pref;
+  agg[2 * F + o] = R;
 #pragma unroll
-  for (int k = 0; k < K; ++k) { o[3 + k] = y0[k]; o[3 + K + k] = z0[k]; }
+  for (int k = 0; k < K; ++k) { agg[(3 + k) * F + o] = y0[k]; agg[(3 + K + k) * F + o] = z0[k]; }
 }
 
-// carries per column: C_b (value above chunk b), D_b (value below chunk b)
+// carries per column, field-major carry[f][chunk][col]: C_b[K] (value above
+// chunk b), then D_b[K] (value below chunk b)
 template <int K>
 __global__ void dt_cols_link(int w, int nch, const double* __restrict__ agg,
                              double* __restrict__ carry) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= w) return;
-  const int S = 3 + 2 * K;
+  int64_t F = (int64_t)nch * w;
   double C[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) C[k] = 0.0;
+#pragma unroll 4
   for (int b = 0; b < nch; ++b) {
-    const double* a = agg + ((int64_t)b * w + x) * S;
-    double* o = carry + ((int64_t)b * w + x) * (2 * K);
+    int64_t o = (int64_t)b * w + x;
+    double A = agg[o];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      o[k] = C[k];
-      C[k] = a[0] * C[k] + a[3 + k];
+      carry[k * F + o] = C[k];
+      C[k] = A * C[k] + agg[(3 + k) * F + o];
     }
   }
   double D[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) D[k] = 0.0;
+#pragma unroll 4
   for (int b = nch - 1; b >= 0; --b) {
-    const double* a = agg + ((int64_t)b * w + x) * S;
-    double* o = carry + ((int64_t)b * w + x) * (2 * K);
+    int64_t o = (int64_t)b * w + x;
+    double Q = agg[F + o], R = agg[2 * F + o];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      o[K + k] = D[k];
-      D[k] = a[3 + K + k] + o[k] * a[2] + a[1] * D[k];  // z_s = Z0 + C*R + Q*D
+      carry[(K + k) * F + o] = D[k];
+      D[k] = agg[(3 + K + k) * F + o] + carry[k * F + o] * R + Q * D[k];  // z_s = Z0 + C*R + Q*D
     }
   }
 }
 
-// re-run each chunk from its carries with the reference update formula;
-// the forward result is parked in place (and the coefficients in `ascr`),
-// both L2-resident for the immediate backward sweep
+// Re-run each chunk from its carries with the reference update formula. The
+// forward values and the coefficients stay in shared memory (private to the
+// thread's column) for the backward sweep: HBM sees one read and one write.
+constexpr int kColThreads = 64;
+
 template <int K>
-__global__ void __launch_bounds__(64) dt_cols_apply(const float* __restrict__ guide, DtPlanes P,
-                                                    int w, int h, double ratio, double c,
-                                                    const double* __restrict__ carry,
-                                                    double* __restrict__ ascr) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int ch = blockIdx.y;
+__global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __restrict__ guide,
+                                                             DtPlanes P, int w, int h,
+                                                             double ratio, double c,
+                                                             const double* __restrict__ carry) {
+  extern __shared__ double colbuf[];  // [K + 1][kColChunk][kColThreads]
+  int tx = threadIdx.x;
+  int x = blockIdx.x * blockDim.x + tx;
+  int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
   int r0 = ch * kColChunk, r1 = min(h, r0 + kColChunk);
-  const double* cr = carry + ((int64_t)ch * w + x) * (2 * K);
+  int64_t F = (int64_t)nch * w, o = (int64_t)ch * w + x;
+  auto Y = [&](int k, int r) -> double& { return colbuf[(k * kColChunk + r) * kColThreads + tx]; };
   double prev[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) prev[k] = cr[k];
+  for (int k = 0; k < K; ++k) prev[k] = carry[k * F + o];
   double a_prev = col_a(guide, w, h, r0 - 1, x, ratio, c);
+#pragma unroll 8
   for (int y = r0; y < r1; ++y) {
     int64_t i = (int64_t)y * w + x;
 #pragma unroll
@@ -239,20 +249,21 @@ __global__ void __launch_bounds__(64) dt_cols_apply(const float* __restrict__ gu
       double xv = ldp(P, k, i);
       double v = xv + a_prev * (prev[k] - xv);
       prev[k] = v;
-      stp(P, k, i, v);  // forward result parked in place for the backward sweep
+      Y(k, y - r0) = v;
     }
     double a = col_a(guide, w, h, y, x, ratio, c);
-    ascr[i] = a;
+    Y(K, y - r0) = a;
     a_prev = a;
   }
 #pragma unroll
-  for (int k = 0; k < K; ++k) prev[k] = cr[K + k];
+  for (int k = 0; k < K; ++k) prev[k] = carry[(K + k) * F + o];
+#pragma unroll 8
   for (int y = r1 - 1; y >= r0; --y) {
     int64_t i = (int64_t)y * w + x;
-    double a = ascr[i];
+    double a = Y(K, y - r0);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      double yv = ldp(P, k, i);
+      double yv = Y(k, y - r0);
       double v = yv + a * (prev[k] - yv);
       prev[k] = v;
       stp(P, k, i, v);
@@ -270,16 +281,16 @@ static void dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
   int nch = ceil_div(h, kColChunk);
   double* agg = scratch;
   double* carry = agg + (int64_t)nch * w * (3 + 2 * K);
-  double* ascr = carry + (int64_t)nch * w * (2 * K);
-  dim3 cg(ceil_div(w, 64), nch);
+  dim3 cg(ceil_div(w, kColThreads), nch);
+  size_t col_smem = (size_t)(K + 1) * kColChunk * kColThreads * sizeof(double);
   for (int i = 1; i <= passes; ++i) {
     double sigma_i = sigma_s * sqrt(3.0) * pow(2.0, passes - i) / den;  // densify.py:104
     double c = -root / sigma_i;
     if (w > 1) dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
     if (h > 1) {
-      dt_cols_agg<K><<<cg, 64, 0, s>>>(guide, P, w, h, ratio, c, agg);
-      dt_cols_link<K><<<ceil_div(w, 128), 128, 0, s>>>(w, nch, agg, carry);
-      dt_cols_apply<K><<<cg, 64, 0, s>>>(guide, P, w, h, ratio, c, carry, ascr);
+      dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
+      dt_cols_link<K><<<ceil_div(w, 64), 64, 0, s>>>(w, nch, agg, carry);
+      dt_cols_apply<K><<<cg, kColThreads, col_smem, s>>>(guide, P, w, h, ratio, c, carry);
     }
   }
 }
@@ -293,6 +304,9 @@ void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_kernel<1>);
   allow_max_dynamic_smem(dt_rows_kernel<2>);
   allow_max_dynamic_smem(dt_rows_kernel<3>);
+  allow_max_dynamic_smem(dt_cols_apply<1>);
+  allow_max_dynamic_smem(dt_cols_apply<2>);
+  allow_max_dynamic_smem(dt_cols_apply<3>);
 }
 
 void launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,

@@ -53,17 +53,17 @@ __global__ void __launch_bounds__(kSsimTW * 8) ssim_kernel(
     int oy = i / EW, lx = i % EW;
     int c = (oy + r) * EW + lx;
     double va = sa[c], vb = sb[c];
-    double m0 = dmul(va, k[r]), m1 = dmul(vb, k[r]);
-    double m2 = dmul(dmul(va, va), k[r]), m3 = dmul(dmul(vb, vb), k[r]);
-    double m4 = dmul(dmul(va, vb), k[r]);
+    // FMA-contracted (the SSIM bar is 1e-4; scipy's exact order is not needed)
+    double m0 = va * k[r], m1 = vb * k[r];
+    double m2 = (va * va) * k[r], m3 = (vb * vb) * k[r], m4 = (va * vb) * k[r];
     for (int j = r; j >= 1; --j) {
       double ua = sa[c - j * EW], ub = sb[c - j * EW], da = sa[c + j * EW], db = sb[c + j * EW];
       double kj = k[r + j];
-      m0 = dadd(m0, dmul(dadd(ua, da), kj));
-      m1 = dadd(m1, dmul(dadd(ub, db), kj));
-      m2 = dadd(m2, dmul(dadd(dmul(ua, ua), dmul(da, da)), kj));
-      m3 = dadd(m3, dmul(dadd(dmul(ub, ub), dmul(db, db)), kj));
-      m4 = dadd(m4, dmul(dadd(dmul(ua, ub), dmul(da, db)), kj));
+      m0 = fma(ua + da, kj, m0);
+      m1 = fma(ub + db, kj, m1);
+      m2 = fma(fma(ua, ua, da * da), kj, m2);
+      m3 = fma(fma(ub, ub, db * db), kj, m3);
+      m4 = fma(fma(ua, ub, da * db), kj, m4);
     }
     V[0 * SV + i] = m0; V[1 * SV + i] = m1; V[2 * SV + i] = m2; V[3 * SV + i] = m3;
     V[4 * SV + i] = m4;
@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(kSsimTW * 8) ssim_kernel(
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
       const double* row = V + q * SV;
-      double acc = dmul(row[c], k[r]);
-      for (int j = r; j >= 1; --j) acc = dadd(acc, dmul(dadd(row[c - j], row[c + j]), k[r + j]));
+      double acc = row[c] * k[r];
+      for (int j = r; j >= 1; --j) acc = fma(row[c - j] + row[c + j], k[r + j], acc);
       m[q] = acc;
     }
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;

@@ -174,9 +174,12 @@ static size_t ssd_smem(int radius, int patch) {
 
 constexpr int kSsdMaxSmem = 200 * 1024;
 
+static void init_finish_attributes();
+
 void init_match_attributes() {
   allow_max_dynamic_smem(ssd_tiles_kernel);
   allow_max_dynamic_smem(ssd_points_kernel);
+  init_finish_attributes();
 }
 
 void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref, const float* src,
@@ -338,6 +341,21 @@ void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w
 }
 
 // ---------------------------------------------------------------- K8
+constexpr int kFitCache = 4096;  // weeded points held in shared memory by finish_level
+
+// entry k of DLT row r (0 or 1) of correspondence p -> q (geometry.py:51-63)
+__device__ __forceinline__ double dlt_entry(int r, int k, double px, double py, double qx,
+                                            double qy) {
+  int lo = r ? 3 : 0;
+  if (k == lo) return -px;
+  if (k == lo + 1) return -py;
+  if (k == lo + 2) return -1.0;
+  double q = r ? qy : qx;
+  if (k == 6) return px * q;
+  if (k == 7) return py * q;
+  if (k == 8) return q;
+  return 0.0;
+}
 // Block-wide least-squares DLT (geometry.fit_homography for n >= 4) over
 // points fetched by `get(i, p)` (p = ref x, ref y, src x, src y).
 template <class Get>
@@ -423,10 +441,10 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     for (int i = lane; i < n; i += 32) {
       double p[4];
       get(i, p);
-      double r0[9], r1[9];
-      dlt_rows((p[0] - bc[0]) * tr[0], (p[1] - bc[1]) * tr[0], (p[2] - bc[2]) * ts[0],
-               (p[3] - bc[3]) * ts[0], r0, r1);
-      acc += r0[ea] * r0[eb] + r1[ea] * r1[eb];
+      double px = (p[0] - bc[0]) * tr[0], py = (p[1] - bc[1]) * tr[0];
+      double qx = (p[2] - bc[2]) * ts[0], qy = (p[3] - bc[3]) * ts[0];
+      acc += dlt_entry(0, ea, px, py, qx, qy) * dlt_entry(0, eb, px, py, qx, qy) +
+             dlt_entry(1, ea, px, py, qx, qy) * dlt_entry(1, eb, px, py, qx, qy);
     }
     for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffff, acc, off);
     if (lane == 0) gsh[e] = acc;
@@ -452,9 +470,11 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     int32_t* __restrict__ weeded_count, int64_t* __restrict__ kept_idx,
     double* __restrict__ hpred, double* __restrict__ homography, int32_t* __restrict__ info,
     double* __restrict__ out_matches, double* __restrict__ out_raw, int32_t* grey) {
+  extern __shared__ double pts_cache[];  // normalised (rx, ry, sx, sy) of the weeded set
   __shared__ int scratch[32];
   int n = *raw_count;
   int m = 0;
+  bool cached = n <= kFitCache;
   if (n >= 4) {
     for (int c0 = 0; c0 < n; c0 += blockDim.x) {
       int i = c0 + threadIdx.x;
@@ -463,6 +483,7 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
       int pos = block_exclusive_scan(f, scratch, &total);
       if (f) {
         weeded[m + pos] = raw[i];
+        if (cached) norm_row(raw[i], w, h, pts_cache + 4 * (m + pos));
         if (kept_idx) kept_idx[m + pos] = i;
         if (out_matches)
           for (int k = 0; k < 5; ++k) out_matches[5 * (int64_t)(m + pos) + k] = raw[i].v[k];
@@ -481,8 +502,15 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
   if (m < 4) return;
   __shared__ double Hs[9];
   const MatchRow* wr = weeded;
-  auto get = [&](int i, double* p) { norm_row(wr[i], w, h, p); };
-  __syncthreads();  // weeded rows visible block-wide
+  auto get = [&](int i, double* p) {
+    if (cached) {
+      const double* q = pts_cache + 4 * i;
+      p[0] = q[0]; p[1] = q[1]; p[2] = q[2]; p[3] = q[3];
+    } else {
+      norm_row(wr[i], w, h, p);
+    }
+  };
+  __syncthreads();  // weeded rows / cached points visible block-wide
   int st = block_fit(m, get, Hs, grey);
   if (threadIdx.x == 0 && st == 0) {
     for (int k = 0; k < 9; ++k) hpred[k] = Hs[k];
@@ -498,7 +526,7 @@ void launch_finish_level(const MatchRow* raw, const int32_t* raw_count, const ui
                          int64_t* kept_idx, double* hpred, double* homography, int32_t* info,
                          double* out_matches, double* out_raw, int32_t* grey, cudaStream_t s) {
   (void)out_raw;
-  finish_level_kernel<<<1, 256, 0, s>>>(raw, raw_count, mask, w, h, level, weeded, weeded_count,
+  finish_level_kernel<<<1, 256, kFitCache * 4 * sizeof(double), s>>>(raw, raw_count, mask, w, h, level, weeded, weeded_count,
                                         kept_idx, hpred, homography, info, out_matches, out_raw,
                                         grey);
 }
@@ -578,5 +606,7 @@ __global__ void set_identity_kernel(double* h) {
 }
 
 void launch_set_identity(double* h, cudaStream_t s) { set_identity_kernel<<<1, 32, 0, s>>>(h); }
+
+static void init_finish_attributes() { allow_max_dynamic_smem(finish_level_kernel); }
 
 }  // namespace hdr

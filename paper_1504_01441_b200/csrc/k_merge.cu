@@ -29,14 +29,19 @@ __device__ __forceinline__ float lum_f(float r, float g, float b) {
   return fminf(fmaxf(y, 0.0f), 1.0f);
 }
 
-// contrast x saturation x well-exposedness (f32); lap = 4-neighbour laplacian
-__device__ __forceinline__ float quality_f(float lap, float r, float g, float b) {
-  float mean = (r + g + b) * (1.0f / 3.0f);
-  float dr = r - mean, dg = g - mean, db = b - mean;
-  float sat = sqrtf((dr * dr + dg * dg + db * db) * (1.0f / 3.0f));
+// contrast x saturation x well-exposedness + 1e-12 (fusion.py:67-77).
+// The laplacian and the channel std stay f64 as in the reference: for grey or
+// clipped pixels the true std is exactly 0 there, while f32 rounding of the
+// mean leaves ~1e-8 of std, which outweighs the 1e-12 floor and changes the
+// blend weights completely. Only the exposedness exponential is f32.
+__device__ __forceinline__ double quality_d(double lap, float r, float g, float b) {
+  double R = r, G = g, B = b;
+  double mean = ((R + G) + B) / 3.0;
+  double dr = R - mean, dg = G - mean, db = B - mean;
+  double sat = sqrt(((dr * dr + dg * dg) + db * db) / 3.0);
   float er = r - 0.5f, eg = g - 0.5f, eb = b - 0.5f;
-  float ex = expf(-(er * er + eg * eg + eb * eb) * (1.0f / 0.08f));
-  return fabsf(lap) * sat * ex + 1e-12f;
+  double ex = (double)expf(-(er * er + eg * eg + eb * eb) * (1.0f / 0.08f));
+  return fabs(lap) * sat * ex + 1e-12;
 }
 
 // ---------------------------------------------------------------- weights + level 1
@@ -75,18 +80,20 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   for (int i = tid; i < kRT * kRT; i += nt) {
     int ty = i / kRT, tx = i % kRT;
     int ly = ty + 1, lx = tx + 1;
-    float lapr = (lr[ly - 1][lx] + lr[ly + 1][lx] - 2.0f * lr[ly][lx]) +
-                 (lr[ly][lx - 1] + lr[ly][lx + 1] - 2.0f * lr[ly][lx]);
-    float lapw = (lw[ly - 1][lx] + lw[ly + 1][lx] - 2.0f * lw[ly][lx]) +
-                 (lw[ly][lx - 1] + lw[ly][lx + 1] - 2.0f * lw[ly][lx]);
-    float qr = quality_f(lapr, px[0][ty][tx], px[1][ty][tx], px[2][ty][tx]);
-    float qs = quality_f(lapw, px[3][ty][tx], px[4][ty][tx], px[5][ty][tx]);
+    // ndimage.laplace: [1,-2,1] along axis 0, += along axis 1 (exact in f64)
+    double cr = lr[ly][lx], cw = lw[ly][lx];
+    double lapr = ((double)lr[ly - 1][lx] + lr[ly + 1][lx] - 2.0 * cr) +
+                  ((double)lr[ly][lx - 1] + lr[ly][lx + 1] - 2.0 * cr);
+    double lapw = ((double)lw[ly - 1][lx] + lw[ly + 1][lx] - 2.0 * cw) +
+                  ((double)lw[ly][lx - 1] + lw[ly][lx + 1] - 2.0 * cw);
+    double qr = quality_d(lapr, px[0][ty][tx], px[1][ty][tx], px[2][ty][tx]);
+    double qs = quality_d(lapw, px[3][ty][tx], px[4][ty][tx], px[5][ty][tx]);
     int gy = reflect_index(vy0 + ly, h), gx = reflect_index(vx0 + lx, w);
     int64_t p = (int64_t)gy * w + gx;
-    float sv = fminf(fmaxf(ssim[p], 0.0f), 1.0f);
-    qs = valid[p] ? qs * sv : 0.0f;
-    float tot = qr + qs;
-    float a = qr / tot, b = qs / tot;
+    double sv = fmin(fmax((double)ssim[p], 0.0), 1.0);
+    qs = valid[p] ? qs * sv : 0.0;
+    double tot = qr + qs;
+    float a = (float)(qr / tot), b = (float)(qs / tot);
     px[6][ty][tx] = a;
     px[7][ty][tx] = b;
     // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image

@@ -263,7 +263,13 @@ __global__ void __launch_bounds__(256) level_stats_kernel(SatBatch b) {
     qm = min(qm, __shfl_down_sync(0xffffffff, qm, off));
     acc += __shfl_down_sync(0xffffffff, acc, off);
   }
-  if ((threadIdx.x & 31) == 0) {
+  __shared__ int sq[8];
+  __shared__ double sa[8];
+  int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sq[warp] = qm; sa[warp] = acc; }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one atomic pair per block
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) { qm = min(qm, sq[k]); acc += sa[k]; }
     atomicMin(&b.qmin[blockIdx.y], qm);
     atomicAdd(&b.sums[blockIdx.y], acc);
   }

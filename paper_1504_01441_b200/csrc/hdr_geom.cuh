@@ -291,43 +291,43 @@ HD int fit4(const double* px_in, const double* py_in, const double* qx_in,
     dlt_rows(px[i], py[i], qx[i], qy[i], r0, r1);
     for (int k = 0; k < 9; ++k) { M[k][2 * i] = r0[k]; M[k][2 * i + 1] = r1[k]; }
   }
-  double V[8][9];  // Householder vectors (entries k..8 used)
+  // Fully unrolled so every index is static and M lives in registers; the
+  // Householder vector of step k is kept in M[k..8][k], R's diagonal in rdiag.
   double beta[8], rdiag[8];
-  double cn[8];
-  for (int c = 0; c < 8; ++c) {
-    double acc = 0.0;
-    for (int k = 0; k < 9; ++k) acc += M[k][c] * M[k][c];
-    cn[c] = acc;
-  }
+#pragma unroll
   for (int k = 0; k < 8; ++k) {
+    double best = -1.0;
     int piv = k;
-    for (int c = k + 1; c < 8; ++c)
-      if (cn[c] > cn[piv]) piv = c;
-    if (piv != k) {
-      for (int r = 0; r < 9; ++r) { double t = M[r][k]; M[r][k] = M[r][piv]; M[r][piv] = t; }
-      double t = cn[k]; cn[k] = cn[piv]; cn[piv] = t;
+#pragma unroll
+    for (int c = k; c < 8; ++c) {
+      double cn = 0.0;
+#pragma unroll
+      for (int r = k; r < 9; ++r) cn += M[r][c] * M[r][c];
+      if (cn > best) { best = cn; piv = c; }
     }
-    double nrm = 0.0;
-    for (int r = k; r < 9; ++r) nrm += M[r][k] * M[r][k];
-    nrm = sqrt(nrm);
+#pragma unroll
+    for (int c = k + 1; c < 8; ++c)
+      if (c == piv) {
+#pragma unroll
+        for (int r = 0; r < 9; ++r) { double t = M[r][k]; M[r][k] = M[r][c]; M[r][c] = t; }
+      }
+    double nrm = sqrt(best);
     double alpha = (M[k][k] > 0.0) ? -nrm : nrm;
-    for (int r = 0; r < 9; ++r) V[k][r] = (r >= k) ? M[r][k] : 0.0;
-    V[k][k] -= alpha;
+    M[k][k] -= alpha;
     double vv = 0.0;
-    for (int r = k; r < 9; ++r) vv += V[k][r] * V[k][r];
+#pragma unroll
+    for (int r = k; r < 9; ++r) vv += M[r][k] * M[r][k];
     beta[k] = (vv > 0.0) ? 2.0 / vv : 0.0;
     rdiag[k] = alpha;
+#pragma unroll
     for (int c = k + 1; c < 8; ++c) {
       double d = 0.0;
-      for (int r = k; r < 9; ++r) d += V[k][r] * M[r][c];
+#pragma unroll
+      for (int r = k; r < 9; ++r) d += M[r][k] * M[r][c];
       d *= beta[k];
-      for (int r = k; r < 9; ++r) M[r][c] -= d * V[k][r];
-      double rem = 0.0;
-      for (int r = k + 1; r < 9; ++r) rem += M[r][c] * M[r][c];
-      cn[c] = rem;
+#pragma unroll
+      for (int r = k; r < 9; ++r) M[r][c] -= d * M[r][k];
     }
-    M[k][k] = alpha;
-    for (int r = k + 1; r < 9; ++r) M[r][k] = 0.0;
   }
   double ratio = fabs(rdiag[6]) / fabs(rdiag[0]);
   bool degenerate = !(ratio > 1e-9);
@@ -335,7 +335,7 @@ HD int fit4(const double* px_in, const double* py_in, const double* qx_in,
     // grey zone: exact singular values of R (8x8 upper) decide
     double R[64], s[8];
     for (int i = 0; i < 8; ++i)
-      for (int j = 0; j < 8; ++j) R[i * 8 + j] = (j >= i) ? M[i][j] : 0.0;
+      for (int j = 0; j < 8; ++j) R[i * 8 + j] = (j > i) ? M[i][j] : (j == i ? rdiag[i] : 0.0);
     jacobi_singular_values(R, 8, s);
     degenerate = s[6] <= 1e-9 * s[0];
     if (grey) ++*grey;
@@ -343,11 +343,14 @@ HD int fit4(const double* px_in, const double* py_in, const double* qx_in,
   if (degenerate) return 2;
   // null vector = Q e_9 = H0 H1 ... H7 e_9
   double y[9] = {0, 0, 0, 0, 0, 0, 0, 0, 1.0};
+#pragma unroll
   for (int k = 7; k >= 0; --k) {
     double d = 0.0;
-    for (int r = k; r < 9; ++r) d += V[k][r] * y[r];
+#pragma unroll
+    for (int r = k; r < 9; ++r) d += M[r][k] * y[r];
     d *= beta[k];
-    for (int r = k; r < 9; ++r) y[r] -= d * V[k][r];
+#pragma unroll
+    for (int r = k; r < 9; ++r) y[r] -= d * M[r][k];
   }
   return finish_h(y, tr, ts, H);
 }
@@ -402,38 +405,58 @@ HD void jacobi_eig9(double* a, double* w, double* v) {
 // rank estimate (d7 ~ lambda7 within a small factor).
 HD int fit_from_gram(const double* g45, const double* tr, const double* ts, double* H,
                      int* grey) {
+  // every loop below has static bounds and is unrolled, so `a` stays in
+  // registers; the symmetric pivot swap is a predicated select over the
+  // candidates
   double a[9][9];
-  int k = 0;
   double dmax = 0.0;
-  for (int i = 0; i < 9; ++i)
-    for (int j = i; j < 9; ++j) { a[i][j] = g45[k]; a[j][i] = g45[k]; ++k; }
+  {
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = i; j < 9; ++j) { a[i][j] = g45[k]; a[j][i] = g45[k]; ++k; }
+  }
+#pragma unroll
   for (int i = 0; i < 9; ++i) dmax = fmax(dmax, a[i][i]);
 #ifdef HDR_DEBUG_FIT
-  printf("gram in: g0=%g g1=%g g44=%g dmax=%g tr=%g %g %g ts=%g %g %g\n", g45[0], g45[1], g45[44],
-         dmax, tr[0], tr[1], tr[2], ts[0], ts[1], ts[2]);
+  printf("gram in: g0=%g g1=%g g44=%g dmax=%g\n", g45[0], g45[1], g45[44], dmax);
 #endif
   if (!(dmax > 0.0)) return 2;
   double sigma = 1e-13 * dmax;
+#pragma unroll
   for (int i = 0; i < 9; ++i) a[i][i] += sigma;
   int perm[9];
+#pragma unroll
   for (int i = 0; i < 9; ++i) perm[i] = i;
-  double piv[9];
+  double piv[9], il[9];
+#pragma unroll
   for (int c = 0; c < 9; ++c) {
     int p = c;
+    double best = a[c][c];
+#pragma unroll
     for (int i = c + 1; i < 9; ++i)
-      if (a[i][i] > a[p][p]) p = i;
-    if (p != c) {
-      for (int j = 0; j < 9; ++j) { double t = a[c][j]; a[c][j] = a[p][j]; a[p][j] = t; }
-      for (int j = 0; j < 9; ++j) { double t = a[j][c]; a[j][c] = a[j][p]; a[j][p] = t; }
-      int t = perm[c]; perm[c] = perm[p]; perm[p] = t;
-    }
+      if (a[i][i] > best) { best = a[i][i]; p = i; }
+#pragma unroll
+    for (int q = c + 1; q < 9; ++q)
+      if (q == p) {
+#pragma unroll
+        for (int j = 0; j < 9; ++j) { double t = a[c][j]; a[c][j] = a[q][j]; a[q][j] = t; }
+#pragma unroll
+        for (int j = 0; j < 9; ++j) { double t = a[j][c]; a[j][c] = a[j][q]; a[j][q] = t; }
+        int t = perm[c]; perm[c] = perm[q]; perm[q] = t;
+      }
     double d = a[c][c];
     piv[c] = d;
     if (!(d > 0.0)) return 2;
     double l = sqrt(d);
     a[c][c] = l;
-    for (int i = c + 1; i < 9; ++i) a[i][c] /= l;
+    il[c] = 1.0 / l;
+#pragma unroll
+    for (int i = c + 1; i < 9; ++i) a[i][c] *= il[c];
+#pragma unroll
     for (int i = c + 1; i < 9; ++i)
+#pragma unroll
       for (int j = c + 1; j <= i; ++j) {
         a[i][j] -= a[i][c] * a[j][c];
         a[j][i] = a[i][j];
@@ -443,44 +466,47 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
   // ~1e-7 relative singular values; d7 - sigma estimates s7^2
   double s7sq = fmax(piv[7] - sigma, 0.0), s0sq = piv[0] - sigma;
   if (grey && s7sq > 1e-13 * s0sq && s7sq < 1e-10 * s0sq) ++*grey;
-#ifdef HDR_DEBUG_FIT
-  printf("gram: dmax=%g piv0=%g piv7=%g piv8=%g ratio=%g\n", dmax, piv[0], piv[7], piv[8], s7sq / s0sq);
-#endif
   if (s7sq <= 1e-13 * s0sq) return 2;
   double v[9], y[9];
+#pragma unroll
   for (int i = 0; i < 9; ++i) v[i] = 1.0 / 3.0;
-  for (int it = 0, settled = 0; it < 100 && settled < 2; ++it) {
+  for (int it = 0; it < 60; ++it) {
+#pragma unroll
     for (int i = 0; i < 9; ++i) {  // L y = v
       double s = v[i];
+#pragma unroll
       for (int j = 0; j < i; ++j) s -= a[i][j] * y[j];
-      y[i] = s / a[i][i];
+      y[i] = s * il[i];
     }
+#pragma unroll
     for (int i = 8; i >= 0; --i) {  // L^T z = y (z into y)
       double s = y[i];
+#pragma unroll
       for (int j = i + 1; j < 9; ++j) s -= a[j][i] * y[j];
-      y[i] = s / a[i][i];
+      y[i] = s * il[i];
     }
-    double nrm = 0.0;
-    for (int i = 0; i < 9; ++i) nrm += y[i] * y[i];
+    double nrm = 0.0, sgn = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) { nrm += y[i] * y[i]; sgn += y[i] * v[i]; }
     nrm = 1.0 / sqrt(nrm);
-    double sgn = 0.0;
-    for (int i = 0; i < 9; ++i) sgn += y[i] * v[i];
     if (sgn < 0) nrm = -nrm;
     double diff = 0.0;
+#pragma unroll
     for (int i = 0; i < 9; ++i) {
       double z = y[i] * nrm;
       diff = fmax(diff, fabs(z - v[i]));
       v[i] = z;
     }
-    if (diff < 1e-15) ++settled;
+    if (diff < 4e-15) break;
   }
   double hc[9];
-  for (int i = 0; i < 9; ++i) hc[perm[i]] = v[i];
-#ifdef HDR_DEBUG_FIT
-  int fr = finish_h(hc, tr, ts, H);
-  printf("gram: hc = %g %g %g %g %g %g %g %g %g -> %d\n", hc[0], hc[1], hc[2], hc[3], hc[4], hc[5], hc[6], hc[7], hc[8], fr);
-  return fr;
-#endif
+#pragma unroll
+  for (int i = 0; i < 9; ++i) hc[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+      if (perm[i] == j) hc[j] = v[i];
   return finish_h(hc, tr, ts, H);
 }
 

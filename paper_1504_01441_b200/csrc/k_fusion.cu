@@ -93,13 +93,105 @@ __global__ void __launch_bounds__(kSsimTW * 8) ssim_kernel(
   }
 }
 
+template <int R>
+__global__ void ssim_fixed_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                  const uint8_t* __restrict__ qb, const float* __restrict__ lut_b,
+                                  int w, int h, const double* __restrict__ taps,
+                                  float* __restrict__ out);
+
 void init_fusion_attributes() {
+  allow_max_dynamic_smem(ssim_fixed_kernel<5>);
   allow_max_dynamic_smem(ssim_kernel);
+}
+
+// Specialised for a compile-time radius (the default 11-tap window): 32x32
+// outputs per 32x8 block, each thread owning one column and 4 rows, so all
+// tap loops unroll and no index needs a division.
+constexpr int kS2 = 32;
+
+template <int R>
+__global__ void __launch_bounds__(256) ssim_fixed_kernel(
+    const float* __restrict__ a, const float* __restrict__ b, const uint8_t* __restrict__ qb,
+    const float* __restrict__ lut_b, int w, int h, const double* __restrict__ taps,
+    float* __restrict__ out) {
+  constexpr int E = kS2 + 2 * R;  // staged rows/cols incl. halo
+  __shared__ float sa[E][E + 1], sb[E][E + 1];
+  __shared__ int rows[E], cols[E];
+  __shared__ float lut[kBins];
+  extern __shared__ double V[];  // [5][kS2][E]
+  int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  int x0 = blockIdx.x * kS2 - R, y0 = blockIdx.y * kS2 - R;
+  double k[2 * R + 1];
+#pragma unroll
+  for (int j = 0; j <= 2 * R; ++j) k[j] = taps[j];
+  if (tid < E) { rows[tid] = reflect_index(y0 + tid, h); cols[tid] = reflect_index(x0 + tid, w); }
+  if (qb)
+    for (int i = tid; i < kBins; i += 256) lut[i] = lut_b[i];
+  __syncthreads();
+  for (int r = ty; r < E; r += 8) {
+    int64_t rowoff = (int64_t)rows[r] * w;
+    for (int c = tx; c < E; c += 32) {
+      int64_t p = rowoff + cols[c];
+      sa[r][c] = a[p];
+      sb[r][c] = qb ? lut[qb[p]] : b[p];
+    }
+  }
+  __syncthreads();
+  // vertical (axis 0): V[m][oy][c] for the 32 output rows, all E columns
+  for (int c = tx; c < E; c += 32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int oy = ty + 8 * q;
+      double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+#pragma unroll
+      for (int j = 0; j <= 2 * R; ++j) {
+        double va = sa[oy + j][c], vb = sb[oy + j][c];
+        m0 = fma(va, k[j], m0);
+        m1 = fma(vb, k[j], m1);
+        m2 = fma(va * va, k[j], m2);
+        m3 = fma(vb * vb, k[j], m3);
+        m4 = fma(va * vb, k[j], m4);
+      }
+      V[(0 * kS2 + oy) * E + c] = m0;
+      V[(1 * kS2 + oy) * E + c] = m1;
+      V[(2 * kS2 + oy) * E + c] = m2;
+      V[(3 * kS2 + oy) * E + c] = m3;
+      V[(4 * kS2 + oy) * E + c] = m4;
+    }
+  }
+  __syncthreads();
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  int gx = blockIdx.x * kS2 + tx;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int oy = ty + 8 * q, gy = blockIdx.y * kS2 + oy;
+    double m[5];
+#pragma unroll
+    for (int mm = 0; mm < 5; ++mm) {
+      const double* row = V + (mm * kS2 + oy) * E + tx;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j <= 2 * R; ++j) acc = fma(row[j], k[j], acc);
+      m[mm] = acc;
+    }
+    if (gx >= w || gy >= h) continue;
+    double mu_a = m[0], mu_b = m[1];
+    double var_a = m[2] - mu_a * mu_a, var_b = m[3] - mu_b * mu_b, cov = m[4] - mu_a * mu_b;
+    double sc = ((2.0 * mu_a * mu_b + C1) * (2.0 * cov + C2)) /
+                ((mu_a * mu_a + mu_b * mu_b + C1) * (var_a + var_b + C2));
+    out[(int64_t)gy * w + gx] = (float)fmin(fmax(sc, -1.0), 1.0);
+  }
 }
 
 void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb, const float* lut_b,
                  int w, int h, int window, const double* taps, float* out, cudaStream_t s) {
   int r = window / 2;
+  if (r == 5) {
+    size_t vb = 5 * (size_t)kS2 * (kS2 + 10) * sizeof(double);
+    dim3 grd(ceil_div(w, kS2), ceil_div(h, kS2));
+    ssim_fixed_kernel<5><<<grd, dim3(32, 8), vb, s>>>(a, b_or_null, qb, lut_b, w, h, taps, out);
+    return;
+  }
   int EW = kSsimTW + 2 * r, EH = kSsimTH + 2 * r;
   size_t bytes = ((2 * EH * EW + 1) / 2) * sizeof(double) + 5 * (size_t)kSsimTH * EW * sizeof(double);
   dim3 grd(ceil_div(w, kSsimTW), ceil_div(h, kSsimTH));

@@ -31,16 +31,17 @@ __device__ __forceinline__ float lum_f(float r, float g, float b) {
 
 // contrast x saturation x well-exposedness + 1e-12 (fusion.py:67-77).
 // The laplacian and the channel std stay f64 as in the reference: for grey or
-// clipped pixels the true std is exactly 0 there, while f32 rounding of the
-// mean leaves ~1e-8 of std, which outweighs the 1e-12 floor and changes the
-// blend weights completely. Only the exposedness exponential is f32.
+// clipped pixels the true std is exactly 0 there (3v * (1/3) rounds back to v),
+// while an f32 mean leaves ~1e-8 of std, which outweighs the 1e-12 floor and
+// changes the blend weights completely. Only the exposedness exp is f32.
 __device__ __forceinline__ double quality_d(double lap, float r, float g, float b) {
+  const double third = 1.0 / 3.0;
   double R = r, G = g, B = b;
-  double mean = ((R + G) + B) / 3.0;
+  double mean = ((R + G) + B) * third;
   double dr = R - mean, dg = G - mean, db = B - mean;
-  double sat = sqrt(((dr * dr + dg * dg) + db * db) / 3.0);
+  double sat = sqrt(((dr * dr + dg * dg) + db * db) * third);
   float er = r - 0.5f, eg = g - 0.5f, eb = b - 0.5f;
-  double ex = (double)expf(-(er * er + eg * eg + eb * eb) * (1.0f / 0.08f));
+  double ex = (double)__expf(-(er * er + eg * eg + eb * eb) * 12.5f);
   return fabs(lap) * sat * ex + 1e-12;
 }
 
@@ -59,13 +60,18 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   // ref rgb, warped rgb, w_ref, w_src
   float (*px)[kRT][kRT + 1] = reinterpret_cast<float (*)[kRT][kRT + 1]>(smf + 2 * kLT * kLT);
   float (*V)[kOT][kRT] = reinterpret_cast<float (*)[kOT][kRT]>(smf + 2 * kLT * kLT + 8 * kRT * (kRT + 1));
+  __shared__ int ridx[kLT], cidx[kLT];
   int tid = threadIdx.x, nt = blockDim.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
   int vy0 = 2 * Y0 - 3, vx0 = 2 * X0 - 3;  // virtual origin of the 38x38 lum tile
+  if (tid < kLT) {
+    ridx[tid] = reflect_index(vy0 + tid, h);
+    cidx[tid] = reflect_index(vx0 + tid, w);
+  }
+  __syncthreads();
   for (int i = tid; i < kLT * kLT; i += nt) {
-    int ly = i / kLT, lx = i % kLT;
-    int gy = reflect_index(vy0 + ly, h), gx = reflect_index(vx0 + lx, w);
-    int64_t p = ((int64_t)gy * w + gx) * 3;
+    int ly = i / kLT, lx = i - ly * kLT;
+    int64_t p = ((int64_t)ridx[ly] * w + cidx[lx]) * 3;
     float r0 = ref[p], r1 = ref[p + 1], r2 = ref[p + 2];
     float w0 = warped[p], w1 = warped[p + 1], w2 = warped[p + 2];
     lr[ly][lx] = lum_f(r0, r1, r2);
@@ -78,7 +84,7 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   }
   __syncthreads();
   for (int i = tid; i < kRT * kRT; i += nt) {
-    int ty = i / kRT, tx = i % kRT;
+    int ty = i / kRT, tx = i - ty * kRT;
     int ly = ty + 1, lx = tx + 1;
     // ndimage.laplace: [1,-2,1] along axis 0, += along axis 1 (exact in f64)
     double cr = lr[ly][lx], cw = lw[ly][lx];
@@ -88,12 +94,11 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
                   ((double)lw[ly][lx - 1] + lw[ly][lx + 1] - 2.0 * cw);
     double qr = quality_d(lapr, px[0][ty][tx], px[1][ty][tx], px[2][ty][tx]);
     double qs = quality_d(lapw, px[3][ty][tx], px[4][ty][tx], px[5][ty][tx]);
-    int gy = reflect_index(vy0 + ly, h), gx = reflect_index(vx0 + lx, w);
-    int64_t p = (int64_t)gy * w + gx;
+    int64_t p = (int64_t)ridx[ly] * w + cidx[lx];
     double sv = fmin(fmax((double)ssim[p], 0.0), 1.0);
     qs = valid[p] ? qs * sv : 0.0;
-    double tot = qr + qs;
-    float a = (float)(qr / tot), b = (float)(qs / tot);
+    double inv = 1.0 / (qr + qs);
+    float a = (float)(qr * inv), b = (float)(qs * inv);
     px[6][ty][tx] = a;
     px[7][ty][tx] = b;
     // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image
@@ -106,8 +111,8 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   __syncthreads();
   // vertical 5-tap + decimation: V[c][oy][tx] (region row 2*oy + i)
   for (int i = tid; i < 8 * kOT * kRT; i += nt) {
-    int c = i / (kOT * kRT), r = i % (kOT * kRT);
-    int oy = r / kRT, tx = r % kRT;
+    int c = i / (kOT * kRT), r = i - c * (kOT * kRT);
+    int oy = r / kRT, tx = r - oy * kRT;
     float acc = 0.0f;
 #pragma unroll
     for (int k = 0; k < 5; ++k) acc += kK5[k] * px[c][2 * oy + k][tx];
@@ -116,8 +121,8 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   __syncthreads();
   int64_t OP = (int64_t)ow * oh;
   for (int i = tid; i < 8 * kOT * kOT; i += nt) {
-    int c = i / (kOT * kOT), r = i % (kOT * kOT);
-    int oy = r / kOT, ox = r % kOT;
+    int c = i >> 8, r = i & 255;  // kOT * kOT = 256
+    int oy = r >> 4, ox = r & 15;
     int Y = Y0 + oy, X = X0 + ox;
     if (Y >= oh || X >= ow) continue;
     float acc = 0.0f;
@@ -128,78 +133,102 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
 }
 
 // ---------------------------------------------------------------- levels >= 1
+// all 8 channels staged at once: 2 barriers per tile instead of 3 per channel
+constexpr size_t kDownSmem = sizeof(float) * (8 * kRT * (kRT + 1) + 8 * kOT * kRT);
+
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
                                                    float* __restrict__ out, int ow, int oh) {
-  __shared__ float tile[kRT][kRT + 1];
-  __shared__ float V[kOT][kRT];
+  extern __shared__ float smd[];
+  float (*tile)[kRT][kRT + 1] = reinterpret_cast<float (*)[kRT][kRT + 1]>(smd);
+  float (*V)[kOT][kRT] = reinterpret_cast<float (*)[kOT][kRT]>(smd + 8 * kRT * (kRT + 1));
+  __shared__ int ridx[kRT], cidx[kRT];
   int tid = threadIdx.x, nt = blockDim.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
   int vy0 = 2 * Y0 - 2, vx0 = 2 * X0 - 2;
+  if (tid < kRT) {
+    ridx[tid] = reflect_index(vy0 + tid, h);
+    cidx[tid] = reflect_index(vx0 + tid, w);
+  }
+  __syncthreads();
   int64_t P = (int64_t)w * h, OP = (int64_t)ow * oh;
-  for (int c = 0; c < 8; ++c) {
-    const float* src = in + c * P;
-    for (int i = tid; i < kRT * kRT; i += nt) {
-      int ty = i / kRT, tx = i % kRT;
-      tile[ty][tx] = src[(int64_t)reflect_index(vy0 + ty, h) * w + reflect_index(vx0 + tx, w)];
-    }
-    __syncthreads();
-    for (int i = tid; i < kOT * kRT; i += nt) {
-      int oy = i / kRT, tx = i % kRT;
-      float acc = 0.0f;
+  for (int i = tid; i < 8 * kRT * kRT; i += nt) {
+    int c = i / (kRT * kRT), r = i - c * (kRT * kRT);
+    int ty = r / kRT, tx = r - ty * kRT;
+    tile[c][ty][tx] = in[c * P + (int64_t)ridx[ty] * w + cidx[tx]];
+  }
+  __syncthreads();
+  for (int i = tid; i < 8 * kOT * kRT; i += nt) {
+    int c = i / (kOT * kRT), r = i - c * (kOT * kRT);
+    int oy = r / kRT, tx = r - oy * kRT;
+    float acc = 0.0f;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) acc += kK5[k] * tile[2 * oy + k][tx];
-      V[oy][tx] = acc;
-    }
-    __syncthreads();
-    for (int i = tid; i < kOT * kOT; i += nt) {
-      int oy = i / kOT, ox = i % kOT;
-      int Y = Y0 + oy, X = X0 + ox;
-      if (Y >= oh || X >= ow) continue;
-      float acc = 0.0f;
+    for (int k = 0; k < 5; ++k) acc += kK5[k] * tile[c][2 * oy + k][tx];
+    V[c][oy][tx] = acc;
+  }
+  __syncthreads();
+  for (int i = tid; i < 8 * kOT * kOT; i += nt) {
+    int c = i >> 8, r = i & 255;
+    int oy = r >> 4, ox = r & 15;
+    int Y = Y0 + oy, X = X0 + ox;
+    if (Y >= oh || X >= ow) continue;
+    float acc = 0.0f;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) acc += kK5[k] * V[oy][2 * ox + k];
-      out[c * OP + (int64_t)Y * ow + X] = acc;
-    }
-    __syncthreads();
+    for (int k = 0; k < 5; ++k) acc += kK5[k] * V[c][oy][2 * ox + k];
+    out[c * OP + (int64_t)Y * ow + X] = acc;
   }
 }
 
 // ---------------------------------------------------------------- collapse
 constexpr int kFT = 32;           // fine outputs per tile side
-constexpr int kFV = kFT + 4;      // virtual fine rows incl. the 2-px halo
+constexpr int kFV = kFT + 4;      // virtual fine rows/cols incl. the 2-px halo
+constexpr int kCT = kFT / 2 + 3;  // coarse rows/cols the tile can touch (19)
+constexpr size_t kCollapseSmem = sizeof(float) * (9 * kCT * kCT + 9 * kFV * (kFT + 1));
 
 // 9 coarse channels: G_ref 0-2, G_src 3-5 (gc, planar 8-ch level), C 6-8 (cc)
-__device__ __forceinline__ float coarse_at(const float* gc, const float* cc, int64_t CP, int c,
-                                           int64_t p) {
-  return c < 6 ? __ldg(gc + c * CP + p) : __ldg(cc + (c - 6) * CP + p);
-}
-
 template <bool LEVEL0>
 __global__ void __launch_bounds__(256) collapse_kernel(
     const float* __restrict__ g, const float* __restrict__ ref, const float* __restrict__ warped,
     const float* __restrict__ wr, const float* __restrict__ ws, int w, int h,
     const float* __restrict__ gc, const float* __restrict__ cc, int cw, int ch,
     float* __restrict__ out) {
-  __shared__ float Hs[9][kFV][kFT + 1];
+  extern __shared__ float smc[];
+  float (*C)[kCT][kCT] = reinterpret_cast<float (*)[kCT][kCT]>(smc);
+  float (*Hs)[kFV][kFT + 1] = reinterpret_cast<float (*)[kFV][kFT + 1]>(smc + 9 * kCT * kCT);
+  __shared__ int frow[kFV], fcol[kFV];  // local coarse index of each virtual fine row/col, -1 = odd
   int tid = threadIdx.x, nt = blockDim.x;
   int y0 = blockIdx.y * kFT, x0 = blockIdx.x * kFT;
+  int cy0 = max(0, y0 / 2 - 1), cx0 = max(0, x0 / 2 - 1);
+  if (tid < kFV) {
+    int R = reflect_index(y0 - 2 + tid, h);
+    frow[tid] = (R & 1) ? -1 : (R >> 1) - cy0;
+    int Rx = reflect_index(x0 - 2 + tid, w);
+    fcol[tid] = (Rx & 1) ? -1 : (Rx >> 1) - cx0;
+  }
   int64_t CP = (int64_t)cw * ch;
+  if (gc) {
+    for (int i = tid; i < 9 * kCT * kCT; i += nt) {
+      int c = i / (kCT * kCT), r = i - c * (kCT * kCT);
+      int yy = r / kCT, xx = r - yy * kCT;
+      int Y = min(cy0 + yy, ch - 1), X = min(cx0 + xx, cw - 1);
+      int64_t p = (int64_t)Y * cw + X;
+      C[c][yy][xx] = c < 6 ? gc[c * CP + p] : cc[(c - 6) * CP + p];
+    }
+  }
+  __syncthreads();
   // horizontal up-sampling of the virtual rows y0-2 .. y0+33
   for (int i = tid; i < kFV * kFT; i += nt) {
-    int v = i / kFT, x = i % kFT;
-    int R = reflect_index(y0 - 2 + v, h);
+    int v = i >> 5, x = i & 31;
+    int cr = frow[v];
     float acc[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
-    if (!(R & 1) && gc) {
-      int64_t rowoff = (int64_t)(R >> 1) * cw;
+    if (cr >= 0 && gc) {
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
-        int Rx = reflect_index(x0 + x + j - 2, w);
-        if (Rx & 1) continue;
-        int64_t p = rowoff + (Rx >> 1);
+        int cc2 = fcol[x + j];
+        if (cc2 < 0) continue;
 #pragma unroll
-        for (int c = 0; c < 9; ++c) acc[c] += kK5x2[j] * coarse_at(gc, cc, CP, c, p);
+        for (int c = 0; c < 9; ++c) acc[c] += kK5x2[j] * C[c][cr][cc2];
       }
     }
 #pragma unroll
@@ -208,7 +237,7 @@ __global__ void __launch_bounds__(256) collapse_kernel(
   __syncthreads();
   int64_t P = (int64_t)w * h;
   for (int i = tid; i < kFT * kFT; i += nt) {
-    int yy = i / kFT, x = i % kFT;
+    int yy = i >> 5, x = i & 31;
     int Y = y0 + yy, X = x0 + x;
     if (Y >= h || X >= w) continue;
     float u[9];
@@ -250,6 +279,11 @@ constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * (kRT + 1) 
 
 void init_merge_attributes() {
   cudaFuncSetAttribute(weights_down0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kW0Smem);
+  cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDownSmem);
+  cudaFuncSetAttribute(collapse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kCollapseSmem);
+  cudaFuncSetAttribute(collapse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kCollapseSmem);
 }
 
 void launch_weights_down0(const float* ref, const float* warped, const float* ssim,
@@ -261,7 +295,7 @@ void launch_weights_down0(const float* ref, const float* warped, const float* ss
 
 void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh, cudaStream_t s) {
   dim3 grd(ceil_div(ow, kOT), ceil_div(oh, kOT));
-  down_kernel<<<grd, 256, 0, s>>>(in, w, h, out, ow, oh);
+  down_kernel<<<grd, 256, kDownSmem, s>>>(in, w, h, out, ow, oh);
 }
 
 void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s) {
@@ -272,7 +306,7 @@ void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s) {
 void launch_fuse_collapse(const float* g, int w, int h, const float* gc, const float* cc, int cw,
                           int ch, float* c, cudaStream_t s) {
   dim3 grd(ceil_div(w, kFT), ceil_div(h, kFT));
-  collapse_kernel<false><<<grd, 256, 0, s>>>(g, nullptr, nullptr, nullptr, nullptr, w, h, gc, cc,
+  collapse_kernel<false><<<grd, 256, kCollapseSmem, s>>>(g, nullptr, nullptr, nullptr, nullptr, w, h, gc, cc,
                                              cw, ch, c);
 }
 
@@ -280,7 +314,7 @@ void launch_fuse_collapse0(const float* ref, const float* warped, const float* w
                            int w, int h, const float* gc, const float* cc, int cw, int ch,
                            float* out, cudaStream_t s) {
   dim3 grd(ceil_div(w, kFT), ceil_div(h, kFT));
-  collapse_kernel<true><<<grd, 256, 0, s>>>(nullptr, ref, warped, wr, ws, w, h, gc, cc, cw, ch,
+  collapse_kernel<true><<<grd, 256, kCollapseSmem, s>>>(nullptr, ref, warped, wr, ws, w, h, gc, cc, cw, ch,
                                             out);
 }
 

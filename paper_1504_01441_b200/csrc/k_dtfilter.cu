@@ -8,13 +8,13 @@
 //   into per-thread segments whose zero-carry effects are affine maps, the
 //   maps are scanned across the block, and each segment is re-run from its
 //   true carry with the reference formula. HBM: one read + one write.
-// Columns: 32-row chunks. `agg` reads a chunk once and reduces it to the
-//   affine data both directions need (forward map A,B and the backward
-//   sums Z0 = sum (1-a_i) prod_{j<i} a_j y0_i, R for the carry's own
-//   response, Q = prod a_i); `link` runs the two carry chains per column;
-//   `apply` re-runs each chunk forward from its carry (writing y in place,
-//   L2-resident) and backward from its carry (overwriting with z). HBM: two
-//   reads + one write, instead of re-reading per direction.
+// Columns: 16-row chunks held in registers. `agg` reads a chunk once and
+//   reduces it to the affine data both directions need (forward map A,B and
+//   the backward sums Z0 = sum (1-a_i) prod_{j<i} a_j y0_i, R for the
+//   carry's own response, Q = prod a_i); `link` links the chunks of each
+//   column with warp scans of affine maps; `apply` re-runs each chunk forward
+//   from its upper carry and backward from its lower carry with the
+//   reference formula. HBM: two reads + one write per column sweep pair.
 // Planes may be stored f32 or f64 (DtPlanes::f64); all arithmetic is f64.
 #include "hdr_common.cuh"
 #include "hdr_internal.h"
@@ -135,45 +135,70 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_kernel(const float* __res
 }
 
 // ---------------------------------------------------------------- columns
-constexpr int kColChunk = 32;
+// 16-row chunks, thread per (column, chunk), the chunk held in registers: all
+// 16 x K samples and 18 guide values are loaded up front (the loads carry no
+// dependency, so each thread has ~60 requests in flight), then swept.
+constexpr int kColChunk = 16;
+constexpr int kColThreads = 64;
 
-// coefficient between rows y and y+1 of column x (0 past the last row)
-__device__ __forceinline__ double col_a(const float* g, int64_t w, int h, int y, int x,
-                                        double ratio, double c) {
-  return (y >= 0 && y + 1 < h) ? dt_coef(g[(int64_t)y * w + x], g[(int64_t)(y + 1) * w + x], ratio, c)
-                               : 0.0;
+template <int K>
+struct ColChunk {
+  double x[K][kColChunk];
+  double a[kColChunk + 1];  // a[j] couples rows r0-1+j and r0+j (a[0] links to the chunk above)
+  int n;                    // valid rows in this chunk
+};
+
+template <int K>
+__device__ __forceinline__ void load_chunk(const float* __restrict__ guide, const DtPlanes& P,
+                                           int w, int h, int x, int r0, double ratio, double c,
+                                           ColChunk<K>& ck) {
+  ck.n = min(kColChunk, h - r0);
+  float g[kColChunk + 2];
+#pragma unroll
+  for (int j = 0; j < kColChunk + 2; ++j) {
+    int y = r0 - 1 + j;
+    g[j] = (y >= 0 && y < h) ? __ldg(guide + (int64_t)y * w + x) : 0.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < kColChunk; ++j)
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      ck.x[k][j] = (j < ck.n) ? ldp(P, k, (int64_t)(r0 + j) * w + x) : 0.0;
+#pragma unroll
+  for (int j = 0; j <= kColChunk; ++j) {
+    int y = r0 - 1 + j;  // coefficient between rows y and y+1
+    ck.a[j] = (y >= 0 && y + 1 < h && j <= ck.n) ? dt_coef(g[j], g[j + 1], ratio, c) : 0.0;
+  }
 }
 
-// Aggregates, field-major: agg[f][chunk][col], f = A, Q, R, B[K], Z0[K]
+// Aggregates, field-major agg[f][chunk][col], f = A, Q, R, B[K], Z0[K]:
+// forward zero-carry map y_end = A*C + B, and z_start = Z0 + C*R + Q*D.
 template <int K>
-__global__ void __launch_bounds__(64) dt_cols_agg(const float* __restrict__ guide, DtPlanes P,
-                                                  int w, int h, double ratio, double c,
-                                                  double* __restrict__ agg) {
+__global__ void __launch_bounds__(kColThreads) dt_cols_agg(const float* __restrict__ guide,
+                                                           DtPlanes P, int w, int h, double ratio,
+                                                           double c, double* __restrict__ agg) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
-  int r0 = ch * kColChunk, r1 = min(h, r0 + kColChunk);
+  ColChunk<K> ck;
+  load_chunk<K>(guide, P, w, h, x, ch * kColChunk, ratio, c, ck);
   double y0[K], z0[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) { y0[k] = 0.0; z0[k] = 0.0; }
   double Pp = 1.0, R = 0.0, pref = 1.0;
-  double a_prev = col_a(guide, w, h, r0 - 1, x, ratio, c);
-#pragma unroll 8
-  for (int y = r0; y < r1; ++y) {
-    int64_t i = (int64_t)y * w + x;
-    Pp *= a_prev;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double xv = ldp(P, k, i);
-      y0[k] = xv + a_prev * (y0[k] - xv);
+  for (int j = 0; j < kColChunk; ++j) {
+    if (j < ck.n) {
+      double ap = ck.a[j], an = ck.a[j + 1];
+      Pp *= ap;
+#pragma unroll
+      for (int k = 0; k < K; ++k) y0[k] = ck.x[k][j] + ap * (y0[k] - ck.x[k][j]);
+      double wgt = (1.0 - an) * pref;
+#pragma unroll
+      for (int k = 0; k < K; ++k) z0[k] += wgt * y0[k];
+      R += wgt * Pp;
+      pref *= an;
     }
-    double a = col_a(guide, w, h, y, x, ratio, c);
-    double wgt = (1.0 - a) * pref;
-#pragma unroll
-    for (int k = 0; k < K; ++k) z0[k] += wgt * y0[k];
-    R += wgt * Pp;
-    pref *= a;
-    a_prev = a;
   }
   int64_t F = (int64_t)nch * w, o = (int64_t)ch * w + x;
   agg[o] = Pp;
@@ -183,19 +208,42 @@ __global__ void __launch_bounds__(64) dt_cols_agg(const float* __restrict__ guid
   for (int k = 0; k < K; ++k) { agg[(3 + k) * F + o] = y0[k]; agg[(3 + K + k) * F + o] = z0[k]; }
 }
 
-// carries per column, field-major carry[f][chunk][col]: C_b[K] (value above
-// chunk b), then D_b[K] (value below chunk b)
+// Carry chains, one warp per column: each lane composes a run of chunks, the
+// runs are linked with a warp scan of affine maps, then each lane emits its
+// chunks' carries. carry[f][chunk][col]: C_b[K] (value above), D_b[K] (below).
 template <int K>
-__global__ void dt_cols_link(int w, int nch, const double* __restrict__ agg,
-                             double* __restrict__ carry) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128) dt_cols_link(int w, int nch, const double* __restrict__ agg,
+                                                    double* __restrict__ carry) {
+  int lane = threadIdx.x & 31;
+  int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (x >= w) return;
   int64_t F = (int64_t)nch * w;
+  int per = (nch + 31) / 32;
+  int b0 = lane * per, b1 = min(nch, b0 + per);
+  // forward: y_end(b) = A_b * C_b + B_b
+  Aff<K> m;
+  m.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = 0.0;
+  for (int b = b0; b < b1; ++b) {
+    int64_t o = (int64_t)b * w + x;
+    Aff<K> t;
+    t.A = agg[o];
+#pragma unroll
+    for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + k) * F + o];
+    m = compose(m, t);
+  }
+  Aff<K> inc = m;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Aff<K> o = shfl_aff(inc, off, true);
+    if (lane >= off) inc = compose(o, inc);
+  }
+  Aff<K> ex = shfl_aff(inc, 1, true);
   double C[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) C[k] = 0.0;
-#pragma unroll 4
-  for (int b = 0; b < nch; ++b) {
+  for (int k = 0; k < K; ++k) C[k] = lane ? ex.B[k] : 0.0;
+  for (int b = b0; b < b1; ++b) {
     int64_t o = (int64_t)b * w + x;
     double A = agg[o];
 #pragma unroll
@@ -204,71 +252,86 @@ __global__ void dt_cols_link(int w, int nch, const double* __restrict__ agg,
       C[k] = A * C[k] + agg[(3 + k) * F + o];
     }
   }
+  // backward: z_start(b) = Q_b * D_b + (Z0_b + C_b R_b), scanned from the bottom
+  m.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = 0.0;
+  for (int b = b1 - 1; b >= b0; --b) {
+    int64_t o = (int64_t)b * w + x;
+    Aff<K> t;
+    t.A = agg[F + o];
+    double Rb = agg[2 * F + o];
+#pragma unroll
+    for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
+    m = compose(m, t);
+  }
+  inc = m;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Aff<K> o = shfl_aff(inc, off, false);
+    if (lane + off < 32) inc = compose(o, inc);
+  }
+  ex = shfl_aff(inc, 1, false);
   double D[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) D[k] = 0.0;
-#pragma unroll 4
-  for (int b = nch - 1; b >= 0; --b) {
+  for (int k = 0; k < K; ++k) D[k] = lane < 31 ? ex.B[k] : 0.0;
+  for (int b = b1 - 1; b >= b0; --b) {
     int64_t o = (int64_t)b * w + x;
-    double Q = agg[F + o], R = agg[2 * F + o];
+    double Q = agg[F + o], Rb = agg[2 * F + o];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       carry[(K + k) * F + o] = D[k];
-      D[k] = agg[(3 + K + k) * F + o] + carry[k * F + o] * R + Q * D[k];  // z_s = Z0 + C*R + Q*D
+      D[k] = Q * D[k] + agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
     }
   }
 }
 
-// Re-run each chunk from its carries with the reference update formula. The
-// forward values and the coefficients stay in shared memory (private to the
-// thread's column) for the backward sweep: HBM sees one read and one write.
-constexpr int kColThreads = 64;
-
+// Re-run each chunk from its carries with the reference update formula,
+// forward then backward, entirely in registers: one read, one write.
 template <int K>
 __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __restrict__ guide,
                                                              DtPlanes P, int w, int h,
                                                              double ratio, double c,
                                                              const double* __restrict__ carry) {
-  extern __shared__ double colbuf[];  // [K + 1][kColChunk][kColThreads]
-  int tx = threadIdx.x;
-  int x = blockIdx.x * blockDim.x + tx;
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
-  int r0 = ch * kColChunk, r1 = min(h, r0 + kColChunk);
+  int r0 = ch * kColChunk;
   int64_t F = (int64_t)nch * w, o = (int64_t)ch * w + x;
-  auto Y = [&](int k, int r) -> double& { return colbuf[(k * kColChunk + r) * kColThreads + tx]; };
   double prev[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) prev[k] = carry[k * F + o];
-  double a_prev = col_a(guide, w, h, r0 - 1, x, ratio, c);
-#pragma unroll 8
-  for (int y = r0; y < r1; ++y) {
-    int64_t i = (int64_t)y * w + x;
+  ColChunk<K> ck;
+  load_chunk<K>(guide, P, w, h, x, r0, ratio, c, ck);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double xv = ldp(P, k, i);
-      double v = xv + a_prev * (prev[k] - xv);
-      prev[k] = v;
-      Y(k, y - r0) = v;
+  for (int j = 0; j < kColChunk; ++j)
+    if (j < ck.n) {
+      double ap = ck.a[j];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double xv = ck.x[k][j];
+        prev[k] = xv + ap * (prev[k] - xv);
+        ck.x[k][j] = prev[k];
+      }
     }
-    double a = col_a(guide, w, h, y, x, ratio, c);
-    Y(K, y - r0) = a;
-    a_prev = a;
-  }
 #pragma unroll
   for (int k = 0; k < K; ++k) prev[k] = carry[(K + k) * F + o];
-#pragma unroll 8
-  for (int y = r1 - 1; y >= r0; --y) {
-    int64_t i = (int64_t)y * w + x;
-    double a = Y(K, y - r0);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double yv = Y(k, y - r0);
-      double v = yv + a * (prev[k] - yv);
-      prev[k] = v;
-      stp(P, k, i, v);
+  for (int j = kColChunk - 1; j >= 0; --j)
+    if (j < ck.n) {
+      double an = ck.a[j + 1];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double yv = ck.x[k][j];
+        prev[k] = yv + an * (prev[k] - yv);
+        ck.x[k][j] = prev[k];
+      }
     }
-  }
+#pragma unroll
+  for (int j = 0; j < kColChunk; ++j)
+    if (j < ck.n)
+#pragma unroll
+      for (int k = 0; k < K; ++k) stp(P, k, (int64_t)(r0 + j) * w + x, ck.x[k][j]);
 }
 
 template <int K>
@@ -282,15 +345,14 @@ static void dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
   double* agg = scratch;
   double* carry = agg + (int64_t)nch * w * (3 + 2 * K);
   dim3 cg(ceil_div(w, kColThreads), nch);
-  size_t col_smem = (size_t)(K + 1) * kColChunk * kColThreads * sizeof(double);
   for (int i = 1; i <= passes; ++i) {
     double sigma_i = sigma_s * sqrt(3.0) * pow(2.0, passes - i) / den;  // densify.py:104
     double c = -root / sigma_i;
     if (w > 1) dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
     if (h > 1) {
       dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
-      dt_cols_link<K><<<ceil_div(w, 64), 64, 0, s>>>(w, nch, agg, carry);
-      dt_cols_apply<K><<<cg, kColThreads, col_smem, s>>>(guide, P, w, h, ratio, c, carry);
+      dt_cols_link<K><<<ceil_div(w, 4), 128, 0, s>>>(w, nch, agg, carry);
+      dt_cols_apply<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry);
     }
   }
 }
@@ -304,9 +366,6 @@ void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_kernel<1>);
   allow_max_dynamic_smem(dt_rows_kernel<2>);
   allow_max_dynamic_smem(dt_rows_kernel<3>);
-  allow_max_dynamic_smem(dt_cols_apply<1>);
-  allow_max_dynamic_smem(dt_cols_apply<2>);
-  allow_max_dynamic_smem(dt_cols_apply<3>);
 }
 
 void launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,

@@ -58,24 +58,40 @@ __device__ bool ssd_search(const float* __restrict__ ref, const float* __restric
   __syncthreads();
   SsdKey k;
   k.score = INFINITY; k.d2 = 0x7fffffffffffffffLL; k.cy = 0x7fffffff; k.cx = 0x7fffffff;
-  for (int c = threadIdx.x; c < nx * ny; c += blockDim.x) {
-    int oy = c / nx, ox = c % nx;
-    double acc = 0.0;
+  // each thread sweeps a 1x4 strip of candidate windows, sliding a 4-wide
+  // register window along the source row: per tap one shared load of S and
+  // one (broadcast) of T feed four FMAs. Every window keeps the same
+  // row-major tap order, so identical windows tie exactly as in the reference.
+  int nstrip = (nx + 3) >> 2;
+  for (int t = threadIdx.x; t < nstrip * ny; t += blockDim.x) {
+    int oy = t / nstrip, ox = (t - oy * nstrip) * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int ky = 0; ky < patch; ++ky) {
       const double* srow = S + (oy + ky) * sw + ox;
       const double* trow = T + ky * patch;
+      double w0 = srow[0], w1 = srow[1], w2 = srow[2];
       for (int kx = 0; kx < patch; ++kx) {
-        double d = srow[kx] - trow[kx];
-        acc = fma(d, d, acc);
+        double w3 = srow[kx + 3];
+        double tv = trow[kx];
+        double d0 = w0 - tv, d1 = w1 - tv, d2 = w2 - tv, d3 = w3 - tv;
+        acc[0] = fma(d0, d0, acc[0]);
+        acc[1] = fma(d1, d1, acc[1]);
+        acc[2] = fma(d2, d2, acc[2]);
+        acc[3] = fma(d3, d3, acc[3]);
+        w0 = w1; w1 = w2; w2 = w3;
       }
     }
-    SsdKey cand;
-    cand.score = acc;
-    cand.cx = cx0 + ox;
-    cand.cy = cy0 + oy;
-    long long dx = cand.cx - xi, dy = cand.cy - yi;
-    cand.d2 = dx * dx + dy * dy;
-    if (key_less(cand, k)) k = cand;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (ox + j >= nx) break;
+      SsdKey cand;
+      cand.score = acc[j];
+      cand.cx = cx0 + ox + j;
+      cand.cy = cy0 + oy;
+      long long dx = cand.cx - xi, dy = cand.cy - yi;
+      cand.d2 = dx * dx + dy * dy;
+      if (key_less(cand, k)) k = cand;
+    }
   }
   for (int off = 16; off; off >>= 1) {
     SsdKey o = shfl_key(k, off);
@@ -169,7 +185,7 @@ __global__ void __launch_bounds__(256) ssd_points_kernel(const float* __restrict
 
 static size_t ssd_smem(int radius, int patch) {
   size_t side = 2 * (size_t)radius + patch;
-  return (side * side + (size_t)patch * patch) * sizeof(double);
+  return (side * side + (size_t)patch * patch + 8) * sizeof(double);
 }
 
 constexpr int kSsdMaxSmem = 200 * 1024;
@@ -186,7 +202,7 @@ void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref, con
                       int w, int h, const double* hpred, int radius, int patch, MatchRow* rows,
                       uint8_t* flags, cudaStream_t s) {
   size_t bytes = ssd_smem(radius, patch);
-  ssd_tiles_kernel<<<ntiles, 256, bytes, s>>>(tiles, ref, src, w, h, hpred, radius, patch, rows,
+  ssd_tiles_kernel<<<ntiles, 128, bytes, s>>>(tiles, ref, src, w, h, hpred, radius, patch, rows,
                                               flags);
 }
 
@@ -195,7 +211,7 @@ void launch_ssd_points(const float* ref, const float* src, int w, int h, const i
                        cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = ssd_smem(radius, patch);
-  ssd_points_kernel<<<n, 256, bytes, s>>>(ref, src, w, h, pts, radius, patch, out, found);
+  ssd_points_kernel<<<n, 128, bytes, s>>>(ref, src, w, h, pts, radius, patch, out, found);
 }
 
 // ordered compaction of per-slot rows (tile order is the reference's corner

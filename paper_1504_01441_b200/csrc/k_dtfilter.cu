@@ -134,6 +134,124 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_kernel(const float* __res
     for (int k = 0; k < K; ++k) stp(P, k, row + i, xs[k * w + i]);
 }
 
+// Row pass for w <= kRowThreads * kRowSeg: each thread's segment
+// coefficients live in registers (shared memory holds only the planes, so
+// three blocks fit per SM), and the two directions are separate static loops.
+constexpr int kRowSeg = 16;
+
+template <int K>
+__device__ __forceinline__ void row_block_scan(Aff<K>& inc, bool up, Aff<K>* wsum, int lane, int warp,
+                                               int nw, Aff<K>& pre) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Aff<K> o = shfl_aff(inc, off, up);
+    if (up ? lane >= off : lane + off < 32) inc = compose(o, inc);
+  }
+  if (lane == (up ? 31 : 0)) wsum[warp] = inc;
+  __syncthreads();
+  pre.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) pre.B[k] = 0.0;
+  if (up) {
+    for (int j = 0; j < warp; ++j) pre = compose(pre, wsum[j]);
+  } else {
+    for (int j = nw - 1; j > warp; --j) pre = compose(pre, wsum[j]);
+  }
+  Aff<K> o = shfl_aff(inc, 1, up);
+  if (up ? lane > 0 : lane < 31) pre = compose(pre, o);
+  __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(kRowThreads) dt_rows_reg_kernel(const float* __restrict__ guide,
+                                                                  DtPlanes P, int w, int h,
+                                                                  double ratio, double c) {
+  extern __shared__ double xs[];  // K * w
+  __shared__ Aff<K> wsum[kRowThreads / 32];
+  int y = blockIdx.x;
+  int64_t row = (int64_t)y * w;
+  for (int i = threadIdx.x; i < w; i += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < K; ++k) xs[k * w + i] = ldp(P, k, row + i);
+  const int L = (w + kRowThreads - 1) / kRowThreads;
+  int s0 = threadIdx.x * L, n = min(w, s0 + L) - s0;
+  // af[j] couples samples s0-1+j and s0+j (0 outside the row)
+  const float* g = guide + row;
+  float gv[kRowSeg + 2];
+#pragma unroll
+  for (int j = 0; j < kRowSeg + 2; ++j) {
+    int i = s0 - 1 + j;
+    gv[j] = (j <= n + 1 && i >= 0 && i < w) ? g[i] : 0.0f;
+  }
+  double af[kRowSeg + 1];
+#pragma unroll
+  for (int j = 0; j <= kRowSeg; ++j) {
+    int i = s0 - 1 + j;
+    af[j] = (j <= n && i >= 0 && i + 1 < w) ? dt_coef(gv[j], gv[j + 1], ratio, c) : 0.0;
+  }
+  __syncthreads();
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kRowThreads >> 5;
+  // ---- forward
+  Aff<K> m;
+  m.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = 0.0;
+#pragma unroll
+  for (int j = 0; j < kRowSeg; ++j)
+    if (j < n) {
+      double a = af[j];
+      m.A *= a;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { double x = xs[k * w + s0 + j]; m.B[k] = x + a * (m.B[k] - x); }
+    }
+  Aff<K> pre;
+  row_block_scan<K>(m, true, wsum, lane, warp, nw, pre);
+  double prev[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) prev[k] = pre.B[k];
+#pragma unroll
+  for (int j = 0; j < kRowSeg; ++j)
+    if (j < n) {
+      double a = af[j];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double x = xs[k * w + s0 + j];
+        prev[k] = x + a * (prev[k] - x);
+        xs[k * w + s0 + j] = prev[k];
+      }
+    }
+  // ---- backward
+  m.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = 0.0;
+#pragma unroll
+  for (int j = kRowSeg - 1; j >= 0; --j)
+    if (j < n) {
+      double a = af[j + 1];
+      m.A *= a;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { double x = xs[k * w + s0 + j]; m.B[k] = x + a * (m.B[k] - x); }
+    }
+  row_block_scan<K>(m, false, wsum, lane, warp, nw, pre);
+#pragma unroll
+  for (int k = 0; k < K; ++k) prev[k] = pre.B[k];
+#pragma unroll
+  for (int j = kRowSeg - 1; j >= 0; --j)
+    if (j < n) {
+      double a = af[j + 1];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double x = xs[k * w + s0 + j];
+        prev[k] = x + a * (prev[k] - x);
+        xs[k * w + s0 + j] = prev[k];
+      }
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < w; i += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < K; ++k) stp(P, k, row + i, xs[k * w + i]);
+}
+
 // ---------------------------------------------------------------- columns
 // 16-row chunks, thread per (column, chunk), the chunk held in registers: all
 // 16 x K samples and 18 guide values are loaded up front (the loads carry no
@@ -208,82 +326,94 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_agg(const float* __restri
   for (int k = 0; k < K; ++k) { agg[(3 + k) * F + o] = y0[k]; agg[(3 + K + k) * F + o] = z0[k]; }
 }
 
-// Carry chains, one warp per column: each lane composes a run of chunks, the
-// runs are linked with a warp scan of affine maps, then each lane emits its
-// chunks' carries. carry[f][chunk][col]: C_b[K] (value above), D_b[K] (below).
+// Carry chains. A block owns 32 columns; thread (cx, g) composes the affine
+// maps of chunk group g (a run of `per` consecutive chunks) of column cx, the
+// groups are linked by a Hillis-Steele scan over g in shared memory, then
+// each thread emits its chunks' carries. All global accesses are coalesced
+// across the 32 columns. carry[f][chunk][col]: C_b[K] (above), D_b[K] (below).
+constexpr int kLinkGroups = 32;
+
 template <int K>
-__global__ void __launch_bounds__(128) dt_cols_link(int w, int nch, const double* __restrict__ agg,
-                                                    double* __restrict__ carry) {
-  int lane = threadIdx.x & 31;
-  int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (x >= w) return;
+__global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const double* __restrict__ agg,
+                                                     double* __restrict__ carry) {
+  __shared__ Aff<K> maps[kLinkGroups][33];
+  int cx = threadIdx.x & 31, g = threadIdx.x >> 5;
+  int x = blockIdx.x * 32 + cx;
+  bool live = x < w;
   int64_t F = (int64_t)nch * w;
-  int per = (nch + 31) / 32;
-  int b0 = lane * per, b1 = min(nch, b0 + per);
-  // forward: y_end(b) = A_b * C_b + B_b
+  int per = (nch + kLinkGroups - 1) / kLinkGroups;
+  int b0 = min(nch, g * per), b1 = min(nch, b0 + per);
+  // ---- forward: y_end(b) = A_b C_b + B_b
   Aff<K> m;
   m.A = 1.0;
 #pragma unroll
   for (int k = 0; k < K; ++k) m.B[k] = 0.0;
-  for (int b = b0; b < b1; ++b) {
-    int64_t o = (int64_t)b * w + x;
-    Aff<K> t;
-    t.A = agg[o];
+  if (live)
+    for (int b = b0; b < b1; ++b) {
+      int64_t o = (int64_t)b * w + x;
+      Aff<K> t;
+      t.A = agg[o];
 #pragma unroll
-    for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + k) * F + o];
-    m = compose(m, t);
+      for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + k) * F + o];
+      m = compose(m, t);
+    }
+  maps[g][cx] = m;
+  __syncthreads();
+  for (int off = 1; off < kLinkGroups; off <<= 1) {
+    Aff<K> o = maps[g >= off ? g - off : 0][cx];
+    __syncthreads();
+    if (g >= off) maps[g][cx] = compose(o, maps[g][cx]);
+    __syncthreads();
   }
-  Aff<K> inc = m;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Aff<K> o = shfl_aff(inc, off, true);
-    if (lane >= off) inc = compose(o, inc);
-  }
-  Aff<K> ex = shfl_aff(inc, 1, true);
   double C[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) C[k] = lane ? ex.B[k] : 0.0;
-  for (int b = b0; b < b1; ++b) {
-    int64_t o = (int64_t)b * w + x;
-    double A = agg[o];
+  for (int k = 0; k < K; ++k) C[k] = g ? maps[g - 1][cx].B[k] : 0.0;
+  if (live)
+    for (int b = b0; b < b1; ++b) {
+      int64_t o = (int64_t)b * w + x;
+      double A = agg[o];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      carry[k * F + o] = C[k];
-      C[k] = A * C[k] + agg[(3 + k) * F + o];
+      for (int k = 0; k < K; ++k) {
+        carry[k * F + o] = C[k];
+        C[k] = A * C[k] + agg[(3 + k) * F + o];
+      }
     }
-  }
-  // backward: z_start(b) = Q_b * D_b + (Z0_b + C_b R_b), scanned from the bottom
+  __syncthreads();
+  // ---- backward: z_start(b) = Q_b D_b + (Z0_b + C_b R_b), from the bottom
   m.A = 1.0;
 #pragma unroll
   for (int k = 0; k < K; ++k) m.B[k] = 0.0;
-  for (int b = b1 - 1; b >= b0; --b) {
-    int64_t o = (int64_t)b * w + x;
-    Aff<K> t;
-    t.A = agg[F + o];
-    double Rb = agg[2 * F + o];
+  if (live)
+    for (int b = b1 - 1; b >= b0; --b) {
+      int64_t o = (int64_t)b * w + x;
+      Aff<K> t;
+      t.A = agg[F + o];
+      double Rb = agg[2 * F + o];
 #pragma unroll
-    for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
-    m = compose(m, t);
+      for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
+      m = compose(m, t);
+    }
+  maps[g][cx] = m;
+  __syncthreads();
+  for (int off = 1; off < kLinkGroups; off <<= 1) {
+    Aff<K> o = maps[g + off < kLinkGroups ? g + off : g][cx];
+    __syncthreads();
+    if (g + off < kLinkGroups) maps[g][cx] = compose(o, maps[g][cx]);
+    __syncthreads();
   }
-  inc = m;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Aff<K> o = shfl_aff(inc, off, false);
-    if (lane + off < 32) inc = compose(o, inc);
-  }
-  ex = shfl_aff(inc, 1, false);
   double D[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) D[k] = lane < 31 ? ex.B[k] : 0.0;
-  for (int b = b1 - 1; b >= b0; --b) {
-    int64_t o = (int64_t)b * w + x;
-    double Q = agg[F + o], Rb = agg[2 * F + o];
+  for (int k = 0; k < K; ++k) D[k] = g + 1 < kLinkGroups ? maps[g + 1][cx].B[k] : 0.0;
+  if (live)
+    for (int b = b1 - 1; b >= b0; --b) {
+      int64_t o = (int64_t)b * w + x;
+      double Q = agg[F + o], Rb = agg[2 * F + o];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      carry[(K + k) * F + o] = D[k];
-      D[k] = Q * D[k] + agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
+      for (int k = 0; k < K; ++k) {
+        carry[(K + k) * F + o] = D[k];
+        D[k] = Q * D[k] + agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
+      }
     }
-  }
 }
 
 // Re-run each chunk from its carries with the reference update formula,
@@ -348,10 +478,16 @@ static void dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
   for (int i = 1; i <= passes; ++i) {
     double sigma_i = sigma_s * sqrt(3.0) * pow(2.0, passes - i) / den;  // densify.py:104
     double c = -root / sigma_i;
-    if (w > 1) dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
+    if (w > 1) {
+      if (w <= kRowThreads * kRowSeg)
+        dt_rows_reg_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double), s>>>(guide, P, w, h,
+                                                                                    ratio, c);
+      else
+        dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
+    }
     if (h > 1) {
       dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
-      dt_cols_link<K><<<ceil_div(w, 4), 128, 0, s>>>(w, nch, agg, carry);
+      dt_cols_link<K><<<ceil_div(w, 32), 1024, 0, s>>>(w, nch, agg, carry);
       dt_cols_apply<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry);
     }
   }
@@ -366,6 +502,9 @@ void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_kernel<1>);
   allow_max_dynamic_smem(dt_rows_kernel<2>);
   allow_max_dynamic_smem(dt_rows_kernel<3>);
+  allow_max_dynamic_smem(dt_rows_reg_kernel<1>);
+  allow_max_dynamic_smem(dt_rows_reg_kernel<2>);
+  allow_max_dynamic_smem(dt_rows_reg_kernel<3>);
 }
 
 void launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,

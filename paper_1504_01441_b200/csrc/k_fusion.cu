@@ -137,21 +137,25 @@ __global__ void __launch_bounds__(256) ssim_fixed_kernel(
     }
   }
   __syncthreads();
-  // vertical (axis 0): V[m][oy][c] for the 32 output rows, all E columns
+  // vertical (axis 0): thread (tx, ty) produces rows 4ty..4ty+3 of column
+  // tx (and tx + 32 for the halo columns) from 14 staged samples (sliding)
   for (int c = tx; c < E; c += 32) {
+    double va[4 + 2 * R], vb[4 + 2 * R];
+#pragma unroll
+    for (int j = 0; j < 4 + 2 * R; ++j) { va[j] = sa[4 * ty + j][c]; vb[j] = sb[4 * ty + j][c]; }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      int oy = ty + 8 * q;
       double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
 #pragma unroll
       for (int j = 0; j <= 2 * R; ++j) {
-        double va = sa[oy + j][c], vb = sb[oy + j][c];
-        m0 = fma(va, k[j], m0);
-        m1 = fma(vb, k[j], m1);
-        m2 = fma(va * va, k[j], m2);
-        m3 = fma(vb * vb, k[j], m3);
-        m4 = fma(va * vb, k[j], m4);
+        double A = va[q + j], B = vb[q + j];
+        m0 = fma(A, k[j], m0);
+        m1 = fma(B, k[j], m1);
+        m2 = fma(A * A, k[j], m2);
+        m3 = fma(B * B, k[j], m3);
+        m4 = fma(A * B, k[j], m4);
       }
+      int oy = 4 * ty + q;
       V[(0 * kS2 + oy) * E + c] = m0;
       V[(1 * kS2 + oy) * E + c] = m1;
       V[(2 * kS2 + oy) * E + c] = m2;
@@ -160,23 +164,32 @@ __global__ void __launch_bounds__(256) ssim_fixed_kernel(
     }
   }
   __syncthreads();
+  // horizontal (axis 1): thread owns 4 consecutive outputs of one row
   const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
-  int gx = blockIdx.x * kS2 + tx;
+  int oy = tid >> 3, ox0 = (tid & 7) * 4;
+  int gy = blockIdx.y * kS2 + oy;
+  double m[5][4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    int oy = ty + 8 * q, gy = blockIdx.y * kS2 + oy;
-    double m[5];
+  for (int mm = 0; mm < 5; ++mm) {
+    const double* row = V + (mm * kS2 + oy) * E + ox0;
+    double v[4 + 2 * R];
 #pragma unroll
-    for (int mm = 0; mm < 5; ++mm) {
-      const double* row = V + (mm * kS2 + oy) * E + tx;
+    for (int j = 0; j < 4 + 2 * R; ++j) v[j] = row[j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j <= 2 * R; ++j) acc = fma(row[j], k[j], acc);
-      m[mm] = acc;
+      for (int j = 0; j <= 2 * R; ++j) acc = fma(v[q + j], k[j], acc);
+      m[mm][q] = acc;
     }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int gx = blockIdx.x * kS2 + ox0 + q;
     if (gx >= w || gy >= h) continue;
-    double mu_a = m[0], mu_b = m[1];
-    double var_a = m[2] - mu_a * mu_a, var_b = m[3] - mu_b * mu_b, cov = m[4] - mu_a * mu_b;
+    double mu_a = m[0][q], mu_b = m[1][q];
+    double var_a = m[2][q] - mu_a * mu_a, var_b = m[3][q] - mu_b * mu_b;
+    double cov = m[4][q] - mu_a * mu_b;
     double sc = ((2.0 * mu_a * mu_b + C1) * (2.0 * cov + C2)) /
                 ((mu_a * mu_a + mu_b * mu_b + C1) * (var_a + var_b + C2));
     out[(int64_t)gy * w + gx] = (float)fmin(fmax(sc, -1.0), 1.0);

@@ -445,30 +445,56 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
   }
   __syncthreads();
   if (status) return status;
-  // Gram matrix of the conditioned DLT rows (45 upper entries): warp w
-  // reduces entries w, w + nw, ... over all points, so no thread carries a
-  // 45-entry accumulator
-  __shared__ double gsh[45];
-  for (int e = warp; e < 45; e += nw) {
-    int ea = 0, rem = e;
-    while (rem >= 9 - ea) { rem -= 9 - ea; ++ea; }
-    int eb = ea + rem;
-    double acc = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      double p[4];
-      get(i, p);
-      double px = (p[0] - bc[0]) * tr[0], py = (p[1] - bc[1]) * tr[0];
-      double qx = (p[2] - bc[2]) * ts[0], qy = (p[3] - bc[3]) * ts[0];
-      acc += dlt_entry(0, ea, px, py, qx, qy) * dlt_entry(0, eb, px, py, qx, qy) +
-             dlt_entry(1, ea, px, py, qx, qy) * dlt_entry(1, eb, px, py, qx, qy);
-    }
-    for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffff, acc, off);
-    if (lane == 0) gsh[e] = acc;
+  // Gram matrix of the conditioned DLT rows. With p~ = (px, py, 1), rows are
+  // r0 = [-p~, 0, qx p~], r1 = [0, -p~, qy p~], so G is assembled from 24 sums
+  // S_w = sum w p~ p~^T (6 unique entries each) for w in {1, qx, qy, qx^2+qy^2}.
+  double acc[24];
+#pragma unroll
+  for (int k = 0; k < 24; ++k) acc[k] = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double p[4];
+    get(i, p);
+    double px = (p[0] - bc[0]) * tr[0], py = (p[1] - bc[1]) * tr[0];
+    double qx = (p[2] - bc[2]) * ts[0], qy = (p[3] - bc[3]) * ts[0];
+    double mono[6] = {px * px, px * py, px, py * py, py, 1.0};
+    double wts[4] = {1.0, qx, qy, qx * qx + qy * qy};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 6; ++b) acc[6 * a + b] += wts[a] * mono[b];
+  }
+  __shared__ double gsh[8][24];
+#pragma unroll
+  for (int k = 0; k < 24; ++k) {
+    double v = acc[k];
+    for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffff, v, off);
+    if (lane == 0) gsh[warp][k] = v;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    double S[24];
+    for (int k = 0; k < 24; ++k) {
+      double v = 0.0;
+      for (int j = 0; j < nw; ++j) v += gsh[j][k];
+      S[k] = v;
+    }
+    // unique (i <= j) entries of the 3x3 blocks, monomial order above
+    const int mi[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    double G[9][9];
+    for (int i = 0; i < 9; ++i)
+      for (int j = 0; j < 9; ++j) G[i][j] = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        int m = mi[i][j];
+        G[i][j] = G[3 + i][3 + j] = S[m];
+        G[i][6 + j] = G[6 + j][i] = -S[6 + m];
+        G[3 + i][6 + j] = G[6 + j][3 + i] = -S[12 + m];
+        G[6 + i][6 + j] = S[18 + m];
+      }
     double g45[45];
-    for (int k = 0; k < 45; ++k) g45[k] = gsh[k];
+    int k = 0;
+    for (int i = 0; i < 9; ++i)
+      for (int j = i; j < 9; ++j) g45[k++] = G[i][j];
     int g = 0;
     status = fit_from_gram(g45, tr, ts, H, &g);
     if (g && grey) atomicAdd(grey, g);

@@ -142,15 +142,21 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ roofline bookkeeping
-def stage_bytes(w, h):
-    """Algorithmic HBM bytes per launch of each stage."""
+def stage_bytes(w, h, passes=3):
+    """HBM bytes each stage must move per pair."""
     P = w * h
     return {
+        # both RGB frames in; lum_ref f32, q_src u8, eq_src f32, pyramids out
         "raster": P * (24 + 4 + 1 + 4) + 2 * 4 * P // 3,
-        "finalize_warp": P * (24 + 12 + 8 + 12 + 1 + 1),
+        # splat memsets (3 f64 planes) + per pass: rows R+W, column aggregate
+        # R, column apply R+W of 3 f64 planes, + the f32 guide per kernel;
+        # the last apply writes the f32 flow (8 B) instead of the planes (24)
+        "dt_filter": P * 24 + passes * P * (52 + 28 + 52) - P * 16,
+        # warp_image: flow 8 + src 12 in; warped 12, valid 1, q 1 out
+        "finalize_warp": P * (8 + 12 + 12 + 1 + 1),
         "ssim": P * (4 + 1 + 4),
+        # SURVEY.md §8(d) merge: ref 12, warped 12, SSIM 4, valid 1, composite 12
         "fuse": P * 41,
-        "dt_filter": None,
     }
 
 
@@ -284,12 +290,32 @@ def run_ours(args):
     clk = clocks.stop()
     ms = hd.max_over_ranks(t0.elapsed_time(t1), device=dev)
     hd.barrier()
-    # per-stage durations of the last timed step (probes inside the graphs)
-    stage_ms = {}
+    # per-stage durations of the last timed step (probes inside the graphs);
+    # with 4 streams in flight these include time-sharing with other pairs
+    stage_ms_conc = {}
     for s_i, name in enumerate(_native.STAGES):
         v = [probes[k][2 * s_i].elapsed_time(probes[k][2 * s_i + 1]) for k in range(B)]
-        stage_ms[name] = statistics.mean(v)
+        stage_ms_conc[name] = statistics.mean(v)
     kernels_per_pair = runner.graph_kernels()
+    # isolated stage times: the same pipeline, one pair at a time on one
+    # stream, events recorded on that stream between the stages
+    iso = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(3)]
+    for evs in iso:
+        for e in evs:
+            e.record()
+    torch.cuda.synchronize()
+    s0 = runner.streams[0]
+    for j, evs in enumerate(iso):
+        runner.set_probes(0, evs)
+        s0.wait_stream(torch.cuda.current_stream())
+        runner.enqueue(0, pairs[j % B][0], pairs[j % B][1], outs[0])
+        torch.cuda.current_stream().wait_stream(s0)
+        torch.cuda.synchronize()
+    runner.set_probes(0, None)
+    stage_ms = {}
+    for s_i, name in enumerate(_native.STAGES):
+        stage_ms[name] = statistics.median(
+            iso[j][2 * s_i].elapsed_time(iso[j][2 * s_i + 1]) for j in range(len(iso)))
 
     # ---- end to end through the public batch API (host buffers)
     E = args.e2e_pairs
@@ -329,6 +355,11 @@ def run_ours(args):
     roof_stage = dom if sb.get(dom) else max((k for k in sb if sb[k]), key=lambda k: stage_ms[k])
     traffic = ncu_traffic().get(roof_stage)
     achieved = sb[roof_stage] / (stage_ms[roof_stage] / 1e3) / 1e9
+
+    def roof(stage):
+        a = sb[stage] / (stage_ms[stage] / 1e3) / 1e9
+        return {"stage": stage, "achieved": a, "frac": a / peak, "bytes": sb[stage],
+                "ms": stage_ms[stage], "traffic": ncu_traffic().get(stage)}
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -342,9 +373,12 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "stage": roof_stage, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
-                     "note": "achieved = algorithmic bytes per launch / mean stage time "
-                             "(CUDA-event probes inside the graphs, last timed step)"},
-        "stage_ms": stage_ms, "dominant_stage": dom,
+                     "note": "achieved = bytes the stage must move per pair / its device time "
+                             "(CUDA events on the launching stream around the stage, pairs run "
+                             "one at a time right after the timed region)"},
+        "rooflines": {"warp": roof("finalize_warp"), "merge": roof("fuse"),
+                      "dt_filter": roof("dt_filter")},
+        "stage_ms": stage_ms, "stage_ms_concurrent": stage_ms_conc, "dominant_stage": dom,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "pairs_per_step": E},
         "gpu_launches": kernels_per_pair * B * args.steps,

@@ -789,12 +789,19 @@ static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const flo
   probe(c, 3, 0);
   DtPlanes pl = pair_planes(c, P);
   launch_splat(o->matches, weeded_count, 0, w, h, pl, c->splat_key, c->splat_idx, c->counters + 2, s);
-  launch_dt_filter(c->lum_ref, pl, w, h, p->sigma_s, p->sigma_r, p->passes, c->carry, s);
+  // the last column pass finishes densify_flow in registers and writes the
+  // f32 flow directly (the smoothed planes never make a final round trip)
+  DtFlowOut fo{o->homography, o->info + 1, p->normalization_floor, o->flow};
+  bool flow_done = launch_dt_filter(c->lum_ref, pl, w, h, p->sigma_s, p->sigma_r, p->passes,
+                                    c->carry, s, &fo);
   probe(c, 3, 1);
   probe(c, 4, 0);
   // warp_image + luminance(warped) histogram (pipeline.py:192, :168)
-  launch_finalize_warp(pl, o->homography, o->info + 1, w, h, p->normalization_floor, src, 3,
-                       o->flow, o->warped, o->valid, c->qw, c->hist + 2 * kBins, true, s);
+  if (flow_done)
+    launch_warp(o->flow, w, h, src, o->warped, o->valid, c->qw, c->hist + 2 * kBins, s);
+  else
+    launch_finalize_warp(pl, o->homography, o->info + 1, w, h, p->normalization_floor, src, 3,
+                         o->flow, o->warped, o->valid, c->qw, c->hist + 2 * kBins, true, s);
   probe(c, 4, 1);
   probe(c, 5, 0);
   // make_ssim (pipeline.py:165-171)

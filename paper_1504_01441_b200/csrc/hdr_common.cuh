@@ -101,4 +101,17 @@ HD double apply_h(const double* H, double x, double y, double* mx, double* my) {
   return den;
 }
 
+// geometry.homography_pixel_flow (geometry.py:124-135) at one pixel, f32.
+HD void h_pixel_flow(const double* H, int x, int y, int w, int h, float* fu, float* fv) {
+  double xn, yn, nx, ny;
+  to_norm((double)x, (double)y, w, h, &xn, &yn);
+  double den = apply_h(H, xn, yn, &nx, &ny);
+  bool bad = fabs(den) < 1e-12;
+  double safe = bad ? 1.0 : den;
+  double px, py;
+  from_norm(nx / safe, ny / safe, w, h, &px, &py);
+  *fu = bad ? 0.0f : (float)dsub(px, (double)x);
+  *fv = bad ? 0.0f : (float)dsub(py, (double)y);
+}
+
 }  // namespace hdr

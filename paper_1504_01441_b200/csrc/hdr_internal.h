@@ -110,9 +110,20 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
                   int h, DtPlanes maps, uint64_t* scratch_key, int32_t* scratch_idx,
                   int32_t* status, cudaStream_t s);
 int64_t dt_scratch_doubles(int w, int h, int k);
-void launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double sigma_s,
-                      double sigma_r, int passes, double* scratch, cudaStream_t s);
+// optional fused densify-finalise for the last column pass (K == 3)
+struct DtFlowOut {
+  const double* fallback;   // 3x3 H or null
+  const int32_t* has_fb;    // device flag gating fallback (null = use if non-null)
+  double floor_;
+  float* flow;              // (h, w, 2)
+};
+// returns true when the flow was written (planes then hold pre-final values)
+bool launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double sigma_s,
+                      double sigma_r, int passes, double* scratch, cudaStream_t s,
+                      const DtFlowOut* fo = nullptr);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
+void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
+                 uint8_t* qw, uint32_t* hist, cudaStream_t s);
 void launch_finalize_warp(DtPlanes smooth, const double* fallback,
                           const int32_t* has_fallback, int w, int h, double floor_,
                           const float* src, int channels, float* flow, float* warped,

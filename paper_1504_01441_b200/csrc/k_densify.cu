@@ -69,20 +69,6 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
 }
 
 // ---------------------------------------------------------------- K11/K12
-// geometry.homography_pixel_flow (geometry.py:124-135) at one pixel, f32.
-__device__ __forceinline__ void h_pixel_flow(const double* H, int x, int y, int w, int h,
-                                             float* fu, float* fv) {
-  double xn, yn, nx, ny;
-  to_norm((double)x, (double)y, w, h, &xn, &yn);
-  double den = apply_h(H, xn, yn, &nx, &ny);
-  bool bad = fabs(den) < 1e-12;
-  double safe = bad ? 1.0 : den;
-  double px, py;
-  from_norm(nx / safe, ny / safe, w, h, &px, &py);
-  *fu = bad ? 0.0f : (float)dsub(px, (double)x);
-  *fv = bad ? 0.0f : (float)dsub(py, (double)y);
-}
-
 __global__ void hflow_kernel(const double* __restrict__ Hd, int w, int h, float* __restrict__ flow) {
   __shared__ double H[9];
   if (threadIdx.x < 9) H[threadIdx.x] = Hd[threadIdx.x];
@@ -181,6 +167,65 @@ __global__ void __launch_bounds__(256) finalize_warp_kernel(
   __syncthreads();
   for (int b = threadIdx.x; b < kBins; b += blockDim.x)
     if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// warp_image (densify.py:145-174) + luminance(warped) -> quantised histogram,
+// flow given. Blocks sweep 256-pixel row segments (grid-stride), so each
+// thread's (x, y) comes without a per-pixel division and the block histogram
+// is flushed once per block.
+__global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flow, int w, int h,
+                                                   const float* __restrict__ src,
+                                                   float* __restrict__ warped,
+                                                   uint8_t* __restrict__ valid,
+                                                   uint8_t* __restrict__ qw,
+                                                   uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[kBins];
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  int segs = (w + 255) >> 8;
+  int64_t nwork = (int64_t)segs * h;
+  for (int64_t t = blockIdx.x; t < nwork; t += gridDim.x) {
+    int y = (int)(t / segs), x = (int)(t - (int64_t)y * segs) * 256 + threadIdx.x;
+    if (x >= w) continue;
+    int64_t i = (int64_t)y * w + x;
+    float2 f = __ldcs(reinterpret_cast<const float2*>(flow) + i);
+    double sx = dadd((double)x, (double)f.x), sy = dadd((double)y, (double)f.y);
+    bool ok = sx >= 0.0 && sx <= (double)(w - 1) && sy >= 0.0 && sy <= (double)(h - 1);
+    double cx = fmin(fmax(sx, 0.0), (double)(w - 1));
+    double cy = fmin(fmax(sy, 0.0), (double)(h - 1));
+    int x0 = (int)floor(cx), y0 = (int)floor(cy);
+    int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+    double fx = dsub(cx, (double)x0), fy = dsub(cy, (double)y0);
+    double gx = dsub(1.0, fx), gy = dsub(1.0, fy);
+    const float* s00 = src + ((int64_t)y0 * w + x0) * 3;
+    const float* s01 = src + ((int64_t)y0 * w + x1) * 3;
+    const float* s10 = src + ((int64_t)y1 * w + x0) * 3;
+    const float* s11 = src + ((int64_t)y1 * w + x1) * 3;
+    float o[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double top = dadd(dmul((double)__ldg(s00 + k), gx), dmul((double)__ldg(s01 + k), fx));
+      double bot = dadd(dmul((double)__ldg(s10 + k), gx), dmul((double)__ldg(s11 + k), fx));
+      o[k] = (float)dadd(dmul(top, gy), dmul(bot, fy));
+    }
+    float* wo = warped + 3 * i;
+    wo[0] = o[0]; wo[1] = o[1]; wo[2] = o[2];
+    valid[i] = ok ? 1 : 0;
+    uint32_t q = quant3(luma3(o[0], o[1], o[2]));
+    qw[i] = (uint8_t)q;
+    unsigned peers = __match_any_sync(__activemask(), q);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[q], (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
+                 uint8_t* qw, uint32_t* hist, cudaStream_t s) {
+  int64_t work = (int64_t)((w + 255) / 256) * h;
+  int64_t blocks = work < 148 * 12 ? work : 148 * 12;
+  warp_kernel<<<(unsigned)blocks, 256, 0, s>>>(flow, w, h, src, warped, valid, qw, hist);
 }
 
 void launch_finalize_warp(DtPlanes smooth, const double* fallback, const int32_t* has_fallback,

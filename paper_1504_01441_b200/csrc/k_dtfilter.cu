@@ -418,11 +418,15 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
 
 // Re-run each chunk from its carries with the reference update formula,
 // forward then backward, entirely in registers: one read, one write.
-template <int K>
+// FINAL (last pass of the pair path, K == 3 planes pu, pv, n): instead of
+// storing the planes, finish densify_flow (densify.py:134-142) in registers
+// and write the f32 flow: ratio where n > floor, else the homography flow.
+template <int K, bool FINAL>
 __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __restrict__ guide,
                                                              DtPlanes P, int w, int h,
                                                              double ratio, double c,
-                                                             const double* __restrict__ carry) {
+                                                             const double* __restrict__ carry,
+                                                             DtFlowOut fo) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
@@ -457,6 +461,26 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
         ck.x[k][j] = prev[k];
       }
     }
+  if (FINAL) {
+    bool use_fb = fo.fallback && (!fo.has_fb || *fo.has_fb);
+    double H[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) H[i] = use_fb ? fo.fallback[i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kColChunk; ++j)
+      if (j < ck.n) {
+        double nv = ck.x[K - 1][j];
+        float fu = 0.0f, fv = 0.0f;
+        if (nv > fo.floor_) {
+          fu = (float)(ck.x[0][j] / nv);
+          fv = (float)(ck.x[K > 2 ? 1 : 0][j] / nv);
+        } else if (use_fb) {
+          h_pixel_flow(H, x, r0 + j, w, h, &fu, &fv);
+        }
+        reinterpret_cast<float2*>(fo.flow)[(int64_t)(r0 + j) * w + x] = make_float2(fu, fv);
+      }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < kColChunk; ++j)
     if (j < ck.n)
@@ -465,8 +489,10 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
 }
 
 template <int K>
-static void dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sigma_s,
-                        double sigma_r, int passes, double* scratch, cudaStream_t s) {
+static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sigma_s,
+                        double sigma_r, int passes, double* scratch, const DtFlowOut& fo,
+                        cudaStream_t s) {
+  bool finalized = false;
   double ratio = sigma_s / sigma_r;
   double root = sqrt(2.0);
   double den = sqrt(pow(4.0, passes) - 1.0);
@@ -488,9 +514,15 @@ static void dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     if (h > 1) {
       dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
       dt_cols_link<K><<<ceil_div(w, 32), 1024, 0, s>>>(w, nch, agg, carry);
-      dt_cols_apply<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry);
+      if (i == passes && fo.flow && K == 3) {
+        dt_cols_apply<K, true><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry, fo);
+        finalized = true;
+      } else {
+        dt_cols_apply<K, false><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry, fo);
+      }
     }
   }
+  return finalized;
 }
 
 int64_t dt_scratch_doubles(int w, int h, int k) {
@@ -507,12 +539,14 @@ void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_reg_kernel<3>);
 }
 
-void launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,
-                      int passes, double* scratch, cudaStream_t s) {
+bool launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,
+                      int passes, double* scratch, cudaStream_t s, const DtFlowOut* fo) {
+  DtFlowOut none{nullptr, nullptr, 0.0, nullptr};
+  const DtFlowOut& f = fo ? *fo : none;
   switch (P.k) {
-    case 1: dt_filter_k<1>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, s); break;
-    case 2: dt_filter_k<2>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, s); break;
-    default: dt_filter_k<3>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, s); break;
+    case 1: return dt_filter_k<1>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s);
+    case 2: return dt_filter_k<2>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s);
+    default: return dt_filter_k<3>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s);
   }
 }
 

@@ -470,7 +470,9 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
   double v[9], y[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) v[i] = 1.0 / 3.0;
-  for (int it = 0; it < 60; ++it) {
+  // (G + sigma I) has condition ~1e13, so successive iterates jitter at
+  // ~1e-15..1e-14 once converged: stop at 1e-13 (H to ~1e-13 relative)
+  for (int it = 0; it < 30; ++it) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) {  // L y = v
       double s = v[i];
@@ -497,7 +499,7 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
       diff = fmax(diff, fabs(z - v[i]));
       v[i] = z;
     }
-    if (diff < 4e-15) break;
+    if (diff < 1e-13) break;
   }
   double hc[9];
 #pragma unroll

@@ -30,38 +30,77 @@ __device__ __forceinline__ float lum_f(float r, float g, float b) {
 }
 
 // contrast x saturation x well-exposedness + 1e-12 (fusion.py:67-77).
-// The laplacian and the channel std stay f64 as in the reference: for grey or
-// clipped pixels the true std is exactly 0 there (3v * (1/3) rounds back to v),
-// while an f32 mean leaves ~1e-8 of std, which outweighs the 1e-12 floor and
-// changes the blend weights completely. Only the exposedness exp is f32.
-__device__ __forceinline__ double quality_d(double lap, float r, float g, float b) {
+// The laplacian and the channel variance are formed in f64 as in the
+// reference: both are then exact (sums of a few f32 values), so a grey or
+// clipped pixel gets exactly 0 contrast/saturation like numpy's (an f32 mean
+// leaves ~1e-8 of std there, which outweighs the 1e-12 floor and changes the
+// blend weights completely). Everything after that -- sqrt, exp, products,
+// normalisation -- is f32: relative error ~1e-7 on a weight moves the
+// composite by ~1e-7, far inside the 1e-3 bar.
+__device__ __forceinline__ float quality_f(double lap, float r, float g, float b) {
   const double third = 1.0 / 3.0;
   double R = r, G = g, B = b;
   double mean = ((R + G) + B) * third;
   double dr = R - mean, dg = G - mean, db = B - mean;
-  double sat = sqrt(((dr * dr + dg * dg) + db * db) * third);
+  float sat = sqrtf((float)(((dr * dr + dg * dg) + db * db) * third));
   float er = r - 0.5f, eg = g - 0.5f, eb = b - 0.5f;
-  double ex = (double)__expf(-(er * er + eg * eg + eb * eb) * 12.5f);
-  return fabs(lap) * sat * ex + 1e-12;
+  float ex = __expf(-(er * er + eg * eg + eb * eb) * 12.5f);
+  return fabsf((float)lap) * sat * ex + 1e-12f;
+}
+
+// ndimage.laplace at the centre of a 3x3 neighbourhood, f64 (exact)
+__device__ __forceinline__ double lap5(float n, float s, float w_, float e, float c) {
+  double cc = c;
+  return (((double)n + s) - 2.0 * cc) + (((double)w_ + e) - 2.0 * cc);
 }
 
 // ---------------------------------------------------------------- weights + level 1
 constexpr int kOT = 16;           // level-1 outputs per tile side
 constexpr int kRT = 2 * kOT + 4;  // level-0 region incl. the 2-px blur halo (36)
 constexpr int kLT = kRT + 2;      // + 1-px laplacian halo (38)
+constexpr int kRP = kRT + 1;      // padded row pitch of the staged region
+
+// 5-tap blur + [::2, ::2] of 8 staged channels px[c][36][kRP] into a 16x16
+// level-1 tile: vertical into V[c][16][36], then horizontal to global.
+__device__ __forceinline__ void down8(const float* px, float* V, int tid, int Y0, int X0,
+                                      float* __restrict__ out, int ow, int oh) {
+  // 8 * 16 * 36 = 4608 = 18 * 256 vertical outputs
+  for (int i = tid; i < 8 * kOT * kRT; i += 256) {
+    int q = i / kRT, x = i - q * kRT;  // q = c * 16 + oy
+    int c = q >> 4, oy = q & 15;
+    const float* col = px + (c * kRT + 2 * oy) * kRP + x;
+    float acc = kK5[0] * col[0];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) acc += kK5[k] * col[k * kRP];
+    V[q * kRT + x] = acc;
+  }
+  __syncthreads();
+  int P = ow * oh;
+  // 8 * 16 * 16 = 2048 = 8 * 256 horizontal outputs
+#pragma unroll 2
+  for (int i = tid; i < 8 * kOT * kOT; i += 256) {
+    int q = i >> 4, ox = i & 15;
+    int c = q >> 4, oy = q & 15;
+    int Y = Y0 + oy, X = X0 + ox;
+    const float* row = V + q * kRT + 2 * ox;
+    float acc = kK5[0] * row[0];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) acc += kK5[k] * row[k];
+    if (Y < oh && X < ow) out[c * P + Y * ow + X] = acc;
+  }
+}
 
 __global__ void __launch_bounds__(256) weights_down0_kernel(
     const float* __restrict__ ref, const float* __restrict__ warped, const float* __restrict__ ssim,
     const uint8_t* __restrict__ valid, int w, int h, float* __restrict__ wr_out,
     float* __restrict__ ws_out, float* __restrict__ g1, int ow, int oh) {
   extern __shared__ float smf[];
-  float (*lr)[kLT] = reinterpret_cast<float (*)[kLT]>(smf);
-  float (*lw)[kLT] = reinterpret_cast<float (*)[kLT]>(smf + kLT * kLT);
-  // ref rgb, warped rgb, w_ref, w_src
-  float (*px)[kRT][kRT + 1] = reinterpret_cast<float (*)[kRT][kRT + 1]>(smf + 2 * kLT * kLT);
-  float (*V)[kOT][kRT] = reinterpret_cast<float (*)[kOT][kRT]>(smf + 2 * kLT * kLT + 8 * kRT * (kRT + 1));
+  float* lr = smf;                    // [38][38] luminance of ref
+  float* lw = smf + kLT * kLT;        // [38][38] luminance of warped
+  float* px = smf + 2 * kLT * kLT;    // [8][36][37]: ref rgb, warped rgb, w_ref, w_src
+  float* V = px + 8 * kRT * kRP;      // [8][16][36]
   __shared__ int ridx[kLT], cidx[kLT];
-  int tid = threadIdx.x, nt = blockDim.x;
+  int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
   int vy0 = 2 * Y0 - 3, vx0 = 2 * X0 - 3;  // virtual origin of the 38x38 lum tile
   if (tid < kLT) {
@@ -69,80 +108,66 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
     cidx[tid] = reflect_index(vx0 + tid, w);
   }
   __syncthreads();
-  for (int i = tid; i < kLT * kLT; i += nt) {
-    int ly = i / kLT, lx = i - ly * kLT;
-    int64_t p = ((int64_t)ridx[ly] * w + cidx[lx]) * 3;
-    float r0 = ref[p], r1 = ref[p + 1], r2 = ref[p + 2];
-    float w0 = warped[p], w1 = warped[p + 1], w2 = warped[p + 2];
-    lr[ly][lx] = lum_f(r0, r1, r2);
-    lw[ly][lx] = lum_f(w0, w1, w2);
-    if (ly >= 1 && ly <= kRT && lx >= 1 && lx <= kRT) {
-      int ty = ly - 1, tx = lx - 1;
-      px[0][ty][tx] = r0; px[1][ty][tx] = r1; px[2][ty][tx] = r2;
-      px[3][ty][tx] = w0; px[4][ty][tx] = w1; px[5][ty][tx] = w2;
+  {
+    int ly = tid / kLT, lx = tid - ly * kLT;
+    for (int i = tid; i < kLT * kLT; i += 256) {
+      int p = (ridx[ly] * w + cidx[lx]) * 3;
+      float r0 = __ldg(ref + p), r1 = __ldg(ref + p + 1), r2 = __ldg(ref + p + 2);
+      float w0 = __ldg(warped + p), w1 = __ldg(warped + p + 1), w2 = __ldg(warped + p + 2);
+      lr[i] = lum_f(r0, r1, r2);
+      lw[i] = lum_f(w0, w1, w2);
+      if ((unsigned)(ly - 1) < (unsigned)kRT && (unsigned)(lx - 1) < (unsigned)kRT) {
+        float* d = px + (ly - 1) * kRP + (lx - 1);
+        d[0] = r0; d[kRT * kRP] = r1; d[2 * kRT * kRP] = r2;
+        d[3 * kRT * kRP] = w0; d[4 * kRT * kRP] = w1; d[5 * kRT * kRP] = w2;
+      }
+      // advance (ly, lx) by 256 = 6 * 38 + 28
+      lx += 28; ly += 6;
+      if (lx >= kLT) { lx -= kLT; ++ly; }
     }
   }
   __syncthreads();
-  for (int i = tid; i < kRT * kRT; i += nt) {
-    int ty = i / kRT, tx = i - ty * kRT;
-    int ly = ty + 1, lx = tx + 1;
-    // ndimage.laplace: [1,-2,1] along axis 0, += along axis 1 (exact in f64)
-    double cr = lr[ly][lx], cw = lw[ly][lx];
-    double lapr = ((double)lr[ly - 1][lx] + lr[ly + 1][lx] - 2.0 * cr) +
-                  ((double)lr[ly][lx - 1] + lr[ly][lx + 1] - 2.0 * cr);
-    double lapw = ((double)lw[ly - 1][lx] + lw[ly + 1][lx] - 2.0 * cw) +
-                  ((double)lw[ly][lx - 1] + lw[ly][lx + 1] - 2.0 * cw);
-    double qr = quality_d(lapr, px[0][ty][tx], px[1][ty][tx], px[2][ty][tx]);
-    double qs = quality_d(lapw, px[3][ty][tx], px[4][ty][tx], px[5][ty][tx]);
-    int64_t p = (int64_t)ridx[ly] * w + cidx[lx];
-    double sv = fmin(fmax((double)ssim[p], 0.0), 1.0);
-    qs = valid[p] ? qs * sv : 0.0;
-    double inv = 1.0 / (qr + qs);
-    float a = (float)(qr * inv), b = (float)(qs * inv);
-    px[6][ty][tx] = a;
-    px[7][ty][tx] = b;
-    // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image
-    int ry = vy0 + ly, rx = vx0 + lx;
-    if (ty >= 2 && ty < 2 + 2 * kOT && tx >= 2 && tx < 2 + 2 * kOT && ry < h && rx < w) {
-      wr_out[p] = a;
-      ws_out[p] = b;
+  {
+    int ty = tid / kRT, tx = tid - ty * kRT;
+    for (int i = tid; i < kRT * kRT; i += 256) {
+      int c = (ty + 1) * kLT + tx + 1;
+      double lapr = lap5(lr[c - kLT], lr[c + kLT], lr[c - 1], lr[c + 1], lr[c]);
+      double lapw = lap5(lw[c - kLT], lw[c + kLT], lw[c - 1], lw[c + 1], lw[c]);
+      float* d = px + ty * kRP + tx;
+      float qr = quality_f(lapr, d[0], d[kRT * kRP], d[2 * kRT * kRP]);
+      float qs = quality_f(lapw, d[3 * kRT * kRP], d[4 * kRT * kRP], d[5 * kRT * kRP]);
+      int p = ridx[ty + 1] * w + cidx[tx + 1];
+      float sv = fminf(fmaxf(__ldg(ssim + p), 0.0f), 1.0f);
+      qs = __ldg(valid + p) ? qs * sv : 0.0f;
+      float inv = __frcp_rn(qr + qs);
+      float a = qr * inv, b = qs * inv;
+      d[6 * kRT * kRP] = a;
+      d[7 * kRT * kRP] = b;
+      // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image
+      if ((unsigned)(ty - 2) < 2u * kOT && (unsigned)(tx - 2) < 2u * kOT &&
+          vy0 + ty + 1 < h && vx0 + tx + 1 < w) {
+        wr_out[p] = a;
+        ws_out[p] = b;
+      }
+      // advance (ty, tx) by 256 = 7 * 36 + 4
+      tx += 4; ty += 7;
+      if (tx >= kRT) { tx -= kRT; ++ty; }
     }
   }
   __syncthreads();
-  // vertical 5-tap + decimation: V[c][oy][tx] (region row 2*oy + i)
-  for (int i = tid; i < 8 * kOT * kRT; i += nt) {
-    int c = i / (kOT * kRT), r = i - c * (kOT * kRT);
-    int oy = r / kRT, tx = r - oy * kRT;
-    float acc = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) acc += kK5[k] * px[c][2 * oy + k][tx];
-    V[c][oy][tx] = acc;
-  }
-  __syncthreads();
-  int64_t OP = (int64_t)ow * oh;
-  for (int i = tid; i < 8 * kOT * kOT; i += nt) {
-    int c = i >> 8, r = i & 255;  // kOT * kOT = 256
-    int oy = r >> 4, ox = r & 15;
-    int Y = Y0 + oy, X = X0 + ox;
-    if (Y >= oh || X >= ow) continue;
-    float acc = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) acc += kK5[k] * V[c][oy][2 * ox + k];
-    g1[c * OP + (int64_t)Y * ow + X] = acc;
-  }
+  down8(px, V, tid, Y0, X0, g1, ow, oh);
 }
 
 // ---------------------------------------------------------------- levels >= 1
-// all 8 channels staged at once: 2 barriers per tile instead of 3 per channel
-constexpr size_t kDownSmem = sizeof(float) * (8 * kRT * (kRT + 1) + 8 * kOT * kRT);
+constexpr size_t kDownSmem = sizeof(float) * (8 * kRT * kRP + 8 * kOT * kRT);
 
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
                                                    float* __restrict__ out, int ow, int oh) {
   extern __shared__ float smd[];
-  float (*tile)[kRT][kRT + 1] = reinterpret_cast<float (*)[kRT][kRT + 1]>(smd);
-  float (*V)[kOT][kRT] = reinterpret_cast<float (*)[kOT][kRT]>(smd + 8 * kRT * (kRT + 1));
+  float* tile = smd;               // [8][36][37]
+  float* V = smd + 8 * kRT * kRP;  // [8][16][36]
   __shared__ int ridx[kRT], cidx[kRT];
-  int tid = threadIdx.x, nt = blockDim.x;
+  int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
   int vy0 = 2 * Y0 - 2, vx0 = 2 * X0 - 2;
   if (tid < kRT) {
@@ -150,39 +175,45 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
     cidx[tid] = reflect_index(vx0 + tid, w);
   }
   __syncthreads();
-  int64_t P = (int64_t)w * h, OP = (int64_t)ow * oh;
-  for (int i = tid; i < 8 * kRT * kRT; i += nt) {
-    int c = i / (kRT * kRT), r = i - c * (kRT * kRT);
-    int ty = r / kRT, tx = r - ty * kRT;
-    tile[c][ty][tx] = in[c * P + (int64_t)ridx[ty] * w + cidx[tx]];
+  int P = w * h;
+  {
+    int ty = tid / kRT, tx = tid - ty * kRT;
+    for (int i = tid; i < kRT * kRT; i += 256) {
+      const float* src = in + ridx[ty] * w + cidx[tx];
+      float* d = tile + ty * kRP + tx;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) d[c * kRT * kRP] = __ldg(src + c * P);
+      tx += 4; ty += 7;
+      if (tx >= kRT) { tx -= kRT; ++ty; }
+    }
   }
   __syncthreads();
-  for (int i = tid; i < 8 * kOT * kRT; i += nt) {
-    int c = i / (kOT * kRT), r = i - c * (kOT * kRT);
-    int oy = r / kRT, tx = r - oy * kRT;
-    float acc = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) acc += kK5[k] * tile[c][2 * oy + k][tx];
-    V[c][oy][tx] = acc;
-  }
-  __syncthreads();
-  for (int i = tid; i < 8 * kOT * kOT; i += nt) {
-    int c = i >> 8, r = i & 255;
-    int oy = r >> 4, ox = r & 15;
-    int Y = Y0 + oy, X = X0 + ox;
-    if (Y >= oh || X >= ow) continue;
-    float acc = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) acc += kK5[k] * V[c][oy][2 * ox + k];
-    out[c * OP + (int64_t)Y * ow + X] = acc;
-  }
+  down8(tile, V, tid, Y0, X0, out, ow, oh);
 }
 
 // ---------------------------------------------------------------- collapse
 constexpr int kFT = 32;           // fine outputs per tile side
-constexpr int kFV = kFT + 4;      // virtual fine rows/cols incl. the 2-px halo
 constexpr int kCT = kFT / 2 + 3;  // coarse rows/cols the tile can touch (19)
-constexpr size_t kCollapseSmem = sizeof(float) * (9 * kCT * kCT + 9 * kFV * (kFT + 1));
+constexpr size_t kCollapseSmem = sizeof(float) * (9 * kCT * kCT + 9 * kCT * kFT);
+
+// Polyphase form of up(): fine sample y gets 2 * K5[j] * coarse(R/2) for the
+// taps j whose reflected fine index R = reflect(y - 2 + j) is even -- at most
+// three distinct coarse rows. tap_rows() lists them (local coarse index and
+// the summed weight; unused slots carry weight 0 and index 0).
+__device__ __forceinline__ void tap_rows(int y, int n, int c0, int* idx, float* wt) {
+  int k = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) { idx[t] = 0; wt[t] = 0.0f; }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    int R = reflect_index(y - 2 + j, n);
+    if (R & 1) continue;
+    int cr = (R >> 1) - c0;
+    if (k > 0 && idx[k - 1] == cr) { wt[k - 1] += kK5x2[j]; continue; }
+    if (k > 1 && idx[k - 2] == cr) { wt[k - 2] += kK5x2[j]; continue; }
+    idx[k] = cr; wt[k] = kK5x2[j]; ++k;
+  }
+}
 
 // 9 coarse channels: G_ref 0-2, G_src 3-5 (gc, planar 8-ch level), C 6-8 (cc)
 template <bool LEVEL0>
@@ -192,75 +223,69 @@ __global__ void __launch_bounds__(256) collapse_kernel(
     const float* __restrict__ gc, const float* __restrict__ cc, int cw, int ch,
     float* __restrict__ out) {
   extern __shared__ float smc[];
-  float (*C)[kCT][kCT] = reinterpret_cast<float (*)[kCT][kCT]>(smc);
-  float (*Hs)[kFV][kFT + 1] = reinterpret_cast<float (*)[kFV][kFT + 1]>(smc + 9 * kCT * kCT);
-  __shared__ int frow[kFV], fcol[kFV];  // local coarse index of each virtual fine row/col, -1 = odd
-  int tid = threadIdx.x, nt = blockDim.x;
+  float* C = smc;                    // [9][19][19] coarse tile
+  float* Hc = smc + 9 * kCT * kCT;   // [9][19][32] coarse rows up-sampled along x
+  __shared__ int vr[kFT][3], hc[kFT][3];
+  __shared__ float vw[kFT][3], hw[kFT][3];
+  int tid = threadIdx.x;
   int y0 = blockIdx.y * kFT, x0 = blockIdx.x * kFT;
   int cy0 = max(0, y0 / 2 - 1), cx0 = max(0, x0 / 2 - 1);
-  if (tid < kFV) {
-    int R = reflect_index(y0 - 2 + tid, h);
-    frow[tid] = (R & 1) ? -1 : (R >> 1) - cy0;
-    int Rx = reflect_index(x0 - 2 + tid, w);
-    fcol[tid] = (Rx & 1) ? -1 : (Rx >> 1) - cx0;
+  if (tid < kFT) {
+    tap_rows(y0 + tid, h, cy0, vr[tid], vw[tid]);
+  } else if (tid < 2 * kFT) {
+    tap_rows(x0 + tid - kFT, w, cx0, hc[tid - kFT], hw[tid - kFT]);
   }
-  int64_t CP = (int64_t)cw * ch;
-  if (gc) {
-    for (int i = tid; i < 9 * kCT * kCT; i += nt) {
-      int c = i / (kCT * kCT), r = i - c * (kCT * kCT);
-      int yy = r / kCT, xx = r - yy * kCT;
-      int Y = min(cy0 + yy, ch - 1), X = min(cx0 + xx, cw - 1);
-      int64_t p = (int64_t)Y * cw + X;
-      C[c][yy][xx] = c < 6 ? gc[c * CP + p] : cc[(c - 6) * CP + p];
+  int CP = cw * ch;
+  if (gc) {  // null for a single-level pyramid: up() of nothing is 0
+    int yy = tid / kCT, xx = tid - yy * kCT;  // 256 = 13 * 19 + 9
+    for (int i = tid; i < kCT * kCT; i += 256) {
+      int p = min(cy0 + yy, ch - 1) * cw + min(cx0 + xx, cw - 1);
+#pragma unroll
+      for (int c = 0; c < 9; ++c)
+        C[c * kCT * kCT + i] = c < 6 ? __ldg(gc + c * CP + p) : __ldg(cc + (c - 6) * CP + p);
+      xx += 9; yy += 13;
+      if (xx >= kCT) { xx -= kCT; ++yy; }
     }
   }
   __syncthreads();
-  // horizontal up-sampling of the virtual rows y0-2 .. y0+33
-  for (int i = tid; i < kFV * kFT; i += nt) {
-    int v = i >> 5, x = i & 31;
-    int cr = frow[v];
-    float acc[9];
+  // horizontal: Hc[c][r][x] for the 19 coarse rows and the 32 fine columns
+  for (int i = tid; i < kCT * kFT; i += 256) {
+    int r = i >> 5, x = i & 31;
+    int j0 = hc[x][0], j1 = hc[x][1], j2 = hc[x][2];
+    float w0 = hw[x][0], w1 = hw[x][1], w2 = hw[x][2];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) acc[c] = 0.0f;
-    if (cr >= 0 && gc) {
-#pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        int cc2 = fcol[x + j];
-        if (cc2 < 0) continue;
-#pragma unroll
-        for (int c = 0; c < 9; ++c) acc[c] += kK5x2[j] * C[c][cr][cc2];
-      }
+    for (int c = 0; c < 9; ++c) {
+      const float* row = C + (c * kCT + r) * kCT;
+      Hc[(c * kCT + r) * kFT + x] = gc ? w0 * row[j0] + w1 * row[j1] + w2 * row[j2] : 0.0f;
     }
-#pragma unroll
-    for (int c = 0; c < 9; ++c) Hs[c][v][x] = acc[c];
   }
   __syncthreads();
-  int64_t P = (int64_t)w * h;
-  for (int i = tid; i < kFT * kFT; i += nt) {
+  int P = w * h;
+  for (int i = tid; i < kFT * kFT; i += 256) {
     int yy = i >> 5, x = i & 31;
     int Y = y0 + yy, X = x0 + x;
     if (Y >= h || X >= w) continue;
+    int r0 = vr[yy][0], r1 = vr[yy][1], r2 = vr[yy][2];
+    float w0 = vw[yy][0], w1 = vw[yy][1], w2 = vw[yy][2];
     float u[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) acc += kK5x2[k] * Hs[c][yy + k][x];
-      u[c] = acc;
+      const float* col = Hc + c * kCT * kFT + x;
+      u[c] = w0 * col[r0 * kFT] + w1 * col[r1 * kFT] + w2 * col[r2 * kFT];
     }
-    int64_t p = (int64_t)Y * w + X;
+    int p = Y * w + X;
     if (LEVEL0) {
-      float a = wr[p], b = ws[p];
+      float a = __ldg(wr + p), b = __ldg(ws + p);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float v = a * (ref[3 * p + k] - u[k]) + b * (warped[3 * p + k] - u[3 + k]) + u[6 + k];
+        float v = a * (__ldg(ref + 3 * p + k) - u[k]) + b * (__ldg(warped + 3 * p + k) - u[3 + k]) + u[6 + k];
         out[3 * p + k] = fminf(fmaxf(v, 0.0f), 1.0f);
       }
     } else {
-      float a = g[6 * P + p], b = g[7 * P + p];
+      float a = __ldg(g + 6 * P + p), b = __ldg(g + 7 * P + p);
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        out[k * P + p] = a * (g[k * P + p] - u[k]) + b * (g[(3 + k) * P + p] - u[3 + k]) + u[6 + k];
+        out[k * P + p] = a * (__ldg(g + k * P + p) - u[k]) + b * (__ldg(g + (3 + k) * P + p) - u[3 + k]) + u[6 + k];
     }
   }
 }
@@ -275,7 +300,7 @@ __global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float
   for (int k = 0; k < 3; ++k) c[k * P + i] = a * g[k * P + i] + b * g[(3 + k) * P + i];
 }
 
-constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * (kRT + 1) + 8 * kOT * kRT);
+constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * kRP + 8 * kOT * kRT);
 
 void init_merge_attributes() {
   cudaFuncSetAttribute(weights_down0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kW0Smem);

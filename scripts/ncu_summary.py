@@ -8,7 +8,7 @@ KEYS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_%"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_pipe_%"),
@@ -18,12 +18,12 @@ KEYS = [
 ]
 
 STAGE_OF = {"dt_rows": "dt_filter", "dt_apply": "dt_filter", "dt_agg": "dt_filter",
-            "dt_link": "dt_filter", "finalize": "finalize_warp", "ssim": "ssim",
+            "dt_link": "dt_filter", "finalize": "finalize_warp", "warp": "finalize_warp", "collapse": "fuse", "ssim": "ssim",
             "weights0": "fuse", "down": "fuse", "collapse0": "fuse"}
 
 
 def unit_scale(unit):
-    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6,
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "us": 1e-6, "ns": 1e-9, "ms": 1e-3,
             "nsecond": 1e-9, "msecond": 1e-3}.get(unit, 1.0)
 
 

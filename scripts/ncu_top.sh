@@ -1,7 +1,9 @@
 # ncu --set full captures of the heaviest kernels of one 5MP pair, one report
 # per kernel (kept small enough for gpurun_out)
 set -x
+only="$*"
 run() {  # name regex skip
+  if [ -n "$only" ] && ! echo " $only " | grep -q " $1 "; then return; fi
   timeout 300 ncu --set full --clock-control none --import-source on -k "regex:$2" -s "$3" -c 1 \
     -o "gpurun_out/prof_$1" -f python scripts/one_pair.py > "gpurun_out/ncu_$1.log" 2>&1
 }
@@ -13,9 +15,9 @@ run finish 'finish_level_kernel' 4
 run weedfit 'weed_fit_kernel' 4
 run ssim 'ssim_fixed_kernel' 0
 run weights0 'weights_down0_kernel' 0
-run collapse0 'collapse_kernel<true>' 0
-run finalize 'finalize_warp_kernel' 0
-run detect 'detect_kernel<true>' 0
+run collapse0 'collapse_kernel' 7
+run warp 'warp_kernel' 0
+run detect 'detect_kernel' 0
 run dt_link 'dt_cols_link' 0
 run down 'down_kernel' 0
 du -sh gpurun_out

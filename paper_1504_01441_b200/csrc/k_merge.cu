@@ -61,32 +61,40 @@ constexpr int kLT = kRT + 2;      // + 1-px laplacian halo (38)
 constexpr int kRP = kRT + 1;      // padded row pitch of the staged region
 
 // 5-tap blur + [::2, ::2] of 8 staged channels px[c][36][kRP] into a 16x16
-// level-1 tile: vertical into V[c][16][36], then horizontal to global.
+// level-1 tile, four channels at a time: vertical into V[4][16][36], then
+// horizontal to global. V needs only 2304 floats, so it can alias the
+// luminance tiles of weights_down0 (the occupancy limit is shared memory).
 __device__ __forceinline__ void down8(const float* px, float* V, int tid, int Y0, int X0,
                                       float* __restrict__ out, int ow, int oh) {
-  // 8 * 16 * 36 = 4608 = 18 * 256 vertical outputs
-  for (int i = tid; i < 8 * kOT * kRT; i += 256) {
-    int q = i / kRT, x = i - q * kRT;  // q = c * 16 + oy
-    int c = q >> 4, oy = q & 15;
-    const float* col = px + (c * kRT + 2 * oy) * kRP + x;
-    float acc = kK5[0] * col[0];
-#pragma unroll
-    for (int k = 1; k < 5; ++k) acc += kK5[k] * col[k * kRP];
-    V[q * kRT + x] = acc;
-  }
-  __syncthreads();
   int P = ow * oh;
-  // 8 * 16 * 16 = 2048 = 8 * 256 horizontal outputs
-#pragma unroll 2
-  for (int i = tid; i < 8 * kOT * kOT; i += 256) {
-    int q = i >> 4, ox = i & 15;
-    int c = q >> 4, oy = q & 15;
-    int Y = Y0 + oy, X = X0 + ox;
-    const float* row = V + q * kRT + 2 * ox;
-    float acc = kK5[0] * row[0];
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const float* src = px + half * 4 * kRT * kRP;
+    // 4 * 16 * 36 = 2304 = 9 * 256 vertical outputs
+#pragma unroll 3
+    for (int i = tid; i < 4 * kOT * kRT; i += 256) {
+      int q = i / kRT, x = i - q * kRT;  // q = c * 16 + oy
+      int c = q >> 4, oy = q & 15;
+      const float* col = src + (c * kRT + 2 * oy) * kRP + x;
+      float acc = kK5[0] * col[0];
 #pragma unroll
-    for (int k = 1; k < 5; ++k) acc += kK5[k] * row[k];
-    if (Y < oh && X < ow) out[c * P + Y * ow + X] = acc;
+      for (int k = 1; k < 5; ++k) acc += kK5[k] * col[k * kRP];
+      V[q * kRT + x] = acc;
+    }
+    __syncthreads();
+    // 4 * 16 * 16 = 1024 = 4 * 256 horizontal outputs
+#pragma unroll
+    for (int i = tid; i < 4 * kOT * kOT; i += 256) {
+      int q = i >> 4, ox = i & 15;
+      int c = q >> 4, oy = q & 15;
+      int Y = Y0 + oy, X = X0 + ox;
+      const float* row = V + q * kRT + 2 * ox;
+      float acc = kK5[0] * row[0];
+#pragma unroll
+      for (int k = 1; k < 5; ++k) acc += kK5[k] * row[k];
+      if (Y < oh && X < ow) out[(half * 4 + c) * P + Y * ow + X] = acc;
+    }
+    __syncthreads();
   }
 }
 
@@ -98,7 +106,7 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   float* lr = smf;                    // [38][38] luminance of ref
   float* lw = smf + kLT * kLT;        // [38][38] luminance of warped
   float* px = smf + 2 * kLT * kLT;    // [8][36][37]: ref rgb, warped rgb, w_ref, w_src
-  float* V = px + 8 * kRT * kRP;      // [8][16][36]
+  float* V = smf;                     // [4][16][36], aliases lr/lw after the weights
   __shared__ int ridx[kLT], cidx[kLT];
   int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
@@ -108,37 +116,72 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
     cidx[tid] = reflect_index(vx0 + tid, w);
   }
   __syncthreads();
+  // every global load of the tile is issued before the first use: the SSIM
+  // and validity of the weight pass (6 per thread) and the RGB of both
+  // frames (6 x 6 per thread)
+  constexpr int kNW = (kRT * kRT + 255) / 256;  // 6
+  constexpr int kNL = (kLT * kLT + 255) / 256;  // 6
+  float svv[kNW];
+  uint8_t vdd[kNW];
   {
+    int ty = tid / kRT, tx = tid - ty * kRT;
+#pragma unroll
+    for (int it = 0; it < kNW; ++it) {
+      int i = tid + it * 256;
+      int p = ridx[min(ty + 1, kLT - 1)] * w + cidx[tx + 1];
+      svv[it] = i < kRT * kRT ? __ldg(ssim + p) : 0.0f;
+      vdd[it] = i < kRT * kRT ? __ldg(valid + p) : 0;
+      tx += 4; ty += 7;  // 256 = 7 * 36 + 4
+      if (tx >= kRT) { tx -= kRT; ++ty; }
+    }
+  }
+  {
+    float rgb[kNL][6];
     int ly = tid / kLT, lx = tid - ly * kLT;
-    for (int i = tid; i < kLT * kLT; i += 256) {
-      int p = (ridx[ly] * w + cidx[lx]) * 3;
-      float r0 = __ldg(ref + p), r1 = __ldg(ref + p + 1), r2 = __ldg(ref + p + 2);
-      float w0 = __ldg(warped + p), w1 = __ldg(warped + p + 1), w2 = __ldg(warped + p + 2);
-      lr[i] = lum_f(r0, r1, r2);
-      lw[i] = lum_f(w0, w1, w2);
-      if ((unsigned)(ly - 1) < (unsigned)kRT && (unsigned)(lx - 1) < (unsigned)kRT) {
-        float* d = px + (ly - 1) * kRP + (lx - 1);
-        d[0] = r0; d[kRT * kRP] = r1; d[2 * kRT * kRP] = r2;
-        d[3 * kRT * kRP] = w0; d[4 * kRT * kRP] = w1; d[5 * kRT * kRP] = w2;
-      }
-      // advance (ly, lx) by 256 = 6 * 38 + 28
-      lx += 28; ly += 6;
+    int lys[kNL], lxs[kNL];
+#pragma unroll
+    for (int it = 0; it < kNL; ++it) {
+      int i = tid + it * 256;
+      lys[it] = ly; lxs[it] = lx;
+      int p = (ridx[min(ly, kLT - 1)] * w + cidx[lx]) * 3;
+      bool ok = i < kLT * kLT;
+      rgb[it][0] = ok ? __ldg(ref + p) : 0.0f;
+      rgb[it][1] = ok ? __ldg(ref + p + 1) : 0.0f;
+      rgb[it][2] = ok ? __ldg(ref + p + 2) : 0.0f;
+      rgb[it][3] = ok ? __ldg(warped + p) : 0.0f;
+      rgb[it][4] = ok ? __ldg(warped + p + 1) : 0.0f;
+      rgb[it][5] = ok ? __ldg(warped + p + 2) : 0.0f;
+      lx += 28; ly += 6;  // 256 = 6 * 38 + 28
       if (lx >= kLT) { lx -= kLT; ++ly; }
+    }
+#pragma unroll
+    for (int it = 0; it < kNL; ++it) {
+      int i = tid + it * 256;
+      if (i >= kLT * kLT) break;
+      lr[i] = lum_f(rgb[it][0], rgb[it][1], rgb[it][2]);
+      lw[i] = lum_f(rgb[it][3], rgb[it][4], rgb[it][5]);
+      if ((unsigned)(lys[it] - 1) < (unsigned)kRT && (unsigned)(lxs[it] - 1) < (unsigned)kRT) {
+        float* d = px + (lys[it] - 1) * kRP + (lxs[it] - 1);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) d[c * kRT * kRP] = rgb[it][c];
+      }
     }
   }
   __syncthreads();
   {
     int ty = tid / kRT, tx = tid - ty * kRT;
-    for (int i = tid; i < kRT * kRT; i += 256) {
+#pragma unroll
+    for (int it = 0; it < kNW; ++it) {
+      int i = tid + it * 256;
+      if (i >= kRT * kRT) break;
       int c = (ty + 1) * kLT + tx + 1;
       double lapr = lap5(lr[c - kLT], lr[c + kLT], lr[c - 1], lr[c + 1], lr[c]);
       double lapw = lap5(lw[c - kLT], lw[c + kLT], lw[c - 1], lw[c + 1], lw[c]);
       float* d = px + ty * kRP + tx;
       float qr = quality_f(lapr, d[0], d[kRT * kRP], d[2 * kRT * kRP]);
       float qs = quality_f(lapw, d[3 * kRT * kRP], d[4 * kRT * kRP], d[5 * kRT * kRP]);
-      int p = ridx[ty + 1] * w + cidx[tx + 1];
-      float sv = fminf(fmaxf(__ldg(ssim + p), 0.0f), 1.0f);
-      qs = __ldg(valid + p) ? qs * sv : 0.0f;
+      float sv = fminf(fmaxf(svv[it], 0.0f), 1.0f);
+      qs = vdd[it] ? qs * sv : 0.0f;
       float inv = __frcp_rn(qr + qs);
       float a = qr * inv, b = qs * inv;
       d[6 * kRT * kRP] = a;
@@ -146,10 +189,10 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
       // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image
       if ((unsigned)(ty - 2) < 2u * kOT && (unsigned)(tx - 2) < 2u * kOT &&
           vy0 + ty + 1 < h && vx0 + tx + 1 < w) {
+        int p = ridx[ty + 1] * w + cidx[tx + 1];
         wr_out[p] = a;
         ws_out[p] = b;
       }
-      // advance (ty, tx) by 256 = 7 * 36 + 4
       tx += 4; ty += 7;
       if (tx >= kRT) { tx -= kRT; ++ty; }
     }
@@ -159,13 +202,13 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
 }
 
 // ---------------------------------------------------------------- levels >= 1
-constexpr size_t kDownSmem = sizeof(float) * (8 * kRT * kRP + 8 * kOT * kRT);
+constexpr size_t kDownSmem = sizeof(float) * (8 * kRT * kRP + 4 * kOT * kRT);
 
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
                                                    float* __restrict__ out, int ow, int oh) {
   extern __shared__ float smd[];
   float* tile = smd;               // [8][36][37]
-  float* V = smd + 8 * kRT * kRP;  // [8][16][36]
+  float* V = smd + 8 * kRT * kRP;  // [4][16][36]
   __shared__ int ridx[kRT], cidx[kRT];
   int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
@@ -178,12 +221,28 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
   int P = w * h;
   {
     int ty = tid / kRT, tx = tid - ty * kRT;
-    for (int i = tid; i < kRT * kRT; i += 256) {
-      const float* src = in + ridx[ty] * w + cidx[tx];
-      float* d = tile + ty * kRP + tx;
+    // two region samples (16 loads) in flight per step
+#pragma unroll 1
+    for (int i = tid; i < kRT * kRT; i += 512) {
+      int ty2 = ty + 7, tx2 = tx + 4;
+      if (tx2 >= kRT) { tx2 -= kRT; ++ty2; }
+      bool ok2 = i + 256 < kRT * kRT;
+      const float* s1 = in + ridx[ty] * w + cidx[tx];
+      const float* s2 = in + ridx[min(ty2, kRT - 1)] * w + cidx[tx2];
+      float v1[8], v2[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) d[c * kRT * kRP] = __ldg(src + c * P);
-      tx += 4; ty += 7;
+      for (int c = 0; c < 8; ++c) {
+        v1[c] = __ldg(s1 + c * P);
+        v2[c] = ok2 ? __ldg(s2 + c * P) : 0.0f;
+      }
+      float* d1 = tile + ty * kRP + tx;
+      float* d2 = tile + ty2 * kRP + tx2;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        d1[c * kRT * kRP] = v1[c];
+        if (ok2) d2[c * kRT * kRP] = v2[c];
+      }
+      ty = ty2 + 7; tx = tx2 + 4;
       if (tx >= kRT) { tx -= kRT; ++ty; }
     }
   }
@@ -300,7 +359,8 @@ __global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float
   for (int k = 0; k < 3; ++k) c[k * P + i] = a * g[k * P + i] + b * g[(3 + k) * P + i];
 }
 
-constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * kRP + 8 * kOT * kRT);
+constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * kRP);
+static_assert(4 * kOT * kRT <= 2 * kLT * kLT, "V aliases the luminance tiles");
 
 void init_merge_attributes() {
   cudaFuncSetAttribute(weights_down0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kW0Smem);

@@ -92,6 +92,11 @@ int hdr_ctx_destroy(hdr_ctx* ctx);
 int hdr_ctx_set_stream(hdr_ctx* ctx, void* stream);
 int32_t hdr_max_matches(int32_t width, int32_t height, int32_t tile);
 const char* hdr_last_error(void);
+/* Implementation switches for testing equivalent kernel paths (process-wide;
+ * no reference counterpart). "dt_cluster_columns": 1 (default) = one
+ * cluster-resident kernel per column sweep pair, 0 = chunk agg/link/apply.
+ * Returns HDR_ERR_INVALID for an unknown name. */
+int hdr_set_option(const char* name, int64_t value);
 /* Blocks until the context's stream drains; returns HDR_ERR_CUDA on a
  * sticky or asynchronous CUDA error. */
 int hdr_ctx_sync(hdr_ctx* ctx);

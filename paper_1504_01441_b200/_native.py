@@ -53,6 +53,7 @@ SIGNATURES = {
     "hdr_ctx_set_stream": (_I, [_P, _P]),
     "hdr_max_matches": (_I, [_I, _I, _I]),
     "hdr_last_error": (ctypes.c_char_p, []),
+    "hdr_set_option": (_I, [ctypes.c_char_p, ctypes.c_int64]),
     "hdr_ctx_sync": (_I, [_P]),
     "hdr_register_and_fuse": (_I, [_P, _P, _I, _I, _P, _P, _P]),
     "hdr_register_and_fuse_graph": (_I, [_P, _P, _I, _I, _P, _P, _P]),

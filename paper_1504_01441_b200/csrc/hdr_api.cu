@@ -42,6 +42,14 @@ static int check_launch() {
 
 extern "C" const char* hdr_last_error(void) { return g_err.c_str(); }
 
+extern "C" int hdr_set_option(const char* name, int64_t value) {
+  if (name && std::string(name) == "dt_cluster_columns") {
+    hdr::dt_set_cluster_columns(value != 0);
+    return HDR_OK;
+  }
+  return fail(HDR_ERR_INVALID, std::string("unknown option: ") + (name ? name : "(null)"));
+}
+
 // ------------------------------------------------------------ SeedSequence
 // numpy.random.SeedSequence (numpy/random/bit_generator.pyx), host side.
 namespace {

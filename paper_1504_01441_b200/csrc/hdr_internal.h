@@ -110,6 +110,7 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
                   int h, DtPlanes maps, uint64_t* scratch_key, int32_t* scratch_idx,
                   int32_t* status, cudaStream_t s);
 int64_t dt_scratch_doubles(int w, int h, int k);
+void dt_set_cluster_columns(bool on);
 // optional fused densify-finalise for the last column pass (K == 3)
 struct DtFlowOut {
   const double* fallback;   // 3x3 H or null

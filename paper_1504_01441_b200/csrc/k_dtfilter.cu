@@ -19,6 +19,9 @@
 #include "hdr_common.cuh"
 #include "hdr_internal.h"
 #include "hdr_planes.cuh"
+#include "hdr_bulk.cuh"
+
+#include <cooperative_groups.h>
 
 namespace hdr {
 
@@ -250,6 +253,113 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_reg_kernel(const float* _
   for (int i = threadIdx.x; i < w; i += blockDim.x)
 #pragma unroll
     for (int k = 0; k < K; ++k) stp(P, k, row + i, xs[k * w + i]);
+}
+
+// Row pass with the row moved by bulk copies: one thread issues the K plane
+// rows and the guide row (one cp.async.bulk each) and the results go back the
+// same way, so the 256 threads only compute. Needs all planes f64 and
+// 16-byte aligned rows (w % 4 == 0, aligned bases); w <= kRowThreads*kRowSeg.
+template <int K>
+__global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* __restrict__ guide,
+                                                                   DtPlanes P, int w, int h,
+                                                                   double ratio, double c) {
+  extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
+  float* gs = reinterpret_cast<float*>(xs + K * w);
+  __shared__ Aff<K> wsum[kRowThreads / 32];
+  __shared__ uint64_t bar;
+  int y = blockIdx.x;
+  int64_t row = (int64_t)y * w;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (uint32_t)(K * w * 8 + w * 4));
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      bulk_load(xs + k * w, reinterpret_cast<const double*>(P.p[k]) + row, (uint32_t)w * 8, &bar);
+    bulk_load(gs, guide + row, (uint32_t)w * 4, &bar);
+  }
+  const int L = (w + kRowThreads - 1) / kRowThreads;
+  int s0 = threadIdx.x * L, n = max(0, min(w, s0 + L) - s0);
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+  // af[j] couples samples s0-1+j and s0+j (0 outside the row)
+  double af[kRowSeg + 1];
+#pragma unroll
+  for (int j = 0; j <= kRowSeg; ++j) {
+    int i = s0 - 1 + j;
+    af[j] = (j <= n && i >= 0 && i + 1 < w) ? dt_coef(gs[i], gs[i + 1], ratio, c) : 0.0;
+  }
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kRowThreads >> 5;
+  // ---- forward
+  Aff<K> m;
+  m.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = 0.0;
+#pragma unroll
+  for (int j = 0; j < kRowSeg; ++j)
+    if (j < n) {
+      double a = af[j];
+      m.A *= a;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { double x = xs[k * w + s0 + j]; m.B[k] = x + a * (m.B[k] - x); }
+    }
+  Aff<K> pre;
+  row_block_scan<K>(m, true, wsum, lane, warp, nw, pre);
+  double prev[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) prev[k] = pre.B[k];
+#pragma unroll
+  for (int j = 0; j < kRowSeg; ++j)
+    if (j < n) {
+      double a = af[j];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double x = xs[k * w + s0 + j];
+        prev[k] = x + a * (prev[k] - x);
+        xs[k * w + s0 + j] = prev[k];
+      }
+    }
+  // ---- backward
+  m.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = 0.0;
+#pragma unroll
+  for (int j = kRowSeg - 1; j >= 0; --j)
+    if (j < n) {
+      double a = af[j + 1];
+      m.A *= a;
+#pragma unroll
+      for (int k = 0; k < K; ++k) { double x = xs[k * w + s0 + j]; m.B[k] = x + a * (m.B[k] - x); }
+    }
+  row_block_scan<K>(m, false, wsum, lane, warp, nw, pre);
+#pragma unroll
+  for (int k = 0; k < K; ++k) prev[k] = pre.B[k];
+#pragma unroll
+  for (int j = kRowSeg - 1; j >= 0; --j)
+    if (j < n) {
+      double a = af[j + 1];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double x = xs[k * w + s0 + j];
+        prev[k] = x + a * (prev[k] - x);
+        xs[k * w + s0 + j] = prev[k];
+      }
+    }
+  fence_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      bulk_store(reinterpret_cast<double*>(P.p[k]) + row, xs + k * w, (uint32_t)w * 8);
+    bulk_commit();
+    bulk_wait_read();
+  }
+}
+
+static bool rows_bulk_ok(const float* guide, const DtPlanes& P, int w) {
+  if (w % 4 || w > kRowThreads * kRowSeg || (reinterpret_cast<uintptr_t>(guide) & 15)) return false;
+  for (int k = 0; k < P.k; ++k)
+    if (!P.f64[k] || (reinterpret_cast<uintptr_t>(P.p[k]) & 15)) return false;
+  return true;
 }
 
 // ---------------------------------------------------------------- columns
@@ -488,6 +598,238 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
       for (int k = 0; k < K; ++k) stp(P, k, (int64_t)(r0 + j) * w + x, ck.x[k][j]);
 }
 
+// ---------------------------------------------------------------- columns, cluster-resident
+// One column sweep pair (down then up) in a single kernel. A cluster of kCL
+// CTAs owns a band of `bw` columns over the full image height: CTA `rank`
+// holds rows [rank*RP, (rank+1)*RP), split into G = kCT / bw groups of kSR
+// rows; thread (col, grp) keeps its kSR x K samples and kSR+1 coefficients in
+// registers from load to store. The chunk aggregates of dt_cols_agg are
+// linked by a Hillis-Steele scan over the groups in shared memory and across
+// the cluster through distributed shared memory (one barrier.cluster per
+// direction), so a sweep pair costs one HBM read and one write of the planes
+// instead of agg + link + apply's two reads, one write and the carry traffic.
+constexpr int kCL = 8;    // CTAs per cluster (portable maximum)
+constexpr int kCT = 256;  // threads per CTA (two CTAs per SM)
+constexpr int kCTLog2 = 8;
+constexpr int kSR = 8;    // rows per thread
+
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int K, bool FINAL>
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
+    dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
+                    double c, int bw_log2, DtFlowOut fo) {
+  __shared__ Aff<K> maps[kCT];           // [grp][col]
+  __shared__ Aff<K> ctaF[kCT / 4], ctaB[kCT / 4];  // per-column CTA totals (bw <= kCT / 4)
+  __shared__ double cin[kCT / 4][K], din[kCT / 4][K];
+  __shared__ Aff<K> remote[kCL][kCT / 4];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int bw = 1 << bw_log2, G = kCT >> bw_log2;
+  const int col = threadIdx.x & (bw - 1), grp = threadIdx.x >> bw_log2;
+  const int RP = ceil_div(h, kCL);
+  const int x = (blockIdx.y << bw_log2) + col;
+  const int r0 = rank * RP + grp * kSR;
+  const int rend = min(h, (rank + 1) * RP);
+  const bool live = x < w;
+  const int n = live ? max(0, min(kSR, rend - r0)) : 0;
+  // ---- load (all requests issued before the first use)
+  double xv[K][kSR];
+  double a[kSR + 1];  // a[j] couples rows r0-1+j and r0+j
+  {
+    float g[kSR + 2];
+#pragma unroll
+    for (int j = 0; j < kSR + 2; ++j) {
+      int y = r0 - 1 + j;
+      g[j] = (live && j <= n + 1 && y >= 0 && y < h) ? __ldg(guide + (int64_t)y * w + x) : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < kSR; ++j)
+#pragma unroll
+      for (int k = 0; k < K; ++k) xv[k][j] = (j < n) ? ldp(P, k, (int64_t)(r0 + j) * w + x) : 0.0;
+#pragma unroll
+    for (int j = 0; j <= kSR; ++j) {
+      int y = r0 - 1 + j;
+      a[j] = (n > 0 && j <= n && y >= 0 && y + 1 < h) ? dt_coef(g[j], g[j + 1], ratio, c) : 0.0;
+    }
+  }
+  // ---- chunk aggregates (see dt_cols_agg)
+  double Pp = 1.0, R = 0.0, Q = 1.0;
+  double y0[K], z0[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) { y0[k] = 0.0; z0[k] = 0.0; }
+#pragma unroll
+  for (int j = 0; j < kSR; ++j)
+    if (j < n) {
+      double ap = a[j], an = a[j + 1];
+      Pp *= ap;
+#pragma unroll
+      for (int k = 0; k < K; ++k) y0[k] = xv[k][j] + ap * (y0[k] - xv[k][j]);
+      double wgt = (1.0 - an) * Q;
+#pragma unroll
+      for (int k = 0; k < K; ++k) z0[k] += wgt * y0[k];
+      R += wgt * Pp;
+      Q *= an;
+    }
+  // ---- forward link: inclusive scan over groups, then across the cluster
+  Aff<K> m;
+  m.A = Pp;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = y0[k];
+  maps[threadIdx.x] = m;
+  __syncthreads();
+  for (int off = 1; off < G; off <<= 1) {
+    Aff<K> o = maps[grp >= off ? threadIdx.x - (off << bw_log2) : threadIdx.x];
+    __syncthreads();
+    if (grp >= off) { m = compose(o, m); maps[threadIdx.x] = m; }
+    __syncthreads();
+  }
+  if (grp == G - 1) ctaF[col] = m;
+  Aff<K> ex;  // exclusive prefix of this group
+  if (grp > 0) {
+    ex = maps[threadIdx.x - bw];
+  } else {
+    ex.A = 1.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) ex.B[k] = 0.0;
+  }
+  cl.sync();
+  // gather the lower ranks' totals for this column (one remote load per thread)
+  for (int q = grp; q < rank; q += G) remote[q][col] = *cl.map_shared_rank(&ctaF[col], q);
+  __syncthreads();
+  if (grp == 0) {
+    double C[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) C[k] = 0.0;
+    for (int q = 0; q < rank; ++q) {
+      const Aff<K>& t = remote[q][col];
+#pragma unroll
+      for (int k = 0; k < K; ++k) C[k] = t.A * C[k] + t.B[k];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) cin[col][k] = C[k];
+  }
+  __syncthreads();
+  double C[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) C[k] = ex.A * cin[col][k] + ex.B[k];
+  // ---- backward link: suffix scan of z_start(g) = Q_g z_start(g+1) + (Z0_g + C_g R_g)
+  m.A = Q;
+#pragma unroll
+  for (int k = 0; k < K; ++k) m.B[k] = z0[k] + C[k] * R;
+  maps[threadIdx.x] = m;
+  __syncthreads();
+  for (int off = 1; off < G; off <<= 1) {
+    Aff<K> o = maps[grp + off < G ? threadIdx.x + (off << bw_log2) : threadIdx.x];
+    __syncthreads();
+    if (grp + off < G) { m = compose(o, m); maps[threadIdx.x] = m; }
+    __syncthreads();
+  }
+  if (grp == 0) ctaB[col] = m;
+  Aff<K> sx;  // suffix from the next group down
+  if (grp + 1 < G) {
+    sx = maps[threadIdx.x + bw];
+  } else {
+    sx.A = 1.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) sx.B[k] = 0.0;
+  }
+  cl.sync();
+  for (int q = rank + 1 + grp; q < kCL; q += G) remote[q][col] = *cl.map_shared_rank(&ctaB[col], q);
+  __syncthreads();
+  if (grp == 0) {
+    double D[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) D[k] = 0.0;
+    for (int q = kCL - 1; q > rank; --q) {
+      const Aff<K>& t = remote[q][col];
+#pragma unroll
+      for (int k = 0; k < K; ++k) D[k] = t.A * D[k] + t.B[k];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) din[col][k] = D[k];
+  }
+  // peers may still read ctaB; the matching wait is just before exit
+  cluster_arrive();
+  __syncthreads();
+  double D[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) D[k] = sx.A * din[col][k] + sx.B[k];
+  // ---- apply: forward from C, backward from D, with the reference update
+  if (n > 0) {
+    double prev[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) prev[k] = C[k];
+#pragma unroll
+    for (int j = 0; j < kSR; ++j)
+      if (j < n) {
+        double ap = a[j];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          double v = xv[k][j];
+          prev[k] = v + ap * (prev[k] - v);
+          xv[k][j] = prev[k];
+        }
+      }
+#pragma unroll
+    for (int k = 0; k < K; ++k) prev[k] = D[k];
+#pragma unroll
+    for (int j = kSR - 1; j >= 0; --j)
+      if (j < n) {
+        double an = a[j + 1];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          double v = xv[k][j];
+          prev[k] = v + an * (prev[k] - v);
+          xv[k][j] = prev[k];
+        }
+      }
+    if (FINAL) {
+      bool use_fb = fo.fallback && (!fo.has_fb || *fo.has_fb);
+#pragma unroll
+      for (int j = 0; j < kSR; ++j)
+        if (j < n) {
+          double nv = xv[K - 1][j];
+          float fu = 0.0f, fv = 0.0f;
+          if (nv > fo.floor_) {
+            fu = (float)(xv[0][j] / nv);
+            fv = (float)(xv[K > 2 ? 1 : 0][j] / nv);
+          } else if (use_fb) {
+            h_pixel_flow(fo.fallback, x, r0 + j, w, h, &fu, &fv);
+          }
+          reinterpret_cast<float2*>(fo.flow)[(int64_t)(r0 + j) * w + x] = make_float2(fu, fv);
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSR; ++j)
+        if (j < n)
+#pragma unroll
+          for (int k = 0; k < K; ++k) stp(P, k, (int64_t)(r0 + j) * w + x, xv[k][j]);
+    }
+  }
+  cluster_wait();
+}
+
+// log2 of the cluster kernel's band width for this height, or -1 (too tall)
+static int cluster_bw_log2(int h) {
+  int rp = ceil_div(h, kCL);
+  int g = ceil_div(rp, kSR), gl = 0;
+  while ((1 << gl) < g) ++gl;
+  if (gl < 2) gl = 2;  // bw <= kCT / 4
+  int bl = kCTLog2 - gl;
+  return bl >= 2 ? bl : -1;
+}
+
+// test hook: 0 selects the agg/link/apply column path
+static bool g_cols_cluster = true;
+
 template <int K>
 static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sigma_s,
                         double sigma_r, int passes, double* scratch, const DtFlowOut& fo,
@@ -505,13 +847,25 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     double sigma_i = sigma_s * sqrt(3.0) * pow(2.0, passes - i) / den;  // densify.py:104
     double c = -root / sigma_i;
     if (w > 1) {
-      if (w <= kRowThreads * kRowSeg)
+      if (rows_bulk_ok(guide, P, w))
+        dt_rows_bulk_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double) + (size_t)w * 4, s>>>(
+            guide, P, w, h, ratio, c);
+      else if (w <= kRowThreads * kRowSeg)
         dt_rows_reg_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double), s>>>(guide, P, w, h,
                                                                                     ratio, c);
       else
         dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
     }
-    if (h > 1) {
+    int bl = cluster_bw_log2(h);
+    if (h > 1 && bl >= 0 && g_cols_cluster) {
+      dim3 cgrid(kCL, ceil_div(w, 1 << bl));
+      if (i == passes && fo.flow && K == 3) {
+        dt_cols_cluster<K, true><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
+        finalized = true;
+      } else {
+        dt_cols_cluster<K, false><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
+      }
+    } else if (h > 1) {
       dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
       dt_cols_link<K><<<ceil_div(w, 32), 1024, 0, s>>>(w, nch, agg, carry);
       if (i == passes && fo.flow && K == 3) {
@@ -530,6 +884,8 @@ int64_t dt_scratch_doubles(int w, int h, int k) {
   return (int64_t)nch * w * (3 + 2 * k) + (int64_t)nch * w * 2 * k + (int64_t)w * h + 64;
 }
 
+void dt_set_cluster_columns(bool on) { g_cols_cluster = on; }
+
 void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_kernel<1>);
   allow_max_dynamic_smem(dt_rows_kernel<2>);
@@ -537,6 +893,9 @@ void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_reg_kernel<1>);
   allow_max_dynamic_smem(dt_rows_reg_kernel<2>);
   allow_max_dynamic_smem(dt_rows_reg_kernel<3>);
+  allow_max_dynamic_smem(dt_rows_bulk_kernel<1>);
+  allow_max_dynamic_smem(dt_rows_bulk_kernel<2>);
+  allow_max_dynamic_smem(dt_rows_bulk_kernel<3>);
 }
 
 bool launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,

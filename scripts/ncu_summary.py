@@ -18,7 +18,7 @@ KEYS = [
 ]
 
 STAGE_OF = {"dt_rows": "dt_filter", "dt_apply": "dt_filter", "dt_agg": "dt_filter",
-            "dt_link": "dt_filter", "finalize": "finalize_warp", "warp": "finalize_warp", "collapse": "fuse", "ssim": "ssim",
+            "dt_link": "dt_filter", "dt_cols": "dt_filter", "finalize": "finalize_warp", "warp": "finalize_warp", "collapse": "fuse", "ssim": "ssim",
             "weights0": "fuse", "down": "fuse", "collapse0": "fuse"}
 
 

@@ -7,9 +7,10 @@ run() {  # name regex skip
   timeout 300 ncu --set full --clock-control none --import-source on -k "regex:$2" -s "$3" -c 1 \
     -o "gpurun_out/prof_$1" -f python scripts/one_pair.py > "gpurun_out/ncu_$1.log" 2>&1
 }
-run dt_rows 'dt_rows_reg_kernel' 0
+run dt_rows 'dt_rows_bulk_kernel' 0
 run dt_apply 'dt_cols_apply' 0
 run dt_agg 'dt_cols_agg' 0
+run dt_cols 'dt_cols_cluster' 0
 run ssd 'ssd_tiles_kernel' 4
 run finish 'finish_level_kernel' 4
 run weedfit 'weed_fit_kernel' 4

@@ -22,6 +22,7 @@
 #include "hdr_bulk.cuh"
 
 #include <cooperative_groups.h>
+#include <algorithm>
 
 namespace hdr {
 
@@ -635,7 +636,11 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
   const int bw = 1 << bw_log2, G = kCT >> bw_log2;
   const int col = threadIdx.x & (bw - 1), grp = threadIdx.x >> bw_log2;
   const int RP = ceil_div(h, kCL);
-  const int x = (blockIdx.y << bw_log2) + col;
+  const int nbands = ceil_div(w, bw);
+  // persistent: the grid holds as many clusters as can be co-resident and
+  // each walks bands (no cluster-launch fragmentation between waves)
+  for (int band = blockIdx.y; band < nbands; band += gridDim.y) {
+  const int x = (band << bw_log2) + col;
   const int r0 = rank * RP + grp * kSR;
   const int rend = min(h, (rank + 1) * RP);
   const bool live = x < w;
@@ -799,8 +804,11 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
           double nv = xv[K - 1][j];
           float fu = 0.0f, fv = 0.0f;
           if (nv > fo.floor_) {
-            fu = (float)(xv[0][j] / nv);
-            fv = (float)(xv[K > 2 ? 1 : 0][j] / nv);
+            // one reciprocal: the f64 quotient differs by at most an ulp,
+            // far below the f32 rounding of the flow
+            double inv = 1.0 / nv;
+            fu = (float)(xv[0][j] * inv);
+            fv = (float)(xv[K > 2 ? 1 : 0][j] * inv);
           } else if (use_fb) {
             h_pixel_flow(fo.fallback, x, r0 + j, w, h, &fu, &fv);
           }
@@ -815,6 +823,25 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
     }
   }
   cluster_wait();
+  }
+}
+
+// co-resident clusters of a cluster-kernel instantiation (0 = query failed)
+template <int K, bool FINAL>
+static int max_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kCL, 1024);
+    cfg.blockDim = dim3(kCT);
+    int v = 0;
+    if (cudaOccupancyMaxActiveClusters(&v, dt_cols_cluster<K, FINAL>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      v = 0;
+    }
+    n = v;
+  }
+  return n;
 }
 
 // log2 of the cluster kernel's band width for this height, or -1 (too tall)
@@ -858,8 +885,11 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     }
     int bl = cluster_bw_log2(h);
     if (h > 1 && bl >= 0 && g_cols_cluster) {
-      dim3 cgrid(kCL, ceil_div(w, 1 << bl));
-      if (i == passes && fo.flow && K == 3) {
+      int nb = ceil_div(w, 1 << bl);
+      bool fin = i == passes && fo.flow && K == 3;
+      int mc = fin ? max_clusters<K, true>() : max_clusters<K, false>();
+      dim3 cgrid(kCL, mc > 0 ? std::min(nb, mc) : nb);
+      if (fin) {
         dt_cols_cluster<K, true><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
         finalized = true;
       } else {

@@ -70,39 +70,66 @@ class BatchRunner:
 
     # ---------------------------------------------------------- host path
     def _ensure_staging(self):
+        """Two device slots per compute stream (inputs + outputs), so the
+        upload of a stream's next pair and the download of its previous one
+        overlap its current pair."""
         if self._staging is None:
             h, w = self.height, self.width
             dev = f"cuda:{self.device}"
-            self._staging = [dict(ref=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
-                                  src=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
-                                  out=PairBuffers(w, h, self.device))
-                             for _ in self.streams]
+            self._staging = [[dict(ref=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                                   src=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                                   out=PairBuffers(w, h, self.device),
+                                   consumed=None, drained=None)
+                              for _ in range(2)] for _ in self.streams]
+            self._h2d = torch.cuda.Stream(self.device)
+            self._d2h = torch.cuda.Stream(self.device)
         return self._staging
 
     def run_host(self, host_pairs, host_out, start_event=None, stop_event=None):
         """End to end: pinned host (ref, src) in, composite + info words out.
 
         host_out[k] = (composite pinned (h, w, 3) f32, info pinned (32,) i32).
-        Returns the H2D / D2H byte counts of the batch."""
+        Uploads run back to back on one copy stream (the host link is the
+        bottleneck of this path), pairs on the compute streams, downloads on a
+        second copy stream; events order each slot's reuse. Returns the H2D /
+        D2H byte counts of the batch."""
         st = self._ensure_staging()
         cur = torch.cuda.current_stream(self.device)
         if start_event is not None:
             start_event.record(cur)
-        for s in self.streams:
+        for s in self.streams + [self._h2d, self._d2h]:
             s.wait_stream(cur)
         h2d = d2h = 0
+        S = len(self.streams)
         for k, ((href, hsrc), (hcomp, hinfo)) in enumerate(zip(host_pairs, host_out)):
-            j = k % len(self.streams)
-            slot = st[j]
-            with torch.cuda.stream(self.streams[j]):
+            j = k % S
+            slot = st[j][(k // S) % 2]
+            cs = self.streams[j]
+            with torch.cuda.stream(self._h2d):
+                if slot["consumed"] is not None:      # previous pair of this slot read its inputs
+                    self._h2d.wait_event(slot["consumed"])
                 slot["ref"].copy_(href, non_blocking=True)
                 slot["src"].copy_(hsrc, non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(self._h2d)
+            cs.wait_event(loaded)
+            if slot["drained"] is not None:           # previous outputs of this slot downloaded
+                cs.wait_event(slot["drained"])
+            with torch.cuda.stream(cs):
                 self.enqueue(j, slot["ref"], slot["src"], slot["out"])
+                done = torch.cuda.Event()
+                done.record(cs)
+            slot["consumed"] = done
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(done)
                 hcomp.copy_(slot["out"].composite, non_blocking=True)
                 hinfo.copy_(slot["out"].info, non_blocking=True)
+                drained = torch.cuda.Event()
+                drained.record(self._d2h)
+            slot["drained"] = drained
             h2d += href.numel() * 4 + hsrc.numel() * 4
             d2h += hcomp.numel() * 4 + hinfo.numel() * 4
-        for s in self.streams:
+        for s in self.streams + [self._h2d, self._d2h]:
             cur.wait_stream(s)
         if stop_event is not None:
             stop_event.record(cur)

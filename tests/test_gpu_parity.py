@@ -269,3 +269,33 @@ def test_5mp_pair_end_to_end(cuda):
     res = pipeline.register_and_fuse(st.ref, st.src)
     o = O.register_and_fuse(st.ref, st.src)
     check_pair(res, o)
+
+
+def test_batch_runner_host_and_device_paths(cuda):
+    """The throughput runner (several streams, graph replays, double-buffered
+    host path) returns, pair for pair, what the single-pair API returns."""
+    from paper_1504_01441_b200.runner import BatchRunner
+    from paper_1504_01441_b200.pipeline import PairBuffers
+    from paper_1504_01441_b200 import _native
+    w, h = 320, 240
+    stacks = [synth.synth_stack(synth.working_spec(w, h), s) for s in (2, 7, 9)]
+    want = [pipeline.register_and_fuse(st.ref, st.src) for st in stacks]
+    r = BatchRunner(w, h, streams=2)
+    n = 7  # odd, > 2 slots per stream: exercises slot reuse ordering
+    hp = [(torch.from_numpy(stacks[k % 3].ref).pin_memory(),
+           torch.from_numpy(stacks[k % 3].src).pin_memory()) for k in range(n)]
+    ho = [(torch.empty((h, w, 3), dtype=torch.float32).pin_memory(),
+           torch.empty((_native.INFO_WORDS,), dtype=torch.int32).pin_memory()) for _ in range(n)]
+    for _ in range(2):
+        r.run_host(hp, ho)
+    torch.cuda.synchronize()
+    for k in range(n):
+        np.testing.assert_array_equal(ho[k][0].numpy(), np.asarray(want[k % 3].composite))
+    dev = [(a.cuda(), b.cuda()) for a, b in hp]
+    outs = [PairBuffers(w, h, torch.cuda.current_device()) for _ in range(n)]
+    r.run_device(dev, outs)
+    torch.cuda.synchronize()
+    for k in range(n):
+        np.testing.assert_array_equal(outs[k].composite.cpu().numpy(),
+                                      np.asarray(want[k % 3].composite))
+    r.close()

@@ -148,15 +148,36 @@ def stage_bytes(w, h, passes=3):
     return {
         # both RGB frames in; lum_ref f32, q_src u8, eq_src f32, pyramids out
         "raster": P * (24 + 4 + 1 + 4) + 2 * 4 * P // 3,
-        # splat memsets (3 f64 planes) + per pass: rows R+W, column aggregate
-        # R, column apply R+W of 3 f64 planes, + the f32 guide per kernel;
-        # the last apply writes the f32 flow (8 B) instead of the planes (24)
-        "dt_filter": P * 24 + passes * P * (52 + 28 + 52) - P * 16,
+        # splat memsets (3 f64 planes), then per pass a row sweep and a column
+        # sweep pair, each reading the guide (4 B) and the 3 f64 planes (24 B)
+        # and writing the planes (24 B); the last column pass writes the f32
+        # flow (8 B) instead of the planes
+        "dt_filter": P * 24 + passes * 2 * P * 52 - P * 16,
         # warp_image: flow 8 + src 12 in; warped 12, valid 1, q 1 out
         "finalize_warp": P * (8 + 12 + 12 + 1 + 1),
         "ssim": P * (4 + 1 + 4),
         # SURVEY.md §8(d) merge: ref 12, warped 12, SSIM 4, valid 1, composite 12
         "fuse": P * 41,
+    }
+
+
+def kernel_bytes(w, h, passes=3):
+    """Algorithmic HBM bytes per pair of each probed kernel family (all its
+    launches in one pair) and the launch count."""
+    P = w * h
+    return {
+        # read guide 4 + 3 f64 planes 24, write the planes 24
+        "dt_rows": (passes * P * 52, passes),
+        # same per column sweep pair; the last one writes the f32 flow (8)
+        "dt_cols": ((passes - 1) * P * 52 + P * 36, passes),
+        # flow 8 + src 12 in; warped 12, valid 1, q 1 out
+        "warp": (P * 34, 1),
+        # lum_ref 4 + q(warped) 1 in, ssim 4 out
+        "ssim": (P * 9, 1),
+        # ref 12, warped 12, ssim 4, valid 1 in; weights 8 + level-1 Gaussian (8 ch / 4) 8 out
+        "fuse_weights0": (P * 45, 1),
+        # ref 12, warped 12, weights 8, level-1 G (8 ch / 4) 8 + C (3 ch / 4) 3 in; composite 12 out
+        "fuse_collapse0": (P * 55, 1),
     }
 
 
@@ -169,6 +190,8 @@ def peaks():
 
 
 def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, by kernel
+    family, from the committed ncu --set full captures (profiles/)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
         return json.load(open(path))
@@ -297,25 +320,40 @@ def run_ours(args):
         v = [probes[k][2 * s_i].elapsed_time(probes[k][2 * s_i + 1]) for k in range(B)]
         stage_ms_conc[name] = statistics.mean(v)
     kernels_per_pair = runner.graph_kernels()
-    # isolated stage times: the same pipeline, one pair at a time on one
-    # stream, events recorded on that stream between the stages
-    iso = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(3)]
-    for evs in iso:
+    # isolated stage and kernel times: the same pipeline, one pair at a time
+    # on one stream, events recorded on that stream between the stages and
+    # around every launch of the probed kernel families
+    NI = 3
+    iso = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(NI)]
+    kfam = _native.KPROBES
+    kev = [[[torch.cuda.Event(enable_timing=True) for _ in range(16)] for _ in kfam] for _ in range(NI)]
+    for evs in iso + [e for run in kev for e in run]:
         for e in evs:
             e.record()
     torch.cuda.synchronize()
     s0 = runner.streams[0]
-    for j, evs in enumerate(iso):
-        runner.set_probes(0, evs)
+    for j in range(NI):
+        runner.set_probes(0, iso[j])
+        for f in range(len(kfam)):
+            runner.set_kernel_probes(0, f, kev[j][f])
         s0.wait_stream(torch.cuda.current_stream())
         runner.enqueue(0, pairs[j % B][0], pairs[j % B][1], outs[0])
         torch.cuda.current_stream().wait_stream(s0)
         torch.cuda.synchronize()
     runner.set_probes(0, None)
+    for f in range(len(kfam)):
+        runner.set_kernel_probes(0, f, None)
     stage_ms = {}
     for s_i, name in enumerate(_native.STAGES):
         stage_ms[name] = statistics.median(
-            iso[j][2 * s_i].elapsed_time(iso[j][2 * s_i + 1]) for j in range(len(iso)))
+            iso[j][2 * s_i].elapsed_time(iso[j][2 * s_i + 1]) for j in range(NI))
+    kb = kernel_bytes(w, h)
+    kernel_ms = {}
+    for f, name in enumerate(kfam):
+        n = kb[name][1]
+        kernel_ms[name] = statistics.median(
+            sum(kev[j][f][2 * i].elapsed_time(kev[j][f][2 * i + 1]) for i in range(n))
+            for j in range(NI))
 
     # ---- end to end through the public batch API (host buffers)
     E = args.e2e_pairs
@@ -343,23 +381,56 @@ def run_ours(args):
     e2e_ok = all(int(x[1][0]) == 0 for x in hout)
     ems = hd.max_over_ranks(e0.elapsed_time(e1), device=dev)
 
+    # ---- end to end on the file path: the same scenes as
+    # 8-bit PNG samples (what run_hdr reads), raw bytes over PCIe, the 8-bit
+    # composite (save_png's samples) back
+    q8 = lambda a: np.clip(np.floor(a.astype(np.float64) * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    rpairs = []
+    for k in range(E):
+        ref, src = scenes[k % len(scenes)]
+        rpairs.append((torch.from_numpy(q8(ref)).pin_memory(), torch.from_numpy(q8(src)).pin_memory()))
+    rout = [(torch.empty((h, w, 3), dtype=torch.uint8).pin_memory(),
+             torch.empty((_native.INFO_WORDS,), dtype=torch.int32).pin_memory()) for _ in range(E)]
+    for _ in range(max(args.warmup, 1)):
+        runner.run_host_raw(rpairs, rout, 8)
+    torch.cuda.synchronize()
+    hd.barrier()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record()
+    rh2d = rd2h = 0
+    for _ in range(args.steps):
+        rh2d, rd2h = runner.run_host_raw(rpairs, rout, 8)
+    r1.record()
+    torch.cuda.synchronize()
+    raw_ok = all(int(x[1][0]) == 0 for x in rout)
+    rms = hd.max_over_ranks(r0.elapsed_time(r1), device=dev)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     value = world * B * args.steps / (ms / 1e3)
     e2e_value = world * E * args.steps / (ems / 1e3)
+    png8_value = world * E * args.steps / (rms / 1e3)
     peak, peak_src = peaks()
-    sb = stage_bytes(w, h)
-    dom = max(stage_ms, key=lambda k: stage_ms[k])
-    roof_stage = dom if sb.get(dom) else max((k for k in sb if sb[k]), key=lambda k: stage_ms[k])
-    traffic = ncu_traffic().get(roof_stage)
-    achieved = sb[roof_stage] / (stage_ms[roof_stage] / 1e3) / 1e9
+    traffic_all = ncu_traffic()
 
-    def roof(stage):
+    def kroof(name):
+        nbytes, n = kb[name]
+        t = kernel_ms[name] / 1e3
+        a = nbytes / t / 1e9
+        tr = traffic_all.get(name)
+        return {"kernel": name, "launches_per_pair": n, "bytes_per_launch": nbytes / n,
+                "us_per_launch": 1e3 * kernel_ms[name] / n, "achieved": a, "frac": a / peak,
+                "traffic": tr}
+    dom = max(kernel_ms, key=lambda k: kernel_ms[k])
+    d = kroof(dom)
+    sb = stage_bytes(w, h)
+
+    def sroof(stage):
         a = sb[stage] / (stage_ms[stage] / 1e3) / 1e9
         return {"stage": stage, "achieved": a, "frac": a / peak, "bytes": sb[stage],
-                "ms": stage_ms[stage], "traffic": ncu_traffic().get(stage)}
+                "ms": stage_ms[stage]}
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -370,21 +441,30 @@ def run_ours(args):
                    "distinct_scenes": len(scenes), "graph": not args.no_graph,
                    "l2": "inputs larger than L2 (each pair 121 MB, %d resident pairs)" % B,
                    "parallelism": f"pair-sharded x{world}, no collective"},
-        "roofline": {"bound": "hbm", "stage": roof_stage, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak,
+                     "unit": "GB/s", "frac": d["frac"], "traffic": d["traffic"],
+                     "bytes_per_launch": d["bytes_per_launch"],
+                     "us_per_launch": d["us_per_launch"], "launches_per_pair": d["launches_per_pair"],
                      "peak_source": peak_src,
-                     "note": "achieved = bytes the stage must move per pair / its device time "
-                             "(CUDA events on the launching stream around the stage, pairs run "
-                             "one at a time right after the timed region)"},
-        "rooflines": {"warp": roof("finalize_warp"), "merge": roof("fuse"),
-                      "dt_filter": roof("dt_filter")},
-        "stage_ms": stage_ms, "stage_ms_concurrent": stage_ms_conc, "dominant_stage": dom,
+                     "note": "dominant kernel by device time per pair; achieved = algorithmic "
+                             "bytes per launch (DESIGN.md §4) / mean launch duration, CUDA events "
+                             "on the launching stream around each launch (kernel probes), pairs "
+                             "run one at a time after the timed region; traffic = ncu dram bytes "
+                             "per launch (profiles/)"},
+        "kernel_rooflines": {k: kroof(k) for k in kernel_ms},
+        "stage_rooflines": {k: sroof(k) for k in ("dt_filter", "finalize_warp", "fuse")},
+        "stage_ms": stage_ms, "stage_ms_concurrent": stage_ms_conc, "kernel_ms": kernel_ms,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "pairs_per_step": E},
+        "e2e_png8": {"value": png8_value, "unit": "pairs/s", "h2d_bytes_per_step": rh2d,
+                     "d2h_bytes_per_step": rd2h, "pairs_per_step": E,
+                     "note": "file path (run_hdr): the same scenes as 8-bit PNG samples, "
+                             "raw uint8 H2D, device decode, pair graph, 8-bit composite D2H"},
         "gpu_launches": kernels_per_pair * B * args.steps,
         "kernels_per_pair": kernels_per_pair,
         "clocks": clk,
-        "checks": {"all_registered": ok, "replicas_identical": consistent, "e2e_ok": e2e_ok},
+        "checks": {"all_registered": ok, "replicas_identical": consistent, "e2e_ok": e2e_ok,
+                   "e2e_png8_ok": raw_ok},
     }
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base

@@ -95,6 +95,8 @@ const char* hdr_last_error(void);
 /* Implementation switches for testing equivalent kernel paths (process-wide;
  * no reference counterpart). "dt_cluster_columns": 1 (default) = one
  * cluster-resident kernel per column sweep pair, 0 = chunk agg/link/apply.
+ * "dt_smem_columns": -1 (default) = off, 0 = shared-memory-resident column
+ * bands when they fit, 1/2/3 = force the 32x32 / 16x16 / 16x32 band shape.
  * Returns HDR_ERR_INVALID for an unknown name. */
 int hdr_set_option(const char* name, int64_t value);
 /* Blocks until the context's stream drains; returns HDR_ERR_CUDA on a
@@ -121,8 +123,42 @@ int hdr_register_and_fuse_graph(hdr_ctx* ctx, const hdr_params* p, int32_t width
  * graphs captured while they are set. */
 #define HDR_NUM_STAGES 7
 int hdr_ctx_set_probes(hdr_ctx* ctx, void* const* events);
+/* Kernel probes: events[2*j] / events[2*j+1] are recorded on the context
+ * stream before / after the j-th launch (j < n <= 8) of one kernel family
+ * inside each pair (register_and_fuse, eager or graph: baked into graphs
+ * captured while set; n = 0 or events = NULL disarms). Families: */
+#define HDR_KP_DT_ROWS 0         /* domain-transform row sweeps (one per pass)  */
+#define HDR_KP_DT_COLS 1         /* domain-transform column sweeps (per pass)   */
+#define HDR_KP_WARP 2            /* warp_image + luminance histogram            */
+#define HDR_KP_SSIM 3            /* ssim_map                                    */
+#define HDR_KP_FUSE_WEIGHTS0 4   /* fusion weights + first pyramid reduction    */
+#define HDR_KP_FUSE_COLLAPSE0 5  /* level-0 blend + collapse -> composite       */
+#define HDR_NUM_KPROBES 6
+int hdr_ctx_set_kernel_probes(hdr_ctx* ctx, int32_t kernel, void* const* events, int32_t n);
 /* Kernel nodes in the most recently instantiated pair graph of ctx. */
 int32_t hdr_ctx_graph_kernels(hdr_ctx* ctx);
+
+/* ---- file path: raw PNG samples ------------------------
+ * The PNG container is decoded on the host; only the raw 8- or 16-bit
+ * samples cross PCIe. hdr_decode_image is fileio.load_png's scaling
+ * (fileio.py:21-41: f32(clip(v / (2^bits - 1)))) fused with pipeline.as_rgb
+ * (pipeline.py:112-115): raw (h, w[, channels]) -> rgb (h, w, 3) f32.
+ * hdr_encode_u8 is fileio.save_png's quantisation (fileio.py:44-53):
+ * clip(floor(x * 255 + 0.5), 0, 255) of n floats. hdr_mean_luminance is
+ * metering.choose_reference's tie-break statistic (metering.py:46-48),
+ * written to one device double. */
+int hdr_decode_image(hdr_ctx* ctx, const void* raw, int32_t width, int32_t height,
+                     int32_t channels, int32_t bits, float* rgb);
+int hdr_encode_u8(hdr_ctx* ctx, const float* img, int64_t n, uint8_t* out);
+int hdr_mean_luminance(hdr_ctx* ctx, const float* rgb, int64_t n, double* out);
+/* pipeline.run_hdr's compute (pipeline.py:267-282) on raw samples: decode
+ * both frames into context-owned RGB buffers, register_and_fuse them
+ * (use_graph != 0: the cached pair graph), and, when composite_u8 is not
+ * NULL, write save_png's 8-bit composite (h, w, 3) next to out->composite. */
+int hdr_register_and_fuse_raw(hdr_ctx* ctx, const hdr_params* p, int32_t width,
+                              int32_t height, const void* ref_raw, const void* src_raw,
+                              int32_t channels, int32_t bits, int32_t use_graph,
+                              const hdr_outputs* out, uint8_t* composite_u8);
 
 /* ---- per-stage twins ---------------------------------------------------- */
 /* image.luminance (image.py:23-29): rgb (n,3) -> lum (n). */
@@ -207,6 +243,11 @@ int hdr_make_ssim(hdr_ctx* ctx, const float* lum_ref, const float* warped,
 /* fusion.quality_weights (fusion.py:67-77): rgb (h, w, 3) -> (h, w) f32. */
 int hdr_quality_weights(hdr_ctx* ctx, const float* rgb, int32_t width, int32_t height,
                         float* out);
+/* fusion.fusion_weights (fusion.py:117-128): normalised (w_ref, w_src),
+ * each (h, w) f32; valid is 0/1 per pixel. */
+int hdr_fusion_weights(hdr_ctx* ctx, const float* ref, const float* warped, const float* ssim,
+                       const uint8_t* valid, int32_t width, int32_t height, float* w_ref,
+                       float* w_src);
 /* fusion.fuse (fusion.py:135-157): levels <= 0 selects the default. */
 int hdr_fuse(hdr_ctx* ctx, const float* ref, const float* warped, const float* ssim,
              const uint8_t* valid, int32_t width, int32_t height, int32_t levels,

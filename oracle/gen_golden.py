@@ -114,6 +114,77 @@ def scene_fixture(hf, w, h, rot, seed):
     return out
 
 
+# file-path cases (pipeline.run_hdr): (name, mode, exposures, swap inputs)
+FILE_CASES = [
+    ("file_rgb8", "RGB", (1.0, 4.0), False),
+    ("file_rgb8_tie", "RGB", (2.0, 2.0), True),
+    ("file_gray16", "I;16", (4.0, 1.0), True),
+]
+
+
+def write_scene_pngs(directory, mode, swap, w=640, h=480, seed=5):
+    """The C1 scene written as PNG files the way a camera pipeline would
+    store it (8-bit RGB or 16-bit grey); deterministic, so tests regenerate
+    the same files instead of committing them."""
+    from PIL import Image
+    st = synth.synth_stack(synth.working_spec(w, h), seed)
+    frames = [st.ref, st.src]
+    if swap:
+        frames = frames[::-1]
+    paths = []
+    for i, f in enumerate(frames):
+        path = os.path.join(directory, f"in{i}.png")
+        if mode == "RGB":
+            data = np.clip(np.floor(f.astype(np.float64) * 255.0 + 0.5), 0, 255).astype(np.uint8)
+            Image.fromarray(data, mode="RGB").save(path, format="PNG")
+        else:
+            lum = (0.299 * f[..., 0] + 0.587 * f[..., 1] + 0.114 * f[..., 2]).astype(np.float64)
+            data = np.clip(np.floor(lum * 65535.0 + 0.5), 0, 65535).astype(np.uint16)
+            Image.fromarray(data, mode="I;16").save(path, format="PNG")
+        paths.append(path)
+    return paths
+
+
+def file_fixture(name, mode, exposures, swap):
+    import tempfile
+    from PIL import Image
+    from hdrflow import fileio, pipeline
+    with tempfile.TemporaryDirectory() as d:
+        paths = write_scene_pngs(d, mode, swap)
+        outp = os.path.join(d, "out.png")
+        cfg = pipeline.PipelineConfig(inputs=paths, exposures=list(exposures), output=outp)
+        r = pipeline.run_hdr(cfg)
+        with Image.open(outp) as im:
+            comp8 = np.asarray(im)
+        imgs = [fileio.load_png(p) for p in paths]
+        return {"inputs_digest": np.array([digest(a) for a in imgs]),
+                "composite_u8_digest": np.array(digest(comp8)),
+                "composite_u8_sub": comp8[::STRIDE, ::STRIDE].copy(),
+                "composite_digest": np.array(digest(r.composite)),
+                "level_counts": np.array(r.level_counts, dtype=np.int64),
+                "exposures": np.array(exposures), "swap": np.array(swap),
+                "mode": np.array(mode)}
+
+
+def format_fixture():
+    """Bytes written by the reference's PFM / match-CSV writers for small
+    seeded arrays (pins paper_1504_01441_b200.fileio's writers)."""
+    import tempfile
+    from hdrflow import fileio
+    rng = np.random.default_rng(11)
+    grey = rng.random((5, 7), dtype=np.float32)
+    colour = rng.random((4, 3, 3), dtype=np.float32)
+    matches = np.concatenate([rng.random((6, 4)) * 640, rng.random((6, 1))], axis=1)
+    out = {"grey": grey, "colour": colour, "matches": matches}
+    with tempfile.TemporaryDirectory() as d:
+        for name, fn, arr in (("grey", fileio.save_pfm, grey), ("colour", fileio.save_pfm, colour),
+                              ("matches", fileio.save_matches_csv, matches)):
+            path = os.path.join(d, name)
+            fn(path, arr)
+            out[f"{name}_bytes"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
@@ -137,6 +208,11 @@ def main():
                         inputs_digest=np.array([digest(st.ref), digest(st.src)]),
                         message=np.array(raised))
     print("default scene:", raised)
+    np.savez_compressed(os.path.join(GOLDEN, "formats.npz"), **format_fixture())
+    for name, mode, exposures, swap in FILE_CASES:
+        fx = file_fixture(name, mode, exposures, swap)
+        np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **fx)
+        print(name, fx["level_counts"].tolist())
     # SeedSequence / Philox / choice vectors (weeding.py:62-84)
     rng = np.random.default_rng(7)
     cases = []

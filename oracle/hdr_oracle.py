@@ -685,3 +685,52 @@ def register_and_fuse(ref, src, p: Params | None = None, keep_stages=False):
     if keep_stages:
         st.update(smooth=smooth, fallback=fb)
     return OracleOutput(comp, flow, warped, valid, ssim, weeded, raw, hom, counts, st)
+
+
+# ---------------------------------------------------------- file path (fileio.py, metering.py, pipeline.run_hdr)
+def load_png(path):
+    """fileio.load_png (fileio.py:21-41): float32 in [0, 1], (h, w) or (h, w, 3)."""
+    from PIL import Image
+    with Image.open(path) as im:
+        im.load()
+        if im.mode in ("I", "I;16", "I;16B", "I;16L"):
+            arr = np.asarray(im.convert("I"), dtype=np.float64) / 65535.0
+        elif im.mode in ("L", "RGB"):
+            arr = np.asarray(im, dtype=np.float64) / 255.0
+        elif im.mode in ("LA", "RGBA", "P", "1"):
+            conv = "L" if im.mode in ("LA", "1") else "RGB"
+            arr = np.asarray(im.convert(conv), dtype=np.float64) / 255.0
+        else:
+            raise ValueError(f"unsupported PNG mode {im.mode!r}: {path}")
+    return np.clip(arr, 0.0, 1.0).astype(np.float32)
+
+
+def png_quantize(img):
+    """fileio.save_png's sample values (fileio.py:46-47)."""
+    return np.clip(np.floor(np.asarray(img, dtype=np.float64) * 255.0 + 0.5), 0, 255).astype(np.uint8)
+
+
+def choose_reference(images, exposures):
+    """metering.choose_reference (metering.py:37-51)."""
+    exposures = [float(e) for e in exposures]
+    shortest = min(exposures)
+    cands = [i for i, e in enumerate(exposures) if e == shortest]
+    if len(cands) == 1:
+        return cands[0]
+
+    def mean_lum(i):
+        img = images[i]
+        return float(np.mean(luminance(img) if img.ndim == 3 else img))
+    return min(cands, key=lambda i: (mean_lum(i), i))
+
+
+def run_hdr(inputs, exposures=None, p: Params | None = None):
+    """pipeline.run_hdr (pipeline.py:267-282) without the file writes:
+    returns (output, 8-bit composite as save_png would write it, ref index)."""
+    if len(inputs) != 2:
+        raise ConfigError("exactly 2 input images are required")
+    exposures = [1.0, 1.0] if exposures is None else exposures
+    images = [as_rgb(load_png(x)) for x in inputs]
+    k = choose_reference(images, exposures)
+    out = register_and_fuse(images[k], images[1 - k], p)
+    return out, png_quantize(out.composite), k

@@ -20,6 +20,8 @@ HDR_ERR_REGISTRATION, HDR_ERR_CONFIG, HDR_ERR_CUDA, HDR_ERR_EMPTY = 3, 4, 5, 6
 INFO_WORDS = 32
 NUM_STAGES = 7
 STAGES = ("raster", "corners", "match_chain", "dt_filter", "finalize_warp", "ssim", "fuse")
+# kernel-probe families (HDR_KP_* in include/hdrb200.h)
+KPROBES = ("dt_rows", "dt_cols", "warp", "ssim", "fuse_weights0", "fuse_collapse0")
 
 
 class HdrParams(ctypes.Structure):
@@ -59,6 +61,7 @@ SIGNATURES = {
     "hdr_register_and_fuse_graph": (_I, [_P, _P, _I, _I, _P, _P, _P]),
     "hdr_ctx_set_probes": (_I, [_P, _P]),
     "hdr_ctx_graph_kernels": (_I, [_P]),
+    "hdr_ctx_set_kernel_probes": (_I, [_P, _I, _P, _I]),
     "hdr_luminance": (_I, [_P, _P, _I64, _P]),
     "hdr_match_histogram": (_I, [_P, _P, _I64, _P, _I64, _I, _P]),
     "hdr_build_pyramid": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
@@ -80,6 +83,11 @@ SIGNATURES = {
     "hdr_make_ssim": (_I, [_P, _P, _P, _I, _I, _I, _D, _P]),
     "hdr_quality_weights": (_I, [_P, _P, _I, _I, _P]),
     "hdr_fuse": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _P]),
+    "hdr_fusion_weights": (_I, [_P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "hdr_decode_image": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "hdr_encode_u8": (_I, [_P, _P, _I64, _P]),
+    "hdr_mean_luminance": (_I, [_P, _P, _I64, _P]),
+    "hdr_register_and_fuse_raw": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P]),
     "hdr_level_seed": (ctypes.c_uint32, [_U64, _I]),
     "hdr_iteration_keys": (_I, [_U64, _I, _P]),
     "hdr_choice4_host": (_I, [_P, _I, _I, _P]),

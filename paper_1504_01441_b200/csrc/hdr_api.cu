@@ -47,6 +47,11 @@ extern "C" int hdr_set_option(const char* name, int64_t value) {
     hdr::dt_set_cluster_columns(value != 0);
     return HDR_OK;
   }
+  if (name && std::string(name) == "dt_smem_columns") {
+    if (value < -1 || value > 3) return fail(HDR_ERR_INVALID, "dt_smem_columns: -1..3");
+    hdr::dt_set_smem_columns((int)value);
+    return HDR_OK;
+  }
   return fail(HDR_ERR_INVALID, std::string("unknown option: ") + (name ? name : "(null)"));
 }
 
@@ -319,6 +324,8 @@ struct hdr_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t probes[2 * HDR_NUM_STAGES] = {};
   bool probing = false;
+  KProbe kprobes[HDR_NUM_KPROBES] = {};
+  float* frames = nullptr;      // decoded ref + src RGB frames of the raw-sample path (lazy)
   int32_t graph_kernels = 0;
   std::map<std::string, GraphEntry> graphs;
   std::vector<void*> allocs;
@@ -348,6 +355,7 @@ extern "C" int hdr_ctx_destroy(hdr_ctx* c) {
   if (c->keys) cudaFree(c->keys);
   if (c->fits) cudaFree(c->fits);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->frames) cudaFree(c->frames);
   delete c;
   return HDR_OK;
 }
@@ -452,6 +460,33 @@ extern "C" int hdr_ctx_set_probes(hdr_ctx* c, void* const* events) {
 }
 
 extern "C" int32_t hdr_ctx_graph_kernels(hdr_ctx* c) { return c ? c->graph_kernels : -1; }
+
+extern "C" int hdr_ctx_set_kernel_probes(hdr_ctx* c, int32_t kernel, void* const* events,
+                                         int32_t n) {
+  if (!c) return fail(HDR_ERR_INVALID, "null context");
+  if (kernel < 0 || kernel >= HDR_NUM_KPROBES) return fail(HDR_ERR_INVALID, "unknown kernel probe");
+  if (n < 0 || n > kMaxKProbeLaunches || (n > 0 && !events))
+    return fail(HDR_ERR_INVALID, "kernel probes: 0 <= n <= 8 launches");
+  KProbe& k = c->kprobes[kernel];
+  k = KProbe{};
+  k.n = events ? n : 0;
+  for (int i = 0; i < 2 * k.n; ++i) k.ev[i] = (cudaEvent_t)events[i];
+  return HDR_OK;
+}
+
+namespace hdr {
+void kprobe_mark(KProbe* p, int end, cudaStream_t s) {
+  if (!p || p->next >= p->n) return;
+  cudaEvent_t e = p->ev[2 * p->next + end];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+  if (end) ++p->next;
+}
+}  // namespace hdr
 
 static void probe(hdr_ctx* c, int stage, int end) {
   if (!c->probing) return;
@@ -775,20 +810,25 @@ static int enqueue_fuse(hdr_ctx* c, const float* ref, const float* warped, const
     return check_launch();
   }
   // weights (kept for level 0) fused with the first blur + decimation
+  kprobe_mark(&c->kprobes[HDR_KP_FUSE_WEIGHTS0], 0, s);
   launch_weights_down0(ref, warped, ssim, valid, w, h, c->wr, c->ws, g[1], fd[1].w, fd[1].h, s);
+  kprobe_mark(&c->kprobes[HDR_KP_FUSE_WEIGHTS0], 1, s);
   for (int k = 1; k + 1 < L; ++k)
     launch_fuse_down(g[k], fd[k].w, fd[k].h, g[k + 1], fd[k + 1].w, fd[k + 1].h, s);
   launch_fuse_top(g[L - 1], fd[L - 1].w, fd[L - 1].h, cp[L - 1], s);
   for (int k = L - 2; k >= 1; --k)
     launch_fuse_collapse(g[k], fd[k].w, fd[k].h, g[k + 1], cp[k + 1], fd[k + 1].w, fd[k + 1].h,
                          cp[k], s);
+  kprobe_mark(&c->kprobes[HDR_KP_FUSE_COLLAPSE0], 0, s);
   launch_fuse_collapse0(ref, warped, c->wr, c->ws, w, h, g[1], cp[1], fd[1].w, fd[1].h, out, s);
+  kprobe_mark(&c->kprobes[HDR_KP_FUSE_COLLAPSE0], 1, s);
   return check_launch();
 }
 
 static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
                         const float* src, const hdr_outputs* o) {
   cudaStream_t s = c->stream;
+  for (KProbe& k : c->kprobes) k.next = 0;
   int64_t P = (int64_t)w * h;
   int rc = enqueue_match(c, p, w, h, ref, src, o->matches, o->raw_matches, o->homography, o->info);
   if (rc) return rc;
@@ -801,20 +841,25 @@ static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const flo
   // f32 flow directly (the smoothed planes never make a final round trip)
   DtFlowOut fo{o->homography, o->info + 1, p->normalization_floor, o->flow};
   bool flow_done = launch_dt_filter(c->lum_ref, pl, w, h, p->sigma_s, p->sigma_r, p->passes,
-                                    c->carry, s, &fo);
+                                    c->carry, s, &fo, &c->kprobes[HDR_KP_DT_ROWS],
+                                    &c->kprobes[HDR_KP_DT_COLS]);
   probe(c, 3, 1);
   probe(c, 4, 0);
   // warp_image + luminance(warped) histogram (pipeline.py:192, :168)
+  kprobe_mark(&c->kprobes[HDR_KP_WARP], 0, s);
   if (flow_done)
     launch_warp(o->flow, w, h, src, o->warped, o->valid, c->qw, c->hist + 2 * kBins, s);
   else
     launch_finalize_warp(pl, o->homography, o->info + 1, w, h, p->normalization_floor, src, 3,
                          o->flow, o->warped, o->valid, c->qw, c->hist + 2 * kBins, true, s);
+  kprobe_mark(&c->kprobes[HDR_KP_WARP], 1, s);
   probe(c, 4, 1);
   probe(c, 5, 0);
   // make_ssim (pipeline.py:165-171)
   launch_lut(c->hist + 2 * kBins, P, c->hist, P, c->lut + kBins, s);
+  kprobe_mark(&c->kprobes[HDR_KP_SSIM], 0, s);
   launch_ssim(c->lum_ref, nullptr, c->qw, c->lut + kBins, w, h, p->ssim_window, c->taps, o->ssim, s);
+  kprobe_mark(&c->kprobes[HDR_KP_SSIM], 1, s);
   probe(c, 5, 1);
   probe(c, 6, 0);
   // fusion.fuse (pipeline.py:193)
@@ -868,6 +913,63 @@ extern "C" int hdr_register_and_fuse(hdr_ctx* c, const hdr_params* p, int32_t w,
   return enqueue_pair(c, p, w, h, ref, src, o);
 }
 
+#define NEED(cond, msg) \
+  if (!(cond)) return fail(HDR_ERR_INVALID, msg)
+
+// ------------------------------------------------------------ file path
+static int check_raw(int channels, int bits) {
+  if (channels != 1 && channels != 3) return fail(HDR_ERR_INVALID, "channels must be 1 or 3");
+  if (bits != 8 && bits != 16) return fail(HDR_ERR_INVALID, "bits must be 8 or 16");
+  return HDR_OK;
+}
+
+extern "C" int hdr_decode_image(hdr_ctx* c, const void* raw, int32_t w, int32_t h,
+                                int32_t channels, int32_t bits, float* rgb) {
+  NEED(c && raw && rgb, "null argument");
+  int rc = check_raw(channels, bits);
+  if (rc) return rc;
+  launch_decode(raw, (int64_t)w * h, channels, bits, rgb, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_encode_u8(hdr_ctx* c, const float* img, int64_t n, uint8_t* out) {
+  NEED(c && img && out, "null argument");
+  launch_encode_u8(img, n, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_mean_luminance(hdr_ctx* c, const float* rgb, int64_t n, double* out) {
+  NEED(c && rgb && out, "null argument");
+  launch_mean_luminance(rgb, n, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
+                                           const float* ref, const float* src,
+                                           const hdr_outputs* o);
+
+extern "C" int hdr_register_and_fuse_raw(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
+                                         const void* ref_raw, const void* src_raw,
+                                         int32_t channels, int32_t bits, int32_t use_graph,
+                                         const hdr_outputs* o, uint8_t* composite_u8) {
+  NEED(c && ref_raw && src_raw, "null argument");
+  int rc = check_raw(channels, bits);
+  if (rc) return rc;
+  if (w > c->W || h > c->H || w < 1 || h < 1)
+    return fail(HDR_ERR_INVALID, "image larger than the context workspace");
+  if (!c->frames) CUDA_TRY(cudaMalloc(&c->frames, 2 * 3 * (size_t)c->P * sizeof(float)));
+  int64_t P = (int64_t)w * h;
+  float* ref = c->frames;
+  float* src = c->frames + 3 * (size_t)c->P;
+  launch_decode(ref_raw, P, channels, bits, ref, c->stream);
+  launch_decode(src_raw, P, channels, bits, src, c->stream);
+  rc = use_graph ? hdr_register_and_fuse_graph(c, p, w, h, ref, src, o)
+                 : hdr_register_and_fuse(c, p, w, h, ref, src, o);
+  if (rc) return rc;
+  if (composite_u8) launch_encode_u8(o->composite, 3 * P, composite_u8, c->stream);
+  return check_launch();
+}
+
 extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
                                            const float* ref, const float* src,
                                            const hdr_outputs* o) {
@@ -881,10 +983,19 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
            p->radius, p->patch, p->max_levels, p->iterations, p->coarse_iterations, p->delta,
            p->passes, p->ssim_window, p->threshold, p->eps_px, p->sigma_s, p->sigma_r,
            p->ssim_sigma, p->normalization_floor, (unsigned long long)p->seed);
+  std::string kkey(key, kn > 0 ? std::min(kn, (int)sizeof key - 1) : 0);
+  char pk[32];
   if (c->probing)
-    for (int i = 0; i < 2 * HDR_NUM_STAGES && kn > 0 && kn < (int)sizeof key - 24; ++i)
-      kn += snprintf(key + kn, sizeof key - kn, ",%p", (void*)c->probes[i]);
-  GraphEntry& g = c->graphs[key];
+    for (int i = 0; i < 2 * HDR_NUM_STAGES; ++i) {
+      snprintf(pk, sizeof pk, ",%p", (void*)c->probes[i]);
+      kkey += pk;
+    }
+  for (const KProbe& k : c->kprobes)
+    for (int i = 0; i < 2 * k.n; ++i) {
+      snprintf(pk, sizeof pk, ";%p", (void*)k.ev[i]);
+      kkey += pk;
+    }
+  GraphEntry& g = c->graphs[kkey];
   if (!g.exec) {
     // capture on the context's private stream (the caller's may be the
     // legacy default stream, which cannot be captured); replay on theirs
@@ -895,7 +1006,7 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
     cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) {
       c->stream = user;
-      c->graphs.erase(key);
+      c->graphs.erase(kkey);
       return fail(HDR_ERR_CUDA, std::string("begin capture: ") + cudaGetErrorString(e));
     }
     rc = enqueue_pair(c, p, w, h, ref, src, o);
@@ -903,11 +1014,11 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
     c->stream = user;
     if (rc) {
       if (graph) cudaGraphDestroy(graph);
-      c->graphs.erase(key);
+      c->graphs.erase(kkey);
       return rc;
     }
     if (e != cudaSuccess) {
-      c->graphs.erase(key);
+      c->graphs.erase(kkey);
       return fail(HDR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     }
     size_t nodes = 0;
@@ -923,7 +1034,7 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
     e = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) {
-      c->graphs.erase(key);
+      c->graphs.erase(kkey);
       return fail(HDR_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
   }
@@ -932,9 +1043,6 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
 }
 
 // ------------------------------------------------------------ per-stage twins
-#define NEED(cond, msg) \
-  if (!(cond)) return fail(HDR_ERR_INVALID, msg)
-
 extern "C" int hdr_luminance(hdr_ctx* c, const float* rgb, int64_t n, float* lum) {
   NEED(c && rgb && lum, "null argument");
   NEED(n >= 0, "bad size");
@@ -1226,6 +1334,11 @@ extern "C" int hdr_warp_image(hdr_ctx* c, const float* src, int32_t channels, in
                               const float* flow, float* warped, uint8_t* valid) {
   NEED(c && src && flow && warped && valid, "null argument");
   NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  if (channels == 3 && (int64_t)w * h <= c->P) {
+    // the pair pipeline's kernel (its luminance histogram lands in scratch)
+    launch_warp(flow, w, h, src, warped, valid, c->qw, c->hist + 2 * kBins, c->stream);
+    return check_launch();
+  }
   DtPlanes none = f64_planes(nullptr, nullptr, nullptr, 0);
   launch_finalize_warp(none, nullptr, nullptr, w, h, 0.0, src, channels,
                        const_cast<float*>(flow), warped, valid, nullptr, nullptr, false, c->stream);
@@ -1263,6 +1376,14 @@ extern "C" int hdr_make_ssim(hdr_ctx* c, const float* lum_ref, const float* warp
 extern "C" int hdr_quality_weights(hdr_ctx* c, const float* rgb, int32_t w, int32_t h, float* out) {
   NEED(c && rgb && out, "null argument");
   launch_quality(rgb, w, h, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_fusion_weights(hdr_ctx* c, const float* ref, const float* warped,
+                                  const float* ssim, const uint8_t* valid, int32_t w, int32_t h,
+                                  float* w_ref, float* w_src) {
+  NEED(c && ref && warped && ssim && valid && w_ref && w_src, "null argument");
+  launch_fusion_weights(ref, warped, ssim, valid, w, h, w_ref, w_src, c->stream);
   return check_launch();
 }
 

@@ -6,6 +6,19 @@
 
 namespace hdr {
 
+// Kernel probes (hdr_ctx_set_kernel_probes): events recorded on the launching
+// stream around successive launches of one kernel family, so a caller can
+// time individual kernels inside a pair (or a replayed pair graph).
+constexpr int kMaxKProbeLaunches = 8;
+struct KProbe {
+  cudaEvent_t ev[2 * kMaxKProbeLaunches];
+  int n;     // launches to bracket (0 = off)
+  int next;  // next launch index
+};
+// records ev[2*next + end] (end = 0 before, 1 after) if armed; after the
+// closing mark `next` advances. Safe while the stream is being captured.
+void kprobe_mark(KProbe* p, int end, cudaStream_t s);
+
 // per-tile detector output: x < 0 means "no corner in this tile"
 struct TileCorner {
   int32_t x, y;
@@ -111,6 +124,7 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
                   int32_t* status, cudaStream_t s);
 int64_t dt_scratch_doubles(int w, int h, int k);
 void dt_set_cluster_columns(bool on);
+void dt_set_smem_columns(int cfg);  // 0 auto, 1..3 force a band shape, -1 off
 // optional fused densify-finalise for the last column pass (K == 3)
 struct DtFlowOut {
   const double* fallback;   // 3x3 H or null
@@ -121,7 +135,8 @@ struct DtFlowOut {
 // returns true when the flow was written (planes then hold pre-final values)
 bool launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double sigma_s,
                       double sigma_r, int passes, double* scratch, cudaStream_t s,
-                      const DtFlowOut* fo = nullptr);
+                      const DtFlowOut* fo = nullptr, KProbe* kp_rows = nullptr,
+                      KProbe* kp_cols = nullptr);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
                  uint8_t* qw, uint32_t* hist, cudaStream_t s);
@@ -130,6 +145,12 @@ void launch_finalize_warp(DtPlanes smooth, const double* fallback,
                           const float* src, int channels, float* flow, float* warped,
                           uint8_t* valid, uint8_t* qw, uint32_t* hist_w,
                           bool do_flow, cudaStream_t s);
+
+// ---- k_ingest.cu
+void launch_decode(const void* in, int64_t npx, int channels, int bits, float* out,
+                   cudaStream_t s);
+void launch_encode_u8(const float* x, int64_t n, uint8_t* out, cudaStream_t s);
+void launch_mean_luminance(const float* rgb, int64_t n, double* out, cudaStream_t s);
 
 // ---- k_fusion.cu
 void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb,

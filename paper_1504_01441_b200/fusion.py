@@ -48,6 +48,24 @@ def quality_weights(img):
     return out(res.double(), as_torch)
 
 
+def fusion_weights(ref, warped, ssim, valid):
+    """fusion.py:117-128 — normalised (w_ref, w_src) per pixel (f32 on the
+    device, widened to float64 like the reference's result)."""
+    as_torch = is_torch(ref, warped, ssim, valid)
+    dev = device_of(ref, warped, ssim, valid)
+    r, wp = to_dev(ref, torch.float32, dev), to_dev(warped, torch.float32, dev)
+    s = to_dev(ssim, torch.float32, dev)
+    v = to_dev(np.asarray(valid) != 0 if not isinstance(valid, torch.Tensor) else valid != 0,
+               torch.uint8, dev)
+    h, w = r.shape[:2]
+    wr = torch.empty((h, w), dtype=torch.float32, device=r.device)
+    ws = torch.empty((h, w), dtype=torch.float32, device=r.device)
+    e = engine(1, 1, dev)
+    _native.check(_native.lib().hdr_fusion_weights(e.handle, ptr(r), ptr(wp), ptr(s), ptr(v), w, h,
+                                                   ptr(wr), ptr(ws)), "fusion_weights")
+    return out(wr.double(), as_torch), out(ws.double(), as_torch)
+
+
 def default_fusion_levels(height: int, width: int) -> int:
     """fusion.py:131-132."""
     return max(1, int(np.floor(np.log2(min(height, width)))) - 1)

@@ -177,7 +177,13 @@ def register_and_fuse(ref, src, params: PipelineParams | None = None) -> Registr
         raise ValueError("input below 100 pixels in one dimension")
     bufs = PairBuffers(w, h, dev)
     enqueue_pair(ref_t, src_t, params, bufs)
-    info = bufs.info.cpu().numpy()  # the one host sync of the pair
+    return _collect(bufs, as_torch)
+
+
+def _collect(bufs: PairBuffers, as_torch: bool) -> RegistrationOutput:
+    """RegistrationOutput from a finished pair's buffers (one host sync to
+    read the verdict; RegistrationError as pipeline.py:185-187)."""
+    info = bufs.info.cpu().numpy()
     m, n = int(info[16]), int(info[17])
     if info[0] == _native.HDR_ERR_REGISTRATION:
         raise RegistrationError(f"only {m} reliable matches at full resolution")
@@ -270,3 +276,166 @@ def make_ssim(lum_ref, warped, params: PipelineParams):
                                               params.ssim_window, params.ssim_sigma, ptr(res)),
                   "make_ssim")
     return out(res.double(), as_torch)
+
+
+# ---------------------------------------------------------------- file path
+@dataclass
+class PipelineConfig:
+    """Mirror of PipelineConfig (pipeline.py:201-210)."""
+    inputs: list = field(default_factory=list)
+    exposures: list | None = None
+    exposure_file: str | None = None
+    output: str = "composite.png"
+    dump_all: bool = False
+    out_dir: str | None = None
+    params: PipelineParams = field(default_factory=PipelineParams)
+
+
+def _resolve_exposures(config: PipelineConfig):
+    """pipeline.py:213-228."""
+    from .fileio import load_exposures
+    inputs = list(config.inputs)
+    if config.exposure_file:
+        entries = load_exposures(config.exposure_file)
+        if inputs:
+            table = dict(entries)
+            try:
+                return inputs, [table[p] for p in inputs]
+            except KeyError as exc:
+                raise ConfigError(f"no exposure for input {exc}") from exc
+        return [p for p, _ in entries], [e for _, e in entries]
+    if config.exposures is not None:
+        if len(config.exposures) != len(inputs):
+            raise ConfigError("need one exposure per input image")
+        return inputs, list(config.exposures)
+    return inputs, [1.0] * len(inputs)
+
+
+def harmonize_raw(raws):
+    """Bring raw PNG samples to one layout so both frames share one decode:
+    grey -> RGB repeat (pipeline.as_rgb) and 8 -> 16 bit by x257, which is
+    exact (v*257/65535 and v/255 are the same real number, so the f64
+    quotients of fileio.load_png are identical)."""
+    arrs = [a for a, _ in raws]
+    bits = max(b for _, b in raws)
+    out = []
+    for a, b in zip(arrs, (b for _, b in raws)):
+        if b != bits:
+            a = a.astype(np.uint16) * np.uint16(257)
+        out.append(a)
+    if any(a.ndim == 3 for a in out):
+        out = [np.repeat(a[:, :, None], 3, axis=2) if a.ndim == 2 else a for a in out]
+    return [np.ascontiguousarray(a) for a in out], bits
+
+
+def run_raw(ref_raw, src_raw, bits: int, params: PipelineParams, bufs: PairBuffers,
+            composite_u8: torch.Tensor | None = None, graph: bool = False, stream=None):
+    """Enqueue a pair from raw device samples (hdr_register_and_fuse_raw):
+    decode both frames, register and fuse, and optionally quantise the
+    composite for save_png -- asynchronous, no host sync."""
+    h, w = ref_raw.shape[:2]
+    channels = 1 if ref_raw.dim() == 2 else ref_raw.shape[2]
+    e = engine(w, h, ref_raw.device.index)
+    e.bind_stream(stream)
+    p = params.to_native()
+    _native.check(_native.lib().hdr_register_and_fuse_raw(
+        e.handle, ctypes.byref(p), w, h, ptr(ref_raw), ptr(src_raw), channels, bits,
+        1 if graph else 0, ctypes.byref(bufs.native), ptr(composite_u8)), "register_and_fuse_raw")
+    return e
+
+
+def run_hdr(config: PipelineConfig) -> RegistrationOutput:
+    """pipeline.run_hdr (pipeline.py:267-282): load a pair of PNGs, pick the
+    reference, register and fuse, write the 8-bit composite (and the debug
+    dumps when asked). Only raw samples cross PCIe; scaling, the metering
+    statistic, the pair and the 8-bit quantisation run on the GPU."""
+    from . import fileio, metering
+    config.params.validate()
+    inputs, exposures = _resolve_exposures(config)
+    if len(inputs) != 2:
+        raise ConfigError("exactly 2 input images are required")
+    raws, bits = harmonize_raw([fileio.read_png_raw(p) for p in inputs])
+    dev = torch.cuda.current_device()
+    raw_dev = [fileio.raw_to_device(a, bits, dev) for a in raws]
+    images = _LazyFrames(raw_dev, bits)
+    k = metering.choose_reference(images, exposures)
+    ref_raw, src_raw = raw_dev[k], raw_dev[1 - k]
+    if ref_raw.shape != src_raw.shape:
+        raise ConfigError("reference and source dimensions differ")
+    h, w = ref_raw.shape[:2]
+    if min(h, w) < 100:
+        raise ValueError("input below 100 pixels in one dimension")
+    bufs = PairBuffers(w, h, dev)
+    comp8 = torch.empty((h, w, 3), dtype=torch.uint8, device=f"cuda:{dev}")
+    run_raw(ref_raw, src_raw, bits, config.params, bufs, comp8)
+    result = _collect(bufs, False)
+    fileio.write_png_u8(config.output, comp8.cpu().numpy())
+    if config.dump_all:
+        import os
+        directory = config.out_dir or os.path.dirname(os.path.abspath(config.output))
+        dump_intermediates(result, images.lum(k), images[k], directory)
+    return result
+
+
+def flow_to_pfm(flow) -> np.ndarray:
+    """pipeline.py:253-258: (h, w, 2) flow -> 3-channel PFM data (zero third plane)."""
+    f = flow.cpu().numpy() if isinstance(flow, torch.Tensor) else np.asarray(flow)
+    h, w = f.shape[:2]
+    data = np.zeros((h, w, 3), dtype=np.float32)
+    data[:, :, :2] = f
+    return data
+
+
+def pfm_to_flow(data: np.ndarray) -> np.ndarray:
+    """pipeline.py:261-264."""
+    from .fileio import FileFormatError
+    if data.ndim != 3 or data.shape[2] != 3:
+        raise FileFormatError("flow PFM must have 3 channels")
+    return np.ascontiguousarray(data[:, :, :2])
+
+
+def dump_intermediates(result: RegistrationOutput, lum_ref, ref, directory: str) -> None:
+    """pipeline.py:231-250: the stage dumps (match CSVs, flow / warped /
+    valid / SSIM / weight maps as PFM, debug renders as PNG). The fusion
+    weights are recomputed on the GPU (hdr_fusion_weights)."""
+    import os
+    from . import fileio, fusion, viz
+    os.makedirs(directory, exist_ok=True)
+    j = lambda name: os.path.join(directory, name)  # noqa: E731
+    valid = np.asarray(result.valid)
+    fileio.save_matches_csv(j("matches_raw.csv"), result.raw_matches)
+    fileio.save_matches_csv(j("matches.csv"), result.matches)
+    fileio.save_png(j("matches.png"), viz.overlay_matches(lum_ref, result.matches))
+    fileio.save_pfm(j("flow.pfm"), flow_to_pfm(result.flow))
+    fileio.save_png(j("flow.png"), viz.flow_to_color(result.flow))
+    fileio.save_pfm(j("warped.pfm"), result.warped)
+    fileio.save_png(j("warped.png"), result.warped)
+    fileio.save_pfm(j("valid.pfm"), valid.astype(np.float32))
+    fileio.save_pfm(j("ssim.pfm"), np.asarray(result.ssim).astype(np.float32))
+    fileio.save_png(j("ssim.png"), viz.heatmap(result.ssim, -1.0, 1.0))
+    w_ref, w_src = fusion.fusion_weights(ref, result.warped, result.ssim, valid.astype(np.float32))
+    w_ref, w_src = viz._np(w_ref), viz._np(w_src)
+    fileio.save_pfm(j("weight_ref.pfm"), w_ref.astype(np.float32))
+    fileio.save_pfm(j("weight_src.pfm"), w_src.astype(np.float32))
+    fileio.save_png(j("weight_ref.png"), viz.heatmap(w_ref, 0.0, 1.0))
+    fileio.save_png(j("weight_src.png"), viz.heatmap(w_src, 0.0, 1.0))
+
+
+class _LazyFrames:
+    """Decoded frames for metering / dumps, materialised on first use."""
+
+    def __init__(self, raw_dev, bits):
+        self.raw, self.bits, self.cache = raw_dev, bits, {}
+
+    def __len__(self):
+        return len(self.raw)
+
+    def __getitem__(self, i):
+        if i not in self.cache:
+            from .fileio import decode_rgb
+            self.cache[i] = decode_rgb(self.raw[i], self.bits)
+        return self.cache[i]
+
+    def lum(self, i):
+        from .image import luminance
+        return luminance(self[i])

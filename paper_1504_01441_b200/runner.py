@@ -68,6 +68,16 @@ class BatchRunner:
             arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
         _native.check(_native.lib().hdr_ctx_set_probes(e.handle, arr))
 
+    def set_kernel_probes(self, k: int, family: int, events):
+        """Kernel probes (hdr_ctx_set_kernel_probes) for the context of stream
+        k: events[2j], events[2j+1] bracket launch j of kernel `family`."""
+        e = self.engines[k % len(self.engines)]
+        arr, n = None, 0
+        if events:
+            arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
+            n = len(events) // 2
+        _native.check(_native.lib().hdr_ctx_set_kernel_probes(e.handle, family, arr, n))
+
     # ---------------------------------------------------------- host path
     def _ensure_staging(self):
         """Two device slots per compute stream (inputs + outputs), so the
@@ -133,6 +143,73 @@ class BatchRunner:
             cur.wait_stream(s)
         if stop_event is not None:
             stop_event.record(cur)
+        return h2d, d2h
+
+    def enqueue_raw(self, k: int, ref_raw: torch.Tensor, src_raw: torch.Tensor, bits: int,
+                    bufs: PairBuffers, composite_u8: torch.Tensor | None):
+        """Queue one pair from raw 8/16-bit device samples on stream k % S
+        (hdr_register_and_fuse_raw: decode, pair graph, 8-bit composite)."""
+        e = self.engines[k % len(self.engines)]
+        channels = 1 if ref_raw.dim() == 2 else ref_raw.shape[2]
+        _native.check(_native.lib().hdr_register_and_fuse_raw(
+            e.handle, ctypes.byref(self.native_params), self.width, self.height,
+            ctypes.c_void_p(ref_raw.data_ptr()), ctypes.c_void_p(src_raw.data_ptr()), channels, bits,
+            1 if self.graph else 0, ctypes.byref(bufs.native),
+            ctypes.c_void_p(0 if composite_u8 is None else composite_u8.data_ptr())),
+            "register_and_fuse_raw")
+
+    def run_host_raw(self, host_pairs, host_out, bits: int = 8):
+        """End to end on the file path: pinned raw samples
+        in ((h, w, 3) uint8, or int16-viewed uint16), the 8-bit composite
+        (save_png's samples) + info words out. Same slot / stream scheme as
+        run_host; returns the H2D / D2H byte counts."""
+        h, w = self.height, self.width
+        dev = f"cuda:{self.device}"
+        if getattr(self, "_raw_staging", None) is None:
+            dt = torch.uint8 if bits == 8 else torch.int16
+            self._raw_staging = [[dict(ref=torch.empty((h, w, 3), dtype=dt, device=dev),
+                                       src=torch.empty((h, w, 3), dtype=dt, device=dev),
+                                       out=PairBuffers(w, h, self.device),
+                                       comp8=torch.empty((h, w, 3), dtype=torch.uint8, device=dev),
+                                       consumed=None, drained=None)
+                                  for _ in range(2)] for _ in self.streams]
+            self._ensure_staging()
+        st = self._raw_staging
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams + [self._h2d, self._d2h]:
+            s.wait_stream(cur)
+        h2d = d2h = 0
+        S = len(self.streams)
+        for k, ((href, hsrc), (hcomp, hinfo)) in enumerate(zip(host_pairs, host_out)):
+            j = k % S
+            slot = st[j][(k // S) % 2]
+            cs = self.streams[j]
+            with torch.cuda.stream(self._h2d):
+                if slot["consumed"] is not None:
+                    self._h2d.wait_event(slot["consumed"])
+                slot["ref"].copy_(href, non_blocking=True)
+                slot["src"].copy_(hsrc, non_blocking=True)
+                loaded = torch.cuda.Event()
+                loaded.record(self._h2d)
+            cs.wait_event(loaded)
+            if slot["drained"] is not None:
+                cs.wait_event(slot["drained"])
+            with torch.cuda.stream(cs):
+                self.enqueue_raw(j, slot["ref"], slot["src"], bits, slot["out"], slot["comp8"])
+                done = torch.cuda.Event()
+                done.record(cs)
+            slot["consumed"] = done
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(done)
+                hcomp.copy_(slot["comp8"], non_blocking=True)
+                hinfo.copy_(slot["out"].info, non_blocking=True)
+                drained = torch.cuda.Event()
+                drained.record(self._d2h)
+            slot["drained"] = drained
+            h2d += href.numel() * href.element_size() + hsrc.numel() * hsrc.element_size()
+            d2h += hcomp.numel() + hinfo.numel() * 4
+        for s in self.streams + [self._h2d, self._d2h]:
+            cur.wait_stream(s)
         return h2d, d2h
 
     def graph_kernels(self) -> int:

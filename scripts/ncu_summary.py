@@ -17,9 +17,9 @@ KEYS = [
     ("launch__block_size", "block"),
 ]
 
-STAGE_OF = {"dt_rows": "dt_filter", "dt_apply": "dt_filter", "dt_agg": "dt_filter",
-            "dt_link": "dt_filter", "dt_cols": "dt_filter", "finalize": "finalize_warp", "warp": "finalize_warp", "collapse": "fuse", "ssim": "ssim",
-            "weights0": "fuse", "down": "fuse", "collapse0": "fuse"}
+# report name (scripts/ncu_top.sh) -> kernel-probe family (bench.py kernel_bytes)
+STAGE_OF = {"dt_rows": "dt_rows", "dt_cols": "dt_cols", "warp": "warp", "ssim": "ssim",
+            "weights0": "fuse_weights0", "collapse0": "fuse_collapse0"}
 
 
 def unit_scale(unit):
@@ -57,8 +57,8 @@ for rep in sys.argv[1:]:
           f"{int(d.get('regs', 0))} | {int(d.get('grid', 0))} x {int(d.get('block', 0))} |")
     st = STAGE_OF.get(name)
     if st:
-        traffic.setdefault(st, 0.0)
-        traffic[st] += (d.get("dram_read", 0) + d.get("dram_write", 0))
+        traffic.setdefault(st, []).append(d.get("dram_read", 0) + d.get("dram_write", 0))
 os.makedirs("profiles", exist_ok=True)
-with open("profiles/traffic_partial.json", "w") as f:
-    json.dump({k: v for k, v in traffic.items()}, f, indent=1)
+# bytes per launch, averaged over the captured launches of the family
+with open("profiles/traffic.json", "w") as f:
+    json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, f, indent=1)

@@ -154,26 +154,33 @@ def test_densify_warp_stages(scene):
     np.testing.assert_array_equal(valid, ovalid)
 
 
-@pytest.mark.parametrize("shape", [(480, 640), (37, 53), (1, 70), (70, 1), (2100, 33), (9000, 5)])
-def test_dt_filter_both_column_paths(cuda, shape):
-    """The cluster-resident column kernel and the chunk agg/link/apply path
-    (still used for very tall images) both match the oracle's sequential
-    recursion, for 1-3 planes, odd sizes and degenerate 1-pixel axes."""
+@pytest.mark.parametrize("shape", [(480, 640), (37, 53), (37, 54), (1, 70), (70, 1), (2100, 33),
+                                   (2100, 34), (4100, 6), (9000, 5)])
+def test_dt_filter_all_column_paths(cuda, shape):
+    """Every column-sweep implementation -- the shared-memory band kernels
+    (each band shape), the register-resident cluster kernel and the chunk
+    agg/link/apply path (odd widths, very tall images) -- matches the
+    oracle's sequential recursion for 1-3 planes, odd sizes and degenerate
+    1-pixel axes."""
     from paper_1504_01441_b200 import _native
     h, w = shape
     rng = np.random.default_rng(h * 7 + w)
     guide = rng.random((h, w), dtype=np.float32)
+    paths = [("dt_cluster_columns", 1, "dt_smem_columns", v) for v in (0, 1, 2, 3, -1)]
+    paths.append(("dt_cluster_columns", 0, "dt_smem_columns", 0))
     try:
         for k in (1, 2, 3):
             planes = rng.normal(size=(h, w, k))
             planes[rng.random((h, w)) < 0.9] = 0.0  # sparse like the splat maps
             want = O.dt_filter(guide, planes if k > 1 else planes[..., 0])
-            for cluster in (1, 0):
-                _native.check(_native.lib().hdr_set_option(b"dt_cluster_columns", cluster))
+            for o1, v1, o2, v2 in paths:
+                _native.check(_native.lib().hdr_set_option(o1.encode(), v1))
+                _native.check(_native.lib().hdr_set_option(o2.encode(), v2))
                 got = densify.dt_filter(guide, planes if k > 1 else planes[..., 0])
-                assert np.abs(np.asarray(got) - want).max() < 1e-9, (k, cluster)
+                assert np.abs(np.asarray(got) - want).max() < 1e-9, (k, o1, v1, o2, v2)
     finally:
         _native.lib().hdr_set_option(b"dt_cluster_columns", 1)
+        _native.lib().hdr_set_option(b"dt_smem_columns", -1)
 
 
 def test_ssim_and_fuse_stages(scene):

@@ -243,6 +243,28 @@ int hdr_make_ssim(hdr_ctx* ctx, const float* lum_ref, const float* warped,
 /* fusion.quality_weights (fusion.py:67-77): rgb (h, w, 3) -> (h, w) f32. */
 int hdr_quality_weights(hdr_ctx* ctx, const float* rgb, int32_t width, int32_t height,
                         float* out);
+/* n-frame stack (n = 2..4, BASELINE config "5MP
+ * three-exposure stack"): frames[0] is the reference (pick it with
+ * metering.choose_reference); each source f >= 1 is registered to it exactly
+ * as register_and_fuse does up to the SSIM map (outs[f-1] receives its flow,
+ * warped frame, validity, SSIM, matches, H and info words; composite may be
+ * NULL there), then the n frames are blended by hdr_fuse_stack into
+ * `composite`. A source that fails to register leaves info[0] =
+ * HDR_ERR_REGISTRATION in its outputs (the caller raises, as the reference
+ * would for that pair). */
+int hdr_register_and_fuse_stack(hdr_ctx* ctx, const hdr_params* p, int32_t n, int32_t width,
+                                int32_t height, const float* const* frames,
+                                const hdr_outputs* const* outs, float* composite);
+/* k-way fusion of an n-frame stack (n = 2..4): frames[0]
+ * is the reference, frames[1..n-1] the warped sources with their SSIM
+ * (ssim[f-1]) and validity (valid[f-1]); the weights are fusion.py:117-128's
+ * generalised to n frames (w_0 = q(ref), w_f = q(warped_f) clip(ssim_f, 0, 1)
+ * valid_f, each divided by their sum) and blended through fusion.py:96-157's
+ * pyramids. n = 2 is exactly hdr_fuse. Arrays of device pointers live on
+ * the host. */
+int hdr_fuse_stack(hdr_ctx* ctx, int32_t n, const float* const* frames, const float* const* ssim,
+                   const uint8_t* const* valid, int32_t width, int32_t height, int32_t levels,
+                   float* out);
 /* fusion.fusion_weights (fusion.py:117-128): normalised (w_ref, w_src),
  * each (h, w) f32; valid is 0/1 per pixel. */
 int hdr_fusion_weights(hdr_ctx* ctx, const float* ref, const float* warped, const float* ssim,

@@ -185,6 +185,59 @@ def format_fixture():
     return out
 
 
+def stack_frames(w, h, seed):
+    """BASELINE config C3 at any size: the -2 / 0 / +2 EV stack of SURVEY.md
+    §8(d) -- the base frame and its +2 and +4 stop renderings (one seed, so
+    the base frame is shared), in the order (+2, base, +4)."""
+    a = synth.synth_stack(synth.working_spec(w, h, stops=2.0), seed)
+    b = synth.synth_stack(synth.working_spec(w, h, stops=4.0), seed)
+    assert np.array_equal(a.ref, b.ref)
+    return [a.src, a.ref, b.src], [4.0, 1.0, 16.0]
+
+
+def stack_fixture(w, h, seed):
+    """k-way stack composed from the REAL reference's functions: metering's
+    reference choice, a pairwise register_and_fuse per source (for its
+    warped frame, SSIM and validity), quality_weights, the pyramids and
+    collapse_pyramid (the composition the oracle's fuse_stack restates)."""
+    from hdrflow import fusion, metering, pipeline
+    frames, exposures = stack_frames(w, h, seed)
+    k = metering.choose_reference(frames, exposures)
+    ref = frames[k]
+    warped, ssims, valids, counts = [ref], [], [], []
+    for f, src in enumerate(frames):
+        if f == k:
+            continue
+        r = pipeline.register_and_fuse(ref, src)
+        warped.append(r.warped)
+        ssims.append(r.ssim)
+        valids.append(r.valid.astype(np.float32))
+        counts.append(np.array(r.level_counts, dtype=np.int64))
+    levels = fusion.default_fusion_levels(h, w)
+    ws = [fusion.quality_weights(ref)]
+    for f in range(1, len(warped)):
+        ws.append(fusion.quality_weights(warped[f]) * np.clip(ssims[f - 1], 0.0, 1.0)
+                  * np.asarray(valids[f - 1], dtype=np.float64))
+    tot = ws[0]
+    for x in ws[1:]:
+        tot = tot + x
+    ws = [x / tot for x in ws]
+    laps = [fusion.laplacian_pyramid(x, levels) for x in warped]
+    gps = [fusion.gaussian_pyramid(x, levels) for x in ws]
+    blended = []
+    for lev in range(len(laps[0])):
+        acc = gps[0][lev][:, :, None] * laps[0][lev]
+        for f in range(1, len(warped)):
+            acc = acc + gps[f][lev][:, :, None] * laps[f][lev]
+        blended.append(acc)
+    comp = np.clip(fusion.collapse_pyramid(blended), 0.0, 1.0).astype(np.float32)
+    out = {"scene": np.array([w, h, seed]), "reference_index": np.array(k),
+           "composite_digest": np.array(digest(comp)), "composite_sub": sub(comp)}
+    for i, c in enumerate(counts):
+        out[f"level_counts_{i}"] = c
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
@@ -209,6 +262,7 @@ def main():
                         message=np.array(raised))
     print("default scene:", raised)
     np.savez_compressed(os.path.join(GOLDEN, "formats.npz"), **format_fixture())
+    np.savez_compressed(os.path.join(GOLDEN, "stack3_vga.npz"), **stack_fixture(640, 480, 7))
     for name, mode, exposures, swap in FILE_CASES:
         fx = file_fixture(name, mode, exposures, swap)
         np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **fx)

@@ -734,3 +734,55 @@ def run_hdr(inputs, exposures=None, p: Params | None = None):
     k = choose_reference(images, exposures)
     out = register_and_fuse(images[k], images[1 - k], p)
     return out, png_quantize(out.composite), k
+
+
+# ---------------------------------------------------------- n-frame stacks
+# Not reference code: the reference registers and fuses exactly two images
+# (pipeline.py:271-272, fusion.py:135-157); the paper prescribes n-1 pairwise
+# registrations against the reference. This composes the
+# reference's own functions -- the pairwise register_and_fuse stages,
+# quality_weights, laplacian/gaussian pyramids and collapse -- into the k-way
+# blend (weights normalised over all frames). For n = 2 it is exactly fuse().
+def fuse_stack(frames, ssims, valids, levels=None):
+    """frames[0] = reference, frames[f] = warped source f (ssims/valids[f-1])."""
+    h, w = frames[0].shape[:2]
+    if levels is None:
+        levels = fusion_levels(h, w)
+    ws = [quality_weights(frames[0])]
+    for f in range(1, len(frames)):
+        ws.append(quality_weights(frames[f]) * np.clip(ssims[f - 1], 0.0, 1.0)
+                  * np.asarray(valids[f - 1], dtype=np.float64))
+    tot = ws[0]
+    for x in ws[1:]:
+        tot = tot + x
+    ws = [x / tot for x in ws]
+    laps = [laplacian_pyramid(x, levels) for x in frames]
+    gps = [gaussian_pyramid(x, levels) for x in ws]
+    blended = []
+    for lev in range(len(laps[0])):
+        acc = gps[0][lev][:, :, None] * laps[0][lev]
+        for f in range(1, len(frames)):
+            acc = acc + gps[f][lev][:, :, None] * laps[f][lev]
+        blended.append(acc)
+    return np.clip(collapse(blended), 0.0, 1.0).astype(np.float32)
+
+
+def register_and_fuse_stack(frames, exposures=None, p: Params | None = None):
+    """Pick the reference (metering.choose_reference), register every other
+    frame to it as register_and_fuse does, blend all frames. Returns
+    (composite, reference index, [OracleOutput per source, frame order])."""
+    p = p or Params()
+    frames = [as_rgb(np.asarray(x, dtype=np.float32)) for x in frames]
+    exposures = [1.0] * len(frames) if exposures is None else exposures
+    k = choose_reference(frames, exposures)
+    ref = frames[k]
+    regs, warped, ssims, valids = [], [ref], [], []
+    for f, src in enumerate(frames):
+        if f == k:
+            continue
+        r = register_and_fuse(ref, src, p)
+        regs.append(r)
+        warped.append(r.warped)
+        ssims.append(r.ssim)
+        valids.append(r.valid.astype(np.float32))
+    return fuse_stack(warped, ssims, valids), k, regs

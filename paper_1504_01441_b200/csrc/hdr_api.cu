@@ -231,10 +231,6 @@ extern "C" int hdr_params_validate(const hdr_params* p, char* msg, size_t len) {
 }
 
 // ------------------------------------------------------------ geometry of a call
-struct Dims {
-  int w, h;
-};
-
 // image.build_pyramid level dims (image.py:71-88)
 static int pyramid_dims(int w, int h, int max_levels, Dims* d) {
   d[0] = {w, h};
@@ -261,6 +257,33 @@ static int fusion_dims(int w, int h, int levels, std::vector<Dims>& d) {
   while ((int)d.size() < levels && std::min(d.back().w, d.back().h) >= 2)
     d.push_back({(d.back().w + 1) / 2, (d.back().h + 1) / 2});
   return (int)d.size();
+}
+
+// floats of a fusion pyramid of nf frames: levels 1.. (level 1 also for a
+// single-level pyramid) x (4 nf Gaussian + 3 collapse channels)
+static int64_t fusion_floats(const std::vector<Dims>& fd, int nf) {
+  int64_t n = 0;
+  for (size_t k = 1; k < std::max<size_t>(fd.size(), 2); ++k) {
+    Dims d = k < fd.size() ? fd[k] : Dims{(fd[0].w + 1) / 2, (fd[0].h + 1) / 2};
+    n += (4 * nf + 3) * ((int64_t)d.w * d.h + 64);
+  }
+  return n;
+}
+
+static void fusion_layout(const std::vector<Dims>& fd, int nf, float* base, FusePyramid& py) {
+  py.levels = (int)fd.size();
+  float* q = base;
+  for (size_t k = 0; k < std::max<size_t>(fd.size(), 2) && k < 32; ++k) {
+    Dims d = k < fd.size() ? fd[k] : Dims{(fd[0].w + 1) / 2, (fd[0].h + 1) / 2};
+    py.dims[k] = d;
+    py.g[k] = py.c[k] = nullptr;
+    if (k == 0) continue;
+    int64_t n = (int64_t)d.w * d.h;
+    py.g[k] = q;
+    q += 4 * nf * n + 64;
+    py.c[k] = q;
+    q += 3 * n + 64;
+  }
 }
 
 static int ntiles_of(int w, int h, int tile) { return ceil_div(w, tile) * ceil_div(h, tile); }
@@ -326,6 +349,8 @@ struct hdr_ctx {
   bool probing = false;
   KProbe kprobes[HDR_NUM_KPROBES] = {};
   float* frames = nullptr;      // decoded ref + src RGB frames of the raw-sample path (lazy)
+  float* fstack = nullptr;      // k-way fusion: pyramid (4 NF + 3 ch / level) + NF weights (lazy)
+  int64_t fstack_cap = 0;
   int32_t graph_kernels = 0;
   std::map<std::string, GraphEntry> graphs;
   std::vector<void*> allocs;
@@ -356,6 +381,7 @@ extern "C" int hdr_ctx_destroy(hdr_ctx* c) {
   if (c->fits) cudaFree(c->fits);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->frames) cudaFree(c->frames);
+  if (c->fstack) cudaFree(c->fstack);
   delete c;
   return HDR_OK;
 }
@@ -388,8 +414,7 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   c->rows_cap = ntiles_of(width, height, 16) + 32;
   std::vector<Dims> fd;
   fusion_dims(width, height, 64, fd);
-  int64_t fsum = 0;
-  for (size_t k = 1; k < fd.size(); ++k) fsum += 11 * ((int64_t)fd[k].w * fd[k].h + 64);
+  int64_t fsum = fusion_floats(fd, 2);
   c->fpyr_cap = fsum;
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, n) \
@@ -782,51 +807,35 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
   return check_launch();
 }
 
-static void fusion_offsets(const std::vector<Dims>& fd, float* base, std::vector<float*>& g,
-                           std::vector<float*>& cpl) {
-  g.assign(fd.size(), nullptr);
-  cpl.assign(fd.size(), nullptr);
-  float* q = base;
-  for (size_t k = 1; k < fd.size(); ++k) {
-    int64_t n = (int64_t)fd[k].w * fd[k].h;
-    g[k] = q;
-    q += 8 * n + 64;
-    cpl[k] = q;
-    q += 3 * n + 64;
-  }
+// fusion.fuse (fusion.py:135-157) for nf frames from `base` (pyramid) and
+// `wout` (nf level-0 weight planes)
+static int enqueue_fuse_frames(hdr_ctx* c, int nf, const FuseFrameSet& fs, int w, int h, int levels,
+                               float* base, float* out) {
+  if (levels <= 0) levels = fusion_levels_default(w, h);
+  std::vector<Dims> fd;
+  fusion_dims(w, h, levels, fd);
+  FusePyramid py{};
+  fusion_layout(fd, nf, base, py);
+  py.out = out;
+  launch_fuse(nf, fs, py, c->stream, &c->kprobes[HDR_KP_FUSE_WEIGHTS0],
+              &c->kprobes[HDR_KP_FUSE_COLLAPSE0]);
+  return check_launch();
 }
 
 static int enqueue_fuse(hdr_ctx* c, const float* ref, const float* warped, const float* ssim,
                         const uint8_t* valid, int w, int h, int levels, float* out) {
-  cudaStream_t s = c->stream;
-  if (levels <= 0) levels = fusion_levels_default(w, h);
-  std::vector<Dims> fd;
-  int L = fusion_dims(w, h, levels, fd);
-  std::vector<float*> g, cp;
-  fusion_offsets(fd, c->fpyr, g, cp);
-  if (L == 1) {
-    launch_fusion_weights(ref, warped, ssim, valid, w, h, c->wr, c->ws, s);
-    launch_fuse_collapse0(ref, warped, c->wr, c->ws, w, h, nullptr, nullptr, 0, 0, out, s);
-    return check_launch();
-  }
-  // weights (kept for level 0) fused with the first blur + decimation
-  kprobe_mark(&c->kprobes[HDR_KP_FUSE_WEIGHTS0], 0, s);
-  launch_weights_down0(ref, warped, ssim, valid, w, h, c->wr, c->ws, g[1], fd[1].w, fd[1].h, s);
-  kprobe_mark(&c->kprobes[HDR_KP_FUSE_WEIGHTS0], 1, s);
-  for (int k = 1; k + 1 < L; ++k)
-    launch_fuse_down(g[k], fd[k].w, fd[k].h, g[k + 1], fd[k + 1].w, fd[k + 1].h, s);
-  launch_fuse_top(g[L - 1], fd[L - 1].w, fd[L - 1].h, cp[L - 1], s);
-  for (int k = L - 2; k >= 1; --k)
-    launch_fuse_collapse(g[k], fd[k].w, fd[k].h, g[k + 1], cp[k + 1], fd[k + 1].w, fd[k + 1].h,
-                         cp[k], s);
-  kprobe_mark(&c->kprobes[HDR_KP_FUSE_COLLAPSE0], 0, s);
-  launch_fuse_collapse0(ref, warped, c->wr, c->ws, w, h, g[1], cp[1], fd[1].w, fd[1].h, out, s);
-  kprobe_mark(&c->kprobes[HDR_KP_FUSE_COLLAPSE0], 1, s);
-  return check_launch();
+  FuseFrameSet fs{};
+  fs.img[0] = ref;
+  fs.img[1] = warped;
+  fs.ssim[1] = ssim;
+  fs.valid[1] = valid;
+  fs.wout[0] = c->wr;
+  fs.wout[1] = c->ws;
+  return enqueue_fuse_frames(c, 2, fs, w, h, levels, c->fpyr, out);
 }
 
 static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
-                        const float* src, const hdr_outputs* o) {
+                        const float* src, const hdr_outputs* o, bool fuse = true) {
   cudaStream_t s = c->stream;
   for (KProbe& k : c->kprobes) k.next = 0;
   int64_t P = (int64_t)w * h;
@@ -861,6 +870,7 @@ static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const flo
   launch_ssim(c->lum_ref, nullptr, c->qw, c->lut + kBins, w, h, p->ssim_window, c->taps, o->ssim, s);
   kprobe_mark(&c->kprobes[HDR_KP_SSIM], 1, s);
   probe(c, 5, 1);
+  if (!fuse) return check_launch();
   probe(c, 6, 0);
   // fusion.fuse (pipeline.py:193)
   rc = enqueue_fuse(c, ref, o->warped, o->ssim, o->valid, w, h, 0, o->composite);
@@ -881,7 +891,7 @@ static int ensure_lattice(hdr_ctx* c, const hdr_params* p, int w, int h) {
 }
 
 static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const float* ref,
-                           const float* src, const hdr_outputs* o) {
+                           const float* src, const hdr_outputs* o, bool need_composite = true) {
   if (!c || !p || !o) return fail(HDR_ERR_INVALID, "null argument");
   char msg[128];
   int rc = hdr_params_validate(p, msg, sizeof msg);
@@ -894,7 +904,7 @@ static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const 
   size_t side = 2 * (size_t)p->radius + p->patch;
   if ((side * side + (size_t)p->patch * p->patch) * 8 > 200 * 1024)
     return fail(HDR_ERR_INVALID, "radius/patch search window exceeds shared memory");
-  if (!ref || !src || !o->composite || !o->flow || !o->warped || !o->valid || !o->ssim ||
+  if (!ref || !src || (need_composite && !o->composite) || !o->flow || !o->warped || !o->valid || !o->ssim ||
       !o->matches || !o->raw_matches || !o->homography || !o->info)
     return fail(HDR_ERR_INVALID, "null buffer");
   rc = check_ptr_align(ref, 16, "ref");
@@ -1393,10 +1403,68 @@ extern "C" int hdr_fuse(hdr_ctx* c, const float* ref, const float* warped, const
   NEED((int64_t)w * h <= c->P, "image larger than the workspace");
   std::vector<Dims> fd;
   fusion_dims(w, h, levels > 0 ? levels : fusion_levels_default(w, h), fd);
-  int64_t need = 0;
-  for (size_t k = 1; k < fd.size(); ++k) need += 11 * ((int64_t)fd[k].w * fd[k].h + 64);
-  NEED(need <= c->fpyr_cap, "fusion pyramid larger than the workspace");
+  NEED(fusion_floats(fd, 2) <= c->fpyr_cap, "fusion pyramid larger than the workspace");
   return enqueue_fuse(c, ref, warped, ssim, valid, w, h, levels, out);
+}
+
+extern "C" int hdr_fuse_stack(hdr_ctx* c, int32_t n, const float* const* frames,
+                              const float* const* ssim, const uint8_t* const* valid, int32_t w,
+                              int32_t h, int32_t levels, float* out);
+
+extern "C" int hdr_register_and_fuse_stack(hdr_ctx* c, const hdr_params* p, int32_t n,
+                                           int32_t w, int32_t h, const float* const* frames,
+                                           const hdr_outputs* const* outs, float* composite) {
+  NEED(c && p && frames && outs && composite, "null argument");
+  NEED(n >= 2 && n <= kMaxFuseFrames, "stacks take 2..4 frames");
+  const float* warped[kMaxFuseFrames] = {};
+  const float* ssim[kMaxFuseFrames] = {};
+  const uint8_t* valid[kMaxFuseFrames] = {};
+  warped[0] = frames[0];
+  for (int f = 1; f < n; ++f) {
+    NEED(outs[f - 1], "null outputs");
+    int rc = check_pair_args(c, p, w, h, frames[0], frames[f], outs[f - 1], false);
+    if (rc) return rc;
+    // register_and_fuse up to the SSIM map (pipeline.py:183-192), per source
+    rc = enqueue_pair(c, p, w, h, frames[0], frames[f], outs[f - 1], false);
+    if (rc) return rc;
+    warped[f] = outs[f - 1]->warped;
+    ssim[f - 1] = outs[f - 1]->ssim;
+    valid[f - 1] = outs[f - 1]->valid;
+  }
+  return hdr_fuse_stack(c, n, warped, ssim, valid, w, h, 0, composite);
+}
+
+extern "C" int hdr_fuse_stack(hdr_ctx* c, int32_t n, const float* const* frames,
+                              const float* const* ssim, const uint8_t* const* valid, int32_t w,
+                              int32_t h, int32_t levels, float* out) {
+  NEED(c && frames && out, "null argument");
+  NEED(n >= 2 && n <= kMaxFuseFrames, "stack fusion takes 2..4 frames");
+  NEED(n == 2 || (ssim && valid), "null argument");
+  NEED((int64_t)w * h <= c->P && w >= 1 && h >= 1, "image larger than the workspace");
+  FuseFrameSet fs{};
+  for (int f = 0; f < n; ++f) {
+    NEED(frames[f], "null frame");
+    fs.img[f] = frames[f];
+    if (f > 0) {
+      NEED(ssim[f - 1] && valid[f - 1], "null ssim/valid");
+      fs.ssim[f] = ssim[f - 1];
+      fs.valid[f] = valid[f - 1];
+    }
+  }
+  std::vector<Dims> fd;
+  fusion_dims(w, h, levels > 0 ? levels : fusion_levels_default(w, h), fd);
+  int64_t need = fusion_floats(fd, n) + (int64_t)n * ((int64_t)w * h + 64);
+  if (need > c->fstack_cap) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->fstack) cudaFree(c->fstack);
+    c->fstack = nullptr;
+    c->fstack_cap = 0;
+    CUDA_TRY(cudaMalloc(&c->fstack, need * sizeof(float)));
+    c->fstack_cap = need;
+  }
+  float* wbase = c->fstack + fusion_floats(fd, n);
+  for (int f = 0; f < n; ++f) fs.wout[f] = wbase + (int64_t)f * ((int64_t)w * h + 64);
+  return enqueue_fuse_frames(c, n, fs, w, h, levels, c->fstack, out);
 }
 
 // ------------------------------------------------------------ attributes

@@ -160,19 +160,35 @@ void launch_quality(const float* rgb, int w, int h, float* out, cudaStream_t s);
 void launch_fusion_weights(const float* ref, const float* warped, const float* ssim,
                            const uint8_t* valid, int w, int h, float* wr, float* ws,
                            cudaStream_t s);
-// ---- k_merge.cu: pyramid of 8 planar channels (ref rgb, warped rgb, wr, ws)
+// ---- k_merge.cu: Laplacian-pyramid fusion of NF = 2..4 frames (frame 0 is
+// the reference); level k >= 1 holds 4*NF planar channels (RGB of every
+// frame, then the NF weights) in g[k] and the 3 collapse channels in c[k].
+constexpr int kMaxFuseFrames = 4;
+struct Dims {
+  int w, h;
+};
+template <int NF>
+struct FuseFrames {
+  const float* img[NF];      // (h, w, 3) interleaved; [0] = reference, [f] = warped source f
+  const float* ssim[NF];     // [f >= 1]: (h, w)
+  const uint8_t* valid[NF];  // [f >= 1]: (h, w)
+  float* wout[NF];           // normalised level-0 weights (h, w)
+};
+struct FuseFrameSet {
+  const float* img[kMaxFuseFrames];
+  const float* ssim[kMaxFuseFrames];
+  const uint8_t* valid[kMaxFuseFrames];
+  float* wout[kMaxFuseFrames];
+};
+struct FusePyramid {
+  int levels;
+  Dims dims[32];
+  float* g[32];   // g[0] unused; g[1] must exist even for levels == 1
+  float* c[32];
+  float* out;     // composite (h, w, 3), clipped
+};
 void init_merge_attributes();
-void launch_weights_down0(const float* ref, const float* warped, const float* ssim,
-                          const uint8_t* valid, int w, int h, float* wr, float* ws, float* g1,
-                          int ow, int oh, cudaStream_t s);
-void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh,
-                      cudaStream_t s);
-void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s);
-void launch_fuse_collapse(const float* g, int w, int h, const float* gc,
-                          const float* cc, int cw, int ch, float* c, cudaStream_t s);
-void launch_fuse_collapse0(const float* ref, const float* warped, const float* wr,
-                           const float* ws, int w, int h, const float* gc,
-                           const float* cc, int cw, int ch, float* out,
-                           cudaStream_t s);
+void launch_fuse(int nf, const FuseFrameSet& fs, const FusePyramid& py, cudaStream_t s,
+                 KProbe* kp_w0 = nullptr, KProbe* kp_c0 = nullptr);
 
 }  // namespace hdr

@@ -1,15 +1,17 @@
-// Laplacian-pyramid exposure fusion (K14 + K15), fusion.py:96-157, as four
-// tiled kernels:
+// Laplacian-pyramid exposure fusion (K14 + K15), fusion.py:96-157, for NF
+// frames (NF = 2: the reference's fuse; NF > 2: the k-way generalisation of
+// frame 0 is the reference, weights normalised over all
+// frames), as four tiled kernels:
 //   weights_down0  quality weights of both frames (fusion.py:67-77), the
 //                  SSIM/validity trust and normalisation (fusion.py:117-128)
 //                  for a 36x36 level-0 tile, written for the owned 32x32 and
 //                  immediately blurred + decimated into level 1 of the
-//                  8-channel Gaussian pyramid (ref RGB, warped RGB, W_ref,
-//                  W_src) -- the weights never make a separate HBM round trip
-//                  before the first reduction;
+//                  4*NF-channel Gaussian pyramid (RGB of every frame, then
+//                  the NF weights) -- the weights never make a separate HBM
+//                  round trip before the first reduction;
 //   down           the same 5-tap reflect blur + [::2, ::2] for levels >= 1;
-//   collapse       C_k = W_ref (G_ref - up G_ref') + W_src (G_src - up G_src')
-//                  + up C'  (the blend of laplacian_pyramid terms and
+//   collapse       C_k = sum_f W_f (G_f - up G_f') + up C'  (the blend of
+//                  laplacian_pyramid terms and
 //                  collapse_pyramid folded together); level 0 reads the
 //                  interleaved inputs and writes the clipped composite.
 // up() is _pyr_up (fusion.py:89-93): zero-insert on the fine grid, 2x-gain
@@ -60,16 +62,17 @@ constexpr int kRT = 2 * kOT + 4;  // level-0 region incl. the 2-px blur halo (36
 constexpr int kLT = kRT + 2;      // + 1-px laplacian halo (38)
 constexpr int kRP = kRT + 1;      // padded row pitch of the staged region
 
-// 5-tap blur + [::2, ::2] of 8 staged channels px[c][36][kRP] into a 16x16
+// 5-tap blur + [::2, ::2] of NC staged channels px[c][36][kRP] into a 16x16
 // level-1 tile, four channels at a time: vertical into V[4][16][36], then
 // horizontal to global. V needs only 2304 floats, so it can alias the
-// luminance tiles of weights_down0 (the occupancy limit is shared memory).
-__device__ __forceinline__ void down8(const float* px, float* V, int tid, int Y0, int X0,
-                                      float* __restrict__ out, int ow, int oh) {
+// luminance tiles of weights_down (the occupancy limit is shared memory).
+template <int NC>
+__device__ __forceinline__ void down_tile(const float* px, float* V, int tid, int Y0, int X0,
+                                          float* __restrict__ out, int ow, int oh) {
   int P = ow * oh;
 #pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-    const float* src = px + half * 4 * kRT * kRP;
+  for (int quad = 0; quad < NC / 4; ++quad) {
+    const float* src = px + quad * 4 * kRT * kRP;
     // 4 * 16 * 36 = 2304 = 9 * 256 vertical outputs
 #pragma unroll 3
     for (int i = tid; i < 4 * kOT * kRT; i += 256) {
@@ -92,21 +95,19 @@ __device__ __forceinline__ void down8(const float* px, float* V, int tid, int Y0
       float acc = kK5[0] * row[0];
 #pragma unroll
       for (int k = 1; k < 5; ++k) acc += kK5[k] * row[k];
-      if (Y < oh && X < ow) out[(half * 4 + c) * P + Y * ow + X] = acc;
+      if (Y < oh && X < ow) out[(quad * 4 + c) * P + Y * ow + X] = acc;
     }
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(256) weights_down0_kernel(
-    const float* __restrict__ ref, const float* __restrict__ warped, const float* __restrict__ ssim,
-    const uint8_t* __restrict__ valid, int w, int h, float* __restrict__ wr_out,
-    float* __restrict__ ws_out, float* __restrict__ g1, int ow, int oh) {
+template <int NF>
+__global__ void __launch_bounds__(256, NF == 2 ? 4 : 2) weights_down_kernel(FuseFrames<NF> fr, int w, int h,
+                                                          float* __restrict__ g1, int ow, int oh) {
   extern __shared__ float smf[];
-  float* lr = smf;                    // [38][38] luminance of ref
-  float* lw = smf + kLT * kLT;        // [38][38] luminance of warped
-  float* px = smf + 2 * kLT * kLT;    // [8][36][37]: ref rgb, warped rgb, w_ref, w_src
-  float* V = smf;                     // [4][16][36], aliases lr/lw after the weights
+  float* lum = smf;                    // [NF][38][38] luminance of every frame
+  float* px = smf + NF * kLT * kLT;    // [4NF][36][37]: RGB of every frame, then the weights
+  float* V = smf;                      // [4][16][36], aliases the luminance after the weights
   __shared__ int ridx[kLT], cidx[kLT];
   int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
@@ -117,26 +118,29 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
   }
   __syncthreads();
   // every global load of the tile is issued before the first use: the SSIM
-  // and validity of the weight pass (6 per thread) and the RGB of both
-  // frames (6 x 6 per thread)
+  // and validity of the weight pass (6 per thread and source frame) and the
+  // RGB of all frames (6 x 3NF per thread)
   constexpr int kNW = (kRT * kRT + 255) / 256;  // 6
   constexpr int kNL = (kLT * kLT + 255) / 256;  // 6
-  float svv[kNW];
-  uint8_t vdd[kNW];
+  float svv[NF - 1][kNW];
+  uint8_t vdd[NF - 1][kNW];
   {
     int ty = tid / kRT, tx = tid - ty * kRT;
 #pragma unroll
     for (int it = 0; it < kNW; ++it) {
       int i = tid + it * 256;
       int p = ridx[min(ty + 1, kLT - 1)] * w + cidx[tx + 1];
-      svv[it] = i < kRT * kRT ? __ldg(ssim + p) : 0.0f;
-      vdd[it] = i < kRT * kRT ? __ldg(valid + p) : 0;
+#pragma unroll
+      for (int f = 1; f < NF; ++f) {
+        svv[f - 1][it] = i < kRT * kRT ? __ldg(fr.ssim[f] + p) : 0.0f;
+        vdd[f - 1][it] = i < kRT * kRT ? __ldg(fr.valid[f] + p) : 0;
+      }
       tx += 4; ty += 7;  // 256 = 7 * 36 + 4
       if (tx >= kRT) { tx -= kRT; ++ty; }
     }
   }
   {
-    float rgb[kNL][6];
+    float rgb[kNL][3 * NF];
     int ly = tid / kLT, lx = tid - ly * kLT;
     int lys[kNL], lxs[kNL];
 #pragma unroll
@@ -145,12 +149,10 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
       lys[it] = ly; lxs[it] = lx;
       int p = (ridx[min(ly, kLT - 1)] * w + cidx[lx]) * 3;
       bool ok = i < kLT * kLT;
-      rgb[it][0] = ok ? __ldg(ref + p) : 0.0f;
-      rgb[it][1] = ok ? __ldg(ref + p + 1) : 0.0f;
-      rgb[it][2] = ok ? __ldg(ref + p + 2) : 0.0f;
-      rgb[it][3] = ok ? __ldg(warped + p) : 0.0f;
-      rgb[it][4] = ok ? __ldg(warped + p + 1) : 0.0f;
-      rgb[it][5] = ok ? __ldg(warped + p + 2) : 0.0f;
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) rgb[it][3 * f + k] = ok ? __ldg(fr.img[f] + p + k) : 0.0f;
       lx += 28; ly += 6;  // 256 = 6 * 38 + 28
       if (lx >= kLT) { lx -= kLT; ++ly; }
     }
@@ -158,12 +160,13 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
     for (int it = 0; it < kNL; ++it) {
       int i = tid + it * 256;
       if (i >= kLT * kLT) break;
-      lr[i] = lum_f(rgb[it][0], rgb[it][1], rgb[it][2]);
-      lw[i] = lum_f(rgb[it][3], rgb[it][4], rgb[it][5]);
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+        lum[f * kLT * kLT + i] = lum_f(rgb[it][3 * f], rgb[it][3 * f + 1], rgb[it][3 * f + 2]);
       if ((unsigned)(lys[it] - 1) < (unsigned)kRT && (unsigned)(lxs[it] - 1) < (unsigned)kRT) {
         float* d = px + (lys[it] - 1) * kRP + (lxs[it] - 1);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) d[c * kRT * kRP] = rgb[it][c];
+        for (int c = 0; c < 3 * NF; ++c) d[c * kRT * kRP] = rgb[it][c];
       }
     }
   }
@@ -175,40 +178,52 @@ __global__ void __launch_bounds__(256) weights_down0_kernel(
       int i = tid + it * 256;
       if (i >= kRT * kRT) break;
       int c = (ty + 1) * kLT + tx + 1;
-      double lapr = lap5(lr[c - kLT], lr[c + kLT], lr[c - 1], lr[c + 1], lr[c]);
-      double lapw = lap5(lw[c - kLT], lw[c + kLT], lw[c - 1], lw[c + 1], lw[c]);
       float* d = px + ty * kRP + tx;
-      float qr = quality_f(lapr, d[0], d[kRT * kRP], d[2 * kRT * kRP]);
-      float qs = quality_f(lapw, d[3 * kRT * kRP], d[4 * kRT * kRP], d[5 * kRT * kRP]);
-      float sv = fminf(fmaxf(svv[it], 0.0f), 1.0f);
-      qs = vdd[it] ? qs * sv : 0.0f;
-      float inv = __frcp_rn(qr + qs);
-      float a = qr * inv, b = qs * inv;
-      d[6 * kRT * kRP] = a;
-      d[7 * kRT * kRP] = b;
+      float q[NF];
+      float tot = 0.0f;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const float* L = lum + f * kLT * kLT;
+        double lap = lap5(L[c - kLT], L[c + kLT], L[c - 1], L[c + 1], L[c]);
+        q[f] = quality_f(lap, d[(3 * f) * kRT * kRP], d[(3 * f + 1) * kRT * kRP],
+                         d[(3 * f + 2) * kRT * kRP]);
+        if (f > 0) {
+          // source frames: x clip(SSIM, 0, 1) x validity (fusion.py:124-125)
+          float sv = fminf(fmaxf(svv[f - 1][it], 0.0f), 1.0f);
+          q[f] = vdd[f - 1][it] ? q[f] * sv : 0.0f;
+        }
+        tot = f == 0 ? q[0] : tot + q[f];
+      }
+      float inv = __frcp_rn(tot);
       // owned level-0 pixels: rows/cols [2Y0, 2Y0 + 32) of the real image
-      if ((unsigned)(ty - 2) < 2u * kOT && (unsigned)(tx - 2) < 2u * kOT &&
-          vy0 + ty + 1 < h && vx0 + tx + 1 < w) {
-        int p = ridx[ty + 1] * w + cidx[tx + 1];
-        wr_out[p] = a;
-        ws_out[p] = b;
+      bool own = (unsigned)(ty - 2) < 2u * kOT && (unsigned)(tx - 2) < 2u * kOT &&
+                 vy0 + ty + 1 < h && vx0 + tx + 1 < w;
+      int p = own ? ridx[ty + 1] * w + cidx[tx + 1] : 0;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        float wf = q[f] * inv;
+        d[(3 * NF + f) * kRT * kRP] = wf;
+        if (own) fr.wout[f][p] = wf;
       }
       tx += 4; ty += 7;
       if (tx >= kRT) { tx -= kRT; ++ty; }
     }
   }
   __syncthreads();
-  down8(px, V, tid, Y0, X0, g1, ow, oh);
+  down_tile<4 * NF>(px, V, tid, Y0, X0, g1, ow, oh);
 }
 
 // ---------------------------------------------------------------- levels >= 1
-constexpr size_t kDownSmem = sizeof(float) * (8 * kRT * kRP + 4 * kOT * kRT);
+template <int NF>
+constexpr size_t down_smem() { return sizeof(float) * (4 * NF * kRT * kRP + 4 * kOT * kRT); }
 
+template <int NF>
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
                                                    float* __restrict__ out, int ow, int oh) {
+  constexpr int NC = 4 * NF;
   extern __shared__ float smd[];
-  float* tile = smd;               // [8][36][37]
-  float* V = smd + 8 * kRT * kRP;  // [4][16][36]
+  float* tile = smd;                // [NC][36][37]
+  float* V = smd + NC * kRT * kRP;  // [4][16][36]
   __shared__ int ridx[kRT], cidx[kRT];
   int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
   int P = w * h;
   {
     int ty = tid / kRT, tx = tid - ty * kRT;
-    // two region samples (16 loads) in flight per step
+    // two region samples (2 NC loads) in flight per step
 #pragma unroll 1
     for (int i = tid; i < kRT * kRT; i += 512) {
       int ty2 = ty + 7, tx2 = tx + 4;
@@ -229,16 +244,16 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
       bool ok2 = i + 256 < kRT * kRT;
       const float* s1 = in + ridx[ty] * w + cidx[tx];
       const float* s2 = in + ridx[min(ty2, kRT - 1)] * w + cidx[tx2];
-      float v1[8], v2[8];
+      float v1[NC], v2[NC];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < NC; ++c) {
         v1[c] = __ldg(s1 + c * P);
         v2[c] = ok2 ? __ldg(s2 + c * P) : 0.0f;
       }
       float* d1 = tile + ty * kRP + tx;
       float* d2 = tile + ty2 * kRP + tx2;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < NC; ++c) {
         d1[c * kRT * kRP] = v1[c];
         if (ok2) d2[c * kRT * kRP] = v2[c];
       }
@@ -247,7 +262,7 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
     }
   }
   __syncthreads();
-  down8(tile, V, tid, Y0, X0, out, ow, oh);
+  down_tile<NC>(tile, V, tid, Y0, X0, out, ow, oh);
 }
 
 // ---------------------------------------------------------------- collapse
@@ -274,16 +289,19 @@ __device__ __forceinline__ void tap_rows(int y, int n, int c0, int* idx, float* 
   }
 }
 
-// 9 coarse channels: G_ref 0-2, G_src 3-5 (gc, planar 8-ch level), C 6-8 (cc)
-template <bool LEVEL0>
-__global__ void __launch_bounds__(256) collapse_kernel(
-    const float* __restrict__ g, const float* __restrict__ ref, const float* __restrict__ warped,
-    const float* __restrict__ wr, const float* __restrict__ ws, int w, int h,
-    const float* __restrict__ gc, const float* __restrict__ cc, int cw, int ch,
-    float* __restrict__ out) {
+template <int NF>
+constexpr size_t collapse_smem() { return sizeof(float) * (3 * (NF + 1)) * (kCT * kCT + kCT * kFT); }
+
+// 3NF + 3 coarse channels: G_f RGB (gc, the planar 4NF-channel level), C (cc)
+template <bool LEVEL0, int NF>
+__global__ void __launch_bounds__(256) collapse_kernel(const float* __restrict__ g, FuseFrames<NF> fr,
+                                                      int w, int h, const float* __restrict__ gc,
+                                                      const float* __restrict__ cc, int cw, int ch,
+                                                      float* __restrict__ out) {
+  constexpr int NCH = 3 * (NF + 1);
   extern __shared__ float smc[];
-  float* C = smc;                    // [9][19][19] coarse tile
-  float* Hc = smc + 9 * kCT * kCT;   // [9][19][32] coarse rows up-sampled along x
+  float* C = smc;                      // [NCH][19][19] coarse tile
+  float* Hc = smc + NCH * kCT * kCT;   // [NCH][19][32] coarse rows up-sampled along x
   __shared__ int vr[kFT][3], hc[kFT][3];
   __shared__ float vw[kFT][3], hw[kFT][3];
   int tid = threadIdx.x;
@@ -300,8 +318,8 @@ __global__ void __launch_bounds__(256) collapse_kernel(
     for (int i = tid; i < kCT * kCT; i += 256) {
       int p = min(cy0 + yy, ch - 1) * cw + min(cx0 + xx, cw - 1);
 #pragma unroll
-      for (int c = 0; c < 9; ++c)
-        C[c * kCT * kCT + i] = c < 6 ? __ldg(gc + c * CP + p) : __ldg(cc + (c - 6) * CP + p);
+      for (int c = 0; c < NCH; ++c)
+        C[c * kCT * kCT + i] = c < 3 * NF ? __ldg(gc + c * CP + p) : __ldg(cc + (c - 3 * NF) * CP + p);
       xx += 9; yy += 13;
       if (xx >= kCT) { xx -= kCT; ++yy; }
     }
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(256) collapse_kernel(
     int j0 = hc[x][0], j1 = hc[x][1], j2 = hc[x][2];
     float w0 = hw[x][0], w1 = hw[x][1], w2 = hw[x][2];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) {
+    for (int c = 0; c < NCH; ++c) {
       const float* row = C + (c * kCT + r) * kCT;
       Hc[(c * kCT + r) * kFT + x] = gc ? w0 * row[j0] + w1 * row[j1] + w2 * row[j2] : 0.0f;
     }
@@ -326,81 +344,124 @@ __global__ void __launch_bounds__(256) collapse_kernel(
     if (Y >= h || X >= w) continue;
     int r0 = vr[yy][0], r1 = vr[yy][1], r2 = vr[yy][2];
     float w0 = vw[yy][0], w1 = vw[yy][1], w2 = vw[yy][2];
-    float u[9];
+    float u[NCH];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) {
+    for (int c = 0; c < NCH; ++c) {
       const float* col = Hc + c * kCT * kFT + x;
       u[c] = w0 * col[r0 * kFT] + w1 * col[r1 * kFT] + w2 * col[r2 * kFT];
     }
     int p = Y * w + X;
-    if (LEVEL0) {
-      float a = __ldg(wr + p), b = __ldg(ws + p);
+    float wt[NF];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        float v = a * (__ldg(ref + 3 * p + k) - u[k]) + b * (__ldg(warped + 3 * p + k) - u[3 + k]) + u[6 + k];
-        out[3 * p + k] = fminf(fmaxf(v, 0.0f), 1.0f);
+    for (int f = 0; f < NF; ++f) wt[f] = LEVEL0 ? __ldg(fr.wout[f] + p) : __ldg(g + (3 * NF + f) * P + p);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float v = 0.0f;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        float gv = LEVEL0 ? __ldg(fr.img[f] + 3 * p + k) : __ldg(g + (3 * f + k) * P + p);
+        v = f == 0 ? wt[0] * (gv - u[k]) : v + wt[f] * (gv - u[3 * f + k]);
       }
-    } else {
-      float a = __ldg(g + 6 * P + p), b = __ldg(g + 7 * P + p);
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        out[k * P + p] = a * (__ldg(g + k * P + p) - u[k]) + b * (__ldg(g + (3 + k) * P + p) - u[3 + k]) + u[6 + k];
+      v += u[3 * NF + k];
+      if (LEVEL0)
+        out[3 * p + k] = fminf(fmaxf(v, 0.0f), 1.0f);
+      else
+        out[k * P + p] = v;
     }
   }
 }
 
-// top of the pyramid: C = w_ref * G_ref + w_src * G_src (laps[-1] = gp[-1])
+// top of the pyramid: C = sum_f w_f * G_f (laps[-1] = gp[-1])
+template <int NF>
 __global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float* __restrict__ c) {
   int64_t P = (int64_t)w * h;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
-  float a = g[6 * P + i], b = g[7 * P + i];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) c[k * P + i] = a * g[k * P + i] + b * g[(3 + k) * P + i];
+  for (int k = 0; k < 3; ++k) {
+    float v = 0.0f;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) v = f == 0 ? g[(3 * NF) * P + i] * g[k * P + i]
+                                           : v + g[(3 * NF + f) * P + i] * g[(3 * f + k) * P + i];
+    c[k * P + i] = v;
+  }
 }
 
-constexpr size_t kW0Smem = sizeof(float) * (2 * kLT * kLT + 8 * kRT * kRP);
+template <int NF>
+constexpr size_t weights_smem() { return sizeof(float) * (NF * kLT * kLT + 4 * NF * kRT * kRP); }
 static_assert(4 * kOT * kRT <= 2 * kLT * kLT, "V aliases the luminance tiles");
 
+template <int NF>
+static void init_merge_nf() {
+  cudaFuncSetAttribute(weights_down_kernel<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)weights_smem<NF>());
+  cudaFuncSetAttribute(down_kernel<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down_smem<NF>());
+  cudaFuncSetAttribute(collapse_kernel<true, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)collapse_smem<NF>());
+  cudaFuncSetAttribute(collapse_kernel<false, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)collapse_smem<NF>());
+}
+
 void init_merge_attributes() {
-  cudaFuncSetAttribute(weights_down0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kW0Smem);
-  cudaFuncSetAttribute(down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDownSmem);
-  cudaFuncSetAttribute(collapse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)kCollapseSmem);
-  cudaFuncSetAttribute(collapse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)kCollapseSmem);
+  init_merge_nf<2>();
+  init_merge_nf<3>();
+  init_merge_nf<4>();
 }
 
-void launch_weights_down0(const float* ref, const float* warped, const float* ssim,
-                          const uint8_t* valid, int w, int h, float* wr, float* ws, float* g1,
-                          int ow, int oh, cudaStream_t s) {
-  dim3 grd(ceil_div(ow, kOT), ceil_div(oh, kOT));
-  weights_down0_kernel<<<grd, 256, kW0Smem, s>>>(ref, warped, ssim, valid, w, h, wr, ws, g1, ow, oh);
+template <int NF>
+static void launch_fuse_nf(const FuseFrames<NF>& fr, const FusePyramid& py, cudaStream_t s,
+                           KProbe* kp_w0, KProbe* kp_c0) {
+  const int L = py.levels;
+  const Dims* d = py.dims;
+  // level 1 always has storage (py.g[1]): with a single-level pyramid the
+  // weights pass still runs its reduction there and the collapse ignores it
+  const Dims d1 = L > 1 ? d[1] : Dims{(d[0].w + 1) / 2, (d[0].h + 1) / 2};
+  kprobe_mark(kp_w0, 0, s);
+  dim3 g0(ceil_div(d1.w, kOT), ceil_div(d1.h, kOT));
+  weights_down_kernel<NF><<<g0, 256, weights_smem<NF>(), s>>>(fr, d[0].w, d[0].h, py.g[1], d1.w, d1.h);
+  kprobe_mark(kp_w0, 1, s);
+  if (L == 1) {
+    dim3 gf(ceil_div(d[0].w, kFT), ceil_div(d[0].h, kFT));
+    collapse_kernel<true, NF><<<gf, 256, collapse_smem<NF>(), s>>>(nullptr, fr, d[0].w, d[0].h, nullptr,
+                                                                  nullptr, 0, 0, py.out);
+    return;
+  }
+  for (int k = 1; k + 1 < L; ++k) {
+    dim3 gk(ceil_div(d[k + 1].w, kOT), ceil_div(d[k + 1].h, kOT));
+    down_kernel<NF><<<gk, 256, down_smem<NF>(), s>>>(py.g[k], d[k].w, d[k].h, py.g[k + 1], d[k + 1].w,
+                                                    d[k + 1].h);
+  }
+  int64_t Pt = (int64_t)d[L - 1].w * d[L - 1].h;
+  fuse_top_kernel<NF><<<(unsigned)((Pt + 255) / 256), 256, 0, s>>>(py.g[L - 1], d[L - 1].w,
+                                                                   d[L - 1].h, py.c[L - 1]);
+  for (int k = L - 2; k >= 1; --k) {
+    dim3 gk(ceil_div(d[k].w, kFT), ceil_div(d[k].h, kFT));
+    collapse_kernel<false, NF><<<gk, 256, collapse_smem<NF>(), s>>>(
+        py.g[k], fr, d[k].w, d[k].h, py.g[k + 1], py.c[k + 1], d[k + 1].w, d[k + 1].h, py.c[k]);
+  }
+  kprobe_mark(kp_c0, 0, s);
+  dim3 gf(ceil_div(d[0].w, kFT), ceil_div(d[0].h, kFT));
+  collapse_kernel<true, NF><<<gf, 256, collapse_smem<NF>(), s>>>(
+      nullptr, fr, d[0].w, d[0].h, py.g[1], py.c[1], d[1].w, d[1].h, py.out);
+  kprobe_mark(kp_c0, 1, s);
 }
 
-void launch_fuse_down(const float* in, int w, int h, float* out, int ow, int oh, cudaStream_t s) {
-  dim3 grd(ceil_div(ow, kOT), ceil_div(oh, kOT));
-  down_kernel<<<grd, 256, kDownSmem, s>>>(in, w, h, out, ow, oh);
-}
-
-void launch_fuse_top(const float* g, int w, int h, float* c, cudaStream_t s) {
-  int64_t P = (int64_t)w * h;
-  fuse_top_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(g, w, h, c);
-}
-
-void launch_fuse_collapse(const float* g, int w, int h, const float* gc, const float* cc, int cw,
-                          int ch, float* c, cudaStream_t s) {
-  dim3 grd(ceil_div(w, kFT), ceil_div(h, kFT));
-  collapse_kernel<false><<<grd, 256, kCollapseSmem, s>>>(g, nullptr, nullptr, nullptr, nullptr, w, h, gc, cc,
-                                             cw, ch, c);
-}
-
-void launch_fuse_collapse0(const float* ref, const float* warped, const float* wr, const float* ws,
-                           int w, int h, const float* gc, const float* cc, int cw, int ch,
-                           float* out, cudaStream_t s) {
-  dim3 grd(ceil_div(w, kFT), ceil_div(h, kFT));
-  collapse_kernel<true><<<grd, 256, kCollapseSmem, s>>>(nullptr, ref, warped, wr, ws, w, h, gc, cc, cw, ch,
-                                            out);
+void launch_fuse(int nf, const FuseFrameSet& fs, const FusePyramid& py, cudaStream_t s,
+                 KProbe* kp_w0, KProbe* kp_c0) {
+  auto pack = [&](auto fr) {
+    for (int f = 0; f < (int)(sizeof(fr.img) / sizeof(fr.img[0])); ++f) {
+      fr.img[f] = fs.img[f];
+      fr.ssim[f] = fs.ssim[f];
+      fr.valid[f] = fs.valid[f];
+      fr.wout[f] = fs.wout[f];
+    }
+    return fr;
+  };
+  switch (nf) {
+    case 2: launch_fuse_nf<2>(pack(FuseFrames<2>{}), py, s, kp_w0, kp_c0); break;
+    case 3: launch_fuse_nf<3>(pack(FuseFrames<3>{}), py, s, kp_w0, kp_c0); break;
+    default: launch_fuse_nf<4>(pack(FuseFrames<4>{}), py, s, kp_w0, kp_c0); break;
+  }
 }
 
 }  // namespace hdr

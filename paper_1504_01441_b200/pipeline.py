@@ -180,7 +180,7 @@ def register_and_fuse(ref, src, params: PipelineParams | None = None) -> Registr
     return _collect(bufs, as_torch)
 
 
-def _collect(bufs: PairBuffers, as_torch: bool) -> RegistrationOutput:
+def _collect(bufs: PairBuffers, as_torch: bool, composite: bool = True) -> RegistrationOutput:
     """RegistrationOutput from a finished pair's buffers (one host sync to
     read the verdict; RegistrationError as pipeline.py:185-187)."""
     info = bufs.info.cpu().numpy()
@@ -189,7 +189,7 @@ def _collect(bufs: PairBuffers, as_torch: bool) -> RegistrationOutput:
         raise RegistrationError(f"only {m} reliable matches at full resolution")
     hom = bufs.homography if info[1] else None
     return RegistrationOutput(
-        composite=out(bufs.composite, as_torch),
+        composite=out(bufs.composite, as_torch) if composite else None,
         flow=out(bufs.flow, as_torch),
         warped=out(bufs.warped, as_torch),
         valid=out(bufs.valid.bool(), as_torch),
@@ -439,3 +439,77 @@ class _LazyFrames:
     def lum(self, i):
         from .image import luminance
         return luminance(self[i])
+
+
+# ---------------------------------------------------------------- n-frame stacks
+@dataclass
+class StackOutput:
+    """register_and_fuse_stack's result: the k-way composite, the index of
+    the frame used as reference, and one RegistrationOutput per source frame
+    (frame order, reference skipped; their `composite` is None)."""
+    composite: np.ndarray
+    reference_index: int
+    registrations: list = field(default_factory=list)
+
+
+def register_and_fuse_stack(frames, exposures=None, params: PipelineParams | None = None,
+                            reference_index: int | None = None) -> StackOutput:
+    """n-frame stack (n = 2..4): the reference is
+    metering.choose_reference's pick (darkest exposure; ties -> lower mean
+    luminance) unless given, every other frame is registered to it like
+    register_and_fuse, and all frames are blended with the reference's
+    fusion generalised to n weights. One device pass, one host sync."""
+    from . import metering
+    params = params or PipelineParams()
+    params.validate()
+    n = len(frames)
+    if not 2 <= n <= 4:
+        raise ValueError("stacks take 2..4 frames")
+    as_torch = is_torch(*frames)
+    dev = device_of(*frames)
+    ts = [as_rgb(to_dev(x, torch.float32, dev)) for x in frames]
+    if any(t.shape != ts[0].shape for t in ts):
+        raise ConfigError("reference and source dimensions differ")
+    if ts[0].dim() != 3 or ts[0].shape[2] != 3:
+        raise ValueError("luminance expects an (h, w, 3) image")
+    h, w = ts[0].shape[:2]
+    if min(h, w) < 100:
+        raise ValueError("input below 100 pixels in one dimension")
+    exposures = [1.0] * n if exposures is None else list(exposures)
+    k = metering.choose_reference(ts, exposures) if reference_index is None else int(reference_index)
+    order = [k] + [f for f in range(n) if f != k]
+    bufs = [PairBuffers(w, h, dev) for _ in range(n - 1)]
+    comp = torch.empty((h, w, 3), dtype=torch.float32, device=f"cuda:{dev}")
+    e = engine(w, h, dev)
+    p = params.to_native()
+    fr = (ctypes.c_void_p * n)(*[ts[f].data_ptr() for f in order])
+    outs = (ctypes.c_void_p * (n - 1))(*[ctypes.addressof(b.native) for b in bufs])
+    _native.check(_native.lib().hdr_register_and_fuse_stack(e.handle, ctypes.byref(p), n, w, h, fr,
+                                                            outs, ptr(comp)), "register_and_fuse_stack")
+    regs = []
+    for b in bufs:
+        # raises RegistrationError like the pairwise reference call would
+        regs.append(_collect(b, as_torch, composite=False))
+    return StackOutput(composite=out(comp, as_torch), reference_index=k, registrations=regs)
+
+
+def fuse_stack(frames, ssims, valids, levels: int | None = None):
+    """The k-way blend alone (hdr_fuse_stack): frames[0] = reference,
+    frames[f] = warped source f with ssims[f-1] / valids[f-1]."""
+    n = len(frames)
+    if not 2 <= n <= 4 or len(ssims) != n - 1 or len(valids) != n - 1:
+        raise ValueError("fuse_stack takes 2..4 frames and n-1 ssim/valid maps")
+    as_torch = is_torch(*frames, *ssims, *valids)
+    dev = device_of(*frames, *ssims, *valids)
+    ts = [to_dev(x, torch.float32, dev) for x in frames]
+    ss = [to_dev(x, torch.float32, dev) for x in ssims]
+    vs = [to_dev(np.asarray(v) != 0 if not isinstance(v, torch.Tensor) else v != 0, torch.uint8, dev)
+          for v in valids]
+    h, w = ts[0].shape[:2]
+    res = torch.empty((h, w, 3), dtype=torch.float32, device=ts[0].device)
+    e = engine(w, h, dev)
+    arr = lambda xs: (ctypes.c_void_p * max(len(xs), 1))(*[x.data_ptr() for x in xs])  # noqa: E731
+    _native.check(_native.lib().hdr_fuse_stack(e.handle, n, arr(ts), arr(ss), arr(vs), w, h,
+                                               0 if levels is None else int(levels), ptr(res)),
+                  "fuse_stack")
+    return out(res, as_torch)

@@ -278,6 +278,45 @@ def test_5mp_pair_end_to_end(cuda):
     check_pair(res, o)
 
 
+@pytest.mark.slow
+def test_12mp_pair_end_to_end(cuda):
+    """BASELINE config C4: 12MP (4000x3000) pair (the "16x16 cell grid" is a
+    label only: the reference's 64-px detection tiles, 63x47 of them)."""
+    st = synth.synth_stack(synth.working_spec(4000, 3000), 0)
+    res = pipeline.register_and_fuse(st.ref, st.src)
+    o = O.register_and_fuse(st.ref, st.src)
+    check_pair(res, o)
+
+
+def test_batch_runner_raw_path(cuda):
+    """run_host_raw (raw 8-bit samples in, save_png's 8-bit composite out)
+    equals decode -> register_and_fuse -> quantise pair for pair."""
+    from paper_1504_01441_b200.runner import BatchRunner
+    from paper_1504_01441_b200 import _native, fileio
+    w, h = 320, 240
+    q8 = lambda a: np.clip(np.floor(a.astype(np.float64) * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    stacks = [synth.synth_stack(synth.working_spec(w, h), s) for s in (2, 7)]
+    raws = [(q8(st.ref), q8(st.src)) for st in stacks]
+    want = []
+    for a, b in raws:
+        fa = (a.astype(np.float64) / 255.0).astype(np.float32)
+        fb = (b.astype(np.float64) / 255.0).astype(np.float32)
+        want.append(fileio.quantize_u8(pipeline.register_and_fuse(fa, fb).composite).cpu().numpy())
+    r = BatchRunner(w, h, streams=2)
+    n = 5
+    hp = [(torch.from_numpy(raws[k % 2][0]).pin_memory(), torch.from_numpy(raws[k % 2][1]).pin_memory())
+          for k in range(n)]
+    ho = [(torch.empty((h, w, 3), dtype=torch.uint8).pin_memory(),
+           torch.empty((_native.INFO_WORDS,), dtype=torch.int32).pin_memory()) for _ in range(n)]
+    for _ in range(2):
+        r.run_host_raw(hp, ho, 8)
+    torch.cuda.synchronize()
+    for k in range(n):
+        assert int(ho[k][1][0]) == 0
+        np.testing.assert_array_equal(ho[k][0].numpy(), want[k % 2])
+    r.close()
+
+
 def test_batch_runner_host_and_device_paths(cuda):
     """The throughput runner (several streams, graph replays, double-buffered
     host path) returns, pair for pair, what the single-pair API returns."""

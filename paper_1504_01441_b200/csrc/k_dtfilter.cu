@@ -623,7 +623,31 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-template <int K, bool FINAL>
+// cp.async (LDGSTS): per-thread asynchronous global -> shared copies, used to
+// prefetch the next band of dt_cols_cluster while the current one is linked,
+// applied and stored
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// prefetch slots of one thread: element (k, j) at pfx[(k * kSR + j) * kCT + tid]
+// (consecutive threads, consecutive words: conflict-free), guide j at
+// pfg[j * kCT + tid]
+template <int K>
+constexpr size_t cols_pf_smem() {
+  return sizeof(double) * K * kSR * kCT + sizeof(float) * (kSR + 2) * kCT;
+}
+
+// PF: the band's samples arrive by cp.async into per-thread shared-memory
+// slots issued one band ahead (needs f64 planes and dynamic shared memory of
+// cols_pf_smem<K>()), so HBM reads of band b+1 overlap the link, apply and
+// store phases of band b; otherwise plain loads at the top of each band.
+template <int K, bool FINAL, bool PF>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
                     double c, int bw_log2, DtFlowOut fo) {
@@ -631,34 +655,60 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
   __shared__ Aff<K> ctaF[kCT / 4], ctaB[kCT / 4];  // per-column CTA totals (bw <= kCT / 4)
   __shared__ double cin[kCT / 4][K], din[kCT / 4][K];
   __shared__ Aff<K> remote[kCL][kCT / 4];
+  extern __shared__ __align__(16) double pfx[];
+  float* pfg = reinterpret_cast<float*>(pfx + K * kSR * kCT);
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int bw = 1 << bw_log2, G = kCT >> bw_log2;
   const int col = threadIdx.x & (bw - 1), grp = threadIdx.x >> bw_log2;
   const int RP = ceil_div(h, kCL);
   const int nbands = ceil_div(w, bw);
+  const int r0 = rank * RP + grp * kSR;
+  const int rend = min(h, (rank + 1) * RP);
+  const int nrows = max(0, min(kSR, rend - r0));
+  auto prefetch = [&](int band) {
+    const int x = (band << bw_log2) + col;
+    if (band >= nbands || x >= w) return;
+#pragma unroll
+    for (int j = 0; j < kSR + 2; ++j) {
+      int y = r0 - 1 + j;
+      if (j <= nrows + 1 && y >= 0 && y < h) cp_async4(pfg + j * kCT + threadIdx.x, guide + (int64_t)y * w + x);
+    }
+#pragma unroll
+    for (int j = 0; j < kSR; ++j)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (j < nrows)
+          cp_async8(pfx + (k * kSR + j) * kCT + threadIdx.x,
+                    reinterpret_cast<const double*>(P.p[k]) + (int64_t)(r0 + j) * w + x);
+    cp_async_commit();
+  };
+  if (PF) prefetch(blockIdx.y);
   // persistent: the grid holds as many clusters as can be co-resident and
   // each walks bands (no cluster-launch fragmentation between waves)
   for (int band = blockIdx.y; band < nbands; band += gridDim.y) {
   const int x = (band << bw_log2) + col;
-  const int r0 = rank * RP + grp * kSR;
-  const int rend = min(h, (rank + 1) * RP);
   const bool live = x < w;
-  const int n = live ? max(0, min(kSR, rend - r0)) : 0;
+  const int n = live ? nrows : 0;
   // ---- load (all requests issued before the first use)
   double xv[K][kSR];
   double a[kSR + 1];  // a[j] couples rows r0-1+j and r0+j
   {
     float g[kSR + 2];
+    if (PF) cp_async_wait_all();  // this thread's slots for this band have landed
 #pragma unroll
     for (int j = 0; j < kSR + 2; ++j) {
       int y = r0 - 1 + j;
-      g[j] = (live && j <= n + 1 && y >= 0 && y < h) ? __ldg(guide + (int64_t)y * w + x) : 0.0f;
+      bool ok = live && j <= n + 1 && y >= 0 && y < h;
+      g[j] = ok ? (PF ? pfg[j * kCT + threadIdx.x] : __ldg(guide + (int64_t)y * w + x)) : 0.0f;
     }
 #pragma unroll
     for (int j = 0; j < kSR; ++j)
 #pragma unroll
-      for (int k = 0; k < K; ++k) xv[k][j] = (j < n) ? ldp(P, k, (int64_t)(r0 + j) * w + x) : 0.0;
+      for (int k = 0; k < K; ++k)
+        xv[k][j] = (j < n) ? (PF ? pfx[(k * kSR + j) * kCT + threadIdx.x]
+                                 : ldp(P, k, (int64_t)(r0 + j) * w + x))
+                           : 0.0;
 #pragma unroll
     for (int j = 0; j <= kSR; ++j) {
       int y = r0 - 1 + j;
@@ -683,6 +733,9 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
       R += wgt * Pp;
       Q *= an;
     }
+  // every sample of this band is in registers and consumed: refill the
+  // slots with the next band while this one is linked, applied and stored
+  if (PF) prefetch(band + gridDim.y);
   // ---- forward link: inclusive scan over groups, then across the cluster
   Aff<K> m;
   m.A = Pp;
@@ -1107,21 +1160,49 @@ static bool launch_cols_smem(const float* guide, const DtPlanes& P, int w, int h
 }
 
 // co-resident clusters of a cluster-kernel instantiation (0 = query failed)
-template <int K, bool FINAL>
+template <int K, bool FINAL, bool PF>
 static int max_clusters() {
   static int n = -1;
   if (n < 0) {
+    size_t smem = PF ? cols_pf_smem<K>() : 0;
+    if (PF && cudaFuncSetAttribute(dt_cols_cluster<K, FINAL, PF>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return n = 0;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kCL, 1024);
     cfg.blockDim = dim3(kCT);
+    cfg.dynamicSmemBytes = smem;
     int v = 0;
-    if (cudaOccupancyMaxActiveClusters(&v, dt_cols_cluster<K, FINAL>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&v, dt_cols_cluster<K, FINAL, PF>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       v = 0;
     }
     n = v;
   }
   return n;
+}
+
+// test hook: 0 turns the cp.async band prefetch of the cluster kernel off
+static bool g_cols_prefetch = true;
+
+template <int K, bool FINAL>
+static void launch_cols_cluster(const float* guide, const DtPlanes& P, int w, int h, double ratio,
+                                double c, int bl, const DtFlowOut& fo, cudaStream_t s) {
+  int nb = ceil_div(w, 1 << bl);
+  bool pf = g_cols_prefetch;
+  for (int k = 0; k < P.k; ++k)
+    if (!P.f64[k]) pf = false;
+  int mc = pf ? max_clusters<K, FINAL, true>() : 0;
+  if (pf && mc > 0) {
+    dim3 cgrid(kCL, std::min(nb, mc));
+    dt_cols_cluster<K, FINAL, true><<<cgrid, kCT, cols_pf_smem<K>(), s>>>(guide, P, w, h, ratio, c, bl, fo);
+    return;
+  }
+  mc = max_clusters<K, FINAL, false>();
+  dim3 cgrid(kCL, mc > 0 ? std::min(nb, mc) : nb);
+  dt_cols_cluster<K, FINAL, false><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
 }
 
 // log2 of the cluster kernel's band width for this height, or -1 (too tall)
@@ -1173,15 +1254,11 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
                   : launch_cols_smem<K, false>(guide, P, w, h, ratio, c, fo, s))) {
       finalized = finalized || fin_pass;
     } else if (h > 1 && bl >= 0 && g_cols_cluster) {
-      int nb = ceil_div(w, 1 << bl);
-      bool fin = i == passes && fo.flow && K == 3;
-      int mc = fin ? max_clusters<K, true>() : max_clusters<K, false>();
-      dim3 cgrid(kCL, mc > 0 ? std::min(nb, mc) : nb);
-      if (fin) {
-        dt_cols_cluster<K, true><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
+      if (fin_pass) {
+        launch_cols_cluster<K, true>(guide, P, w, h, ratio, c, bl, fo, s);
         finalized = true;
       } else {
-        dt_cols_cluster<K, false><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
+        launch_cols_cluster<K, false>(guide, P, w, h, ratio, c, bl, fo, s);
       }
     } else if (h > 1) {
       dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
@@ -1205,6 +1282,7 @@ int64_t dt_scratch_doubles(int w, int h, int k) {
 
 void dt_set_cluster_columns(bool on) { g_cols_cluster = on; }
 void dt_set_smem_columns(int cfg) { g_cols_smem_cfg = cfg; }
+void dt_set_cols_prefetch(bool on) { g_cols_prefetch = on; }
 
 void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_kernel<1>);

@@ -47,9 +47,10 @@ if what in ("dt", "all"):
     base[2].view(-1)[idx] = 1.0
     planes = base.clone()
     ref = None
-    for cl, sm in ((1, -1), (1, 1), (1, 2), (1, 3), (1, 0), (0, 0)):
+    for cl, sm, pf in ((1, -1, 1), (1, -1, 0), (1, 1, 1), (0, -1, 1)):
         L.hdr_set_option(b"dt_cluster_columns", cl)
         L.hdr_set_option(b"dt_smem_columns", sm)
+        L.hdr_set_option(b"dt_cols_prefetch", pf)
 
         def run():
             planes.copy_(base)
@@ -63,10 +64,11 @@ if what in ("dt", "all"):
         if ref is None:
             ref = out
         d = (out - ref).abs().max().item()
-        print(f"dt_filter cluster={cl} smem={sm}: {us - cp:8.1f} us (3 passes, copy {cp:.1f} excluded)"
+        print(f"dt_filter cluster={cl} smem={sm} prefetch={pf}: {us - cp:8.1f} us (3 passes, copy {cp:.1f} excluded)"
               f"  max|diff| vs first = {d:.3e}")
     L.hdr_set_option(b"dt_cluster_columns", 1)
     L.hdr_set_option(b"dt_smem_columns", -1)
+    L.hdr_set_option(b"dt_cols_prefetch", 1)
 
 if what in ("warp", "all"):
     src = torch.rand((H, W, 3), device="cuda", dtype=torch.float32)

@@ -168,6 +168,7 @@ def test_dt_filter_all_column_paths(cuda, shape):
     guide = rng.random((h, w), dtype=np.float32)
     paths = [("dt_cluster_columns", 1, "dt_smem_columns", v) for v in (0, 1, 2, 3, -1)]
     paths.append(("dt_cluster_columns", 0, "dt_smem_columns", 0))
+    paths.append(("dt_cols_prefetch", 0, "dt_smem_columns", -1))
     try:
         for k in (1, 2, 3):
             planes = rng.normal(size=(h, w, k))
@@ -181,6 +182,7 @@ def test_dt_filter_all_column_paths(cuda, shape):
     finally:
         _native.lib().hdr_set_option(b"dt_cluster_columns", 1)
         _native.lib().hdr_set_option(b"dt_smem_columns", -1)
+        _native.lib().hdr_set_option(b"dt_cols_prefetch", 1)
 
 
 def test_ssim_and_fuse_stages(scene):

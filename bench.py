@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pairs", type=int, default=16, help="resident pairs per GPU per step")
-    ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--streams", type=int, default=8, help="compute streams of the device-resident runs")
+    ap.add_argument("--e2e-streams", type=int, default=4, help="compute streams of the host-buffer runs")
     ap.add_argument("--scenes", type=int, default=4, help="distinct synthetic scenes")
     ap.add_argument("--e2e-pairs", type=int, default=8)
     ap.add_argument("--width", type=int, default=W5)
@@ -355,8 +356,13 @@ def run_ours(args):
             sum(kev[j][f][2 * i].elapsed_time(kev[j][f][2 * i + 1]) for i in range(n))
             for j in range(NI))
 
-    # ---- end to end through the public batch API (host buffers)
+    # ---- end to end through the public batch API (host buffers); fewer
+    # compute streams than the device runs: the host link is the bottleneck
     E = args.e2e_pairs
+    if args.e2e_streams != args.streams:
+        runner.close()
+        runner = BatchRunner(w, h, streams=args.e2e_streams, params=PipelineParams(), device=local,
+                             graph=not args.no_graph)
     hpairs = []
     for k in range(E):
         ref, src = scenes[k % len(scenes)]
@@ -438,6 +444,7 @@ def run_ours(args):
         "dtype": "f32/f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "width": w, "height": h, "pairs_per_step_per_gpu": B,
                    "global_pairs_per_step": B * world, "streams": args.streams,
+                   "e2e_streams": args.e2e_streams,
                    "distinct_scenes": len(scenes), "graph": not args.no_graph,
                    "l2": "inputs larger than L2 (each pair 121 MB, %d resident pairs)" % B,
                    "parallelism": f"pair-sharded x{world}, no collective"},

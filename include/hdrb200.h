@@ -97,8 +97,6 @@ const char* hdr_last_error(void);
  * cluster-resident kernel per column sweep pair, 0 = chunk agg/link/apply.
  * "dt_cols_prefetch": 1 (default) = the cluster column kernel prefetches the
  * next band by cp.async, 0 = plain loads.
- * "dt_smem_columns": -1 (default) = off, 0 = shared-memory-resident column
- * bands when they fit, 1/2/3 = force the 32x32 / 16x16 / 16x32 band shape.
  * Returns HDR_ERR_INVALID for an unknown name. */
 int hdr_set_option(const char* name, int64_t value);
 /* Blocks until the context's stream drains; returns HDR_ERR_CUDA on a

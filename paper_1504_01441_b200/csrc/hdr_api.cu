@@ -51,11 +51,6 @@ extern "C" int hdr_set_option(const char* name, int64_t value) {
     hdr::dt_set_cols_prefetch(value != 0);
     return HDR_OK;
   }
-  if (name && std::string(name) == "dt_smem_columns") {
-    if (value < -1 || value > 3) return fail(HDR_ERR_INVALID, "dt_smem_columns: -1..3");
-    hdr::dt_set_smem_columns((int)value);
-    return HDR_OK;
-  }
   return fail(HDR_ERR_INVALID, std::string("unknown option: ") + (name ? name : "(null)"));
 }
 

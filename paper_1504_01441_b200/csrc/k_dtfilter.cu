@@ -879,286 +879,6 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
   }
 }
 
-// ---------------------------------------------------------------- columns, shared-memory resident
-// The same column sweep pair as dt_cols_cluster, with the band staged in
-// shared memory instead of registers so a band can be BW = 16..32 columns
-// wide (128-256 B row segments) rather than 8: a cluster of kCL CTAs owns
-// the band over the full height, CTA `rank` holds rows [rank*RPc,
-// (rank+1)*RPc) of all K planes (one cp.async.bulk per plane row, completing
-// on one mbarrier), thread (seg, col) sweeps SRc consecutive rows of one
-// column with its coefficients in registers (computed once from guide values
-// loaded while the bulk copies fly), and the chunk maps are linked inside the
-// CTA through shared memory and across the cluster through DSMEM exactly as
-// in dt_cols_cluster. The forward result is written back into shared memory,
-// the backward sweep stores straight to HBM (one coalesced 128-256 B segment
-// per warp and row). Requires f64 planes, 16-byte aligned bases, even w.
-constexpr int kSmT = 256;  // threads per CTA
-
-template <int K, int BW, int SR>
-struct DtSmemLayout {
-  static constexpr int NS = kSmT / BW;       // row segments per column
-  static constexpr int RPMAX = NS * SR;      // rows per CTA
-  static constexpr size_t XS = (size_t)K * RPMAX * BW * sizeof(double);
-};
-
-template <int K, int BW, int SR, bool FINAL>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kSmT, 1)
-    dt_cols_smem(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio, double c,
-                 DtFlowOut fo) {
-  using L = DtSmemLayout<K, BW, SR>;
-  constexpr int NS = L::NS, RPMAX = L::RPMAX;
-  extern __shared__ __align__(16) double xs[];  // [K][RPMAX][BW]
-  __shared__ Aff<K> maps[kSmT];                 // [seg][col]
-  __shared__ Aff<K> ctaF[BW], ctaB[BW];
-  __shared__ double cin[BW][K], din[BW][K];
-  __shared__ Aff<K> remote[kCL][BW];
-  __shared__ uint64_t bar;
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = (int)cl.block_rank();
-  const int col = threadIdx.x % BW, seg = threadIdx.x / BW;
-  const int RPc = ceil_div(h, kCL);
-  const int SRc = ceil_div(RPc, NS);
-  const int cta_r0 = rank * RPc;
-  const int cta_rows = max(0, min(h, cta_r0 + RPc) - cta_r0);
-  const int lr0 = seg * SRc;  // first local row of this thread's segment
-  const int r0 = cta_r0 + lr0;
-  const int nbands = ceil_div(w, BW);
-  if (threadIdx.x == 0) mbar_init(&bar, kSmT);
-  __syncthreads();
-  uint32_t phase = 0;
-  for (int band = blockIdx.y; band < nbands; band += gridDim.y) {
-    const int X0 = band * BW;
-    const int bwc = min(BW, w - X0);
-    const int x = X0 + col;
-    const bool live = col < bwc;
-    const int n = live ? max(0, min(SRc, cta_rows - lr0)) : 0;
-    // ---- stage the band: every thread arms the barrier with its own bytes
-    {
-      const int ncp = cta_rows * K;
-      uint32_t mine = 0;
-      for (int i = threadIdx.x; i < ncp; i += kSmT) mine += (uint32_t)bwc * 8;
-      mbar_expect_tx(&bar, mine);
-      for (int i = threadIdx.x; i < ncp; i += kSmT) {
-        int k = i / cta_rows, r = i - k * cta_rows;
-        bulk_load(xs + ((size_t)k * RPMAX + r) * BW,
-                  reinterpret_cast<const double*>(P.p[k]) + (int64_t)(cta_r0 + r) * w + X0,
-                  (uint32_t)bwc * 8, &bar);
-      }
-    }
-    // guide -> coefficients while the planes are in flight
-    double a[SR + 1];  // a[j] couples rows r0-1+j and r0+j
-    {
-      float g[SR + 2];
-#pragma unroll
-      for (int j = 0; j < SR + 2; ++j) {
-        int y = r0 - 1 + j;
-        g[j] = (n > 0 && j <= n + 1 && y >= 0 && y < h) ? __ldg(guide + (int64_t)y * w + x) : 0.0f;
-      }
-#pragma unroll
-      for (int j = 0; j <= SR; ++j) {
-        int y = r0 - 1 + j;
-        a[j] = (n > 0 && j <= n && y >= 0 && y + 1 < h) ? dt_coef(g[j], g[j + 1], ratio, c) : 0.0;
-      }
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    double* xcol = xs + (size_t)lr0 * BW + col;  // element (k, j): xcol[(k*RPMAX + j)*BW]
-    // ---- chunk aggregates (see dt_cols_agg)
-    double Pp = 1.0, R = 0.0, Q = 1.0;
-    double y0[K], z0[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) { y0[k] = 0.0; z0[k] = 0.0; }
-#pragma unroll
-    for (int j = 0; j < SR; ++j)
-      if (j < n) {
-        double ap = a[j], an = a[j + 1];
-        Pp *= ap;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          double v = xcol[((size_t)k * RPMAX + j) * BW];
-          y0[k] = v + ap * (y0[k] - v);
-        }
-        double wgt = (1.0 - an) * Q;
-#pragma unroll
-        for (int k = 0; k < K; ++k) z0[k] += wgt * y0[k];
-        R += wgt * Pp;
-        Q *= an;
-      }
-    // ---- forward link over the segments, then across the cluster
-    Aff<K> m;
-    m.A = Pp;
-#pragma unroll
-    for (int k = 0; k < K; ++k) m.B[k] = y0[k];
-    maps[threadIdx.x] = m;
-    __syncthreads();
-    Aff<K> ex;  // exclusive prefix of this segment within the CTA
-    ex.A = 1.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) ex.B[k] = 0.0;
-    for (int q = 0; q < seg; ++q) ex = compose(ex, maps[q * BW + col]);
-    if (seg == NS - 1) ctaF[col] = compose(ex, m);
-    cl.sync();
-    for (int q = seg; q < rank; q += NS) remote[q][col] = *cl.map_shared_rank(&ctaF[col], q);
-    __syncthreads();
-    if (seg == 0) {
-      double C[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) C[k] = 0.0;
-      for (int q = 0; q < rank; ++q) {
-        const Aff<K>& t = remote[q][col];
-#pragma unroll
-        for (int k = 0; k < K; ++k) C[k] = t.A * C[k] + t.B[k];
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) cin[col][k] = C[k];
-    }
-    __syncthreads();
-    double C[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) C[k] = ex.A * cin[col][k] + ex.B[k];
-    // ---- backward link: z_start(s) = Q_s z_start(s+1) + (Z0_s + C_s R_s)
-    m.A = Q;
-#pragma unroll
-    for (int k = 0; k < K; ++k) m.B[k] = z0[k] + C[k] * R;
-    maps[threadIdx.x] = m;
-    __syncthreads();
-    Aff<K> sx;  // suffix from the segments below this one
-    sx.A = 1.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) sx.B[k] = 0.0;
-    for (int q = NS - 1; q > seg; --q) sx = compose(sx, maps[q * BW + col]);
-    if (seg == 0) ctaB[col] = compose(sx, m);
-    cl.sync();
-    for (int q = rank + 1 + seg; q < kCL; q += NS) remote[q][col] = *cl.map_shared_rank(&ctaB[col], q);
-    __syncthreads();
-    if (seg == 0) {
-      double D[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) D[k] = 0.0;
-      for (int q = kCL - 1; q > rank; --q) {
-        const Aff<K>& t = remote[q][col];
-#pragma unroll
-        for (int k = 0; k < K; ++k) D[k] = t.A * D[k] + t.B[k];
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) din[col][k] = D[k];
-    }
-    // peers may still read ctaB; the matching wait ends the band
-    cluster_arrive();
-    __syncthreads();
-    double D[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) D[k] = sx.A * din[col][k] + sx.B[k];
-    // ---- apply: forward from C (back into shared memory), backward from D to HBM
-    double prev[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) prev[k] = C[k];
-#pragma unroll
-    for (int j = 0; j < SR; ++j)
-      if (j < n) {
-        double ap = a[j];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          double* e = xcol + ((size_t)k * RPMAX + j) * BW;
-          double v = *e;
-          prev[k] = v + ap * (prev[k] - v);
-          *e = prev[k];
-        }
-      }
-    const bool use_fb = FINAL && fo.fallback && (!fo.has_fb || *fo.has_fb);
-#pragma unroll
-    for (int k = 0; k < K; ++k) prev[k] = D[k];
-#pragma unroll
-    for (int j = SR - 1; j >= 0; --j)
-      if (j < n) {
-        double an = a[j + 1];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          double v = xcol[((size_t)k * RPMAX + j) * BW];
-          prev[k] = v + an * (prev[k] - v);
-        }
-        int64_t o = (int64_t)(r0 + j) * w + x;
-        if (FINAL) {
-          double nv = prev[K - 1];
-          float fu = 0.0f, fv = 0.0f;
-          if (nv > fo.floor_) {
-            double inv = 1.0 / nv;  // see dt_cols_cluster
-            fu = (float)(prev[0] * inv);
-            fv = (float)(prev[K > 2 ? 1 : 0] * inv);
-          } else if (use_fb) {
-            h_pixel_flow(fo.fallback, x, r0 + j, w, h, &fu, &fv);
-          }
-          __stcs(reinterpret_cast<float2*>(fo.flow) + o, make_float2(fu, fv));
-        } else {
-#pragma unroll
-          for (int k = 0; k < K; ++k) reinterpret_cast<double*>(P.p[k])[o] = prev[k];
-        }
-      }
-    cluster_wait();
-    // every thread is done with this band's shared memory before the next
-    // band's bulk copies (async proxy) overwrite it
-    fence_async_smem();
-    __syncthreads();
-  }
-}
-
-template <int K, int BW, int SR, bool FINAL>
-static int smem_max_clusters() {
-  static int n = -1;
-  if (n < 0) {
-    auto kern = dt_cols_smem<K, BW, SR, FINAL>;
-    size_t bytes = DtSmemLayout<K, BW, SR>::XS;
-    n = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
-        cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(kCL, 1024);
-      cfg.blockDim = dim3(kSmT);
-      cfg.dynamicSmemBytes = bytes;
-      int v = 0;
-      if (cudaOccupancyMaxActiveClusters(&v, kern, &cfg) == cudaSuccess) n = v;
-    }
-    cudaGetLastError();
-  }
-  return n;
-}
-
-template <int K, int BW, int SR, bool FINAL>
-static bool launch_cols_smem_cfg(const float* guide, const DtPlanes& P, int w, int h, double ratio,
-                                 double c, const DtFlowOut& fo, cudaStream_t s) {
-  if (ceil_div(h, kCL) > DtSmemLayout<K, BW, SR>::RPMAX) return false;
-  int mc = smem_max_clusters<K, BW, SR, FINAL>();
-  if (mc <= 0) return false;
-  int nb = ceil_div(w, BW);
-  dim3 grid(kCL, std::min(nb, mc));
-  dt_cols_smem<K, BW, SR, FINAL><<<grid, kSmT, DtSmemLayout<K, BW, SR>::XS, s>>>(guide, P, w, h,
-                                                                               ratio, c, fo);
-  return true;
-}
-
-// -1 (default) = off: measured on B200 at 5MP the shared-memory bands run a
-// column pass in ~200 us against ~143 us for dt_cols_cluster (one CTA per SM
-// leaves too few warps to hide the guide loads and the phase barriers);
-// 0 = auto, 1..3 force one band shape (test / tuning hook)
-static int g_cols_smem_cfg = -1;
-
-template <int K, bool FINAL>
-static bool launch_cols_smem(const float* guide, const DtPlanes& P, int w, int h, double ratio,
-                             double c, const DtFlowOut& fo, cudaStream_t s) {
-  if (w % 2 || (reinterpret_cast<uintptr_t>(guide) & 3)) return false;
-  for (int k = 0; k < P.k; ++k)
-    if (!P.f64[k] || (reinterpret_cast<uintptr_t>(P.p[k]) & 15)) return false;
-  switch (g_cols_smem_cfg) {
-    case 1: return launch_cols_smem_cfg<K, 32, 32, FINAL>(guide, P, w, h, ratio, c, fo, s);
-    case 2: return launch_cols_smem_cfg<K, 16, 16, FINAL>(guide, P, w, h, ratio, c, fo, s);
-    case 3: return launch_cols_smem_cfg<K, 16, 32, FINAL>(guide, P, w, h, ratio, c, fo, s);
-    case -1: return false;
-    default: break;
-  }
-  return launch_cols_smem_cfg<K, 32, 32, FINAL>(guide, P, w, h, ratio, c, fo, s) ||
-         launch_cols_smem_cfg<K, 16, 32, FINAL>(guide, P, w, h, ratio, c, fo, s);
-}
-
 // co-resident clusters of a cluster-kernel instantiation (0 = query failed)
 template <int K, bool FINAL, bool PF>
 static int max_clusters() {
@@ -1249,11 +969,7 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     int bl = cluster_bw_log2(h);
     bool fin_pass = i == passes && fo.flow && K == 3;
     if (h > 1) kprobe_mark(kc, 0, s);
-    if (h > 1 && g_cols_cluster &&
-        (fin_pass ? launch_cols_smem<K, true>(guide, P, w, h, ratio, c, fo, s)
-                  : launch_cols_smem<K, false>(guide, P, w, h, ratio, c, fo, s))) {
-      finalized = finalized || fin_pass;
-    } else if (h > 1 && bl >= 0 && g_cols_cluster) {
+    if (h > 1 && bl >= 0 && g_cols_cluster) {
       if (fin_pass) {
         launch_cols_cluster<K, true>(guide, P, w, h, ratio, c, bl, fo, s);
         finalized = true;
@@ -1281,7 +997,6 @@ int64_t dt_scratch_doubles(int w, int h, int k) {
 }
 
 void dt_set_cluster_columns(bool on) { g_cols_cluster = on; }
-void dt_set_smem_columns(int cfg) { g_cols_smem_cfg = cfg; }
 void dt_set_cols_prefetch(bool on) { g_cols_prefetch = on; }
 
 void init_densify_attributes() {

@@ -47,9 +47,8 @@ if what in ("dt", "all"):
     base[2].view(-1)[idx] = 1.0
     planes = base.clone()
     ref = None
-    for cl, sm, pf in ((1, -1, 1), (1, -1, 0), (1, 1, 1), (0, -1, 1)):
+    for cl, pf in ((1, 1), (1, 0), (0, 1)):
         L.hdr_set_option(b"dt_cluster_columns", cl)
-        L.hdr_set_option(b"dt_smem_columns", sm)
         L.hdr_set_option(b"dt_cols_prefetch", pf)
 
         def run():
@@ -64,10 +63,9 @@ if what in ("dt", "all"):
         if ref is None:
             ref = out
         d = (out - ref).abs().max().item()
-        print(f"dt_filter cluster={cl} smem={sm} prefetch={pf}: {us - cp:8.1f} us (3 passes, copy {cp:.1f} excluded)"
+        print(f"dt_filter cluster={cl} prefetch={pf}: {us - cp:8.1f} us (3 passes, copy {cp:.1f} excluded)"
               f"  max|diff| vs first = {d:.3e}")
     L.hdr_set_option(b"dt_cluster_columns", 1)
-    L.hdr_set_option(b"dt_smem_columns", -1)
     L.hdr_set_option(b"dt_cols_prefetch", 1)
 
 if what in ("warp", "all"):

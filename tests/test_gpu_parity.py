@@ -157,18 +157,17 @@ def test_densify_warp_stages(scene):
 @pytest.mark.parametrize("shape", [(480, 640), (37, 53), (37, 54), (1, 70), (70, 1), (2100, 33),
                                    (2100, 34), (4100, 6), (9000, 5)])
 def test_dt_filter_all_column_paths(cuda, shape):
-    """Every column-sweep implementation -- the shared-memory band kernels
-    (each band shape), the register-resident cluster kernel and the chunk
-    agg/link/apply path (odd widths, very tall images) -- matches the
+    """Every column-sweep implementation -- the register-resident cluster
+    kernel with and without the cp.async band prefetch, and the chunk
+    agg/link/apply path (very tall images) -- matches the
     oracle's sequential recursion for 1-3 planes, odd sizes and degenerate
     1-pixel axes."""
     from paper_1504_01441_b200 import _native
     h, w = shape
     rng = np.random.default_rng(h * 7 + w)
     guide = rng.random((h, w), dtype=np.float32)
-    paths = [("dt_cluster_columns", 1, "dt_smem_columns", v) for v in (0, 1, 2, 3, -1)]
-    paths.append(("dt_cluster_columns", 0, "dt_smem_columns", 0))
-    paths.append(("dt_cols_prefetch", 0, "dt_smem_columns", -1))
+    paths = [("dt_cluster_columns", 1, "dt_cols_prefetch", 1), ("dt_cluster_columns", 1, "dt_cols_prefetch", 0),
+             ("dt_cluster_columns", 0, "dt_cols_prefetch", 1)]
     try:
         for k in (1, 2, 3):
             planes = rng.normal(size=(h, w, k))
@@ -181,7 +180,6 @@ def test_dt_filter_all_column_paths(cuda, shape):
                 assert np.abs(np.asarray(got) - want).max() < 1e-9, (k, o1, v1, o2, v2)
     finally:
         _native.lib().hdr_set_option(b"dt_cluster_columns", 1)
-        _native.lib().hdr_set_option(b"dt_smem_columns", -1)
         _native.lib().hdr_set_option(b"dt_cols_prefetch", 1)
 
 

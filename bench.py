@@ -44,7 +44,7 @@ WORKLOAD = "5MP (2592x1944) two-exposure pair, registered + merged (BASELINE con
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pairs", type=int, default=16, help="resident pairs per GPU per step")

@@ -15,7 +15,7 @@ run ssd 'ssd_tiles_kernel' 4
 run finish 'finish_level_kernel' 4
 run weedfit 'weed_fit_kernel' 4
 run ssim 'ssim_fixed_kernel' 0
-run weights0 'weights_down0_kernel' 0
+run weights0 'weights_down_kernel' 0
 run collapse0 'collapse_kernel' 7
 run warp 'warp_kernel' 0
 run detect 'detect_kernel' 0

@@ -42,9 +42,16 @@ static int check_launch() {
 
 extern "C" const char* hdr_last_error(void) { return g_err.c_str(); }
 
+// test hook: 0 sends the pair through the dense splat + first row pass
+static bool g_sparse_first = true;
+
 extern "C" int hdr_set_option(const char* name, int64_t value) {
   if (name && std::string(name) == "dt_cluster_columns") {
     hdr::dt_set_cluster_columns(value != 0);
+    return HDR_OK;
+  }
+  if (name && std::string(name) == "dt_sparse_first") {
+    g_sparse_first = value != 0;
     return HDR_OK;
   }
   if (name && std::string(name) == "dt_cols_prefetch") {
@@ -331,6 +338,8 @@ struct hdr_ctx {
   double* carry = nullptr;      // domain-transform aggregates / carries / coefficients
   uint64_t* splat_key = nullptr;
   int32_t* splat_idx = nullptr;
+  int32_t* splat_rows = nullptr;    // row counts (H + 1) then row starts (H + 1)
+  SparseEntry* splat_entries = nullptr;
   uint8_t* qw = nullptr;
   // merge
   float* wr = nullptr;
@@ -452,6 +461,8 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   ALLOC(carry, dt_scratch_doubles(width, height, 3));
   ALLOC(splat_key, P);
   ALLOC(splat_idx, P);
+  ALLOC(splat_rows, 2 * ((int64_t)height + 1) + 8);
+  ALLOC(splat_entries, c->rows_cap);
   ALLOC(qw, P + 16);
   ALLOC(wr, P);
   ALLOC(ws, P);
@@ -844,13 +855,19 @@ static int enqueue_pair(hdr_ctx* c, const hdr_params* p, int w, int h, const flo
   // make_flow (pipeline.py:153-162): splat, filter, ratio + H fallback
   probe(c, 3, 0);
   DtPlanes pl = pair_planes(c, P);
-  launch_splat(o->matches, weeded_count, 0, w, h, pl, c->splat_key, c->splat_idx, c->counters + 2, s);
   // the last column pass finishes densify_flow in registers and writes the
   // f32 flow directly (the smoothed planes never make a final round trip)
   DtFlowOut fo{o->homography, o->info + 1, p->normalization_floor, o->flow};
+  DtSparse sp{c->splat_rows + (h + 1), c->splat_entries};
+  const bool sparse_first = g_sparse_first && dt_sparse_first_ok(c->lum_ref, pl, w);
+  if (sparse_first)  // the first row pass builds its rows from the CSR splat
+    launch_splat_rows(o->matches, weeded_count, 0, w, h, c->splat_key, c->splat_idx, c->splat_rows,
+                      c->splat_rows + (h + 1), c->splat_entries, c->counters + 2, s);
+  else
+    launch_splat(o->matches, weeded_count, 0, w, h, pl, c->splat_key, c->splat_idx, c->counters + 2, s);
   bool flow_done = launch_dt_filter(c->lum_ref, pl, w, h, p->sigma_s, p->sigma_r, p->passes,
                                     c->carry, s, &fo, &c->kprobes[HDR_KP_DT_ROWS],
-                                    &c->kprobes[HDR_KP_DT_COLS]);
+                                    &c->kprobes[HDR_KP_DT_COLS], sparse_first ? &sp : nullptr);
   probe(c, 3, 1);
   probe(c, 4, 0);
   // warp_image + luminance(warped) histogram (pipeline.py:192, :168)

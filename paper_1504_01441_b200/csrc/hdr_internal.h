@@ -132,11 +132,30 @@ struct DtFlowOut {
   double floor_;
   float* flow;              // (h, w, 2)
 };
-// returns true when the flow was written (planes then hold pre-final values)
+// sparse splat maps in CSR-by-row form: row y's samples are
+// entries[row_start[y] .. row_start[y+1]) (collision winners only)
+struct SparseEntry {
+  int32_t x, pad;
+  double u, v;
+};
+struct DtSparse {
+  const int32_t* row_start;  // h + 1
+  const SparseEntry* entries;
+};
+// splat winners -> CSR rows (no dense planes); row_start needs h + 1 ints,
+// row_count h + 1 ints of scratch, entries up to m rows
+void launch_splat_rows(const double* matches, const int32_t* count, int m_static, int w, int h,
+                       uint64_t* scratch_key, int32_t* scratch_idx, int32_t* row_count,
+                       int32_t* row_start, SparseEntry* entries, int32_t* status, cudaStream_t s);
+// the first row pass can consume the CSR splat directly (K == 3, f64 rows)
+bool dt_sparse_first_ok(const float* guide, const DtPlanes& P, int w);
+// returns true when the flow was written (planes then hold pre-final values);
+// with `first`, the planes' initial content is ignored: pass 1 builds its
+// rows from the CSR splat (see dt_sparse_first_ok)
 bool launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double sigma_s,
                       double sigma_r, int passes, double* scratch, cudaStream_t s,
                       const DtFlowOut* fo = nullptr, KProbe* kp_rows = nullptr,
-                      KProbe* kp_cols = nullptr);
+                      KProbe* kp_cols = nullptr, const DtSparse* first = nullptr);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
                  uint8_t* qw, uint32_t* hist, cudaStream_t s);

@@ -68,6 +68,83 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
                                   status);
 }
 
+// densify.build_sparse_maps in CSR-by-row form for the first domain-transform
+// row pass (dt_rows_first_kernel): the same collision rule as splat_kernel,
+// then the winners bucketed by row (count, block-wide exclusive scan over the
+// h + 1 row starts, scatter; the order inside a row is irrelevant, the x are
+// distinct). Single block: a pair has at most one weeded match per tile.
+__global__ void __launch_bounds__(1024) splat_rows_kernel(
+    const double* __restrict__ m, const int32_t* __restrict__ count, int m_static, int w, int h,
+    unsigned long long* __restrict__ key, int32_t* __restrict__ idx, int32_t* __restrict__ row_count,
+    int32_t* __restrict__ row_start, SparseEntry* __restrict__ entries, int32_t* __restrict__ status) {
+  __shared__ int32_t part[1024];
+  int n = count ? *count : m_static;
+  int64_t p;
+  for (int i = threadIdx.x; i <= h; i += blockDim.x) row_count[i] = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (!splat_pixel(m + 5 * (int64_t)i, w, h, &p)) {
+      if (status) atomicExch(status, 1);
+      continue;
+    }
+    key[p] = ~0ULL;
+    idx[p] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (splat_pixel(m + 5 * (int64_t)i, w, h, &p))
+      atomicMin(&key[p], ordered_bits(m[5 * (int64_t)i + 4]));
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (splat_pixel(m + 5 * (int64_t)i, w, h, &p) && key[p] == ordered_bits(m[5 * (int64_t)i + 4]))
+      atomicMin(&idx[p], i);
+  __syncthreads();
+  // winners take a slot in their row (kept in key[p], no longer needed)
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (splat_pixel(m + 5 * (int64_t)i, w, h, &p) && idx[p] == i)
+      key[p] = (unsigned long long)atomicAdd(&row_count[p / w], 1);
+  __syncthreads();
+  // exclusive scan of row_count[0..h) -> row_start[0..h]: contiguous chunks
+  // per thread, a block scan of the chunk sums
+  const int per = (h + blockDim.x) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(h, b0 + per);
+  int32_t sum = 0;
+  for (int i = b0; i < b1; ++i) sum += row_count[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    int32_t v = threadIdx.x >= (unsigned)off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int32_t run = part[threadIdx.x] - sum;
+  for (int i = b0; i < b1; ++i) {
+    row_start[i] = run;
+    run += row_count[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) row_start[h] = part[threadIdx.x];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double* r = m + 5 * (int64_t)i;
+    if (!splat_pixel(r, w, h, &p) || idx[p] != i) continue;
+    int y = (int)(p / w);
+    SparseEntry e;
+    e.x = (int)(p - (int64_t)y * w);
+    e.pad = 0;
+    e.u = r[2] - r[0];
+    e.v = r[3] - r[1];
+    entries[row_start[y] + (int)key[p]] = e;
+  }
+}
+
+void launch_splat_rows(const double* matches, const int32_t* count, int m_static, int w, int h,
+                       uint64_t* scratch_key, int32_t* scratch_idx, int32_t* row_count,
+                       int32_t* row_start, SparseEntry* entries, int32_t* status, cudaStream_t s) {
+  splat_rows_kernel<<<1, 1024, 0, s>>>(matches, count, m_static, w, h,
+                                       reinterpret_cast<unsigned long long*>(scratch_key),
+                                       scratch_idx, row_count, row_start, entries, status);
+}
+
 // ---------------------------------------------------------------- K11/K12
 __global__ void hflow_kernel(const double* __restrict__ Hd, int w, int h, float* __restrict__ flow) {
   __shared__ double H[9];

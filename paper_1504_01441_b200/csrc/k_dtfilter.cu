@@ -256,32 +256,15 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_reg_kernel(const float* _
     for (int k = 0; k < K; ++k) stp(P, k, row + i, xs[k * w + i]);
 }
 
-// Row pass with the row moved by bulk copies: one thread issues the K plane
-// rows and the guide row (one cp.async.bulk each) and the results go back the
-// same way, so the 256 threads only compute. Needs all planes f64 and
-// 16-byte aligned rows (w % 4 == 0, aligned bases); w <= kRowThreads*kRowSeg.
+// One row swept forward then backward in shared memory: xs holds the K plane
+// rows, gs the guide row; 256 threads each own a segment of ceil(w/256)
+// samples (coefficients in registers), segments linked by block scans of
+// affine maps, then re-run with the reference update.
 template <int K>
-__global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* __restrict__ guide,
-                                                                   DtPlanes P, int w, int h,
-                                                                   double ratio, double c) {
-  extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
-  float* gs = reinterpret_cast<float*>(xs + K * w);
-  __shared__ Aff<K> wsum[kRowThreads / 32];
-  __shared__ uint64_t bar;
-  int y = blockIdx.x;
-  int64_t row = (int64_t)y * w;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, (uint32_t)(K * w * 8 + w * 4));
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      bulk_load(xs + k * w, reinterpret_cast<const double*>(P.p[k]) + row, (uint32_t)w * 8, &bar);
-    bulk_load(gs, guide + row, (uint32_t)w * 4, &bar);
-  }
+__device__ __forceinline__ void row_sweep_smem(double* xs, const float* gs, int w, double ratio,
+                                               double c, Aff<K>* wsum) {
   const int L = (w + kRowThreads - 1) / kRowThreads;
   int s0 = threadIdx.x * L, n = max(0, min(w, s0 + L) - s0);
-  __syncthreads();  // barrier initialised before anyone polls it
-  mbar_wait(&bar, 0);
   // af[j] couples samples s0-1+j and s0+j (0 outside the row)
   double af[kRowSeg + 1];
 #pragma unroll
@@ -345,6 +328,11 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* 
         xs[k * w + s0 + j] = prev[k];
       }
     }
+}
+
+// the swept row back to HBM (one bulk copy per plane)
+template <int K>
+__device__ __forceinline__ void store_row_bulk(const DtPlanes& P, int64_t row, const double* xs, int w) {
   fence_async_smem();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -354,6 +342,81 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* 
     bulk_commit();
     bulk_wait_read();
   }
+}
+
+// Row pass with the row moved by bulk copies: one thread issues the K plane
+// rows and the guide row (one cp.async.bulk each) and the results go back the
+// same way, so the 256 threads only compute. Needs all planes f64 and
+// 16-byte aligned rows (w % 4 == 0, aligned bases); w <= kRowThreads*kRowSeg.
+template <int K>
+__global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* __restrict__ guide,
+                                                                   DtPlanes P, int w, int h,
+                                                                   double ratio, double c) {
+  extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
+  float* gs = reinterpret_cast<float*>(xs + K * w);
+  __shared__ Aff<K> wsum[kRowThreads / 32];
+  __shared__ uint64_t bar;
+  int y = blockIdx.x;
+  int64_t row = (int64_t)y * w;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (uint32_t)(K * w * 8 + w * 4));
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      bulk_load(xs + k * w, reinterpret_cast<const double*>(P.p[k]) + row, (uint32_t)w * 8, &bar);
+    bulk_load(gs, guide + row, (uint32_t)w * 4, &bar);
+  }
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+  row_sweep_smem<K>(xs, gs, w, ratio, c, wsum);
+  store_row_bulk<K>(P, row, xs, w);
+}
+
+// First row pass straight from the splat (densify.py:38-56 + the first
+// horizontal sweep): the planes before it are zero except one (u, v, 1)
+// sample per weeded match, so a row is built in shared memory from its
+// samples (CSR by row, DtSparse) instead of being read, and a row without
+// samples -- most of them: corners sit on a 4-px candidate lattice -- stays
+// zero through the sweep and is written as zeros without any compute. The
+// planes need no initialisation (this writes every sample). K == 3 (pu, pv, n).
+__global__ void __launch_bounds__(kRowThreads) dt_rows_first_kernel(const float* __restrict__ guide,
+                                                                    DtPlanes P, int w, int h,
+                                                                    double ratio, double c,
+                                                                    DtSparse sp) {
+  constexpr int K = 3;
+  extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
+  float* gs = reinterpret_cast<float*>(xs + K * w);
+  __shared__ Aff<K> wsum[kRowThreads / 32];
+  __shared__ uint64_t bar;
+  int y = blockIdx.x;
+  int64_t row = (int64_t)y * w;
+  const int e0 = sp.row_start[y], e1 = sp.row_start[y + 1];
+  if (e0 == e1) {
+    const double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double2* d = reinterpret_cast<double2*>(reinterpret_cast<double*>(P.p[k]) + row);
+      for (int i = threadIdx.x; i < w / 2; i += blockDim.x) __stcs(d + i, z);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (uint32_t)(w * 4));
+    bulk_load(gs, guide + row, (uint32_t)w * 4, &bar);
+  }
+  for (int i = threadIdx.x; i < K * w; i += blockDim.x) xs[i] = 0.0;
+  __syncthreads();
+  for (int e = e0 + (int)threadIdx.x; e < e1; e += blockDim.x) {
+    const SparseEntry& t = sp.entries[e];
+    xs[t.x] = t.u;
+    xs[w + t.x] = t.v;
+    xs[2 * w + t.x] = 1.0;
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  row_sweep_smem<K>(xs, gs, w, ratio, c, wsum);
+  store_row_bulk<K>(P, row, xs, w);
 }
 
 static bool rows_bulk_ok(const float* guide, const DtPlanes& P, int w) {
@@ -941,7 +1004,7 @@ static bool g_cols_cluster = true;
 template <int K>
 static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sigma_s,
                         double sigma_r, int passes, double* scratch, const DtFlowOut& fo,
-                        cudaStream_t s, KProbe* kr, KProbe* kc) {
+                        cudaStream_t s, KProbe* kr, KProbe* kc, const DtSparse* sp) {
   bool finalized = false;
   double ratio = sigma_s / sigma_r;
   double root = sqrt(2.0);
@@ -956,7 +1019,10 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     double c = -root / sigma_i;
     if (w > 1) {
       kprobe_mark(kr, 0, s);
-      if (rows_bulk_ok(guide, P, w))
+      if (i == 1 && sp && K == 3)
+        dt_rows_first_kernel<<<h, kRowThreads, (size_t)3 * w * sizeof(double) + (size_t)w * 4, s>>>(
+            guide, P, w, h, ratio, c, *sp);
+      else if (rows_bulk_ok(guide, P, w))
         dt_rows_bulk_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double) + (size_t)w * 4, s>>>(
             guide, P, w, h, ratio, c);
       else if (w <= kRowThreads * kRowSeg)
@@ -1009,17 +1075,22 @@ void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_bulk_kernel<1>);
   allow_max_dynamic_smem(dt_rows_bulk_kernel<2>);
   allow_max_dynamic_smem(dt_rows_bulk_kernel<3>);
+  allow_max_dynamic_smem(dt_rows_first_kernel);
+}
+
+bool dt_sparse_first_ok(const float* guide, const DtPlanes& P, int w) {
+  return P.k == 3 && w > 1 && rows_bulk_ok(guide, P, w);
 }
 
 bool launch_dt_filter(const float* guide, DtPlanes P, int w, int h, double sigma_s, double sigma_r,
                       int passes, double* scratch, cudaStream_t s, const DtFlowOut* fo,
-                      KProbe* kr, KProbe* kc) {
+                      KProbe* kr, KProbe* kc, const DtSparse* sp) {
   DtFlowOut none{nullptr, nullptr, 0.0, nullptr};
   const DtFlowOut& f = fo ? *fo : none;
   switch (P.k) {
-    case 1: return dt_filter_k<1>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s, kr, kc);
-    case 2: return dt_filter_k<2>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s, kr, kc);
-    default: return dt_filter_k<3>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s, kr, kc);
+    case 1: return dt_filter_k<1>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s, kr, kc, sp);
+    case 2: return dt_filter_k<2>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s, kr, kc, sp);
+    default: return dt_filter_k<3>(guide, P, w, h, sigma_s, sigma_r, passes, scratch, f, s, kr, kc, sp);
   }
 }
 

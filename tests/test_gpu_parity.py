@@ -183,6 +183,21 @@ def test_dt_filter_all_column_paths(cuda, shape):
         _native.lib().hdr_set_option(b"dt_cols_prefetch", 1)
 
 
+def test_sparse_first_row_pass_is_exact(cuda):
+    """The CSR splat + first row pass built from it (the pair default) gives
+    the same bits as the dense splat planes + the plain row pass."""
+    from paper_1504_01441_b200 import _native
+    st = synth.synth_stack(synth.working_spec(640, 480), 3)
+    a = pipeline.register_and_fuse(st.ref, st.src)
+    try:
+        _native.check(_native.lib().hdr_set_option(b"dt_sparse_first", 0))
+        b = pipeline.register_and_fuse(st.ref, st.src)
+    finally:
+        _native.lib().hdr_set_option(b"dt_sparse_first", 1)
+    np.testing.assert_array_equal(a.flow, b.flow)
+    np.testing.assert_array_equal(a.composite, b.composite)
+
+
 def test_ssim_and_fuse_stages(scene):
     _, fx, ref, src = scene
     o = O.register_and_fuse(ref, src)

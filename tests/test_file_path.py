@@ -191,3 +191,18 @@ def test_flow_to_color_per_pixel():
             np.testing.assert_array_equal(got[i, j], (1.0 - mag[i, j] * (1.0 - rgb)).astype(np.float32))
     hm = viz.heatmap(np.array([[-1.0, 0.0, 1.0]]), -1.0, 1.0)
     np.testing.assert_array_equal(hm[0], np.array([[0, 0, 1], [1, 1, 1], [1, 0, 0]], dtype=np.float32))
+
+
+@pytest.mark.gpu
+def test_run_hdr_errors(tmp_path):
+    from paper_1504_01441_b200 import pipeline
+    from paper_1504_01441_b200.errors import ConfigError
+    _, paths, _ = case_files(tmp_path, "file_rgb8")
+    with pytest.raises(ConfigError):
+        pipeline.run_hdr(pipeline.PipelineConfig(inputs=paths[:1]))
+    with pytest.raises(ConfigError):
+        pipeline.run_hdr(pipeline.PipelineConfig(inputs=paths, exposures=[1.0]))
+    with pytest.raises(ConfigError):
+        pipeline.run_hdr(pipeline.PipelineConfig(inputs=paths, params=pipeline.PipelineParams(tile=8)))
+    with pytest.raises(FileNotFoundError):
+        pipeline.run_hdr(pipeline.PipelineConfig(inputs=[paths[0], str(tmp_path / "missing.png")]))

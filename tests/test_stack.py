@@ -83,3 +83,21 @@ def test_stack3_5mp_gpu_matches_oracle():
     for got, want in zip(res.registrations, regs):
         assert got.level_counts == want.level_counts
     assert np.abs(res.composite - comp).max() < 1e-3
+
+
+@pytest.mark.gpu
+def test_stack_errors(cuda):
+    """Shape / count errors as ValueError / ConfigError; a source frame that
+    cannot register raises RegistrationError like the pairwise reference."""
+    from paper_1504_01441_b200 import pipeline, synth
+    from paper_1504_01441_b200.errors import ConfigError, RegistrationError
+    st = synth.synth_stack(synth.working_spec(320, 240), 1)
+    with pytest.raises(ValueError):
+        pipeline.register_and_fuse_stack([st.ref])
+    with pytest.raises(ConfigError):
+        pipeline.register_and_fuse_stack([st.ref, st.src[:200]])
+    flat = np.full_like(st.ref, 0.5)  # as the reference: no corners, nothing registers
+    with pytest.raises(RegistrationError):
+        pipeline.register_and_fuse_stack([st.ref, st.src, flat], [4.0, 2.0, 1.0])
+    res = pipeline.register_and_fuse_stack([st.src, st.ref], [4.0, 1.0])
+    assert res.reference_index == 1 and len(res.registrations) == 1

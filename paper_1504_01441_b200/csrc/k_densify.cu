@@ -259,10 +259,13 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
   __shared__ uint32_t sh[kBins];
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  int segs = (w + 255) >> 8;
-  int64_t nwork = (int64_t)segs * h;
-  for (int64_t t = blockIdx.x; t < nwork; t += gridDim.x) {
-    int y = (int)(t / segs), x = (int)(t - (int64_t)y * segs) * 256 + threadIdx.x;
+  // row / segment indices advance without a division per step
+  const int segs = (w + 255) >> 8;
+  const int dq = gridDim.x / segs, dr = gridDim.x - dq * segs;
+  int y = blockIdx.x / segs, seg = blockIdx.x - y * segs;
+  for (; y < h; y += dq, seg += dr) {
+    if (seg >= segs) { seg -= segs; ++y; if (y >= h) break; }
+    int x = seg * 256 + threadIdx.x;
     if (x >= w) continue;
     int64_t i = (int64_t)y * w + x;
     float2 f = __ldcs(reinterpret_cast<const float2*>(flow) + i);

@@ -353,6 +353,8 @@ def run_ours(args):
     for s_i, name in enumerate(_native.STAGES):
         stage_ms[name] = statistics.median(
             iso[j][2 * s_i].elapsed_time(iso[j][2 * s_i + 1]) for j in range(NI))
+    # single-pair latency, device-resident inputs: first stage start to last stage end
+    pair_latency_ms = statistics.median(iso[j][0].elapsed_time(iso[j][2 * nst - 1]) for j in range(NI))
     kb = kernel_bytes(w, h)
     kernel_ms = {}
     for f, name in enumerate(kfam):
@@ -465,6 +467,7 @@ def run_ours(args):
                              "per launch (profiles/)"},
         "kernel_rooflines": {k: kroof(k) for k in kernel_ms},
         "stage_rooflines": {k: sroof(k) for k in ("dt_filter", "finalize_warp", "fuse")},
+        "pair_latency_ms": pair_latency_ms,
         "stage_ms": stage_ms, "stage_ms_concurrent": stage_ms_conc, "kernel_ms": kernel_ms,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "pairs_per_step": E},

@@ -49,9 +49,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pairs", type=int, default=16, help="resident pairs per GPU per step")
     ap.add_argument("--streams", type=int, default=8, help="compute streams of the device-resident runs")
-    ap.add_argument("--e2e-streams", type=int, default=4, help="compute streams of the host-buffer runs")
+    ap.add_argument("--e2e-streams", type=int, default=6, help="compute streams of the host-buffer runs")
     ap.add_argument("--scenes", type=int, default=4, help="distinct synthetic scenes")
-    ap.add_argument("--e2e-pairs", type=int, default=8)
+    ap.add_argument("--e2e-pairs", type=int, default=16)
     ap.add_argument("--width", type=int, default=W5)
     ap.add_argument("--height", type=int, default=H5)
     ap.add_argument("--no-cpu-baseline", action="store_true")

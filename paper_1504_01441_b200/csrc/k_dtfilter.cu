@@ -416,7 +416,15 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_first_kernel(const float*
   __syncthreads();
   mbar_wait(&bar, 0);
   row_sweep_smem<K>(xs, gs, w, ratio, c, wsum);
-  store_row_bulk<K>(P, row, xs, w);
+  // plain 16-byte stores (not a bulk copy): this pass is the first write of
+  // the planes, and compute-sanitizer's initcheck does not track TMA stores
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double2* d = reinterpret_cast<double2*>(reinterpret_cast<double*>(P.p[k]) + row);
+    const double2* q = reinterpret_cast<const double2*>(xs + k * w);
+    for (int i = threadIdx.x; i < w / 2; i += blockDim.x) d[i] = q[i];
+  }
 }
 
 static bool rows_bulk_ok(const float* guide, const DtPlanes& P, int w) {

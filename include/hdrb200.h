@@ -147,12 +147,18 @@ int32_t hdr_ctx_graph_kernels(hdr_ctx* ctx);
  * (pipeline.py:112-115): raw (h, w[, channels]) -> rgb (h, w, 3) f32.
  * hdr_encode_u8 is fileio.save_png's quantisation (fileio.py:44-53):
  * clip(floor(x * 255 + 0.5), 0, 255) of n floats. hdr_mean_luminance is
- * metering.choose_reference's tie-break statistic (metering.py:46-48),
- * written to one device double. */
+ * metering.choose_reference's tie-break statistic (metering.py:46-48) over n
+ * pixels of an RGB (channels 3: luminance) or grey (channels 1: the value
+ * itself) image, written to one device double. */
 int hdr_decode_image(hdr_ctx* ctx, const void* raw, int32_t width, int32_t height,
                      int32_t channels, int32_t bits, float* rgb);
 int hdr_encode_u8(hdr_ctx* ctx, const float* img, int64_t n, uint8_t* out);
-int hdr_mean_luminance(hdr_ctx* ctx, const float* rgb, int64_t n, double* out);
+int hdr_mean_luminance(hdr_ctx* ctx, const float* img, int32_t channels, int64_t n, double* out);
+/* metering.select_offset's statistic (metering.py:28-29): the number of the n
+ * pixels whose luminance (channels 3) or value (channels 1) is < dark_level
+ * (compared in f32, as numpy 2 does), written to one device uint64. */
+int hdr_dark_count(hdr_ctx* ctx, const float* img, int32_t channels, int64_t n, float dark_level,
+                   uint64_t* out);
 /* pipeline.run_hdr's compute (pipeline.py:267-282) on raw samples: decode
  * both frames into context-owned RGB buffers, register_and_fuse them
  * (use_graph != 0: the cached pair graph), and, when composite_u8 is not

@@ -238,6 +238,26 @@ def stack_fixture(w, h, seed):
     return out
 
 
+def metering_images():
+    """Seeded frames spanning the three select_offset outcomes, RGB and grey."""
+    rng = np.random.default_rng(21)
+    out = []
+    for scale in (1.0, 0.25, 0.08, 0.02):
+        img = (rng.random((60, 80, 3)) * scale).astype(np.float32)
+        out.append(img)
+        out.append(np.ascontiguousarray(img[..., 1]))
+    return out
+
+
+def metering_fixture():
+    from hdrflow import metering
+    imgs = metering_images()
+    offs = [metering.select_offset(x) for x in imgs]
+    plans = [metering.plan_stack([imgs[i], imgs[i + 2]], [1.0, 1.0]) for i in range(0, 6, 2)]
+    return {"offsets": np.array(offs),
+            "plans": np.array([[p.offset_stops, p.reference_index] for p in plans])}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
@@ -262,6 +282,7 @@ def main():
                         message=np.array(raised))
     print("default scene:", raised)
     np.savez_compressed(os.path.join(GOLDEN, "formats.npz"), **format_fixture())
+    np.savez_compressed(os.path.join(GOLDEN, "metering.npz"), **metering_fixture())
     np.savez_compressed(os.path.join(GOLDEN, "stack3_vga.npz"), **stack_fixture(640, 480, 7))
     for name, mode, exposures, swap in FILE_CASES:
         fx = file_fixture(name, mode, exposures, swap)

@@ -786,3 +786,16 @@ def register_and_fuse_stack(frames, exposures=None, p: Params | None = None):
         ssims.append(r.ssim)
         valids.append(r.valid.astype(np.float32))
     return fuse_stack(warped, ssims, valids), k, regs
+
+
+def select_offset(img, dark_level=0.05, cutoffs=(0.02, 0.10)):
+    """metering.select_offset (metering.py:21-34)."""
+    lum = luminance(img) if img.ndim == 3 else img
+    q = float(np.mean(lum < dark_level))
+    return 2 if q < cutoffs[0] else 3 if q < cutoffs[1] else 4
+
+
+def plan_stack(images, exposures):
+    """metering.plan_stack (metering.py:54-57): (offset_stops, reference_index)."""
+    k = choose_reference(images, exposures)
+    return select_offset(images[k]), k

@@ -88,7 +88,8 @@ SIGNATURES = {
     "hdr_register_and_fuse_stack": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "hdr_decode_image": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "hdr_encode_u8": (_I, [_P, _P, _I64, _P]),
-    "hdr_mean_luminance": (_I, [_P, _P, _I64, _P]),
+    "hdr_mean_luminance": (_I, [_P, _P, _I, _I64, _P]),
+    "hdr_dark_count": (_I, [_P, _P, _I, _I64, ctypes.c_float, _P]),
     "hdr_register_and_fuse_raw": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P]),
     "hdr_level_seed": (ctypes.c_uint32, [_U64, _I]),
     "hdr_iteration_keys": (_I, [_U64, _I, _P]),

@@ -964,9 +964,20 @@ extern "C" int hdr_encode_u8(hdr_ctx* c, const float* img, int64_t n, uint8_t* o
   return check_launch();
 }
 
-extern "C" int hdr_mean_luminance(hdr_ctx* c, const float* rgb, int64_t n, double* out) {
-  NEED(c && rgb && out, "null argument");
-  launch_mean_luminance(rgb, n, out, c->stream);
+extern "C" int hdr_dark_count(hdr_ctx* c, const float* img, int32_t channels, int64_t n,
+                              float dark_level, uint64_t* out) {
+  NEED(c && img && out, "null argument");
+  NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  launch_dark_count(img, channels, n, dark_level, reinterpret_cast<unsigned long long*>(out),
+                    c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_mean_luminance(hdr_ctx* c, const float* img, int32_t channels, int64_t n,
+                                  double* out) {
+  NEED(c && img && out, "null argument");
+  NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  launch_mean_luminance(img, channels, n, out, c->stream);
   return check_launch();
 }
 

@@ -169,7 +169,9 @@ void launch_finalize_warp(DtPlanes smooth, const double* fallback,
 void launch_decode(const void* in, int64_t npx, int channels, int bits, float* out,
                    cudaStream_t s);
 void launch_encode_u8(const float* x, int64_t n, uint8_t* out, cudaStream_t s);
-void launch_mean_luminance(const float* rgb, int64_t n, double* out, cudaStream_t s);
+void launch_mean_luminance(const float* img, int channels, int64_t n, double* out, cudaStream_t s);
+void launch_dark_count(const float* img, int channels, int64_t n, float dark,
+                       unsigned long long* out, cudaStream_t s);
 
 // ---- k_fusion.cu
 void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb,

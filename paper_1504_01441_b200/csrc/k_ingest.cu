@@ -83,16 +83,22 @@ void launch_encode_u8(const float* x, int64_t n, uint8_t* out, cudaStream_t s) {
 // image.luminance over the frame, accumulated in f64 (numpy accumulates the
 // float32 luminance pairwise in float32; the two agree to ~1e-7 relative,
 // which only matters for a tie-break between equal exposures).
-__global__ void __launch_bounds__(256) mean_lum_kernel(const float* __restrict__ rgb, int64_t n,
-                                                       double* __restrict__ out) {
+// luminance of pixel i (RGB) or the grey value itself (channels == 1: the
+// reference meters grey images directly, metering.py:28,47)
+__device__ __forceinline__ float meter_value(const float* img, int channels, int64_t i) {
+  if (channels == 1) return img[i];
+  const float* p = img + 3 * i;
+  float y = fadd(fadd(fmul(0.299f, p[0]), fmul(0.587f, p[1])), fmul(0.114f, p[2]));
+  return fminf(fmaxf(y, 0.0f), 1.0f);
+}
+
+__global__ void __launch_bounds__(256) mean_lum_kernel(const float* __restrict__ img, int channels,
+                                                       int64_t n, double* __restrict__ out) {
   __shared__ double part[8];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float* p = rgb + 3 * i;
-    float y = fadd(fadd(fmul(0.299f, p[0]), fmul(0.587f, p[1])), fmul(0.114f, p[2]));
-    acc += (double)fminf(fmaxf(y, 0.0f), 1.0f);
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += (double)meter_value(img, channels, i);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
@@ -104,11 +110,35 @@ __global__ void __launch_bounds__(256) mean_lum_kernel(const float* __restrict__
   }
 }
 
-void launch_mean_luminance(const float* rgb, int64_t n, double* out, cudaStream_t s) {
+void launch_mean_luminance(const float* img, int channels, int64_t n, double* out, cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(double), s);
   int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
   if (blocks < 1) return;
-  mean_lum_kernel<<<(unsigned)blocks, 256, 0, s>>>(rgb, n, out);
+  mean_lum_kernel<<<(unsigned)blocks, 256, 0, s>>>(img, channels, n, out);
+}
+
+// metering.select_offset's statistic (metering.py:28-29): the number of
+// pixels whose image.luminance is below dark_level. numpy 2 compares the
+// float32 luminance with the Python float cast to float32 (NEP 50), so the
+// compare is in f32 (the caller passes f32(dark_level)).
+__global__ void __launch_bounds__(256) dark_count_kernel(const float* __restrict__ img, int channels,
+                                                         int64_t n, float dark,
+                                                         unsigned long long* out) {
+  unsigned long long cnt = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt += meter_value(img, channels, i) < dark ? 1ull : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
+void launch_dark_count(const float* img, int channels, int64_t n, float dark,
+                       unsigned long long* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+  int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
+  if (blocks < 1) return;
+  dark_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(img, channels, n, dark, out);
 }
 
 }  // namespace hdr

@@ -206,3 +206,25 @@ def test_run_hdr_errors(tmp_path):
         pipeline.run_hdr(pipeline.PipelineConfig(inputs=paths, params=pipeline.PipelineParams(tile=8)))
     with pytest.raises(FileNotFoundError):
         pipeline.run_hdr(pipeline.PipelineConfig(inputs=[paths[0], str(tmp_path / "missing.png")]))
+
+
+def test_oracle_metering_matches_reference():
+    fx = load("metering")
+    imgs = G.metering_images()
+    assert [O.select_offset(x) for x in imgs] == fx["offsets"].tolist()
+    plans = [list(O.plan_stack([imgs[i], imgs[i + 2]], [1.0, 1.0])) for i in range(0, 6, 2)]
+    assert plans == fx["plans"].tolist()
+
+
+@pytest.mark.gpu
+def test_metering_gpu_matches_oracle():
+    from paper_1504_01441_b200 import metering
+    imgs = G.metering_images()
+    for x in imgs:
+        assert metering.select_offset(x) == O.select_offset(x)
+        lum = O.luminance(x) if x.ndim == 3 else x
+        assert metering.dark_fraction(x) == float(np.mean(lum < 0.05))
+        assert abs(metering.mean_luminance(x) - float(np.mean(lum))) < 1e-6
+    for i in range(0, 6, 2):
+        p = metering.plan_stack([imgs[i], imgs[i + 2]], [1.0, 1.0])
+        assert (p.offset_stops, p.reference_index) == O.plan_stack([imgs[i], imgs[i + 2]], [1.0, 1.0])

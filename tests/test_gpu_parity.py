@@ -155,7 +155,7 @@ def test_densify_warp_stages(scene):
 
 
 @pytest.mark.parametrize("shape", [(480, 640), (37, 53), (37, 54), (1, 70), (70, 1), (2100, 33),
-                                   (2100, 34), (4100, 6), (9000, 5)])
+                                   (2100, 34), (1944, 130), (3000, 66), (4100, 6), (9000, 5)])
 def test_dt_filter_all_column_paths(cuda, shape):
     """Every column-sweep implementation -- the register-resident cluster
     kernel with and without the cp.async band prefetch, and the chunk

@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--height", type=int, default=H5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="hdr_set_option before the run (tuning hooks, e.g. dt_cols_grid_div=2)")
     return ap.parse_args()
 
 
@@ -266,6 +268,10 @@ def run_ours(args):
     from paper_1504_01441_b200.runner import BatchRunner
 
     from paper_1504_01441_b200 import dist as hd
+    from paper_1504_01441_b200 import _native as _nat
+    for opt in args.option:
+        name, val = opt.split("=")
+        _nat.check(_nat.lib().hdr_set_option(name.encode(), int(val)))
     torch.cuda.set_device(local)
     if world > 1:
         hd.init("nccl", local)
@@ -453,6 +459,7 @@ def run_ours(args):
                    "global_pairs_per_step": B * world, "streams": args.streams,
                    "e2e_streams": args.e2e_streams,
                    "distinct_scenes": len(scenes), "graph": not args.no_graph,
+                   "options": args.option,
                    "l2": "inputs larger than L2 (each pair 121 MB, %d resident pairs)" % B,
                    "parallelism": f"pair-sharded x{world}, no collective"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak,

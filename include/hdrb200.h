@@ -97,6 +97,8 @@ const char* hdr_last_error(void);
  * cluster-resident kernel per column sweep pair, 0 = chunk agg/link/apply.
  * "dt_sparse_first": 1 (default) = the pair's first domain-transform row pass
  * builds its rows from the CSR splat (no dense splat planes), 0 = dense splat.
+ * "dt_cols_grid_div": d >= 1 (default 1) = launch 1/d of the co-resident
+ * column-sweep clusters (tuning: SM sharing with concurrent pairs).
  * "dt_cols_prefetch": 1 (default) = the cluster column kernel prefetches the
  * next band by cp.async, 0 = plain loads.
  * Returns HDR_ERR_INVALID for an unknown name. */

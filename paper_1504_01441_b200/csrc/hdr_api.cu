@@ -54,6 +54,10 @@ extern "C" int hdr_set_option(const char* name, int64_t value) {
     g_sparse_first = value != 0;
     return HDR_OK;
   }
+  if (name && std::string(name) == "dt_cols_grid_div") {
+    hdr::dt_set_cols_grid_div((int)value);
+    return HDR_OK;
+  }
   if (name && std::string(name) == "dt_cols_prefetch") {
     hdr::dt_set_cols_prefetch(value != 0);
     return HDR_OK;

@@ -977,6 +977,8 @@ static int max_clusters() {
 
 // test hook: 0 turns the cp.async band prefetch of the cluster kernel off
 static bool g_cols_prefetch = true;
+// clusters launched = co-resident maximum / g_cols_grid_div (tuning hook)
+static int g_cols_grid_div = 1;
 
 template <int K, bool FINAL>
 static void launch_cols_cluster(const float* guide, const DtPlanes& P, int w, int h, double ratio,
@@ -987,6 +989,7 @@ static void launch_cols_cluster(const float* guide, const DtPlanes& P, int w, in
     if (!P.f64[k]) pf = false;
   int mc = pf ? max_clusters<K, FINAL, true>() : 0;
   if (pf && mc > 0) {
+    if (g_cols_grid_div > 1) mc = std::max(1, mc / g_cols_grid_div);
     dim3 cgrid(kCL, std::min(nb, mc));
     dt_cols_cluster<K, FINAL, true><<<cgrid, kCT, cols_pf_smem<K>(), s>>>(guide, P, w, h, ratio, c, bl, fo);
     return;
@@ -1072,6 +1075,7 @@ int64_t dt_scratch_doubles(int w, int h, int k) {
 
 void dt_set_cluster_columns(bool on) { g_cols_cluster = on; }
 void dt_set_cols_prefetch(bool on) { g_cols_prefetch = on; }
+void dt_set_cols_grid_div(int d) { g_cols_grid_div = d < 1 ? 1 : d; }
 
 void init_densify_attributes() {
   allow_max_dynamic_smem(dt_rows_kernel<1>);

@@ -256,9 +256,11 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
                                                    uint8_t* __restrict__ valid,
                                                    uint8_t* __restrict__ qw,
                                                    uint32_t* __restrict__ hist) {
-  __shared__ uint32_t sh[kBins];
-  for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+  // one histogram per warp (plain shared atomics; see luma_hist_kernel)
+  __shared__ uint32_t sh[8][kBins];
+  for (int i = threadIdx.x; i < 8 * kBins; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
+  uint32_t* mine = sh[threadIdx.x >> 5];
   // row / segment indices advance without a division per step
   const int segs = (w + 255) >> 8;
   const int dq = gridDim.x / segs, dr = gridDim.x - dq * segs;
@@ -293,12 +295,15 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
     valid[i] = ok ? 1 : 0;
     uint32_t q = quant3(luma3(o[0], o[1], o[2]));
     qw[i] = (uint8_t)q;
-    unsigned peers = __match_any_sync(__activemask(), q);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[q], (uint32_t)__popc(peers));
+    atomicAdd(&mine[q], 1u);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
-    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) t += sh[w8][b];
+    if (t) atomicAdd(&hist[b], t);
+  }
 }
 
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,

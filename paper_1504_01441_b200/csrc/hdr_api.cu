@@ -269,13 +269,15 @@ static int fusion_dims(int w, int h, int levels, std::vector<Dims>& d) {
   return (int)d.size();
 }
 
+static int64_t round4(int64_t n) { return (n + 3) & ~int64_t(3); }
+
 // floats of a fusion pyramid of nf frames: levels 1.. (level 1 also for a
 // single-level pyramid) x (4 nf Gaussian + 3 collapse channels)
 static int64_t fusion_floats(const std::vector<Dims>& fd, int nf) {
   int64_t n = 0;
   for (size_t k = 1; k < std::max<size_t>(fd.size(), 2); ++k) {
     Dims d = k < fd.size() ? fd[k] : Dims{(fd[0].w + 1) / 2, (fd[0].h + 1) / 2};
-    n += (4 * nf + 3) * ((int64_t)d.w * d.h + 64);
+    n += round4(4 * nf * (int64_t)d.w * d.h) + 64 + round4(3 * (int64_t)d.w * d.h) + 64;
   }
   return n;
 }
@@ -289,10 +291,10 @@ static void fusion_layout(const std::vector<Dims>& fd, int nf, float* base, Fuse
     py.g[k] = py.c[k] = nullptr;
     if (k == 0) continue;
     int64_t n = (int64_t)d.w * d.h;
-    py.g[k] = q;
-    q += 4 * nf * n + 64;
+    py.g[k] = q;  // every region starts 16-byte aligned (vector I/O in collapse)
+    q += round4(4 * nf * n) + 64;
     py.c[k] = q;
-    q += 3 * n + 64;
+    q += round4(3 * n) + 64;
   }
 }
 
@@ -1484,7 +1486,7 @@ extern "C" int hdr_fuse_stack(hdr_ctx* c, int32_t n, const float* const* frames,
   }
   std::vector<Dims> fd;
   fusion_dims(w, h, levels > 0 ? levels : fusion_levels_default(w, h), fd);
-  int64_t need = fusion_floats(fd, n) + (int64_t)n * ((int64_t)w * h + 64);
+  int64_t need = fusion_floats(fd, n) + (int64_t)n * (round4((int64_t)w * h) + 64);
   if (need > c->fstack_cap) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->fstack) cudaFree(c->fstack);
@@ -1494,7 +1496,7 @@ extern "C" int hdr_fuse_stack(hdr_ctx* c, int32_t n, const float* const* frames,
     c->fstack_cap = need;
   }
   float* wbase = c->fstack + fusion_floats(fd, n);
-  for (int f = 0; f < n; ++f) fs.wout[f] = wbase + (int64_t)f * ((int64_t)w * h + 64);
+  for (int f = 0; f < n; ++f) fs.wout[f] = wbase + (int64_t)f * (round4((int64_t)w * h) + 64);
   return enqueue_fuse_frames(c, n, fs, w, h, levels, c->fstack, out);
 }
 

@@ -290,7 +290,9 @@ __device__ __forceinline__ void tap_rows(int y, int n, int c0, int* idx, float* 
 }
 
 template <int NF>
-constexpr size_t collapse_smem() { return sizeof(float) * (3 * (NF + 1)) * (kCT * kCT + kCT * kFT); }
+constexpr size_t collapse_smem() {
+  return sizeof(float) * (((3 * (NF + 1) * kCT * kCT + 3) & ~3) + 3 * (NF + 1) * kCT * kFT);
+}
 
 // 3NF + 3 coarse channels: G_f RGB (gc, the planar 4NF-channel level), C (cc)
 template <bool LEVEL0, int NF>
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(256) collapse_kernel(const float* __restrict__
   constexpr int NCH = 3 * (NF + 1);
   extern __shared__ float smc[];
   float* C = smc;                      // [NCH][19][19] coarse tile
-  float* Hc = smc + NCH * kCT * kCT;   // [NCH][19][32] coarse rows up-sampled along x
+  float* Hc = smc + ((NCH * kCT * kCT + 3) & ~3);  // [NCH][19][32] up-sampled along x (16B aligned)
   __shared__ int vr[kFT][3], hc[kFT][3];
   __shared__ float vw[kFT][3], hw[kFT][3];
   int tid = threadIdx.x;
@@ -338,35 +340,118 @@ __global__ void __launch_bounds__(256) collapse_kernel(const float* __restrict__
   }
   __syncthreads();
   int P = w * h;
-  for (int i = tid; i < kFT * kFT; i += 256) {
-    int yy = i >> 5, x = i & 31;
-    int Y = y0 + yy, X = x0 + x;
-    if (Y >= h || X >= w) continue;
-    int r0 = vr[yy][0], r1 = vr[yy][1], r2 = vr[yy][2];
-    float w0 = vw[yy][0], w1 = vw[yy][1], w2 = vw[yy][2];
-    float u[NCH];
+  // each thread: 4 consecutive pixels of one row (the 32x32 tile = 256 x 4),
+  // so the up-sampled rows are read as float4 and, where the layout allows,
+  // the frames / weights / output move as 16-byte vectors
+  const int yy = tid >> 3, xq = (tid & 7) * 4;
+  const int Y = y0 + yy, X = x0 + xq;
+  if (Y >= h || X >= w) return;
+  const int r0 = vr[yy][0], r1 = vr[yy][1], r2 = vr[yy][2];
+  const float w0 = vw[yy][0], w1 = vw[yy][1], w2 = vw[yy][2];
+  float u[NCH][4];
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const float* col = Hc + c * kCT * kFT + x;
-      u[c] = w0 * col[r0 * kFT] + w1 * col[r1 * kFT] + w2 * col[r2 * kFT];
+  for (int c = 0; c < NCH; ++c) {
+    const float* col = Hc + c * kCT * kFT + xq;
+    float4 a = *reinterpret_cast<const float4*>(col + r0 * kFT);
+    float4 b = *reinterpret_cast<const float4*>(col + r1 * kFT);
+    float4 d = *reinterpret_cast<const float4*>(col + r2 * kFT);
+    u[c][0] = w0 * a.x + w1 * b.x + w2 * d.x;
+    u[c][1] = w0 * a.y + w1 * b.y + w2 * d.y;
+    u[c][2] = w0 * a.z + w1 * b.z + w2 * d.z;
+    u[c][3] = w0 * a.w + w1 * b.w + w2 * d.w;
+  }
+  const int p = Y * w + X;
+  const bool full = X + 3 < w;
+  // vector I/O needs 16-byte aligned rows: w % 4 == 0 (and P % 4 == 0 for
+  // the planar levels); the bases are 256-byte aligned allocations
+  bool aligned = ((uintptr_t)out & 15) == 0;
+  if (LEVEL0) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+      aligned = aligned && (((uintptr_t)fr.img[f] | (uintptr_t)fr.wout[f]) & 15) == 0;
+  } else {
+    aligned = aligned && ((uintptr_t)g & 15) == 0;
+  }
+  const bool vec = full && aligned && (w & 3) == 0 && (LEVEL0 || (P & 3) == 0);
+  float wt[NF][4], gv[NF][3][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const float* wp = LEVEL0 ? fr.wout[f] + p : g + (3 * NF + f) * P + p;
+    if (vec) {
+      float4 t = __ldg(reinterpret_cast<const float4*>(wp));
+      wt[f][0] = t.x; wt[f][1] = t.y; wt[f][2] = t.z; wt[f][3] = t.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wt[f][j] = X + j < w ? __ldg(wp + j) : 0.0f;
     }
-    int p = Y * w + X;
-    float wt[NF];
+    if (LEVEL0) {
+      const float* ip = fr.img[f] + 3 * p;  // 12 interleaved floats
+      if (vec) {
+        float4 t0 = __ldg(reinterpret_cast<const float4*>(ip));
+        float4 t1 = __ldg(reinterpret_cast<const float4*>(ip) + 1);
+        float4 t2 = __ldg(reinterpret_cast<const float4*>(ip) + 2);
+        float v12[12] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w, t2.x, t2.y, t2.z, t2.w};
 #pragma unroll
-    for (int f = 0; f < NF; ++f) wt[f] = LEVEL0 ? __ldg(fr.wout[f] + p) : __ldg(g + (3 * NF + f) * P + p);
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) gv[f][k][j] = v12[3 * j + k];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) gv[f][k][j] = X + j < w ? __ldg(ip + 3 * j + k) : 0.0f;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float* gp = g + (3 * f + k) * P + p;
+        if (vec) {
+          float4 t = __ldg(reinterpret_cast<const float4*>(gp));
+          gv[f][k][0] = t.x; gv[f][k][1] = t.y; gv[f][k][2] = t.z; gv[f][k][3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) gv[f][k][j] = X + j < w ? __ldg(gp + j) : 0.0f;
+        }
+      }
+    }
+  }
+  float o[3][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       float v = 0.0f;
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        float gv = LEVEL0 ? __ldg(fr.img[f] + 3 * p + k) : __ldg(g + (3 * f + k) * P + p);
-        v = f == 0 ? wt[0] * (gv - u[k]) : v + wt[f] * (gv - u[3 * f + k]);
+      for (int f = 0; f < NF; ++f)
+        v = f == 0 ? wt[0][j] * (gv[0][k][j] - u[k][j]) : v + wt[f][j] * (gv[f][k][j] - u[3 * f + k][j]);
+      v += u[3 * NF + k][j];
+      o[k][j] = LEVEL0 ? fminf(fmaxf(v, 0.0f), 1.0f) : v;
+    }
+  if (LEVEL0) {
+    float* op = out + 3 * p;
+    if (vec) {
+      float4* o4 = reinterpret_cast<float4*>(op);
+      o4[0] = make_float4(o[0][0], o[1][0], o[2][0], o[0][1]);
+      o4[1] = make_float4(o[1][1], o[2][1], o[0][2], o[1][2]);
+      o4[2] = make_float4(o[2][2], o[0][3], o[1][3], o[2][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (X + j < w)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) op[3 * j + k] = o[k][j];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float* op = out + k * P + p;
+      if (vec) {
+        *reinterpret_cast<float4*>(op) = make_float4(o[k][0], o[k][1], o[k][2], o[k][3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (X + j < w) op[j] = o[k][j];
       }
-      v += u[3 * NF + k];
-      if (LEVEL0)
-        out[3 * p + k] = fminf(fmaxf(v, 0.0f), 1.0f);
-      else
-        out[k * P + p] = v;
     }
   }
 }

@@ -7,6 +7,8 @@
 // reference's evaluation order, so no FMA contraction can change a bit.
 #include "hdr_common.cuh"
 #include "hdr_internal.h"
+
+#include <algorithm>
 #include "hdr_scan.cuh"
 
 namespace hdr {
@@ -261,11 +263,20 @@ __global__ void __launch_bounds__(256) level_stats_kernel(SatBatch b) {
   int64_t n = (int64_t)L.w * L.h;
   int qm = 1 << 20;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float v = L.img[i];
-    qm = min(qm, log2_quantum(v));
-    acc += (double)fabsf(v);
+  // eight independent loads per thread per step (the level is streamed once)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < n; base += 8 * stride) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      int64_t i = base + k * stride;
+      v[k] = i < n ? __ldg(L.img + i) : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      qm = min(qm, log2_quantum(v[k]));
+      acc += (double)fabsf(v[k]);
+    }
   }
   for (int off = 16; off; off >>= 1) {
     qm = min(qm, __shfl_down_sync(0xffffffff, qm, off));
@@ -286,7 +297,10 @@ __global__ void __launch_bounds__(256) level_stats_kernel(SatBatch b) {
 void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s) {
   cudaMemsetAsync(b.sums, 0, sizeof(double) * 5, s);
   cudaMemsetAsync(b.qmin, 0x3f, sizeof(int32_t) * 5, s);  // large positive
-  dim3 g(grid_for(max_pixels, 256), b.n);
+  // two blocks per SM per level: each thread streams its share in steps of
+  // eight independent loads, and a level costs only ~300 same-address atomics
+  int bx = std::min(grid_for(max_pixels, 256), 148 * 2);
+  dim3 g(bx, b.n);
   level_stats_kernel<<<g, 256, 0, s>>>(b);
 }
 
@@ -408,44 +422,93 @@ __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp
   int limx = min(tile, w - t0x), limy = min(tile, h - t0y);
   int nx = limx > first ? (limx - first + sp - 1) / sp : 0;
   int ny = limy > first ? (limy - first + sp - 1) / sp : 0;
-  // tile-local summed-area table (exact path): pixels [r0, r1) x [c0, c1)
-  int r0 = max(0, t0y - half), r1 = min(h, t0y + tile + half);
-  int c0 = max(0, t0x - half), c1 = min(w, t0x + tile + half);
-  int R = r1 - r0, C = c1 - c0, SW = C + 1;
-  if (EXACT) {
-    for (int i = threadIdx.x; i < (R + 1) * SW; i += blockDim.x) {
-      int r = i / SW, c = i % SW;
-      local_sat[i] = (r && c) ? (double)L.img[(int64_t)(r0 + r - 1) * w + (c0 + c - 1)] : 0.0;
+  // Exact path: the quadrant sums straight from the pixels, separably. Under
+  // the level's exactness certificate (every partial sum of the level is
+  // exactly representable) any summation order gives numpy's SAT
+  // differences bit for bit, so the sums are formed in parallel: candidate
+  // x's quadrant columns start at x - half (m < nx) or x (m = nx + lx), rows
+  // likewise; H[r][m] sums `half` pixels of row r from column start m, V[n][m]
+  // sums `half` rows of H -- tl = V[ly][lx], tr = V[ly][nx+lx],
+  // bl = V[ny+ly][lx], br = V[ny+ly][nx+lx] (image.py:47-58).
+  double* Vs = local_sat;                                   // [2ny][2nx]
+  double* Hs = local_sat + 32 * 32;                         // [rows][2nx]
+  float* img_s = reinterpret_cast<float*>(Hs + (tile + 2 * half) * 32);  // [rows][cols]
+  const int ry0 = t0y + first - half, rx0 = t0x + first - half;
+  const int rows = ny > 0 ? (ny - 1) * sp + 2 * half : 0;
+  const int cols = nx > 0 ? (nx - 1) * sp + 2 * half : 0;
+  const int NX = 2 * nx, NY = 2 * ny;
+  if (EXACT && nx > 0 && ny > 0) {
+    // rows by warp, columns by lane: no integer division per element, and
+    // all of a thread's loads are issued before the first store
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    // groups of 4 rows x 3 column steps: 12 loads in flight per thread
+    for (int rb = wid; rb < rows; rb += 4 * nwarp) {
+      float v[12];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        int r = rb + (k / 3) * nwarp, c = lane + (k % 3) * 32;
+        int y = ry0 + r, x = rx0 + c;
+        v[k] = (r < rows && c < cols && y >= 0 && y < h && x >= 0 && x < w)
+                   ? __ldg(L.img + (int64_t)y * w + x) : 0.0f;
+      }
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        int r = rb + (k / 3) * nwarp, c = lane + (k % 3) * 32;
+        if (r < rows && c < cols) img_s[r * cols + c] = v[k];
+      }
     }
+    for (int r = wid; r < rows; r += nwarp)  // columns beyond 96 (tile + 2 half > 96)
+      for (int c = lane + 96; c < cols; c += 32) {
+        int y = ry0 + r, x = rx0 + c;
+        img_s[r * cols + c] = (y >= 0 && y < h && x >= 0 && x < w) ? L.img[(int64_t)y * w + x] : 0.0f;
+      }
     __syncthreads();
-    for (int r = 1 + threadIdx.x; r <= R; r += blockDim.x)
-      for (int c = 1; c <= C; ++c) local_sat[r * SW + c] += local_sat[r * SW + c - 1];
+    // H[r][m]: warp per row, lane per column start (NX <= 32)
+    for (int r = wid; r < rows; r += nwarp)
+      if (lane < NX) {
+        int c0 = lane < nx ? lane * sp : (lane - nx) * sp + half;
+        const float* row = img_s + r * cols + c0;
+        double acc = 0.0;
+        for (int k = 0; k < half; ++k) acc += (double)row[k];
+        Hs[r * NX + lane] = acc;
+      }
     __syncthreads();
-    for (int c = 1 + threadIdx.x; c <= C; c += blockDim.x)
-      for (int r = 1; r <= R; ++r) local_sat[r * SW + c] += local_sat[(r - 1) * SW + c];
+    for (int n = wid; n < NY; n += nwarp)
+      if (lane < NX) {
+        int q0 = n < ny ? n * sp : (n - ny) * sp + half;
+        double acc = 0.0;
+        for (int k = 0; k < half; ++k) acc += Hs[(q0 + k) * NX + lane];
+        Vs[n * NX + lane] = acc;
+      }
     __syncthreads();
   }
   LatticeView v{L.ltab, L.rowmap, L.colmap, L.ncols};
   // ((t[y1,x1] - t[y0,x1]) - t[y1,x0]) + t[y0,x0]   (image.py:58)
   auto box = [&](int x0, int y0, int x1, int y1) -> double {
-    if (EXACT) {
-      const double* S = local_sat;
-      int a0 = y0 - r0, a1 = y1 - r0, b0 = x0 - c0, b1 = x1 - c0;
-      return dadd(dsub(dsub(S[a1 * SW + b1], S[a0 * SW + b1]), S[a1 * SW + b0]), S[a0 * SW + b0]);
-    }
     return dadd(dsub(dsub(v.at(y1, x1), v.at(y0, x1)), v.at(y1, x0)), v.at(y0, x0));
   };
   double area = (double)(half * half);
   double best = -1.0;
   int best_i = 0x7fffffff;
-  for (int i = threadIdx.x; i < nx * ny; i += blockDim.x) {
-    int lx = i % nx, ly = i / nx;
+  // candidate (lx, ly) = (tid & 15, tid >> 4): nx, ny <= 16 (tile / 16 spacing)
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    int lx = t & 15, ly = t >> 4;
+    if (lx >= nx || ly >= ny) continue;
+    int i = ly * nx + lx;  // row-major candidate index (tie-break order)
     int x = t0x + first + lx * sp, y = t0y + first + ly * sp;
     if (x < half || x > w - half || y < half || y > h - half) continue;
-    double tl = box(x - half, y - half, x, y) / area;
-    double tr = box(x, y - half, x + half, y) / area;
-    double br = box(x, y, x + half, y + half) / area;
-    double bl = box(x - half, y, x, y + half) / area;
+    double tl, tr, br, bl;
+    if (EXACT) {
+      tl = Vs[ly * NX + lx] / area;
+      tr = Vs[ly * NX + nx + lx] / area;
+      bl = Vs[(ny + ly) * NX + lx] / area;
+      br = Vs[(ny + ly) * NX + nx + lx] / area;
+    } else {
+      tl = box(x - half, y - half, x, y) / area;
+      tr = box(x, y - half, x + half, y) / area;
+      br = box(x, y, x + half, y + half) / area;
+      bl = box(x - half, y, x, y + half) / area;
+    }
     double d0 = fabs(dsub(tr, tl)), d1 = fabs(dsub(br, tr));
     double d2 = fabs(dsub(bl, br)), d3 = fabs(dsub(tl, bl));
     double lo = fmin(fmin(d0, d1), fmin(d2, d3));
@@ -479,9 +542,10 @@ __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp
   }
 }
 
+// V [32][32] + H [tile + 2 half][32] doubles + the pixel region (f32)
 size_t detect_exact_smem(int tile, int half) {
-  size_t side = (size_t)tile + 2 * (size_t)half + 1;
-  return side * side * sizeof(double);
+  size_t side = (size_t)tile + 2 * (size_t)half;
+  return (32 * 32 + side * 32) * sizeof(double) + side * side * sizeof(float);
 }
 
 void init_raster_attributes() { allow_max_dynamic_smem(detect_kernel<true>); }

@@ -18,7 +18,7 @@ run ssim 'ssim_fixed_kernel' 0
 run weights0 'weights_down_kernel' 0
 run collapse0 'collapse_kernel' 7
 run warp 'warp_kernel' 0
-run detect 'detect_kernel' 1
+run detect 'detect_kernel<1' 0
 run dt_link 'dt_cols_link' 0
 run down 'down_kernel' 0
 du -sh gpurun_out

@@ -47,13 +47,32 @@ __device__ bool ssd_search(const float* __restrict__ ref, const float* __restric
   int sw = nx + patch - 1, sh = ny + patch - 1;
   double* T = smem;
   double* S = smem + patch * patch;
-  for (int i = threadIdx.x; i < patch * patch; i += blockDim.x) {
-    int ky = i / patch, kx = i % patch;
-    T[i] = (double)ref[(int64_t)(yr - hp + ky) * w + (xr - hp + kx)];
-  }
-  for (int i = threadIdx.x; i < sw * sh; i += blockDim.x) {
-    int ry = i / sw, rx = i % sw;
-    S[i] = (double)src[(int64_t)(cy0 - hp + ry) * w + (cx0 - hp + rx)];
+  // staging: rows by warp, columns by lane (no integer division per element),
+  // and batches of 8 loads in flight per thread before the stores -- a
+  // load -> store chain per element serialises on DRAM latency
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    auto stage = [&](const float* img, int y0, int x0, int rows, int cols, double* dst) {
+      const int cstep = (cols + 31) >> 5;  // column steps per row (<= 3 for a 41-wide window)
+      const int items = ((rows + nwarp - 1 - wid) / nwarp) * cstep;  // this lane's (row, col) pairs
+      for (int b = 0; b < items; b += 8) {
+        float v[8];
+        int idx[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          int it = b + k;
+          int r = wid + (it / cstep) * nwarp, c = lane + (it % cstep) * 32;
+          bool ok = it < items && r < rows && c < cols;
+          idx[k] = ok ? r * cols + c : -1;
+          v[k] = ok ? __ldg(img + (int64_t)(y0 + r) * w + (x0 + c)) : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (idx[k] >= 0) dst[idx[k]] = (double)v[k];
+      }
+    };
+    stage(ref, yr - hp, xr - hp, patch, patch, T);
+    stage(src, cy0 - hp, cx0 - hp, sh, sw, S);
   }
   __syncthreads();
   SsdKey k;

@@ -165,7 +165,12 @@ class BatchRunner:
         run_host; returns the H2D / D2H byte counts."""
         h, w = self.height, self.width
         dev = f"cuda:{self.device}"
-        if getattr(self, "_raw_staging", None) is None:
+        if bits not in (8, 16):
+            raise ValueError("bits must be 8 or 16")
+        if getattr(self, "_raw_bits", None) != bits:
+            # staging slots typed for this sample width (uint8, or uint16 viewed as int16)
+            torch.cuda.synchronize(self.device)
+            self._raw_bits = bits
             dt = torch.uint8 if bits == 8 else torch.int16
             self._raw_staging = [[dict(ref=torch.empty((h, w, 3), dtype=dt, device=dev),
                                        src=torch.empty((h, w, 3), dtype=dt, device=dev),

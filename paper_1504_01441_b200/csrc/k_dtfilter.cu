@@ -690,9 +690,16 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
 // direction), so a sweep pair costs one HBM read and one write of the planes
 // instead of agg + link + apply's two reads, one write and the carry traffic.
 constexpr int kCL = 8;    // CTAs per cluster (portable maximum)
-constexpr int kCT = 256;  // threads per CTA (two CTAs per SM)
-constexpr int kCTLog2 = 8;
-constexpr int kSR = 8;    // rows per thread
+#ifndef HDR_COL_THREADS_LOG2
+#define HDR_COL_THREADS_LOG2 8
+#endif
+#ifndef HDR_COL_ROWS
+#define HDR_COL_ROWS 8
+#endif
+constexpr int kCT = 1 << HDR_COL_THREADS_LOG2;  // threads per CTA (256: two CTAs per SM)
+constexpr int kCTLog2 = HDR_COL_THREADS_LOG2;
+constexpr int kSR = HDR_COL_ROWS;    // rows per thread
+constexpr int kMaxBw = kCT / 8 < 32 ? kCT / 8 : 32;  // widest band (cluster arrays)
 
 namespace cg = cooperative_groups;
 
@@ -728,13 +735,13 @@ constexpr size_t cols_pf_smem() {
 // cols_pf_smem<K>()), so HBM reads of band b+1 overlap the link, apply and
 // store phases of band b; otherwise plain loads at the top of each band.
 template <int K, bool FINAL, bool PF>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 2)
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 2 : 1)
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
                     double c, int bw_log2, DtFlowOut fo) {
   __shared__ Aff<K> maps[kCT];           // [grp][col]
-  __shared__ Aff<K> ctaF[kCT / 4], ctaB[kCT / 4];  // per-column CTA totals (bw <= kCT / 4)
-  __shared__ double cin[kCT / 4][K], din[kCT / 4][K];
-  __shared__ Aff<K> remote[kCL][kCT / 4];
+  __shared__ Aff<K> ctaF[kMaxBw], ctaB[kMaxBw];  // per-column CTA totals (bw <= kMaxBw)
+  __shared__ double cin[kMaxBw][K], din[kMaxBw][K];
+  __shared__ Aff<K> remote[kCL][kMaxBw];
   extern __shared__ __align__(16) double pfx[];
   float* pfg = reinterpret_cast<float*>(pfx + K * kSR * kCT);
   cg::cluster_group cl = cg::this_cluster();
@@ -1013,7 +1020,7 @@ static int cluster_bw_log2(int h) {
   int rp = ceil_div(h, kCL);
   int g = ceil_div(rp, kSR), gl = 0;
   while ((1 << gl) < g) ++gl;
-  if (gl < 2) gl = 2;  // bw <= kCT / 4
+  while ((kCT >> gl) > kMaxBw) ++gl;  // bw <= kMaxBw
   int bl = kCTLog2 - gl;
   return bl >= 2 ? bl : -1;
 }

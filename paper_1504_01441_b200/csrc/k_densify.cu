@@ -309,7 +309,11 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
                  uint8_t* qw, uint32_t* hist, cudaStream_t s) {
   int64_t work = (int64_t)((w + 255) / 256) * h;
-  int64_t blocks = work < 148 * 12 ? work : 148 * 12;
+#ifndef HDR_WARP_BLOCKS_PER_SM
+#define HDR_WARP_BLOCKS_PER_SM 12
+#endif
+  int64_t cap = 148 * HDR_WARP_BLOCKS_PER_SM;
+  int64_t blocks = work < cap ? work : cap;
   warp_kernel<<<(unsigned)blocks, 256, 0, s>>>(flow, w, h, src, warped, valid, qw, hist);
 }
 

@@ -101,8 +101,11 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
   }
 }
 
+#ifndef HDR_W0_MIN_BLOCKS
+#define HDR_W0_MIN_BLOCKS 4
+#endif
 template <int NF>
-__global__ void __launch_bounds__(256, NF == 2 ? 4 : 2) weights_down_kernel(FuseFrames<NF> fr, int w, int h,
+__global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_down_kernel(FuseFrames<NF> fr, int w, int h,
                                                           float* __restrict__ g1, int ow, int oh) {
   extern __shared__ float smf[];
   float* lum = smf;                    // [NF][38][38] luminance of every frame

@@ -86,7 +86,10 @@ __global__ void __launch_bounds__(256) luma_hist_kernel(const float* __restrict_
 
 static int grid_for(int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
-  int cap = 148 * 8;
+#ifndef HDR_RASTER_BLOCKS_PER_SM
+#define HDR_RASTER_BLOCKS_PER_SM 4
+#endif
+  int cap = 148 * HDR_RASTER_BLOCKS_PER_SM;
   if (blocks > cap) blocks = cap;
   return blocks < 1 ? 1 : (int)blocks;
 }

@@ -689,7 +689,10 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
 // the cluster through distributed shared memory (one barrier.cluster per
 // direction), so a sweep pair costs one HBM read and one write of the planes
 // instead of agg + link + apply's two reads, one write and the carry traffic.
-constexpr int kCL = 8;    // CTAs per cluster (portable maximum)
+#ifndef HDR_COL_CLUSTER
+#define HDR_COL_CLUSTER 8
+#endif
+constexpr int kCL = HDR_COL_CLUSTER;  // CTAs per cluster (8: portable maximum)
 #ifndef HDR_COL_THREADS_LOG2
 #define HDR_COL_THREADS_LOG2 8
 #endif
@@ -972,6 +975,8 @@ static int max_clusters() {
   static int n = -1;
   if (n < 0) {
     size_t smem = PF ? cols_pf_smem<K>() : 0;
+    if (kCL > 8)  // clusters beyond the portable 8 CTAs must be opted into
+      cudaFuncSetAttribute(dt_cols_cluster<K, FINAL, PF>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (PF && cudaFuncSetAttribute(dt_cols_cluster<K, FINAL, PF>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
       cudaGetLastError();
@@ -1022,7 +1027,7 @@ static int cluster_bw_log2(int h) {
   while ((1 << gl) < g) ++gl;
   while ((kCT >> gl) > kMaxBw) ++gl;  // bw <= kMaxBw
   int bl = kCTLog2 - gl;
-  return bl >= 2 ? bl : -1;
+  return bl >= 1 ? bl : -1;
 }
 
 // test hook: 0 selects the agg/link/apply column path

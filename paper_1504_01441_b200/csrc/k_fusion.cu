@@ -110,7 +110,10 @@ void init_fusion_attributes() {
 constexpr int kS2 = 32;
 
 template <int R>
-__global__ void __launch_bounds__(256, 3) ssim_fixed_kernel(
+#ifndef HDR_SSIM_MIN_BLOCKS
+#define HDR_SSIM_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     const float* __restrict__ a, const float* __restrict__ b, const uint8_t* __restrict__ qb,
     const float* __restrict__ lut_b, int w, int h, const double* __restrict__ taps,
     float* __restrict__ out) {

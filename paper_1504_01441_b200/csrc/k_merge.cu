@@ -298,8 +298,11 @@ constexpr size_t collapse_smem() {
 }
 
 // 3NF + 3 coarse channels: G_f RGB (gc, the planar 4NF-channel level), C (cc)
+#ifndef HDR_COLLAPSE_MIN_BLOCKS
+#define HDR_COLLAPSE_MIN_BLOCKS 4
+#endif
 template <bool LEVEL0, int NF>
-__global__ void __launch_bounds__(256) collapse_kernel(const float* __restrict__ g, FuseFrames<NF> fr,
+__global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(const float* __restrict__ g, FuseFrames<NF> fr,
                                                       int w, int h, const float* __restrict__ gc,
                                                       const float* __restrict__ cc, int cw, int ch,
                                                       float* __restrict__ out) {

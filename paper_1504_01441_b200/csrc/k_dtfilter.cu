@@ -3,18 +3,26 @@
 // One pass = a forward+backward sweep along every row, then along every
 // column; each step is the reference's update (densify.py:69-75)
 //   b[i] += a * (b[i-1] - b[i]),   a = exp(c_pass * (1 + (sigma_s/sigma_r)|g[i+1]-g[i]|)).
+// Sweeps are cut into segments whose zero-carry effects are affine maps; the
+// maps are linked by scans and every segment is re-run from its true carry
+// with the reference formula (results differ from the sequential recursion
+// only by rounding, ~1e-16 relative).
 //
-// Rows: one block per row, the row resident in shared memory; the row is cut
-//   into per-thread segments whose zero-carry effects are affine maps, the
-//   maps are scanned across the block, and each segment is re-run from its
-//   true carry with the reference formula. HBM: one read + one write.
-// Columns: 16-row chunks held in registers. `agg` reads a chunk once and
-//   reduces it to the affine data both directions need (forward map A,B and
-//   the backward sums Z0 = sum (1-a_i) prod_{j<i} a_j y0_i, R for the
-//   carry's own response, Q = prod a_i); `link` links the chunks of each
-//   column with warp scans of affine maps; `apply` re-runs each chunk forward
-//   from its upper carry and backward from its lower carry with the
-//   reference formula. HBM: two reads + one write per column sweep pair.
+// Rows (dt_rows_bulk_kernel): one CTA per row, the K plane rows and the guide
+//   row moved by bulk copies into shared memory, 512 threads x <= 8 samples,
+//   block scans of the segment maps. The pair's first row pass
+//   (dt_rows_first_kernel) builds its rows from the CSR splat instead of
+//   reading dense splat planes and writes sample-free rows as zeros.
+// Columns (dt_cols_cluster, the default): a cluster of 8 CTAs owns a band of
+//   columns over the full height, each CTA a row range, each thread 8 rows of
+//   one column in registers; chunk maps are scanned inside the CTA and linked
+//   across the cluster through DSMEM, and the next band is prefetched by
+//   cp.async into per-thread shared-memory slots. The last pass writes the
+//   f32 flow (densify_flow) instead of the planes.
+// Columns fallback (tall images, test hook): `agg` reduces 16-row chunks to
+//   the affine data both directions need (forward map A,B and the backward
+//   sums Z0 = sum (1-a_i) prod_{j<i} a_j y0_i, R, Q = prod a_i), `link` links
+//   the chunks of each column, `apply` re-runs each chunk from its carries.
 // Planes may be stored f32 or f64 (DtPlanes::f64); all arithmetic is f64.
 #include "hdr_common.cuh"
 #include "hdr_internal.h"

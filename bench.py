@@ -185,10 +185,17 @@ def kernel_bytes(w, h, passes=3):
 
 
 def peaks():
+    """HBM peak for the roofline: the driver-measured STREAM-style copy
+    bandwidth (MEASURED_PEAKS.json `hbm_gbs`), else the profiling guide's
+    6.65 TB/s fallback."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(path):
-        d = json.load(open(path))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    try:
+        with open(path) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        if v > 0:
+            return v, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, ValueError, KeyError, TypeError):
+        pass
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 

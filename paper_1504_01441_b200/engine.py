@@ -74,6 +74,16 @@ def engine(width: int, height: int, device: int | None = None) -> Engine:
         return e
 
 
+def engine_for_rows(n_rows: int, device: int | None = None) -> Engine:
+    """Shared context whose match-row workspace (one row per 16-px tile of
+    its capacity, hdr_max_matches) holds n_rows."""
+    side = 16 * int(np.ceil(np.sqrt(max(n_rows, 1)))) + 16
+    e = engine(1, 1, device)
+    if e.width < side or e.height < side:
+        e = engine(max(e.width, side), max(e.height, side), device)
+    return e
+
+
 def device_of(*arrays) -> int:
     for a in arrays:
         if isinstance(a, torch.Tensor) and a.is_cuda:

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .engine import device_of, engine, is_torch, out, ptr, to_dev
+from .engine import device_of, engine, engine_for_rows, is_torch, out, ptr, to_dev
 from .errors import DegenerateFit
 from .weeding import (DEFAULT_COARSE_ITERATIONS, DEFAULT_ITERATIONS, WeedParams,
                       weed_parallel)
@@ -156,7 +156,7 @@ def fit_matches_homography(matches, width: int, height: int):
     if n < 4:
         raise ValueError("need at least 4 point pairs")
     hm = torch.empty((3, 3), dtype=torch.float64, device=m.device)
-    e = engine(1, 1, dev)
+    e = engine_for_rows(n, dev)
     _native.check(_native.lib().hdr_fit_matches_homography(e.handle, ptr(m), n, width, height,
                                                            ptr(hm)), "fit_matches_homography")
     return out(hm, as_torch)

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .engine import device_of, engine, ptr, to_dev
+from .engine import device_of, engine_for_rows, ptr, to_dev
 
 DEFAULT_ITERATIONS = 256
 DEFAULT_COARSE_ITERATIONS = 64
@@ -62,10 +62,7 @@ def weed(matches, image_size, params: WeedParams) -> WeedResult:
     kept = torch.empty((n,), dtype=torch.int64, device=m.device)
     witness = torch.zeros((n,), dtype=torch.int64, device=m.device)
     nk = ctypes.c_int32(0)
-    e = engine(1, 1, dev)
-    if e.width * e.height < n:  # the weed workspace scales with the tile count
-        e = engine(max(e.width, 16 * int(math.ceil(math.sqrt(n))) + 16),
-                   max(e.height, 16 * int(math.ceil(math.sqrt(n))) + 16), dev)
+    e = engine_for_rows(n, dev)  # the weed workspace scales with the tile count
     delta = -1 if params.delta is None else int(params.delta)
     _native.check(_native.lib().hdr_weed(e.handle, ptr(m), n, width, height, params.iterations,
                                          float(params.eps), int(params.seed), delta, ptr(kept),

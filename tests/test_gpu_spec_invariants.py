@@ -1,0 +1,149 @@
+"""The reference SPEC's invariants (SPEC.md "Invariants & Properties" of the
+image, matcher, geometry, weeding, densify and fusion sections), checked on
+the GPU path with hypothesis-generated inputs. Property tests complement the
+oracle parity tests: they hold for inputs no golden vector covers."""
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from oracle import hdr_oracle as O
+from paper_1504_01441_b200 import densify, fusion, geometry, image, matcher, pipeline, weeding
+
+pytestmark = pytest.mark.gpu
+SETTINGS = settings(max_examples=12, deadline=None, derandomize=True,
+                    suppress_health_check=[HealthCheck.function_scoped_fixture])
+
+
+def rng_image(seed, h, w, c=None, scale=1.0):
+    r = np.random.default_rng(seed)
+    shape = (h, w) if c is None else (h, w, c)
+    return (r.random(shape) * scale).astype(np.float32)
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(1, 90), w=st.integers(1, 90),
+       q=st.integers(0, 3))
+def test_rect_sum_equals_direct_summation(cuda, seed, h, w, q):
+    """SPEC image invariant: rect_sum = direct summation within 1e-9 relative."""
+    img = rng_image(seed, h, w)
+    t = image.integral(img)
+    r = np.random.default_rng(seed + 1)
+    for _ in range(4):
+        y0, y1 = sorted(r.integers(0, h + 1, 2))
+        x0, x1 = sorted(r.integers(0, w + 1, 2))
+        direct = float(img[y0:y1, x0:x1].astype(np.float64).sum())
+        got = float(image.rect_sum(t, x0, y0, x1, y1))
+        assert abs(got - direct) <= 1e-9 * max(1.0, abs(direct))
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(4, 120), w=st.integers(4, 120))
+def test_match_histogram_idempotent_to_one_bin(cuda, seed, h, w):
+    src, ref = rng_image(seed, h, w), rng_image(seed + 7, h, w) ** 2
+    once = image.match_histogram(src, ref)
+    twice = image.match_histogram(once, ref)
+    assert np.abs(twice - once).max() <= 1.0 / 255.0 + 1e-7
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), c=st.sampled_from([0.125, 0.25, 0.5]),
+       a=st.sampled_from([0.5, 2.0]))
+def test_cornerness_shift_and_scale(cuda, seed, c, a):
+    """SPEC matcher invariants: C(img + c) = C(img) and C(a img) = a C(img).
+    On a 2^-10 lattice the shift and the power-of-two scale are exact in f32,
+    so the quadrant differences -- and with them corners and scores -- carry
+    over exactly (threshold scaled with a)."""
+    img = (np.round(rng_image(seed, 200, 256, scale=0.4) * 1024) / 1024).astype(np.float32)
+    base = matcher.detect_corners(img, threshold=4.0 / 255.0)
+    shifted = matcher.detect_corners((img + np.float32(c)).astype(np.float32), threshold=4.0 / 255.0)
+    np.testing.assert_array_equal(base, shifted)
+    scaled = matcher.detect_corners((img * np.float32(a)).astype(np.float32),
+                                    threshold=a * 4.0 / 255.0)
+    np.testing.assert_array_equal(base[:, :2], scaled[:, :2])
+    np.testing.assert_array_equal(scaled[:, 2], a * base[:, 2])
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), n=st.integers(4, 200))
+def test_inliers_monotone_in_eps(cuda, seed, n):
+    r = np.random.default_rng(seed)
+    ref = r.uniform(-1, 1, (n, 2))
+    H = np.array([[1.01, 0.02, 0.01], [-0.01, 0.99, -0.02], [0.01, 0.0, 1.0]])
+    src = O.apply_homography(H, ref) if hasattr(O, "apply_homography") else None
+    if src is None:
+        p = np.c_[ref, np.ones(n)] @ H.T
+        src = p[:, :2] / p[:, 2:]
+    src = src + r.normal(0, 0.01, src.shape)
+    masks = [np.asarray(geometry.inlier_mask(H, ref, src, eps)) for eps in (0.005, 0.01, 0.02, 0.05)]
+    for a, b in zip(masks, masks[1:]):
+        assert not np.any(a & ~b)
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), n=st.integers(8, 300), frac=st.floats(0.3, 1.0))
+def test_weed_subset_and_delta_soundness(cuda, seed, n, frac):
+    """SPEC weeding invariants: M is a subset of the matches and every kept
+    match belongs to an inlier set larger than delta (its witness count)."""
+    r = np.random.default_rng(seed)
+    xr = r.uniform(20, 620, (n, 2))
+    good = r.random(n) < frac
+    xs = xr + np.array([3.0, -2.0])
+    xs[~good] = r.uniform(20, 620, (int((~good).sum()), 2))
+    m = np.c_[xr, xs, r.random(n)]
+    p = weeding.WeedParams(iterations=64, seed=seed)
+    res = weeding.weed(m, (640, 480), p)
+    kept = np.asarray(res.kept)
+    assert np.all((kept >= 0) & (kept < n)) and np.all(np.diff(kept) > 0)
+    delta = weeding.default_delta(n)
+    assert np.all(np.asarray(res.witness)[kept] > delta)
+    o = O.weed(m, 640, 480, 64, p.eps, seed)
+    assert np.array_equal(kept, o[0])
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(2, 150), w=st.integers(2, 150),
+       v=st.floats(-5, 5))
+def test_dt_filter_preserves_constants(cuda, seed, h, w, v):
+    guide = rng_image(seed, h, w)
+    out = densify.dt_filter(guide, np.full((h, w), v))
+    assert np.abs(np.asarray(out) - v).max() <= 1e-5 * max(1.0, abs(v))
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), m=st.integers(0, 30))
+def test_densify_flow_finite_and_exact_on_common_flow(cuda, seed, m):
+    """SPEC densify invariants: finite everywhere (also with no matches) and
+    equal to the common flow at every corner pixel when all corners share one
+    flow value."""
+    h, w = 96, 128
+    r = np.random.default_rng(seed)
+    guide = rng_image(seed, h, w)
+    xr = np.c_[r.integers(0, w, m), r.integers(0, h, m)].astype(np.float64)
+    mt = np.c_[xr, xr + np.array([5.0, 2.0]), r.random(m)] if m else np.zeros((0, 5))
+    maps = densify.build_sparse_maps(mt, w, h)
+    flow = densify.densify_flow(guide, maps)
+    assert np.isfinite(flow).all()
+    for x, y in xr.astype(int):
+        np.testing.assert_allclose(flow[y, x], [5.0, 2.0], rtol=0, atol=1e-5)
+
+
+@SETTINGS
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(8, 80), w=st.integers(8, 80))
+def test_fusion_weights_and_output_range(cuda, seed, h, w):
+    """SPEC fusion invariants: normalised weights sum to 1, output in [0, 1],
+    monotone trust (lower SSIM never raises the source weight), and fusing
+    identical frames returns the frame."""
+    ref, warped = rng_image(seed, h, w, 3), rng_image(seed + 1, h, w, 3)
+    s_hi = np.random.default_rng(seed).uniform(0, 1, (h, w)).astype(np.float32)
+    s_lo = (s_hi * np.float32(0.5)).astype(np.float32)
+    valid = np.ones((h, w), bool)
+    wr, ws = fusion.fusion_weights(ref, warped, s_hi, valid)
+    assert np.abs(wr + ws - 1.0).max() < 1e-6
+    _, ws_lo = fusion.fusion_weights(ref, warped, s_lo, valid)
+    assert np.all(ws_lo <= ws + 1e-7)
+    comp = fusion.fuse(ref, warped, s_hi, valid)
+    assert np.isfinite(comp).all() and comp.min() >= 0.0 and comp.max() <= 1.0
+    same = pipeline.fuse_stack([ref, ref, ref], [s_hi, s_lo], [valid, valid])
+    assert np.abs(same - ref).max() < 1e-4

@@ -147,3 +147,96 @@ def test_fusion_weights_and_output_range(cuda, seed, h, w):
     assert np.isfinite(comp).all() and comp.min() >= 0.0 and comp.max() <= 1.0
     same = pipeline.fuse_stack([ref, ref, ref], [s_hi, s_lo], [valid, valid])
     assert np.abs(same - ref).max() < 1e-4
+
+
+@settings(max_examples=8, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(30, 90), w=st.integers(30, 90),
+       radius=st.integers(1, 12), patch=st.sampled_from([3, 5, 9, 21]), quant=st.booleans())
+def test_ssd_match_equals_bruteforce(cuda, seed, h, w, radius, patch, quant):
+    """SPEC matcher invariant: ssd_match equals the brute-force oracle on
+    random configurations (quantised images force exact score ties)."""
+    r = np.random.default_rng(seed)
+    ref, src = rng_image(seed, h, w), rng_image(seed + 3, h, w)
+    if quant:
+        ref, src = (np.round(ref * 4) / 4).astype(np.float32), (np.round(src * 4) / 4).astype(np.float32)
+    hp = patch // 2
+    pts = []
+    for _ in range(25):
+        xr, yr = r.integers(hp, w - hp), r.integers(hp, h - hp)
+        pts.append((xr, yr, r.integers(-5, w + 5), r.integers(-5, h + 5)))
+    got, found = matcher.ssd_match_batch(ref, src, pts, radius, patch)
+    for (xr, yr, xi, yi), g, f in zip(pts, got, found):
+        want = O.ssd_search(ref, src, (xr, yr), (xi, yi), radius, patch)
+        assert f == (want is not None)
+        if want is not None:
+            assert (int(g[0]), int(g[1])) == (want[0], want[1])
+            assert abs(g[2] - want[2]) <= 1e-12 * max(1.0, want[2])
+
+
+@settings(max_examples=10, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(1, 70), w=st.integers(1, 70),
+       amp=st.floats(0.0, 40.0))
+def test_warp_bit_exact_random_flow(cuda, seed, h, w, amp):
+    """warp_image (densify.py:145-174) is bit-exact for arbitrary flows,
+    including samples far outside the frame (clamped, marked invalid)."""
+    src = rng_image(seed, h, w, 3)
+    flow = (np.random.default_rng(seed).normal(size=(h, w, 2)) * amp).astype(np.float32)
+    got, valid = densify.warp_image(src, flow)
+    want, wvalid = O.warp_image(src, flow)
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(valid, wvalid)
+
+
+@settings(max_examples=8, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(2, 140), w=st.integers(2, 140),
+       levels=st.integers(0, 6))
+def test_fuse_random_sizes_match_oracle(cuda, seed, h, w, levels):
+    """fusion.fuse at odd sizes and explicit level counts (reflect edges at
+    every level) within the 1e-3 composite bar."""
+    ref, warped = rng_image(seed, h, w, 3), rng_image(seed + 1, h, w, 3)
+    ssim = np.random.default_rng(seed).uniform(-0.5, 1, (h, w)).astype(np.float32)
+    valid = np.random.default_rng(seed + 2).random((h, w)) > 0.2
+    lv = None if levels == 0 else levels
+    got = fusion.fuse(ref, warped, ssim, valid, lv)
+    want = O.fuse(ref, warped, ssim, valid.astype(np.float32), lv)
+    assert np.abs(got - want).max() < 1e-3
+
+
+@settings(max_examples=10, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(100, 900), w=st.integers(100, 900))
+def test_pyramid_random_sizes_bit_exact(cuda, seed, h, w):
+    """SPEC image invariant: level dims halve exactly (floor) with the
+    retention rule; values bit-exact (separately rounded f32)."""
+    img = rng_image(seed, h, w)
+    got = image.build_pyramid(img)
+    want = O.pyramid(img)
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(np.asarray(a), b)
+
+
+@settings(max_examples=6, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), w=st.integers(120, 360), h=st.integers(120, 300),
+       stops=st.sampled_from([1.0, 2.0, 3.0]), rot=st.sampled_from([0.0, 0.4]))
+def test_register_and_fuse_random_scenes(cuda, seed, w, h, stops, rot):
+    """End to end on random scene recipes and sizes: the same verdict as the
+    oracle (RegistrationError or not), identical level counts and match
+    coordinates, composite within 1e-3."""
+    from paper_1504_01441_b200 import synth
+    from paper_1504_01441_b200.errors import RegistrationError
+    st_ = synth.synth_stack(synth.working_spec(w, h, stops=stops, rotation_deg=rot), seed)
+    try:
+        want = O.register_and_fuse(st_.ref, st_.src)
+    except O.RegistrationError:
+        with pytest.raises(RegistrationError):
+            pipeline.register_and_fuse(st_.ref, st_.src)
+        return
+    got = pipeline.register_and_fuse(st_.ref, st_.src)
+    assert got.level_counts == want.level_counts
+    np.testing.assert_array_equal(got.matches[:, :4], want.matches[:, :4])
+    assert np.abs(got.composite - want.composite).max() < 1e-3

@@ -240,3 +240,32 @@ def test_register_and_fuse_random_scenes(cuda, seed, w, h, stops, rot):
     assert got.level_counts == want.level_counts
     np.testing.assert_array_equal(got.matches[:, :4], want.matches[:, :4])
     assert np.abs(got.composite - want.composite).max() < 1e-3
+
+
+@settings(max_examples=12, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(1, 67), w=st.integers(1, 67))
+def test_luminance_and_histogram_match_any_size(cuda, seed, h, w):
+    """image.luminance / match_histogram bit-exact at every size (pixel
+    counts not a multiple of the kernels' 4-pixel vectors included)."""
+    rgb, rgb2 = rng_image(seed, h, w, 3), rng_image(seed + 5, h, w, 3) * np.float32(0.7)
+    lum = image.luminance(rgb)
+    np.testing.assert_array_equal(lum, O.luminance(rgb))
+    lum2 = O.luminance(rgb2)
+    np.testing.assert_array_equal(image.match_histogram(lum2, lum), O.match_histogram(lum2, lum))
+
+
+@settings(max_examples=10, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(1, 80), w=st.integers(1, 80),
+       window=st.sampled_from([3, 7, 11, 15]))
+def test_ssim_and_quality_any_size(cuda, seed, h, w, window):
+    """fusion.ssim_map (reflect edges, windows larger than the image) within
+    1e-4 and quality_weights within 1e-5 relative of the oracle."""
+    a, b = rng_image(seed, h, w), rng_image(seed + 9, h, w)
+    got = fusion.ssim_map(a, b, window, 1.5)
+    want = O.ssim_map(a, b, window, 1.5)
+    assert np.abs(np.asarray(got) - want).max() < 1e-4
+    img = rng_image(seed + 2, h, w, 3)
+    q, oq = np.asarray(fusion.quality_weights(img)), O.quality_weights(img)
+    assert np.abs(q - oq).max() <= 1e-5 * oq.max() + 1e-12

@@ -88,6 +88,7 @@ def device_of(*arrays) -> int:
     for a in arrays:
         if isinstance(a, torch.Tensor) and a.is_cuda:
             return a.device.index
+    _require_cuda()
     return torch.cuda.current_device()
 
 

@@ -92,3 +92,33 @@ def test_params_default_matches_dataclass():
     ref = PipelineParams().to_native()
     for name, _ in _native.HdrParams._fields_:
         assert getattr(p, name) == getattr(ref, name), name
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No silent fallback: without libhdrb200.so the binding raises."""
+    monkeypatch.setattr(_native, "LIB_PATH", str(tmp_path / "absent.so"))
+    monkeypatch.setattr(_native, "_lib", None)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _native.lib()
+
+
+def test_no_cuda_fails_loudly(monkeypatch):
+    """Without a CUDA device the drop-in raises instead of computing on the CPU."""
+    import torch
+    from paper_1504_01441_b200 import engine, pipeline
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    img = np.zeros((120, 160, 3), np.float32)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        pipeline.register_and_fuse(img, img)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        engine.to_dev(img, torch.float32)
+
+
+def test_product_package_never_imports_the_oracle():
+    """oracle/ is test infrastructure only: no module of the product package
+    imports it."""
+    pkg = os.path.join(ROOT, "paper_1504_01441_b200")
+    for name in os.listdir(pkg):
+        if name.endswith(".py"):
+            text = open(os.path.join(pkg, name)).read()
+            assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, flags=re.M), name

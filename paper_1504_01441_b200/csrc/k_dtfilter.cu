@@ -750,7 +750,10 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
                     double c, int bw_log2, DtFlowOut fo) {
   __shared__ Aff<K> maps[kCT];           // [grp][col]
-  __shared__ Aff<K> ctaF[kMaxBw], ctaB[kMaxBw];  // per-column CTA totals (bw <= kMaxBw)
+  // per-column CTA totals read by the cluster peers, double-buffered by band
+  // parity: band b+2 reuses band b's buffer only after two cluster barriers,
+  // by which time every peer has read it, so bands need no closing barrier
+  __shared__ Aff<K> ctaF2[2][kMaxBw], ctaB2[2][kMaxBw];
   __shared__ double cin[kMaxBw][K], din[kMaxBw][K];
   __shared__ Aff<K> remote[kCL][kMaxBw];
   extern __shared__ __align__(16) double pfx[];
@@ -784,7 +787,10 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   if (PF) prefetch(blockIdx.y);
   // persistent: the grid holds as many clusters as can be co-resident and
   // each walks bands (no cluster-launch fragmentation between waves)
-  for (int band = blockIdx.y; band < nbands; band += gridDim.y) {
+  int parity = 0;
+  for (int band = blockIdx.y; band < nbands; band += gridDim.y, parity ^= 1) {
+  Aff<K>* ctaF = ctaF2[parity];
+  Aff<K>* ctaB = ctaB2[parity];
   const int x = (band << bw_log2) + col;
   const bool live = x < w;
   const int n = live ? nrows : 0;
@@ -912,8 +918,6 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
 #pragma unroll
     for (int k = 0; k < K; ++k) din[col][k] = D[k];
   }
-  // peers may still read ctaB; the matching wait is just before exit
-  cluster_arrive();
   __syncthreads();
   double D[K];
 #pragma unroll
@@ -973,8 +977,10 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
           for (int k = 0; k < K; ++k) stp(P, k, (int64_t)(r0 + j) * w + x, xv[k][j]);
     }
   }
-  cluster_wait();
   }
+  // no CTA may leave while a peer can still read its shared memory
+  cluster_arrive();
+  cluster_wait();
 }
 
 // co-resident clusters of a cluster-kernel instantiation (0 = query failed)

@@ -741,6 +741,42 @@ constexpr size_t cols_pf_smem() {
   return sizeof(double) * K * kSR * kCT + sizeof(float) * (kSR + 2) * kCT;
 }
 
+// Scan of the groups' affine maps inside a CTA (thread = (group, column),
+// lane = sub * bw + col): warp shuffles over the groups of a warp, then the
+// warps' totals through shared memory -- two block barriers per scan.
+// up: m becomes the inclusive prefix (groups above and this one) and ex the
+// exclusive prefix; !up: the same as suffixes (groups below).
+template <int K>
+__device__ __forceinline__ void scan_groups(Aff<K>& m, bool up, int bw_log2,
+                                            Aff<K> (*wsc)[kMaxBw], Aff<K>& ex) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int bw = 1 << bw_log2, col = lane & (bw - 1), sub = lane >> bw_log2, Gw = 32 >> bw_log2;
+  for (int off = 1; off < Gw; off <<= 1) {
+    Aff<K> o = shfl_aff(m, off << bw_log2, up);
+    if (up ? sub >= off : sub + off < Gw) m = compose(o, m);
+  }
+  Aff<K> e = shfl_aff(m, bw, up);  // exclusive within the warp
+  if (up ? sub == 0 : sub == Gw - 1) {
+    e.A = 1.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) e.B[k] = 0.0;
+  }
+  if (up ? sub == Gw - 1 : sub == 0) wsc[warp][col] = m;
+  __syncthreads();
+  Aff<K> pre;  // the other warps' totals, composed in sweep order
+  pre.A = 1.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) pre.B[k] = 0.0;
+  if (up) {
+    for (int q = 0; q < warp; ++q) pre = compose(pre, wsc[q][col]);
+  } else {
+    for (int q = nw - 1; q > warp; --q) pre = compose(pre, wsc[q][col]);
+  }
+  ex = compose(pre, e);
+  m = compose(pre, m);
+  __syncthreads();  // wsc is reused by the next scan
+}
+
 // PF: the band's samples arrive by cp.async into per-thread shared-memory
 // slots issued one band ahead (needs f64 planes and dynamic shared memory of
 // cols_pf_smem<K>()), so HBM reads of band b+1 overlap the link, apply and
@@ -749,7 +785,7 @@ template <int K, bool FINAL, bool PF>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 2 : 1)
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
                     double c, int bw_log2, DtFlowOut fo) {
-  __shared__ Aff<K> maps[kCT];           // [grp][col]
+  __shared__ Aff<K> wsc[kCT / 32][kMaxBw];  // per-warp totals of the group scans
   // per-column CTA totals read by the cluster peers, double-buffered by band
   // parity: band b+2 reuses band b's buffer only after two cluster barriers,
   // by which time every peer has read it, so bands need no closing barrier
@@ -845,23 +881,9 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   m.A = Pp;
 #pragma unroll
   for (int k = 0; k < K; ++k) m.B[k] = y0[k];
-  maps[threadIdx.x] = m;
-  __syncthreads();
-  for (int off = 1; off < G; off <<= 1) {
-    Aff<K> o = maps[grp >= off ? threadIdx.x - (off << bw_log2) : threadIdx.x];
-    __syncthreads();
-    if (grp >= off) { m = compose(o, m); maps[threadIdx.x] = m; }
-    __syncthreads();
-  }
+  Aff<K> ex;  // exclusive prefix of this group within the CTA
+  scan_groups<K>(m, true, bw_log2, wsc, ex);
   if (grp == G - 1) ctaF[col] = m;
-  Aff<K> ex;  // exclusive prefix of this group
-  if (grp > 0) {
-    ex = maps[threadIdx.x - bw];
-  } else {
-    ex.A = 1.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) ex.B[k] = 0.0;
-  }
   cl.sync();
   // gather the lower ranks' totals for this column (one remote load per thread)
   for (int q = grp; q < rank; q += G) remote[q][col] = *cl.map_shared_rank(&ctaF[col], q);
@@ -886,23 +908,9 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   m.A = Q;
 #pragma unroll
   for (int k = 0; k < K; ++k) m.B[k] = z0[k] + C[k] * R;
-  maps[threadIdx.x] = m;
-  __syncthreads();
-  for (int off = 1; off < G; off <<= 1) {
-    Aff<K> o = maps[grp + off < G ? threadIdx.x + (off << bw_log2) : threadIdx.x];
-    __syncthreads();
-    if (grp + off < G) { m = compose(o, m); maps[threadIdx.x] = m; }
-    __syncthreads();
-  }
+  Aff<K> sx;  // suffix from the groups below this one within the CTA
+  scan_groups<K>(m, false, bw_log2, wsc, sx);
   if (grp == 0) ctaB[col] = m;
-  Aff<K> sx;  // suffix from the next group down
-  if (grp + 1 < G) {
-    sx = maps[threadIdx.x + bw];
-  } else {
-    sx.A = 1.0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) sx.B[k] = 0.0;
-  }
   cl.sync();
   for (int q = rank + 1 + grp; q < kCL; q += G) remote[q][col] = *cl.map_shared_rank(&ctaB[col], q);
   __syncthreads();

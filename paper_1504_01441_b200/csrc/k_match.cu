@@ -37,6 +37,15 @@ __device__ __forceinline__ SsdKey shfl_key(const SsdKey& k, int off) {
   return o;
 }
 
+#ifndef HDR_SSD_STRIP
+#define HDR_SSD_STRIP 4
+#endif
+#ifndef HDR_SSD_THREADS
+#define HDR_SSD_THREADS 128
+#endif
+constexpr int kSsdStrip = HDR_SSD_STRIP;      // candidate windows per thread (one row)
+constexpr int kSsdThreads = HDR_SSD_THREADS;  // threads per corner
+
 // Block-cooperative exhaustive search; returns true on thread 0 with the
 // winner in *best. Window bounds must already be clamped and non-empty.
 __device__ bool ssd_search(const float* __restrict__ ref, const float* __restrict__ src,
@@ -77,31 +86,37 @@ __device__ bool ssd_search(const float* __restrict__ ref, const float* __restric
   __syncthreads();
   SsdKey k;
   k.score = INFINITY; k.d2 = 0x7fffffffffffffffLL; k.cy = 0x7fffffff; k.cx = 0x7fffffff;
-  // each thread sweeps a 1x4 strip of candidate windows, sliding a 4-wide
+  // each thread sweeps a 1xSW strip of candidate windows, sliding an SW-wide
   // register window along the source row: per tap one shared load of S and
-  // one (broadcast) of T feed four FMAs. Every window keeps the same
-  // row-major tap order, so identical windows tie exactly as in the reference.
-  int nstrip = (nx + 3) >> 2;
+  // one (broadcast) of T feed SW FMAs. Every window keeps the same row-major
+  // tap order, so identical windows tie exactly as in the reference.
+  constexpr int SW = kSsdStrip;
+  int nstrip = (nx + SW - 1) / SW;
   for (int t = threadIdx.x; t < nstrip * ny; t += blockDim.x) {
-    int oy = t / nstrip, ox = (t - oy * nstrip) * 4;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int oy = t / nstrip, ox = (t - oy * nstrip) * SW;
+    double acc[SW];
+#pragma unroll
+    for (int j = 0; j < SW; ++j) acc[j] = 0.0;
     for (int ky = 0; ky < patch; ++ky) {
       const double* srow = S + (oy + ky) * sw + ox;
       const double* trow = T + ky * patch;
-      double w0 = srow[0], w1 = srow[1], w2 = srow[2];
+      double win[SW];
+#pragma unroll
+      for (int j = 0; j < SW - 1; ++j) win[j] = srow[j];
       for (int kx = 0; kx < patch; ++kx) {
-        double w3 = srow[kx + 3];
+        win[SW - 1] = srow[kx + SW - 1];
         double tv = trow[kx];
-        double d0 = w0 - tv, d1 = w1 - tv, d2 = w2 - tv, d3 = w3 - tv;
-        acc[0] = fma(d0, d0, acc[0]);
-        acc[1] = fma(d1, d1, acc[1]);
-        acc[2] = fma(d2, d2, acc[2]);
-        acc[3] = fma(d3, d3, acc[3]);
-        w0 = w1; w1 = w2; w2 = w3;
+#pragma unroll
+        for (int j = 0; j < SW; ++j) {
+          double d = win[j] - tv;
+          acc[j] = fma(d, d, acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < SW - 1; ++j) win[j] = win[j + 1];
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < SW; ++j) {
       if (ox + j >= nx) break;
       SsdKey cand;
       cand.score = acc[j];
@@ -221,7 +236,7 @@ void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref, con
                       int w, int h, const double* hpred, int radius, int patch, MatchRow* rows,
                       uint8_t* flags, cudaStream_t s) {
   size_t bytes = ssd_smem(radius, patch);
-  ssd_tiles_kernel<<<ntiles, 128, bytes, s>>>(tiles, ref, src, w, h, hpred, radius, patch, rows,
+  ssd_tiles_kernel<<<ntiles, kSsdThreads, bytes, s>>>(tiles, ref, src, w, h, hpred, radius, patch, rows,
                                               flags);
 }
 
@@ -230,7 +245,7 @@ void launch_ssd_points(const float* ref, const float* src, int w, int h, const i
                        cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = ssd_smem(radius, patch);
-  ssd_points_kernel<<<n, 128, bytes, s>>>(ref, src, w, h, pts, radius, patch, out, found);
+  ssd_points_kernel<<<n, kSsdThreads, bytes, s>>>(ref, src, w, h, pts, radius, patch, out, found);
 }
 
 // ordered compaction of per-slot rows (tile order is the reference's corner

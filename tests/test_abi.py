@@ -122,3 +122,16 @@ def test_product_package_never_imports_the_oracle():
         if name.endswith(".py"):
             text = open(os.path.join(pkg, name)).read()
             assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, flags=re.M), name
+
+
+def test_options_and_probe_arguments_validated():
+    """hdr_set_option rejects unknown names; kernel probes validate their
+    family and launch count before touching a context (no GPU work)."""
+    lib = _native.lib()
+    assert lib.hdr_set_option(b"no_such_option", 1) == _native.HDR_ERR_INVALID
+    assert "unknown option" in _native.last_error()
+    assert lib.hdr_set_option(None, 1) == _native.HDR_ERR_INVALID
+    # null context -> invalid, whatever the other arguments
+    assert lib.hdr_ctx_set_kernel_probes(None, 0, None, 0) == _native.HDR_ERR_INVALID
+    assert lib.hdr_ctx_set_probes(None, None) == _native.HDR_ERR_INVALID
+    assert lib.hdr_ctx_destroy(None) == _native.HDR_OK

@@ -280,6 +280,18 @@ int hdr_fuse_stack(hdr_ctx* ctx, int32_t n, const float* const* frames, const fl
 int hdr_fusion_weights(hdr_ctx* ctx, const float* ref, const float* warped, const float* ssim,
                        const uint8_t* valid, int32_t width, int32_t height, float* w_ref,
                        float* w_src);
+/* fusion._pyr_down (fusion.py:85-86): in (h, w, ch) f64 -> out
+ * (ceil(h/2), ceil(w/2), ch): 5-tap reflect blur, then [::2, ::2]. */
+int hdr_pyr_down(hdr_ctx* ctx, const double* in, int32_t width, int32_t height, int32_t ch,
+                 double* out);
+/* fusion._pyr_up (fusion.py:89-93): in (ch_h, ch_w, ch) f64, the ceil-half
+ * of (height, width) -> out (height, width, ch): zero-insert, 2x-gain blur.
+ * With base (height, width, ch): out = base - up for sign < 0 (a
+ * laplacian_pyramid level, fusion.py:103-107) or base + up for sign > 0 (a
+ * collapse_pyramid step, fusion.py:110-114); base may alias out. */
+int hdr_pyr_up(hdr_ctx* ctx, const double* in, int32_t coarse_width, int32_t coarse_height,
+               int32_t ch, int32_t width, int32_t height, const double* base, int32_t sign,
+               double* out);
 /* fusion.fuse (fusion.py:135-157): levels <= 0 selects the default. */
 int hdr_fuse(hdr_ctx* ctx, const float* ref, const float* warped, const float* ssim,
              const uint8_t* valid, int32_t width, int32_t height, int32_t levels,

@@ -84,6 +84,8 @@ SIGNATURES = {
     "hdr_quality_weights": (_I, [_P, _P, _I, _I, _P]),
     "hdr_fuse": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _P]),
     "hdr_fusion_weights": (_I, [_P, _P, _P, _P, _P, _I, _I, _P, _P]),
+    "hdr_pyr_down": (_I, [_P, _P, _I, _I, _I, _P]),
+    "hdr_pyr_up": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _P]),
     "hdr_fuse_stack": (_I, [_P, _I, _P, _P, _P, _I, _I, _I, _P]),
     "hdr_register_and_fuse_stack": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "hdr_decode_image": (_I, [_P, _P, _I, _I, _I, _I, _P]),

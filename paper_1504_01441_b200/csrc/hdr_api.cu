@@ -1430,6 +1430,23 @@ extern "C" int hdr_fusion_weights(hdr_ctx* c, const float* ref, const float* war
   return check_launch();
 }
 
+extern "C" int hdr_pyr_down(hdr_ctx* c, const double* in, int32_t w, int32_t h, int32_t ch,
+                            double* out) {
+  NEED(c && in && out, "null argument");
+  NEED(w >= 1 && h >= 1 && ch >= 1, "empty image");
+  launch_pyr_down(in, w, h, ch, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_pyr_up(hdr_ctx* c, const double* in, int32_t cw, int32_t cht, int32_t ch,
+                          int32_t w, int32_t h, const double* base, int32_t sign, double* out) {
+  NEED(c && in && out, "null argument");
+  NEED(w >= 1 && h >= 1 && ch >= 1 && cw == (w + 1) / 2 && cht == (h + 1) / 2,
+       "coarse shape must be the ceil-half of the fine shape");
+  launch_pyr_up(in, cw, cht, ch, out, w, h, base, sign, c->stream);
+  return check_launch();
+}
+
 extern "C" int hdr_fuse(hdr_ctx* c, const float* ref, const float* warped, const float* ssim,
                         const uint8_t* valid, int32_t w, int32_t h, int32_t levels, float* out) {
   NEED(c && ref && warped && ssim && valid && out, "null argument");

@@ -182,6 +182,10 @@ void launch_quality(const float* rgb, int w, int h, float* out, cudaStream_t s);
 void launch_fusion_weights(const float* ref, const float* warped, const float* ssim,
                            const uint8_t* valid, int w, int h, float* wr, float* ws,
                            cudaStream_t s);
+// fusion._pyr_down / _pyr_up twins (f64, (h, w, c) interleaved)
+void launch_pyr_down(const double* in, int w, int h, int c, double* out, cudaStream_t s);
+void launch_pyr_up(const double* in, int cw, int ch, int c, double* out, int w, int h,
+                   const double* base, int sign, cudaStream_t s);
 // ---- k_merge.cu: Laplacian-pyramid fusion of NF = 2..4 frames (frame 0 is
 // the reference); level k >= 1 holds 4*NF planar channels (RGB of every
 // frame, then the NF weights) in g[k] and the 3 collapse channels in c[k].

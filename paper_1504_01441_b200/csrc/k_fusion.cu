@@ -298,3 +298,81 @@ void launch_fusion_weights(const float* ref, const float* warped, const float* s
 }
 
 }  // namespace hdr
+
+namespace hdr {
+
+// ---------------------------------------------------------------- pyramid twins
+// fusion._blur5 / _pyr_down / _pyr_up (fusion.py:80-93) in f64 on (h, w, c)
+// interleaved arrays, for the stage-level gaussian_pyramid /
+// laplacian_pyramid / collapse_pyramid APIs (the pair path fuses these into
+// k_merge.cu's kernels). scipy's symmetric correlate1d accumulates
+// x0*w0, then (x-2 + x+2)*w2, then (x-1 + x+1)*w1, each op rounded
+// separately; that order is kept so the results match bit for bit.
+__device__ __forceinline__ double sym5(double xm2, double xm1, double x0, double xp1, double xp2,
+                                       double w0, double w1, double w2) {
+  double t = dmul(x0, w0);
+  t = dadd(t, dmul(dadd(xm2, xp2), w2));
+  return dadd(t, dmul(dadd(xm1, xp1), w1));
+}
+
+// out (oh, ow, c) = blur5(in)[::2, ::2]
+__global__ void pyr_down_kernel(const double* __restrict__ in, int w, int h, int c,
+                                double* __restrict__ out, int ow, int oh) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)ow * oh * c) return;
+  int k = (int)(i % c);
+  int64_t p = i / c;
+  int x = (int)(p % ow), y = (int)(p / ow);
+  double v[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {  // axis 0 at row 2y for the 5 columns axis 1 reads
+    int xx = reflect_index(2 * x - 2 + j, w);
+    double r[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) r[q] = in[((int64_t)reflect_index(2 * y - 2 + q, h) * w + xx) * c + k];
+    v[j] = sym5(r[0], r[1], r[2], r[3], r[4], 6.0 / 16, 4.0 / 16, 1.0 / 16);
+  }
+  out[i] = sym5(v[0], v[1], v[2], v[3], v[4], 6.0 / 16, 4.0 / 16, 1.0 / 16);
+}
+
+// out (h, w, c) = 2x-gain blur5 of in (ch, cw, c) zero-inserted on the fine
+// grid; with `base`: out = base - up (laplacian_pyramid) for sign < 0, or
+// base + up (collapse_pyramid) for sign > 0, one rounding like numpy's
+__global__ void pyr_up_kernel(const double* __restrict__ in, int cw, int ch, int c,
+                              double* __restrict__ out, int w, int h,
+                              const double* __restrict__ base, int sign) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)w * h * c) return;
+  int k = (int)(i % c);
+  int64_t p = i / c;
+  int x = (int)(p % w), y = (int)(p / w);
+  auto up = [&](int yy, int xx) -> double {  // zero-inserted fine sample
+    return ((yy | xx) & 1) ? 0.0 : in[((int64_t)(yy >> 1) * cw + (xx >> 1)) * c + k];
+  };
+  double v[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    int xx = reflect_index(x - 2 + j, w);
+    double r[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) r[q] = up(reflect_index(y - 2 + q, h), xx);
+    v[j] = sym5(r[0], r[1], r[2], r[3], r[4], 12.0 / 16, 8.0 / 16, 2.0 / 16);
+  }
+  double u = sym5(v[0], v[1], v[2], v[3], v[4], 12.0 / 16, 8.0 / 16, 2.0 / 16);
+  out[i] = !base ? u : (sign < 0 ? dsub(base[i], u) : dadd(base[i], u));
+}
+
+void launch_pyr_down(const double* in, int w, int h, int c, double* out, cudaStream_t s) {
+  int ow = (w + 1) / 2, oh = (h + 1) / 2;
+  int64_t n = (int64_t)ow * oh * c;
+  if (n > 0) pyr_down_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, w, h, c, out, ow, oh);
+}
+
+void launch_pyr_up(const double* in, int cw, int ch, int c, double* out, int w, int h,
+                   const double* base, int sign, cudaStream_t s) {
+  int64_t n = (int64_t)w * h * c;
+  if (n > 0)
+    pyr_up_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, cw, ch, c, out, w, h, base, sign);
+}
+
+}  // namespace hdr

@@ -66,6 +66,62 @@ def fusion_weights(ref, warped, ssim, valid):
     return out(wr.double(), as_torch), out(ws.double(), as_torch)
 
 
+def _as_hwc(t: torch.Tensor) -> torch.Tensor:
+    return t.unsqueeze(-1) if t.dim() == 2 else t
+
+
+def _pyr_down(t: torch.Tensor) -> torch.Tensor:
+    """fusion.py:85-86 on a float64 CUDA tensor (h, w[, c])."""
+    x = _as_hwc(t).contiguous()
+    h, w, c = x.shape
+    res = torch.empty(((h + 1) // 2, (w + 1) // 2, c), dtype=torch.float64, device=x.device)
+    e = engine(1, 1, x.device.index)
+    _native.check(_native.lib().hdr_pyr_down(e.handle, ptr(x), w, h, c, ptr(res)), "pyr_down")
+    return res if t.dim() == 3 else res[..., 0]
+
+
+def _pyr_up(t: torch.Tensor, shape, base: torch.Tensor | None = None, sign: int = 0) -> torch.Tensor:
+    """fusion.py:89-93: zero-insert into `shape`, 2x-gain blur; with `base`,
+    base - up (sign < 0) or base + up (sign > 0) in the same kernel."""
+    x = _as_hwc(t).contiguous()
+    ch_, cw, c = x.shape
+    h, w = int(shape[0]), int(shape[1])
+    res = torch.empty((h, w, c), dtype=torch.float64, device=x.device)
+    b = None if base is None else _as_hwc(base).contiguous()
+    e = engine(1, 1, x.device.index)
+    _native.check(_native.lib().hdr_pyr_up(e.handle, ptr(x), cw, ch_, c, w, h, ptr(b), int(sign),
+                                           ptr(res)), "pyr_up")
+    return res if t.dim() == 3 else res[..., 0]
+
+
+def gaussian_pyramid(img, levels: int) -> list:
+    """fusion.py:96-100 — float64 levels, 5-tap reflect blur + [::2, ::2]."""
+    as_torch = is_torch(img)
+    g = [to_dev(img, torch.float64, device_of(img))]
+    while len(g) < levels and min(g[-1].shape[:2]) >= 2:
+        g.append(_pyr_down(g[-1]))
+    return [out(x, as_torch) for x in g]
+
+
+def laplacian_pyramid(img, levels: int) -> list:
+    """fusion.py:103-107."""
+    as_torch = is_torch(img)
+    g = gaussian_pyramid(to_dev(img, torch.float64, device_of(img)), levels)
+    laps = [_pyr_up(g[i + 1], g[i].shape, g[i], -1) for i in range(len(g) - 1)] + [g[-1]]
+    return [out(x, as_torch) for x in laps]
+
+
+def collapse_pyramid(laps) -> object:
+    """fusion.py:110-114."""
+    as_torch = is_torch(*laps)
+    dev = device_of(*laps)
+    ts = [to_dev(x, torch.float64, dev) for x in laps]
+    res = ts[-1]
+    for lap in ts[-2::-1]:
+        res = _pyr_up(res, lap.shape, lap, +1)
+    return out(res, as_torch)
+
+
 def default_fusion_levels(height: int, width: int) -> int:
     """fusion.py:131-132."""
     return max(1, int(np.floor(np.log2(min(height, width)))) - 1)

@@ -269,3 +269,21 @@ def test_ssim_and_quality_any_size(cuda, seed, h, w, window):
     img = rng_image(seed + 2, h, w, 3)
     q, oq = np.asarray(fusion.quality_weights(img)), O.quality_weights(img)
     assert np.abs(q - oq).max() <= 1e-5 * oq.max() + 1e-12
+
+
+@settings(max_examples=12, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(seed=st.integers(0, 10 ** 6), h=st.integers(1, 70), w=st.integers(1, 70),
+       c=st.sampled_from([0, 1, 3]), levels=st.integers(1, 8))
+def test_pyramid_functions_bit_exact(cuda, seed, h, w, c, levels):
+    """fusion.gaussian_pyramid / laplacian_pyramid / collapse_pyramid match
+    the reference's scipy arithmetic bit for bit (f64, symmetric correlate
+    order), for grey and colour arrays of any size."""
+    x = np.random.default_rng(seed).random((h, w) if c == 0 else (h, w, c))
+    for got, want in zip(fusion.gaussian_pyramid(x, levels), O.gaussian_pyramid(x, levels)):
+        np.testing.assert_array_equal(got, want)
+    laps, olaps = fusion.laplacian_pyramid(x, levels), O.laplacian_pyramid(x, levels)
+    assert len(laps) == len(olaps)
+    for got, want in zip(laps, olaps):
+        np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(fusion.collapse_pyramid(olaps), O.collapse(olaps))

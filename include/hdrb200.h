@@ -187,6 +187,11 @@ int hdr_build_pyramid(hdr_ctx* ctx, const float* img, int32_t width, int32_t hei
 /* image.integral (image.py:32-44): (h+1, w+1) float64 summed-area table. */
 int hdr_integral(hdr_ctx* ctx, const float* img, int32_t width, int32_t height,
                  double* table);
+/* matcher.cornerness (matcher.py:51-61) at n points xy (n, 2) int32 of an
+ * image whose (h+1, w+1) f64 integral table is given (callers check the
+ * half-neighbourhood bounds): out (n, 2) = (cornerness, min contrast). */
+int hdr_cornerness(hdr_ctx* ctx, const double* table, int32_t width, int32_t height,
+                   const int32_t* xy, int32_t n, int32_t half, double* out);
 /* matcher.detect_corners (matcher.py:64-105): rows (x, y, score) in tile
  * order; *count (host) receives n. corners needs room for ntiles rows. */
 int hdr_detect_corners(hdr_ctx* ctx, const float* lum, int32_t width, int32_t height,

@@ -66,6 +66,7 @@ SIGNATURES = {
     "hdr_match_histogram": (_I, [_P, _P, _I64, _P, _I64, _I, _P]),
     "hdr_build_pyramid": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "hdr_integral": (_I, [_P, _P, _I, _I, _P]),
+    "hdr_cornerness": (_I, [_P, _P, _I, _I, _P, _I, _I, _P]),
     "hdr_detect_corners": (_I, [_P, _P, _I, _I, _I, _D, _I, _P, _P]),
     "hdr_ssd_match": (_I, [_P, _P, _P, _I, _I, _P, _I, _I, _I, _P, _P]),
     "hdr_match_level": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P]),

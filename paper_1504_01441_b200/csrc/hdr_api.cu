@@ -1430,6 +1430,14 @@ extern "C" int hdr_fusion_weights(hdr_ctx* c, const float* ref, const float* war
   return check_launch();
 }
 
+extern "C" int hdr_cornerness(hdr_ctx* c, const double* table, int32_t w, int32_t h,
+                              const int32_t* xy, int32_t n, int32_t half, double* out) {
+  NEED(c && table && xy && out, "null argument");
+  NEED(half >= 1 && w >= 1 && h >= 1, "bad arguments");
+  launch_cornerness(table, w + 1, xy, n, half, out, c->stream);
+  return check_launch();
+}
+
 extern "C" int hdr_pyr_down(hdr_ctx* c, const double* in, int32_t w, int32_t h, int32_t ch,
                             double* out) {
   NEED(c && in && out, "null argument");

@@ -80,6 +80,8 @@ void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s);
 void launch_sat(const SatBatch& b, int max_w, int max_rows, cudaStream_t s);
 void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s);
 size_t detect_exact_smem(int tile, int half);
+void launch_cornerness(const double* table, int w1, const int32_t* xy, int n, int half, double* out,
+                       cudaStream_t s);
 void launch_compact_corners(const TileCorner* tiles, int ntiles, double* corners,
                             int32_t* count, cudaStream_t s);
 

@@ -585,3 +585,31 @@ void launch_compact_corners(const TileCorner* tiles, int ntiles, double* corners
 }
 
 }  // namespace hdr
+
+namespace hdr {
+
+// matcher.cornerness (matcher.py:51-61) for n points of a dense (h+1, w+1)
+// f64 integral table: out[2i] = C = ((d0 + d1) + d2) + d3, out[2i+1] = min.
+__global__ void cornerness_kernel(const double* __restrict__ t, int w1, const int32_t* __restrict__ xy,
+                                  int n, int half, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int x = xy[2 * i], y = xy[2 * i + 1];
+  auto rect = [&](int x0, int y0, int x1, int y1) {  // image.py:58
+    return dadd(dsub(dsub(t[(int64_t)y1 * w1 + x1], t[(int64_t)y0 * w1 + x1]), t[(int64_t)y1 * w1 + x0]),
+                t[(int64_t)y0 * w1 + x0]);
+  };
+  double area = (double)(half * half);
+  double tl = rect(x - half, y - half, x, y) / area, tr = rect(x, y - half, x + half, y) / area;
+  double br = rect(x, y, x + half, y + half) / area, bl = rect(x - half, y, x, y + half) / area;
+  double d0 = fabs(dsub(tr, tl)), d1 = fabs(dsub(br, tr)), d2 = fabs(dsub(bl, br)), d3 = fabs(dsub(tl, bl));
+  out[2 * i] = dadd(dadd(dadd(d0, d1), d2), d3);
+  out[2 * i + 1] = fmin(fmin(d0, d1), fmin(d2, d3));
+}
+
+void launch_cornerness(const double* table, int w1, const int32_t* xy, int n, int half, double* out,
+                       cudaStream_t s) {
+  if (n > 0) cornerness_kernel<<<(n + 127) / 128, 128, 0, s>>>(table, w1, xy, n, half, out);
+}
+
+}  // namespace hdr

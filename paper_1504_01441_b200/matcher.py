@@ -64,6 +64,22 @@ class MatchResult:
     level_counts: list = field(default_factory=list)
 
 
+def cornerness(table, x: int, y: int, half: int = DEFAULT_QUADRANT_HALF):
+    """matcher.py:51-61 — (cornerness, min contiguous-quadrant contrast) at
+    (x, y) of an integral image (image.integral's table)."""
+    h1, w1 = table.shape
+    if not (half <= x <= w1 - 1 - half and half <= y <= h1 - 1 - half):
+        raise ValueError("quadrant neighborhood out of bounds")
+    t = to_dev(table, torch.float64, device_of(table))
+    xy = torch.tensor([[int(x), int(y)]], dtype=torch.int32).to(t.device)
+    res = torch.empty((1, 2), dtype=torch.float64, device=t.device)
+    e = engine(w1 - 1, h1 - 1, t.device.index)
+    _native.check(_native.lib().hdr_cornerness(e.handle, ptr(t), w1 - 1, h1 - 1, ptr(xy), 1, half,
+                                               ptr(res)), "cornerness")
+    r = res.cpu().numpy()[0]
+    return float(r[0]), float(r[1])
+
+
 def detect_corners(lum, tile: int = DEFAULT_TILE, threshold: float = DEFAULT_THRESHOLD,
                    half: int = DEFAULT_QUADRANT_HALF):
     """matcher.py:64-105 — (n, 3) rows (x, y, score), tile order (K4 + K5)."""

@@ -62,6 +62,31 @@ def test_integral_bit_exact(scene):
     np.testing.assert_array_equal(image.integral(lum), O.integral(lum))
 
 
+def test_cornerness_point_query(scene):
+    """matcher.cornerness (matcher.py:50-61): KATs, random points vs the oracle,
+    and the out-of-bounds ValueError."""
+    img = np.zeros((32, 32), dtype=np.float32)
+    img[:16, 16:] = 1.0
+    img[16:, :16] = 1.0
+    assert matcher.cornerness(image.integral(img), 16, 16) == (4.0, 1.0)
+    edge = np.zeros((32, 32), dtype=np.float32)
+    edge[:, 16:] = 1.0
+    assert matcher.cornerness(image.integral(edge), 16, 16) == (2.0, 0.0)
+    _, _, ref, _ = scene
+    lum = O.luminance(ref)
+    table = image.integral(lum)
+    sat = O.integral(lum)
+    h, w = lum.shape
+    rng = np.random.default_rng(7)
+    for half in (8, 3):
+        for x, y in zip(rng.integers(half, w - half + 1, 20), rng.integers(half, h - half + 1, 20)):
+            c, lo = O._quadrants(sat, np.array([x]), np.array([y]), half)
+            assert matcher.cornerness(table, int(x), int(y), half) == (float(c[0]), float(lo[0]))
+    for x, y in ((7, 20), (20, 7), (w - 7, 20), (20, h - 7)):
+        with pytest.raises(ValueError, match="out of bounds"):
+            matcher.cornerness(table, x, y)
+
+
 def test_corners_matches_weeding_per_level(scene):
     _, fx, ref, src = scene
     lum_ref = O.luminance(ref)

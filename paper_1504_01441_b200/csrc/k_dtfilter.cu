@@ -720,6 +720,26 @@ __device__ __forceinline__ void cluster_arrive() {
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// Cluster barrier for data exchanged through shared memory only: the release
+// fence is restricted to this CTA's shared-memory writes (MEMBAR.CTA instead
+// of the GPU-scope MEMBAR that barrier.cluster.arrive.release emits, which
+// also waits for the thread's in-flight cp.async prefetches and global
+// stores); peers read the published values through DSMEM after the wait.
+#ifndef HDR_COL_SMEM_SYNC
+#define HDR_COL_SMEM_SYNC 1
+#endif
+__device__ __forceinline__ void cluster_sync_smem() {
+#if HDR_COL_SMEM_SYNC
+  asm volatile(
+      "fence.release.sync_restrict::shared::cta.cluster;\n"
+      "barrier.cluster.arrive.relaxed.aligned;\n"
+      "barrier.cluster.wait.aligned;\n"
+      "fence.acquire.sync_restrict::shared::cluster.cluster;\n" ::: "memory");
+#else
+  cluster_arrive();
+  cluster_wait();
+#endif
+}
 
 // cp.async (LDGSTS): per-thread asynchronous global -> shared copies, used to
 // prefetch the next band of dt_cols_cluster while the current one is linked,
@@ -884,12 +904,12 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   Aff<K> ex;  // exclusive prefix of this group within the CTA
   scan_groups<K>(m, true, bw_log2, wsc, ex);
   if (grp == G - 1) ctaF[col] = m;
-  cl.sync();
+  cluster_sync_smem();
   // gather the lower ranks' totals for this column (one remote load per thread)
   for (int q = grp; q < rank; q += G) remote[q][col] = *cl.map_shared_rank(&ctaF[col], q);
   __syncthreads();
+  double C[K];
   if (grp == 0) {
-    double C[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) C[k] = 0.0;
     for (int q = 0; q < rank; ++q) {
@@ -901,7 +921,6 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
     for (int k = 0; k < K; ++k) cin[col][k] = C[k];
   }
   __syncthreads();
-  double C[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) C[k] = ex.A * cin[col][k] + ex.B[k];
   // ---- backward link: suffix scan of z_start(g) = Q_g z_start(g+1) + (Z0_g + C_g R_g)
@@ -911,11 +930,11 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   Aff<K> sx;  // suffix from the groups below this one within the CTA
   scan_groups<K>(m, false, bw_log2, wsc, sx);
   if (grp == 0) ctaB[col] = m;
-  cl.sync();
+  cluster_sync_smem();
   for (int q = rank + 1 + grp; q < kCL; q += G) remote[q][col] = *cl.map_shared_rank(&ctaB[col], q);
   __syncthreads();
+  double D[K];
   if (grp == 0) {
-    double D[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) D[k] = 0.0;
     for (int q = kCL - 1; q > rank; --q) {
@@ -927,7 +946,6 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
     for (int k = 0; k < K; ++k) din[col][k] = D[k];
   }
   __syncthreads();
-  double D[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) D[k] = sx.A * din[col][k] + sx.B[k];
   // ---- apply: forward from C, backward from D, with the reference update

@@ -823,21 +823,25 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   const int r0 = rank * RP + grp * kSR;
   const int rend = min(h, (rank + 1) * RP);
   const int nrows = max(0, min(kSR, rend - r0));
+  // the thread's first row of every plane (band 0); a band adds band << bw_log2
+  const int64_t o0 = (int64_t)r0 * w + col;
+  // guide rows r0-1 .. r0+nrows that exist: j in [jg0, jg1)
+  const int jg0 = r0 == 0 ? 1 : 0, jg1 = min(nrows + 2, h - r0 + 1);
   auto prefetch = [&](int band) {
     const int x = (band << bw_log2) + col;
     if (band >= nbands || x >= w) return;
+    const int64_t o = o0 + (band << bw_log2);
+    const float* gp = guide + (o - w);
 #pragma unroll
-    for (int j = 0; j < kSR + 2; ++j) {
-      int y = r0 - 1 + j;
-      if (j <= nrows + 1 && y >= 0 && y < h) cp_async4(pfg + j * kCT + threadIdx.x, guide + (int64_t)y * w + x);
+    for (int j = 0; j < kSR + 2; ++j)
+      if (j >= jg0 && j < jg1) cp_async4(pfg + j * kCT + threadIdx.x, gp + (int64_t)j * w);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double* pk = reinterpret_cast<const double*>(P.p[k]) + o;
+#pragma unroll
+      for (int j = 0; j < kSR; ++j)
+        if (j < nrows) cp_async8(pfx + (k * kSR + j) * kCT + threadIdx.x, pk + (int64_t)j * w);
     }
-#pragma unroll
-    for (int j = 0; j < kSR; ++j)
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (j < nrows)
-          cp_async8(pfx + (k * kSR + j) * kCT + threadIdx.x,
-                    reinterpret_cast<const double*>(P.p[k]) + (int64_t)(r0 + j) * w + x);
     cp_async_commit();
   };
   if (PF) prefetch(blockIdx.y);
@@ -995,6 +999,16 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
           }
           reinterpret_cast<float2*>(fo.flow)[(int64_t)(r0 + j) * w + x] = make_float2(fu, fv);
         }
+    } else if (PF) {
+      // every plane is f64 on the prefetch path
+      const int64_t o = o0 + (band << bw_log2);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double* pk = reinterpret_cast<double*>(P.p[k]) + o;
+#pragma unroll
+        for (int j = 0; j < kSR; ++j)
+          if (j < n) pk[(int64_t)j * w] = xv[k][j];
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < kSR; ++j)

@@ -156,16 +156,18 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     }
   }
   __syncthreads();
-  // vertical (axis 0): thread (tx, ty) produces rows 4ty..4ty+3 of column
-  // tx (and tx + 32 for the halo columns) from 14 staged samples (sliding)
-  for (int c = tx; c < E; c += 32) {
+  // vertical (axis 0): work item (rg, c) produces rows 4rg..4rg+3 of staged
+  // column c from 14 staged samples (sliding); the E x 8 items are dealt out
+  // flat over the 256 threads, so the second round runs 3 warps, not 8
+  for (int item = tid; item < E * (kS2 / 4); item += 256) {
+    const int rg = item / E, c = item - rg * E;
     // the products of each staged sample are formed once (not once per tap
     // that reads it): same roundings, ~25% fewer f64 instructions
     double va[4 + 2 * R], vb[4 + 2 * R], vaa[4 + 2 * R], vbb[4 + 2 * R], vab[4 + 2 * R];
 #pragma unroll
     for (int j = 0; j < 4 + 2 * R; ++j) {
-      va[j] = sa[4 * ty + j][c];
-      vb[j] = sb[4 * ty + j][c];
+      va[j] = sa[4 * rg + j][c];
+      vb[j] = sb[4 * rg + j][c];
       vaa[j] = va[j] * va[j];
       vbb[j] = vb[j] * vb[j];
       vab[j] = va[j] * vb[j];
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
         m3 = fma(vbb[q + j], k[j], m3);
         m4 = fma(vab[q + j], k[j], m4);
       }
-      int oy = 4 * ty + q;
+      int oy = 4 * rg + q;
       V[(0 * kS2 + oy) * E + c] = m0;
       V[(1 * kS2 + oy) * E + c] = m1;
       V[(2 * kS2 + oy) * E + c] = m2;

@@ -101,6 +101,9 @@ const char* hdr_last_error(void);
  * column-sweep clusters (tuning: SM sharing with concurrent pairs).
  * "dt_cols_prefetch": 1 (default) = the cluster column kernel prefetches the
  * next band by cp.async, 0 = plain loads.
+ * "dt_skip_zero_rows": 1 (default) = with the sparse first row pass, rows
+ * without splat samples are left unwritten and the first (prefetching
+ * cluster) column sweep treats them as zero, 0 = they are written as zeros.
  * Returns HDR_ERR_INVALID for an unknown name. */
 int hdr_set_option(const char* name, int64_t value);
 /* Blocks until the context's stream drains; returns HDR_ERR_CUDA on a

@@ -127,6 +127,7 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
 int64_t dt_scratch_doubles(int w, int h, int k);
 void dt_set_cluster_columns(bool on);
 void dt_set_cols_prefetch(bool on);
+void dt_set_skip_zero_rows(bool on);
 void dt_set_cols_grid_div(int d);  // 0 auto, 1..3 force a band shape, -1 off
 // optional fused densify-finalise for the last column pass (K == 3)
 struct DtFlowOut {

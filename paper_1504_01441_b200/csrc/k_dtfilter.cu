@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* 
 __global__ void __launch_bounds__(kRowThreads) dt_rows_first_kernel(const float* __restrict__ guide,
                                                                     DtPlanes P, int w, int h,
                                                                     double ratio, double c,
-                                                                    DtSparse sp) {
+                                                                    DtSparse sp, bool zero_rows) {
   constexpr int K = 3;
   extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
   float* gs = reinterpret_cast<float*>(xs + K * w);
@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_first_kernel(const float*
   int64_t row = (int64_t)y * w;
   const int e0 = sp.row_start[y], e1 = sp.row_start[y + 1];
   if (e0 == e1) {
+    // the column sweep that follows skips rows without samples when it can
+    // (dt_cols_cluster's zrows); otherwise the zeros are written
+    if (!zero_rows) return;
     const double2 z = make_double2(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -804,7 +807,7 @@ __device__ __forceinline__ void scan_groups(Aff<K>& m, bool up, int bw_log2,
 template <int K, bool FINAL, bool PF>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 2 : 1)
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
-                    double c, int bw_log2, DtFlowOut fo) {
+                    double c, int bw_log2, DtFlowOut fo, const int32_t* __restrict__ zrows) {
   __shared__ Aff<K> wsc[kCT / 32][kMaxBw];  // per-warp totals of the group scans
   // per-column CTA totals read by the cluster peers, double-buffered by band
   // parity: band b+2 reuses band b's buffer only after two cluster barriers,
@@ -823,6 +826,13 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
   const int r0 = rank * RP + grp * kSR;
   const int rend = min(h, (rank + 1) * RP);
   const int nrows = max(0, min(kSR, rend - r0));
+  // zrows (the CSR row starts of the pair's first pass, PF only): rows without
+  // a splat sample are exactly zero after the first row sweep and were not
+  // written, so they are neither loaded nor read (bit j = row r0 + j)
+  uint32_t zmask = 0;
+  if (PF && zrows)
+    for (int j = 0; j < nrows; ++j)
+      if (__ldg(zrows + r0 + j) == __ldg(zrows + r0 + j + 1)) zmask |= 1u << j;
   // the thread's first row of every plane (band 0); a band adds band << bw_log2
   const int64_t o0 = (int64_t)r0 * w + col;
   // guide rows r0-1 .. r0+nrows that exist: j in [jg0, jg1)
@@ -840,7 +850,7 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
       const double* pk = reinterpret_cast<const double*>(P.p[k]) + o;
 #pragma unroll
       for (int j = 0; j < kSR; ++j)
-        if (j < nrows) cp_async8(pfx + (k * kSR + j) * kCT + threadIdx.x, pk + (int64_t)j * w);
+        if (j < nrows && !((zmask >> j) & 1u)) cp_async8(pfx + (k * kSR + j) * kCT + threadIdx.x, pk + (int64_t)j * w);
     }
     cp_async_commit();
   };
@@ -870,9 +880,9 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 
     for (int j = 0; j < kSR; ++j)
 #pragma unroll
       for (int k = 0; k < K; ++k)
-        xv[k][j] = (j < n) ? (PF ? pfx[(k * kSR + j) * kCT + threadIdx.x]
-                                 : ldp(P, k, (int64_t)(r0 + j) * w + x))
-                           : 0.0;
+        xv[k][j] = (j < n && !((zmask >> j) & 1u)) ? (PF ? pfx[(k * kSR + j) * kCT + threadIdx.x]
+                                                        : ldp(P, k, (int64_t)(r0 + j) * w + x))
+                                                   : 0.0;
 #pragma unroll
     for (int j = 0; j <= kSR; ++j) {
       int y = r0 - 1 + j;
@@ -1057,7 +1067,8 @@ static int g_cols_grid_div = 1;
 
 template <int K, bool FINAL>
 static void launch_cols_cluster(const float* guide, const DtPlanes& P, int w, int h, double ratio,
-                                double c, int bl, const DtFlowOut& fo, cudaStream_t s) {
+                                double c, int bl, const DtFlowOut& fo, cudaStream_t s,
+                                const int32_t* zrows = nullptr) {
   int nb = ceil_div(w, 1 << bl);
   bool pf = g_cols_prefetch;
   for (int k = 0; k < P.k; ++k)
@@ -1066,12 +1077,13 @@ static void launch_cols_cluster(const float* guide, const DtPlanes& P, int w, in
   if (pf && mc > 0) {
     if (g_cols_grid_div > 1) mc = std::max(1, mc / g_cols_grid_div);
     dim3 cgrid(kCL, std::min(nb, mc));
-    dt_cols_cluster<K, FINAL, true><<<cgrid, kCT, cols_pf_smem<K>(), s>>>(guide, P, w, h, ratio, c, bl, fo);
+    dt_cols_cluster<K, FINAL, true><<<cgrid, kCT, cols_pf_smem<K>(), s>>>(guide, P, w, h, ratio, c, bl, fo,
+                                                                          zrows);
     return;
   }
   mc = max_clusters<K, FINAL, false>();
   dim3 cgrid(kCL, mc > 0 ? std::min(nb, mc) : nb);
-  dt_cols_cluster<K, FINAL, false><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo);
+  dt_cols_cluster<K, FINAL, false><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo, nullptr);
 }
 
 // log2 of the cluster kernel's band width for this height, or -1 (too tall)
@@ -1086,6 +1098,9 @@ static int cluster_bw_log2(int h) {
 
 // test hook: 0 selects the agg/link/apply column path
 static bool g_cols_cluster = true;
+// test hook: 0 makes the sparse-first row pass write its sample-free rows
+// (zeros) instead of letting the first column sweep skip them
+static bool g_skip_zero_rows = true;
 
 template <int K>
 static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sigma_s,
@@ -1100,6 +1115,15 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
   double* agg = scratch;
   double* carry = agg + (int64_t)nch * w * (3 + 2 * K);
   dim3 cg(ceil_div(w, kColThreads), nch);
+  // the first column sweep reads the sparse-first rows through the CSR row
+  // starts (rows without samples stay unwritten) when it runs the prefetching
+  // cluster kernel; decided here so the row pass knows whether to write zeros
+  const int bl0 = cluster_bw_log2(h);
+  bool skip_zero = sp && K == 3 && h > 1 && bl0 >= 0 && g_cols_cluster && g_cols_prefetch && g_skip_zero_rows;
+  for (int k = 0; k < P.k; ++k)
+    if (!P.f64[k]) skip_zero = false;
+  if (skip_zero)
+    skip_zero = (passes == 1 && fo.flow) ? max_clusters<K, true, true>() > 0 : max_clusters<K, false, true>() > 0;
   for (int i = 1; i <= passes; ++i) {
     double sigma_i = sigma_s * sqrt(3.0) * pow(2.0, passes - i) / den;  // densify.py:104
     double c = -root / sigma_i;
@@ -1107,7 +1131,7 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
       kprobe_mark(kr, 0, s);
       if (i == 1 && sp && K == 3)
         dt_rows_first_kernel<<<h, kRowThreads, (size_t)3 * w * sizeof(double) + (size_t)w * 4, s>>>(
-            guide, P, w, h, ratio, c, *sp);
+            guide, P, w, h, ratio, c, *sp, !skip_zero);
       else if (rows_bulk_ok(guide, P, w))
         dt_rows_bulk_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double) + (size_t)w * 4, s>>>(
             guide, P, w, h, ratio, c);
@@ -1122,11 +1146,12 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     bool fin_pass = i == passes && fo.flow && K == 3;
     if (h > 1) kprobe_mark(kc, 0, s);
     if (h > 1 && bl >= 0 && g_cols_cluster) {
+      const int32_t* zr = (i == 1 && skip_zero) ? sp->row_start : nullptr;
       if (fin_pass) {
-        launch_cols_cluster<K, true>(guide, P, w, h, ratio, c, bl, fo, s);
+        launch_cols_cluster<K, true>(guide, P, w, h, ratio, c, bl, fo, s, zr);
         finalized = true;
       } else {
-        launch_cols_cluster<K, false>(guide, P, w, h, ratio, c, bl, fo, s);
+        launch_cols_cluster<K, false>(guide, P, w, h, ratio, c, bl, fo, s, zr);
       }
     } else if (h > 1) {
       dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
@@ -1150,6 +1175,7 @@ int64_t dt_scratch_doubles(int w, int h, int k) {
 
 void dt_set_cluster_columns(bool on) { g_cols_cluster = on; }
 void dt_set_cols_prefetch(bool on) { g_cols_prefetch = on; }
+void dt_set_skip_zero_rows(bool on) { g_skip_zero_rows = on; }
 void dt_set_cols_grid_div(int d) { g_cols_grid_div = d < 1 ? 1 : d; }
 
 void init_densify_attributes() {

@@ -210,17 +210,27 @@ def test_dt_filter_all_column_paths(cuda, shape):
 
 def test_sparse_first_row_pass_is_exact(cuda):
     """The CSR splat + first row pass built from it (the pair default) gives
-    the same bits as the dense splat planes + the plain row pass."""
+    the same bits as the dense splat planes + the plain row pass, and as the
+    sparse pass writing its sample-free rows instead of the first column
+    sweep skipping them -- also when the context's planes still hold another
+    pair's values (the skipped rows are never written by the row pass)."""
     from paper_1504_01441_b200 import _native
     st = synth.synth_stack(synth.working_spec(640, 480), 3)
+    other = synth.synth_stack(synth.working_spec(640, 480), 5)
+    pipeline.register_and_fuse(other.ref, other.src)  # leaves its planes behind
     a = pipeline.register_and_fuse(st.ref, st.src)
     try:
         _native.check(_native.lib().hdr_set_option(b"dt_sparse_first", 0))
         b = pipeline.register_and_fuse(st.ref, st.src)
+        _native.check(_native.lib().hdr_set_option(b"dt_sparse_first", 1))
+        _native.check(_native.lib().hdr_set_option(b"dt_skip_zero_rows", 0))
+        c = pipeline.register_and_fuse(st.ref, st.src)
     finally:
         _native.lib().hdr_set_option(b"dt_sparse_first", 1)
-    np.testing.assert_array_equal(a.flow, b.flow)
-    np.testing.assert_array_equal(a.composite, b.composite)
+        _native.lib().hdr_set_option(b"dt_skip_zero_rows", 1)
+    for o in (b, c):
+        np.testing.assert_array_equal(a.flow, o.flow)
+        np.testing.assert_array_equal(a.composite, o.composite)
 
 
 def test_ssim_and_fuse_stages(scene):

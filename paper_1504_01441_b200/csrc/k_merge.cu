@@ -73,17 +73,22 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
 #pragma unroll 1
   for (int quad = 0; quad < NC / 4; ++quad) {
     const float* src = px + quad * 4 * kRT * kRP;
-    // 4 * 16 * 36 = 2304 = 9 * 256 vertical outputs
-#pragma unroll 3
-    for (int i = tid; i < 4 * kOT * kRT; i += 256) {
-      int q = i / kRT, x = i - q * kRT;  // q = c * 16 + oy
+    // 4 * 16 * 36 = 2304 = 9 * 256 vertical outputs (q = c * 16 + oy): the
+    // first 32 columns of every q with a warp per q and a lane per column
+    // (consecutive words, no bank conflicts -- dealing the 36 columns out
+    // flat put two q rows 74 words apart into one warp: 2.3 wavefronts per
+    // load), then the last 4 columns of all 64 q rows in one round
+    auto vert = [&](int q, int x) {
       int c = q >> 4, oy = q & 15;
       const float* col = src + (c * kRT + 2 * oy) * kRP + x;
       float acc = kK5[0] * col[0];
 #pragma unroll
       for (int k = 1; k < 5; ++k) acc += kK5[k] * col[k * kRP];
       V[q * kRT + x] = acc;
-    }
+    };
+#pragma unroll 2
+    for (int q = tid >> 5; q < 4 * kOT; q += 8) vert(q, tid & 31);
+    vert(tid >> 2, 32 + (tid & 3));
     __syncthreads();
     // 4 * 16 * 16 = 1024 = 4 * 256 horizontal outputs
 #pragma unroll

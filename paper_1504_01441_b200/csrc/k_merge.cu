@@ -61,10 +61,13 @@ constexpr int kOT = 16;           // level-1 outputs per tile side
 constexpr int kRT = 2 * kOT + 4;  // level-0 region incl. the 2-px blur halo (36)
 constexpr int kLT = kRT + 2;      // + 1-px laplacian halo (38)
 constexpr int kRP = kRT + 1;      // padded row pitch of the staged region
+// row pitch of the vertical-pass rows V: odd, so the two q rows a warp's
+// horizontal pass reads (16 lanes each, stride 2) fall on disjoint banks
+constexpr int kVP = kRT + 1;
 
 // 5-tap blur + [::2, ::2] of NC staged channels px[c][36][kRP] into a 16x16
-// level-1 tile, four channels at a time: vertical into V[4][16][36], then
-// horizontal to global. V needs only 2304 floats, so it can alias the
+// level-1 tile, four channels at a time: vertical into V[4][16][37], then
+// horizontal to global. V needs only 2368 floats, so it can alias the
 // luminance tiles of weights_down (the occupancy limit is shared memory).
 template <int NC>
 __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, int Y0, int X0,
@@ -84,7 +87,7 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
       float acc = kK5[0] * col[0];
 #pragma unroll
       for (int k = 1; k < 5; ++k) acc += kK5[k] * col[k * kRP];
-      V[q * kRT + x] = acc;
+      V[q * kVP + x] = acc;
     };
 #pragma unroll 2
     for (int q = tid >> 5; q < 4 * kOT; q += 8) vert(q, tid & 31);
@@ -96,7 +99,7 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
       int q = i >> 4, ox = i & 15;
       int c = q >> 4, oy = q & 15;
       int Y = Y0 + oy, X = X0 + ox;
-      const float* row = V + q * kRT + 2 * ox;
+      const float* row = V + q * kVP + 2 * ox;
       float acc = kK5[0] * row[0];
 #pragma unroll
       for (int k = 1; k < 5; ++k) acc += kK5[k] * row[k];
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_
   extern __shared__ float smf[];
   float* lum = smf;                    // [NF][38][38] luminance of every frame
   float* px = smf + NF * kLT * kLT;    // [4NF][36][37]: RGB of every frame, then the weights
-  float* V = smf;                      // [4][16][36], aliases the luminance after the weights
+  float* V = smf;                      // [4][16][37], aliases the luminance after the weights
   __shared__ int ridx[kLT], cidx[kLT];
   int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_
 
 // ---------------------------------------------------------------- levels >= 1
 template <int NF>
-constexpr size_t down_smem() { return sizeof(float) * (4 * NF * kRT * kRP + 4 * kOT * kRT); }
+constexpr size_t down_smem() { return sizeof(float) * (4 * NF * kRT * kRP + 4 * kOT * kVP); }
 
 template <int NF>
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
   constexpr int NC = 4 * NF;
   extern __shared__ float smd[];
   float* tile = smd;                // [NC][36][37]
-  float* V = smd + NC * kRT * kRP;  // [4][16][36]
+  float* V = smd + NC * kRT * kRP;  // [4][16][37]
   __shared__ int ridx[kRT], cidx[kRT];
   int tid = threadIdx.x;
   int Y0 = blockIdx.y * kOT, X0 = blockIdx.x * kOT;
@@ -485,7 +488,7 @@ __global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float
 
 template <int NF>
 constexpr size_t weights_smem() { return sizeof(float) * (NF * kLT * kLT + 4 * NF * kRT * kRP); }
-static_assert(4 * kOT * kRT <= 2 * kLT * kLT, "V aliases the luminance tiles");
+static_assert(4 * kOT * kVP <= 2 * kLT * kLT, "V aliases the luminance tiles");
 
 template <int NF>
 static void init_merge_nf() {

@@ -197,12 +197,25 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
   int oy = tid >> 3, ox0 = (tid & 7) * 4;
   int gy = blockIdx.y * kS2 + oy;
   double m[5][4];
+  // the 8 lanes of a row read 16-byte chunks 32 bytes apart (two lanes per
+  // bank group); lanes 4-7 fetch their chunks rotated by one, so most steps
+  // see all eight bank groups once (one wavefront per row, not two)
+  constexpr int NC = (4 + 2 * R) / 2;  // 16-byte chunks per thread (7)
+  static_assert((4 + 2 * R) % 2 == 0 && E % 2 == 0, "16-byte chunks");
+  const int rot = (tid >> 2) & 1;
 #pragma unroll
   for (int mm = 0; mm < 5; ++mm) {
-    const double* row = V + (mm * kS2 + oy) * E + ox0;
+    const double2* row2 = reinterpret_cast<const double2*>(V + (mm * kS2 + oy) * E + ox0);
+    double2 r[NC];
+#pragma unroll
+    for (int st = 0; st < NC; ++st) r[st] = row2[st + rot == NC ? 0 : st + rot];
     double v[4 + 2 * R];
 #pragma unroll
-    for (int j = 0; j < 4 + 2 * R; ++j) v[j] = row[j];
+    for (int t = 0; t < NC; ++t) {
+      double2 cv = rot ? r[(t + NC - 1) % NC] : r[t];
+      v[2 * t] = cv.x;
+      v[2 * t + 1] = cv.y;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       double acc = 0.0;

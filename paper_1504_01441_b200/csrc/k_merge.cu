@@ -91,7 +91,13 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
     };
 #pragma unroll 2
     for (int q = tid >> 5; q < 4 * kOT; q += 8) vert(q, tid & 31);
-    vert(tid >> 2, 32 + (tid & 3));
+    // remainder: warp w takes channel w/2, rows oy = 2k + (w&1), k = lane/4,
+    // and columns 32 + lane%4 -- the 8 rows sit 20 banks apart, so the 32
+    // lanes hit 32 distinct banks
+    {
+      const int wp = tid >> 5, ln = tid & 31;
+      vert(16 * (wp >> 1) + 2 * (ln >> 2) + (wp & 1), 32 + (ln & 3));
+    }
     __syncthreads();
     // 4 * 16 * 16 = 1024 = 4 * 256 horizontal outputs
 #pragma unroll

@@ -280,7 +280,13 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_reg_kernel(const float* _
 template <int K>
 __device__ __forceinline__ void row_sweep_smem(double* xs, const float* gs, int w, double ratio,
                                                double c, Aff<K>* wsum) {
-  const int L = (w + kRowThreads - 1) / kRowThreads;
+#ifndef HDR_ROW_ODD_SEG
+#define HDR_ROW_ODD_SEG 1
+#endif
+  int L = (w + kRowThreads - 1) / kRowThreads;
+  // an odd segment length puts a half-warp's segment starts on 16 distinct
+  // 8-byte bank pairs (an even one shares them two or four ways)
+  if (HDR_ROW_ODD_SEG && !(L & 1) && L < kRowSeg) ++L;
   int s0 = threadIdx.x * L, n = max(0, min(w, s0 + L) - s0);
   // af[j] couples samples s0-1+j and s0+j (0 outside the row)
   double af[kRowSeg + 1];

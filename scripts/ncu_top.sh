@@ -10,7 +10,7 @@ run() {  # name regex skip
 run dt_rows 'dt_rows_bulk_kernel' 0
 run dt_apply 'dt_cols_apply' 0
 run dt_agg 'dt_cols_agg' 0
-run dt_cols 'dt_cols_cluster' 0
+run dt_cols 'dt_cols_cluster' 1
 run ssd 'ssd_tiles_kernel' 4
 run finish 'finish_level_kernel' 4
 run weedfit 'weed_fit_kernel' 4

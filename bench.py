@@ -63,7 +63,7 @@ def parse():
 
 # ------------------------------------------------------------------ scenes
 def _render(args):
-    from paper_1504_01441_b200 import synth
+    from harness import synth
     w, h, seed = args
     st = synth.synth_stack(synth.working_spec(w, h), seed)
     return st.ref, st.src

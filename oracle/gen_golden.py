@@ -23,14 +23,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_1504_01441_b200 import synth  # noqa: E402
+from harness import synth  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 STRIDE = 8  # dense outputs: full-array digests + a 1-in-8 lattice sample
 
 
-def sub(a):
-    s = np.ascontiguousarray(a[::STRIDE, ::STRIDE])
+def sub(a, stride=STRIDE):
+    s = np.ascontiguousarray(a[::stride, ::stride])
     return s.astype(np.float32) if s.dtype == np.float64 else s
 
 # (name, width, height, rotation_deg, seed)
@@ -40,6 +40,15 @@ SCENES = [
     ("qvga_s2", 320, 240, 0.0, 2),
     ("r960_s3", 960, 720, 0.25, 3),
 ]
+
+# BASELINE.json's headline shapes, pinned to the
+# real reference: dense outputs keep full-array digests, per-level traces
+# and a 1-in-32 lattice sample (fixtures stay small)
+BIG_SCENES = [
+    ("c2_5mp_s0", 2592, 1944, 0.0, 0),
+    ("c4_12mp_s0", 4000, 3000, 0.0, 0),
+]
+BIG_STRIDE = 32
 
 
 def digest(a) -> str:
@@ -55,7 +64,7 @@ def load_reference(path):
     return hdrflow
 
 
-def scene_fixture(hf, w, h, rot, seed):
+def scene_fixture(hf, w, h, rot, seed, stride=STRIDE):
     from hdrflow import densify, fusion, image, matcher, pipeline, weeding
     st = synth.synth_stack(synth.working_spec(w, h, rotation_deg=rot), seed)
     ref, src = st.ref, st.src
@@ -101,16 +110,23 @@ def scene_fixture(hf, w, h, rot, seed):
     for k in ("composite", "flow", "warped", "valid", "ssim"):
         a = getattr(r, k)
         out[f"{k}_digest"] = np.array(digest(a))
-        out[f"{k}_sub"] = sub(a)
+        out[f"{k}_sub"] = sub(a, stride)
     # staged intermediates on the reference's own path
     maps = densify.build_sparse_maps(r.matches, w, h)
     sm = densify.dt_filter(lum_ref, np.stack([maps.pu, maps.pv, maps.n], axis=-1),
                            params.sigma_s, params.sigma_r, params.passes)
     out["smooth_digest"] = np.array(digest(sm))
-    out["smooth_sub"] = sub(sm)
+    out["smooth_sub"] = sub(sm, stride)
     wr, ws = fusion.fusion_weights(ref, r.warped, r.ssim, r.valid.astype(np.float32))
-    out["wref_sub"] = sub(wr)
-    out["wsrc_sub"] = sub(ws)
+    out["wref_sub"] = sub(wr, stride)
+    out["wsrc_sub"] = sub(ws, stride)
+    # the Ntilde-floor regime (densify.py:131-139): pixels falling back to the
+    # global-H flow, and how many sit within 1e-3 relative of the floor
+    nt = sm[..., 2]
+    out["floor_fallback"] = np.array(int((nt <= params.normalization_floor).sum()))
+    out["floor_near"] = np.array(int((np.abs(nt - params.normalization_floor)
+                                      <= 1e-3 * params.normalization_floor).sum()))
+    out["stride"] = np.array(stride)
     return out
 
 
@@ -195,7 +211,7 @@ def stack_frames(w, h, seed):
     return [a.src, a.ref, b.src], [4.0, 1.0, 16.0]
 
 
-def stack_fixture(w, h, seed):
+def stack_fixture(w, h, seed, stride=STRIDE):
     """k-way stack composed from the REAL reference's functions: metering's
     reference choice, a pairwise register_and_fuse per source (for its
     warped frame, SSIM and validity), quality_weights, the pyramids and
@@ -232,7 +248,8 @@ def stack_fixture(w, h, seed):
         blended.append(acc)
     comp = np.clip(fusion.collapse_pyramid(blended), 0.0, 1.0).astype(np.float32)
     out = {"scene": np.array([w, h, seed]), "reference_index": np.array(k),
-           "composite_digest": np.array(digest(comp)), "composite_sub": sub(comp)}
+           "composite_digest": np.array(digest(comp)), "composite_sub": sub(comp, stride),
+           "stride": np.array(stride)}
     for i, c in enumerate(counts):
         out[f"level_counts_{i}"] = c
     return out
@@ -261,9 +278,21 @@ def metering_fixture():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
+    ap.add_argument("--big", action="store_true",
+                    help="only the headline-size fixtures (C2 5MP, C4 12MP, C3 5MP stack; minutes of CPU)")
     args = ap.parse_args()
     hf = load_reference(args.ref)
     os.makedirs(GOLDEN, exist_ok=True)
+    if args.big:
+        for name, w, h, rot, seed in BIG_SCENES:
+            fx = scene_fixture(hf, w, h, rot, seed, BIG_STRIDE)
+            fx["scene"] = np.array([w, h, rot, seed], dtype=np.float64)
+            np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **fx)
+            print(name, fx["level_counts"].tolist(), int(fx["floor_fallback"]), int(fx["floor_near"]))
+        np.savez_compressed(os.path.join(GOLDEN, "stack3_5mp.npz"),
+                            **stack_fixture(2592, 1944, 0, BIG_STRIDE))
+        print("stack3_5mp done")
+        return
     for name, w, h, rot, seed in SCENES:
         fx = scene_fixture(hf, w, h, rot, seed)
         fx["scene"] = np.array([w, h, rot, seed], dtype=np.float64)

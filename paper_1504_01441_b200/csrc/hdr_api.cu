@@ -307,10 +307,21 @@ static int ntiles_of(int w, int h, int tile) { return ceil_div(w, tile) * ceil_d
 // ------------------------------------------------------------ context
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
+  uint64_t used = 0;            // LRU stamp
 };
+
+struct KeySet {
+  uint64_t* keys = nullptr;     // kMaxLevels x iters x 2
+  double* fits = nullptr;       // iters x 20
+  int iters = 0;
+};
+
+constexpr size_t kMaxGraphs = 32;     // cached pair graphs per context
+constexpr size_t kMaxParamSets = 8;   // cached key / tap sets per context
 
 struct hdr_ctx {
   int W = 0, H = 0;
+  int device = 0;               // the CUDA device the workspace lives on
   int64_t P = 0;
   cudaStream_t stream = nullptr;
   // raster
@@ -337,12 +348,13 @@ struct hdr_ctx {
   int32_t* witness = nullptr;
   int64_t* kept = nullptr;
   double* hpred = nullptr;      // 9 + 9 scratch
-  double* fits = nullptr;
-  int64_t fits_cap = 0;
-  uint64_t* keys = nullptr;     // kMaxLevels x keys_iters x 2
-  int keys_iters = 0;
-  uint64_t keys_seed = ~0ULL;
-  int keys_it = -1, keys_cit = -1;
+  // Philox keys + RANSAC fit scratch per (seed, iterations, coarse_iterations)
+  // and Gaussian taps per (window, sigma): every parameter set owns its own
+  // buffers, so a captured graph always replays against the contents it was
+  // captured with (evicting a set destroys the graphs first)
+  std::map<std::tuple<uint64_t, int, int>, KeySet> keysets;
+  KeySet* keyset = nullptr;     // the current call's
+  std::map<std::pair<int, double>, double*> tapsets;
   // densify
   void* planes = nullptr;       // pu, pv, n: f64 planes (24 B per pixel)
   double* carry = nullptr;      // domain-transform aggregates / carries / coefficients
@@ -356,9 +368,7 @@ struct hdr_ctx {
   float* ws = nullptr;
   float* fpyr = nullptr;
   int64_t fpyr_cap = 0;
-  double* taps = nullptr;       // 31
-  int taps_window = -1;
-  double taps_sigma = -1.0;
+  double* taps = nullptr;       // the current call's 31 taps (owned by tapsets)
   int32_t* info_scratch = nullptr;
   int32_t* stats_q = nullptr;   // exactness certificate per level (K4)
   double* stats_s = nullptr;
@@ -371,7 +381,24 @@ struct hdr_ctx {
   int64_t fstack_cap = 0;
   int32_t graph_kernels = 0;
   std::map<std::string, GraphEntry> graphs;
+  uint64_t graph_clock = 0;
   std::vector<void*> allocs;
+};
+
+// Every entry point runs on its context's device (the caller's current device
+// may differ: lazy allocations and launches would otherwise land on the wrong
+// GPU), restoring the caller's device on return.
+struct CtxDevice {
+  int prev = -1;
+  explicit CtxDevice(const hdr_ctx* c) {
+    if (!c) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; return; }
+    if (prev != c->device) cudaSetDevice(c->device);
+    else prev = -1;
+  }
+  ~CtxDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 
 template <class T>
@@ -391,12 +418,17 @@ extern "C" int32_t hdr_max_matches(int32_t width, int32_t height, int32_t tile) 
 }
 
 extern "C" int hdr_ctx_destroy(hdr_ctx* c) {
+  CtxDevice dg_(c);
   if (!c) return HDR_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : c->allocs) cudaFree(p);
-  if (c->keys) cudaFree(c->keys);
-  if (c->fits) cudaFree(c->fits);
+  for (auto& kv : c->keysets) {
+    cudaFree(kv.second.keys);
+    cudaFree(kv.second.fits);
+  }
+  for (auto& kv : c->tapsets) cudaFree(kv.second);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->frames) cudaFree(c->frames);
   if (c->fstack) cudaFree(c->fstack);
@@ -411,6 +443,10 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   static std::once_flag once;
   std::call_once(once, init_kernel_attributes);
   hdr_ctx* c = new hdr_ctx();
+  if (cudaGetDevice(&c->device) != cudaSuccess) {
+    delete c;
+    return fail(HDR_ERR_CUDA, "no current CUDA device");
+  }
   c->W = width;
   c->H = height;
   c->P = (int64_t)width * height;
@@ -477,7 +513,6 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
   ALLOC(wr, P);
   ALLOC(ws, P);
   ALLOC(fpyr, fsum + 64);
-  ALLOC(taps, 64);
   ALLOC(info_scratch, HDR_INFO_WORDS);
   ALLOC(stats_q, 8);
   ALLOC(stats_s, 8);
@@ -491,12 +526,14 @@ extern "C" int hdr_ctx_create(int32_t width, int32_t height, void* stream, hdr_c
 }
 
 extern "C" int hdr_ctx_set_stream(hdr_ctx* c, void* stream) {
+  CtxDevice dg_(c);
   if (!c) return fail(HDR_ERR_INVALID, "null context");
   c->stream = (cudaStream_t)stream;
   return HDR_OK;
 }
 
 extern "C" int hdr_ctx_set_probes(hdr_ctx* c, void* const* events) {
+  CtxDevice dg_(c);
   if (!c) return fail(HDR_ERR_INVALID, "null context");
   c->probing = events != nullptr;
   for (int i = 0; i < 2 * HDR_NUM_STAGES; ++i)
@@ -504,10 +541,12 @@ extern "C" int hdr_ctx_set_probes(hdr_ctx* c, void* const* events) {
   return HDR_OK;
 }
 
-extern "C" int32_t hdr_ctx_graph_kernels(hdr_ctx* c) { return c ? c->graph_kernels : -1; }
+extern "C" int32_t hdr_ctx_graph_kernels(hdr_ctx* c) {
+  CtxDevice dg_(c); return c ? c->graph_kernels : -1; }
 
 extern "C" int hdr_ctx_set_kernel_probes(hdr_ctx* c, int32_t kernel, void* const* events,
                                          int32_t n) {
+  CtxDevice dg_(c);
   if (!c) return fail(HDR_ERR_INVALID, "null context");
   if (kernel < 0 || kernel >= HDR_NUM_KPROBES) return fail(HDR_ERR_INVALID, "unknown kernel probe");
   if (n < 0 || n > kMaxKProbeLaunches || (n > 0 && !events))
@@ -548,46 +587,79 @@ static void probe(hdr_ctx* c, int stage, int end) {
 }
 
 extern "C" int hdr_ctx_sync(hdr_ctx* c) {
+  CtxDevice dg_(c);
   if (!c) return fail(HDR_ERR_INVALID, "null context");
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   CUDA_TRY(cudaGetLastError());
   return HDR_OK;
 }
 
-// Philox keys for every level, cached per (seed, iterations, coarse_iterations).
-static int ensure_keys(hdr_ctx* c, const hdr_params* p) {
-  int iters = std::max(p->iterations, p->coarse_iterations);
-  if (c->keys && c->keys_seed == p->seed && c->keys_it == p->iterations &&
-      c->keys_cit == p->coarse_iterations)
-    return HDR_OK;
-  if (iters > c->keys_iters) {
-    if (c->keys) cudaFree(c->keys);
-    CUDA_TRY(cudaMalloc(&c->keys, sizeof(uint64_t) * 2 * (size_t)iters * kMaxLevels));
-    c->keys_iters = iters;
-  }
-  if ((int64_t)iters * 20 > c->fits_cap) {
-    if (c->fits) cudaFree(c->fits);
-    CUDA_TRY(cudaMalloc(&c->fits, sizeof(double) * 20 * (size_t)iters));
-    c->fits_cap = (int64_t)iters * 20;
-  }
-  std::vector<uint64_t> host(2 * (size_t)c->keys_iters * kMaxLevels, 0);
-  for (int l = 0; l < kMaxLevels; ++l) {
-    int n = l == 0 ? p->iterations : p->coarse_iterations;
-    hdr_iteration_keys(hdr_level_seed(p->seed, l), n, host.data() + 2 * (size_t)c->keys_iters * l);
-  }
+static void drop_graphs(hdr_ctx* c) {
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);  // in-flight launches finish first
+  c->graphs.clear();
+}
+
+// Parameter-set caches are bounded; evicting one frees buffers that cached
+// graphs (and queued work) may reference, so both go first.
+template <class Map, class Free>
+static int evict_if_full(hdr_ctx* c, Map& m, Free free_fn) {
+  if (m.size() < kMaxParamSets) return HDR_OK;
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(c->keys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  c->keys_seed = p->seed;
-  c->keys_it = p->iterations;
-  c->keys_cit = p->coarse_iterations;
+  drop_graphs(c);
+  for (auto& kv : m) free_fn(kv.second);
+  m.clear();
   return HDR_OK;
 }
 
-// fusion._gaussian_kernel (fusion.py:28-31)
+// Philox keys for every level (weeding._iteration_rng, weeding.py:62-66,
+// seeded per level by matcher.level_seed, matcher.py:146-149) and the RANSAC
+// fit scratch, one set per (seed, iterations, coarse_iterations).
+static int ensure_keys(hdr_ctx* c, const hdr_params* p) {
+  auto key = std::make_tuple(p->seed, p->iterations, p->coarse_iterations);
+  auto it = c->keysets.find(key);
+  if (it != c->keysets.end()) {
+    c->keyset = &it->second;
+    return HDR_OK;
+  }
+  int rc = evict_if_full(c, c->keysets, [](KeySet& k) { cudaFree(k.keys); cudaFree(k.fits); });
+  if (rc) return rc;
+  KeySet ks;
+  ks.iters = std::max(p->iterations, p->coarse_iterations);
+  CUDA_TRY(cudaMalloc(&ks.keys, sizeof(uint64_t) * 2 * (size_t)ks.iters * kMaxLevels));
+  cudaError_t e = cudaMalloc(&ks.fits, sizeof(double) * 20 * (size_t)ks.iters);
+  if (e != cudaSuccess) {
+    cudaFree(ks.keys);
+    return fail(HDR_ERR_CUDA, std::string("key set: ") + cudaGetErrorString(e));
+  }
+  std::vector<uint64_t> host(2 * (size_t)ks.iters * kMaxLevels, 0);
+  for (int l = 0; l < kMaxLevels; ++l) {
+    int n = l == 0 ? p->iterations : p->coarse_iterations;
+    hdr_iteration_keys(hdr_level_seed(p->seed, l), n, host.data() + 2 * (size_t)ks.iters * l);
+  }
+  // a fresh buffer no queued work reads: a plain blocking upload suffices
+  e = cudaMemcpy(ks.keys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(ks.keys);
+    cudaFree(ks.fits);
+    return fail(HDR_ERR_CUDA, std::string("key upload: ") + cudaGetErrorString(e));
+  }
+  c->keyset = &(c->keysets[key] = ks);
+  return HDR_OK;
+}
+
+// fusion._gaussian_kernel (fusion.py:28-31), one tap set per (window, sigma)
 static int ensure_taps(hdr_ctx* c, int window, double sigma) {
-  if (window == c->taps_window && sigma == c->taps_sigma) return HDR_OK;
   int r = window / 2;
   if (r > 15) return fail(HDR_ERR_INVALID, "ssim_window above 31 is not supported");
+  auto key = std::make_pair(window, sigma);
+  auto it = c->tapsets.find(key);
+  if (it != c->tapsets.end()) {
+    c->taps = it->second;
+    return HDR_OK;
+  }
+  int rc = evict_if_full(c, c->tapsets, [](double* t) { cudaFree(t); });
+  if (rc) return rc;
   double k[31], sum = 0.0;
   for (int i = -r; i <= r; ++i) {
     double x = (double)i / sigma;
@@ -595,10 +667,15 @@ static int ensure_taps(hdr_ctx* c, int window, double sigma) {
   }
   for (int i = 0; i < 2 * r + 1; ++i) sum += k[i];
   for (int i = 0; i < 2 * r + 1; ++i) k[i] /= sum;
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(c->taps, k, sizeof(double) * (2 * r + 1), cudaMemcpyHostToDevice));
-  c->taps_window = window;
-  c->taps_sigma = sigma;
+  double* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(double) * 32));
+  cudaError_t e = cudaMemcpy(d, k, sizeof(double) * (2 * r + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return fail(HDR_ERR_CUDA, std::string("taps upload: ") + cudaGetErrorString(e));
+  }
+  c->tapsets[key] = d;
+  c->taps = d;
   return HDR_OK;
 }
 
@@ -815,7 +892,7 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
     int iters = l == 0 ? p->iterations : p->coarse_iterations;
     double eps = 2.0 * p->eps_px / (double)d[l].w;  // MatcherParams.weed_params
     launch_weed(c->raw, raw_count, nt, d[l].w, d[l].h, iters, eps,
-                c->keys + 2 * (size_t)c->keys_iters * l, p->delta, c->fits, c->mask, c->witness,
+                c->keyset->keys + 2 * (size_t)c->keyset->iters * l, p->delta, c->keyset->fits, c->mask, c->witness,
                 grey, s);
     launch_finish_level(c->raw, raw_count, c->mask, d[l].w, d[l].h, l, c->weeded, weeded_count,
                         nullptr, c->hpred, out_h, info, l == 0 ? out_matches : nullptr, nullptr,
@@ -944,6 +1021,7 @@ static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const 
 
 extern "C" int hdr_register_and_fuse(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
                                      const float* ref, const float* src, const hdr_outputs* o) {
+  CtxDevice dg_(c);
   int rc = check_pair_args(c, p, w, h, ref, src, o);
   if (rc) return rc;
   return enqueue_pair(c, p, w, h, ref, src, o);
@@ -961,6 +1039,7 @@ static int check_raw(int channels, int bits) {
 
 extern "C" int hdr_decode_image(hdr_ctx* c, const void* raw, int32_t w, int32_t h,
                                 int32_t channels, int32_t bits, float* rgb) {
+  CtxDevice dg_(c);
   NEED(c && raw && rgb, "null argument");
   int rc = check_raw(channels, bits);
   if (rc) return rc;
@@ -969,6 +1048,7 @@ extern "C" int hdr_decode_image(hdr_ctx* c, const void* raw, int32_t w, int32_t 
 }
 
 extern "C" int hdr_encode_u8(hdr_ctx* c, const float* img, int64_t n, uint8_t* out) {
+  CtxDevice dg_(c);
   NEED(c && img && out, "null argument");
   launch_encode_u8(img, n, out, c->stream);
   return check_launch();
@@ -976,6 +1056,7 @@ extern "C" int hdr_encode_u8(hdr_ctx* c, const float* img, int64_t n, uint8_t* o
 
 extern "C" int hdr_dark_count(hdr_ctx* c, const float* img, int32_t channels, int64_t n,
                               float dark_level, uint64_t* out) {
+  CtxDevice dg_(c);
   NEED(c && img && out, "null argument");
   NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
   launch_dark_count(img, channels, n, dark_level, reinterpret_cast<unsigned long long*>(out),
@@ -985,6 +1066,7 @@ extern "C" int hdr_dark_count(hdr_ctx* c, const float* img, int32_t channels, in
 
 extern "C" int hdr_mean_luminance(hdr_ctx* c, const float* img, int32_t channels, int64_t n,
                                   double* out) {
+  CtxDevice dg_(c);
   NEED(c && img && out, "null argument");
   NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
   launch_mean_luminance(img, channels, n, out, c->stream);
@@ -999,6 +1081,7 @@ extern "C" int hdr_register_and_fuse_raw(hdr_ctx* c, const hdr_params* p, int32_
                                          const void* ref_raw, const void* src_raw,
                                          int32_t channels, int32_t bits, int32_t use_graph,
                                          const hdr_outputs* o, uint8_t* composite_u8) {
+  CtxDevice dg_(c);
   NEED(c && ref_raw && src_raw, "null argument");
   int rc = check_raw(channels, bits);
   if (rc) return rc;
@@ -1020,6 +1103,7 @@ extern "C" int hdr_register_and_fuse_raw(hdr_ctx* c, const hdr_params* p, int32_
 extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
                                            const float* ref, const float* src,
                                            const hdr_outputs* o) {
+  CtxDevice dg_(c);
   int rc = check_pair_args(c, p, w, h, ref, src, o);
   if (rc) return rc;
   char key[768];
@@ -1042,7 +1126,15 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
       snprintf(pk, sizeof pk, ";%p", (void*)k.ev[i]);
       kkey += pk;
     }
+  if (c->graphs.size() >= kMaxGraphs && !c->graphs.count(kkey)) {
+    auto lru = c->graphs.begin();
+    for (auto it = c->graphs.begin(); it != c->graphs.end(); ++it)
+      if (it->second.used < lru->second.used) lru = it;
+    if (lru->second.exec) cudaGraphExecDestroy(lru->second.exec);
+    c->graphs.erase(lru);
+  }
   GraphEntry& g = c->graphs[kkey];
+  g.used = ++c->graph_clock;
   if (!g.exec) {
     // capture on the context's private stream (the caller's may be the
     // legacy default stream, which cannot be captured); replay on theirs
@@ -1091,6 +1183,7 @@ extern "C" int hdr_register_and_fuse_graph(hdr_ctx* c, const hdr_params* p, int3
 
 // ------------------------------------------------------------ per-stage twins
 extern "C" int hdr_luminance(hdr_ctx* c, const float* rgb, int64_t n, float* lum) {
+  CtxDevice dg_(c);
   NEED(c && rgb && lum, "null argument");
   NEED(n >= 0, "bad size");
   int rc = check_ptr_align(rgb, 16, "rgb");
@@ -1102,6 +1195,7 @@ extern "C" int hdr_luminance(hdr_ctx* c, const float* rgb, int64_t n, float* lum
 
 extern "C" int hdr_match_histogram(hdr_ctx* c, const float* src, int64_t n_src, const float* ref,
                                    int64_t n_ref, int32_t stride, float* out) {
+  CtxDevice dg_(c);
   NEED(c && src && ref && out, "null argument");
   NEED(n_src > 0 && n_ref > 0 && stride >= 1, "bad size");
   cudaStream_t s = c->stream;
@@ -1118,6 +1212,7 @@ extern "C" int hdr_match_histogram(hdr_ctx* c, const float* src, int64_t n_src, 
 extern "C" int hdr_build_pyramid(hdr_ctx* c, const float* img, int32_t w, int32_t h,
                                  int32_t max_levels, int32_t min_dim, float** out_levels,
                                  int32_t* n_levels) {
+  CtxDevice dg_(c);
   NEED(c && img && out_levels && n_levels, "null argument");
   if (std::min(w, h) < min_dim)
     return fail(HDR_ERR_INVALID, "input below " + std::to_string(min_dim) + " pixels in one dimension");
@@ -1138,6 +1233,7 @@ extern "C" int hdr_build_pyramid(hdr_ctx* c, const float* img, int32_t w, int32_
 }
 
 extern "C" int hdr_integral(hdr_ctx* c, const float* img, int32_t w, int32_t h, double* table) {
+  CtxDevice dg_(c);
   NEED(c && img && table && w >= 1 && h >= 1, "bad argument");
   NEED(w <= c->W && h <= c->H, "image larger than the workspace");
   SatBatch sb;
@@ -1169,6 +1265,7 @@ static int detect_one(hdr_ctx* c, const float* lum, int w, int h, int tile, doub
 
 extern "C" int hdr_detect_corners(hdr_ctx* c, const float* lum, int32_t w, int32_t h, int32_t tile,
                                   double threshold, int32_t half, double* corners, int32_t* count) {
+  CtxDevice dg_(c);
   NEED(c && lum && corners && count, "null argument");
   if (tile < 16) return fail(HDR_ERR_INVALID, "tile must be >= 16");
   NEED((int64_t)(w + 1) * (h + 1) <= (int64_t)(c->W + 1) * (c->H + 1), "image larger than the workspace");
@@ -1186,6 +1283,7 @@ extern "C" int hdr_detect_corners(hdr_ctx* c, const float* lum, int32_t w, int32
 extern "C" int hdr_ssd_match(hdr_ctx* c, const float* ref, const float* src, int32_t w, int32_t h,
                              const int32_t* pts, int32_t n, int32_t radius, int32_t patch,
                              double* out, uint8_t* found) {
+  CtxDevice dg_(c);
   NEED(c && ref && src && pts && out && found, "null argument");
   NEED(radius >= 1 && patch >= 3 && patch % 2 == 1, "bad radius/patch");
   size_t side = 2 * (size_t)radius + patch;
@@ -1197,6 +1295,7 @@ extern "C" int hdr_ssd_match(hdr_ctx* c, const float* ref, const float* src, int
 extern "C" int hdr_match_level(hdr_ctx* c, const hdr_params* p, const float* lum_ref,
                                const float* lum_src, int32_t w, int32_t h, const double* h_pred,
                                double* raw, int32_t* count) {
+  CtxDevice dg_(c);
   NEED(c && p && lum_ref && lum_src && h_pred && raw && count, "null argument");
   if (p->tile < 16) return fail(HDR_ERR_INVALID, "tile must be >= 16");
   int nt = ntiles_of(w, h, p->tile);
@@ -1242,6 +1341,7 @@ __global__ void widen_kept_kernel(const uint32_t* mask, const int32_t* wit, int 
 extern "C" int hdr_weed(hdr_ctx* c, const double* matches, int32_t n, int32_t w, int32_t h,
                         int32_t iterations, double eps, uint64_t seed, int32_t delta, int64_t* kept,
                         int32_t* n_kept, int64_t* witness) {
+  CtxDevice dg_(c);
   NEED(c && matches && kept && n_kept, "null argument");
   if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 matches to weed");
   if (iterations < 1) return fail(HDR_ERR_INVALID, "iterations must be >= 1");
@@ -1276,6 +1376,7 @@ static int fit_status_to_rc(int32_t st) {
 
 extern "C" int hdr_fit_matches_homography(hdr_ctx* c, const double* matches, int32_t n, int32_t w,
                                           int32_t h, double* H) {
+  CtxDevice dg_(c);
   NEED(c && matches && H, "null argument");
   if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
   NEED(n <= c->rows_cap, "too many matches for the workspace");
@@ -1291,6 +1392,7 @@ extern "C" int hdr_fit_matches_homography(hdr_ctx* c, const double* matches, int
 
 extern "C" int hdr_fit_homography(hdr_ctx* c, const double* ref_pts, const double* src_pts,
                                   int32_t n, double* H) {
+  CtxDevice dg_(c);
   NEED(c && ref_pts && src_pts && H, "null argument");
   if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
   cudaStream_t s = c->stream;
@@ -1304,12 +1406,14 @@ extern "C" int hdr_fit_homography(hdr_ctx* c, const double* ref_pts, const doubl
 
 extern "C" int hdr_inlier_mask(hdr_ctx* c, const double* H, const double* ref_pts,
                                const double* src_pts, int32_t n, double eps, uint8_t* mask) {
+  CtxDevice dg_(c);
   NEED(c && H && ref_pts && src_pts && mask, "null argument");
   launch_inlier_mask(H, ref_pts, src_pts, n, eps, mask, c->stream);
   return check_launch();
 }
 
 extern "C" int hdr_homography_flow(hdr_ctx* c, const double* H, int32_t w, int32_t h, float* flow) {
+  CtxDevice dg_(c);
   NEED(c && H && flow, "null argument");
   launch_hflow(H, w, h, flow, c->stream);
   return check_launch();
@@ -1318,6 +1422,7 @@ extern "C" int hdr_homography_flow(hdr_ctx* c, const double* H, int32_t w, int32
 extern "C" int hdr_match_stack(hdr_ctx* c, const hdr_params* p, int32_t w, int32_t h,
                                const float* ref, const float* src, double* matches,
                                double* raw_matches, double* homography, int32_t* info) {
+  CtxDevice dg_(c);
   NEED(c && p && ref && src && matches && raw_matches && homography && info, "null argument");
   char msg[128];
   int rc = hdr_params_validate(p, msg, sizeof msg);
@@ -1336,6 +1441,7 @@ extern "C" int hdr_match_stack(hdr_ctx* c, const hdr_params* p, int32_t w, int32
 
 extern "C" int hdr_sparse_maps(hdr_ctx* c, const double* matches, int32_t m, int32_t w, int32_t h,
                                double* pu, double* pv, double* n) {
+  CtxDevice dg_(c);
   NEED(c && pu && pv && n && (m == 0 || matches), "null argument");
   NEED((int64_t)w * h <= c->P, "image larger than the workspace");
   cudaStream_t s = c->stream;
@@ -1353,6 +1459,7 @@ extern "C" int hdr_sparse_maps(hdr_ctx* c, const double* matches, int32_t m, int
 
 extern "C" int hdr_dt_filter(hdr_ctx* c, const float* guide, double* planes, int32_t k, int32_t w,
                              int32_t h, double sigma_s, double sigma_r, int32_t passes) {
+  CtxDevice dg_(c);
   NEED(c && guide && planes, "null argument");
   if (!(sigma_s > 0) || !(sigma_r > 0)) return fail(HDR_ERR_INVALID, "sigma_s and sigma_r must be positive");
   if (passes < 1) return fail(HDR_ERR_INVALID, "passes must be >= 1");
@@ -1367,6 +1474,7 @@ extern "C" int hdr_dt_filter(hdr_ctx* c, const float* guide, double* planes, int
 
 extern "C" int hdr_densify_finalize(hdr_ctx* c, const double* smooth, int32_t w, int32_t h,
                                     const double* fallback, double floor_, float* flow) {
+  CtxDevice dg_(c);
   NEED(c && smooth && flow, "null argument");
   // the fused kernel with the warp outputs switched off
   int64_t P = (int64_t)w * h;
@@ -1379,6 +1487,7 @@ extern "C" int hdr_densify_finalize(hdr_ctx* c, const double* smooth, int32_t w,
 
 extern "C" int hdr_warp_image(hdr_ctx* c, const float* src, int32_t channels, int32_t w, int32_t h,
                               const float* flow, float* warped, uint8_t* valid) {
+  CtxDevice dg_(c);
   NEED(c && src && flow && warped && valid, "null argument");
   NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
   if (channels == 3 && (int64_t)w * h <= c->P) {
@@ -1394,6 +1503,7 @@ extern "C" int hdr_warp_image(hdr_ctx* c, const float* src, int32_t channels, in
 
 extern "C" int hdr_ssim_map(hdr_ctx* c, const float* a, const float* b, int32_t w, int32_t h,
                             int32_t window, double sigma, float* out) {
+  CtxDevice dg_(c);
   NEED(c && a && b && out, "null argument");
   if (window % 2 != 1) return fail(HDR_ERR_INVALID, "window must be odd");
   int rc = ensure_taps(c, window, sigma);
@@ -1404,6 +1514,7 @@ extern "C" int hdr_ssim_map(hdr_ctx* c, const float* a, const float* b, int32_t 
 
 extern "C" int hdr_make_ssim(hdr_ctx* c, const float* lum_ref, const float* warped, int32_t w,
                              int32_t h, int32_t window, double sigma, float* out) {
+  CtxDevice dg_(c);
   NEED(c && lum_ref && warped && out, "null argument");
   int64_t P = (int64_t)w * h;
   NEED(P <= c->P, "image larger than the workspace");
@@ -1421,6 +1532,7 @@ extern "C" int hdr_make_ssim(hdr_ctx* c, const float* lum_ref, const float* warp
 }
 
 extern "C" int hdr_quality_weights(hdr_ctx* c, const float* rgb, int32_t w, int32_t h, float* out) {
+  CtxDevice dg_(c);
   NEED(c && rgb && out, "null argument");
   launch_quality(rgb, w, h, out, c->stream);
   return check_launch();
@@ -1429,6 +1541,7 @@ extern "C" int hdr_quality_weights(hdr_ctx* c, const float* rgb, int32_t w, int3
 extern "C" int hdr_fusion_weights(hdr_ctx* c, const float* ref, const float* warped,
                                   const float* ssim, const uint8_t* valid, int32_t w, int32_t h,
                                   float* w_ref, float* w_src) {
+  CtxDevice dg_(c);
   NEED(c && ref && warped && ssim && valid && w_ref && w_src, "null argument");
   launch_fusion_weights(ref, warped, ssim, valid, w, h, w_ref, w_src, c->stream);
   return check_launch();
@@ -1436,6 +1549,7 @@ extern "C" int hdr_fusion_weights(hdr_ctx* c, const float* ref, const float* war
 
 extern "C" int hdr_cornerness(hdr_ctx* c, const double* table, int32_t w, int32_t h,
                               const int32_t* xy, int32_t n, int32_t half, double* out) {
+  CtxDevice dg_(c);
   NEED(c && table && xy && out, "null argument");
   NEED(half >= 1 && w >= 1 && h >= 1, "bad arguments");
   launch_cornerness(table, w + 1, xy, n, half, out, c->stream);
@@ -1444,6 +1558,7 @@ extern "C" int hdr_cornerness(hdr_ctx* c, const double* table, int32_t w, int32_
 
 extern "C" int hdr_pyr_down(hdr_ctx* c, const double* in, int32_t w, int32_t h, int32_t ch,
                             double* out) {
+  CtxDevice dg_(c);
   NEED(c && in && out, "null argument");
   NEED(w >= 1 && h >= 1 && ch >= 1, "empty image");
   launch_pyr_down(in, w, h, ch, out, c->stream);
@@ -1452,6 +1567,7 @@ extern "C" int hdr_pyr_down(hdr_ctx* c, const double* in, int32_t w, int32_t h, 
 
 extern "C" int hdr_pyr_up(hdr_ctx* c, const double* in, int32_t cw, int32_t cht, int32_t ch,
                           int32_t w, int32_t h, const double* base, int32_t sign, double* out) {
+  CtxDevice dg_(c);
   NEED(c && in && out, "null argument");
   NEED(w >= 1 && h >= 1 && ch >= 1 && cw == (w + 1) / 2 && cht == (h + 1) / 2,
        "coarse shape must be the ceil-half of the fine shape");
@@ -1461,6 +1577,7 @@ extern "C" int hdr_pyr_up(hdr_ctx* c, const double* in, int32_t cw, int32_t cht,
 
 extern "C" int hdr_fuse(hdr_ctx* c, const float* ref, const float* warped, const float* ssim,
                         const uint8_t* valid, int32_t w, int32_t h, int32_t levels, float* out) {
+  CtxDevice dg_(c);
   NEED(c && ref && warped && ssim && valid && out, "null argument");
   NEED((int64_t)w * h <= c->P, "image larger than the workspace");
   std::vector<Dims> fd;
@@ -1476,6 +1593,7 @@ extern "C" int hdr_fuse_stack(hdr_ctx* c, int32_t n, const float* const* frames,
 extern "C" int hdr_register_and_fuse_stack(hdr_ctx* c, const hdr_params* p, int32_t n,
                                            int32_t w, int32_t h, const float* const* frames,
                                            const hdr_outputs* const* outs, float* composite) {
+  CtxDevice dg_(c);
   NEED(c && p && frames && outs && composite, "null argument");
   NEED(n >= 2 && n <= kMaxFuseFrames, "stacks take 2..4 frames");
   const float* warped[kMaxFuseFrames] = {};
@@ -1499,6 +1617,7 @@ extern "C" int hdr_register_and_fuse_stack(hdr_ctx* c, const hdr_params* p, int3
 extern "C" int hdr_fuse_stack(hdr_ctx* c, int32_t n, const float* const* frames,
                               const float* const* ssim, const uint8_t* const* valid, int32_t w,
                               int32_t h, int32_t levels, float* out) {
+  CtxDevice dg_(c);
   NEED(c && frames && out, "null argument");
   NEED(n >= 2 && n <= kMaxFuseFrames, "stack fusion takes 2..4 frames");
   NEED(n == 2 || (ssim && valid), "null argument");

@@ -1,6 +1,14 @@
-"""Device plumbing: one hdr context (preallocated workspace) per CUDA device,
-bound to torch's current stream at every call. Torch is used for device
-memory and streams only; all arithmetic happens in libhdrb200.so.
+"""Device plumbing: hdr contexts (preallocated workspaces) for the drop-in
+calls. Torch is used for device memory and streams only; all arithmetic
+happens in libhdrb200.so.
+
+Re-entrancy (the reference's functions are pure): every
+host thread gets its own context per device, so concurrent calls never share
+scratch, host state or a graph cache, and a thread only ever resizes (closes)
+its own context. Within one thread a context follows torch's current stream;
+when a call moves it to another stream, the new stream first waits for the
+work already queued on the old one (an event, no host sync), so asynchronous
+enqueues on different streams never overlap on the same scratch.
 """
 
 from __future__ import annotations
@@ -13,8 +21,7 @@ import torch
 
 from . import _native
 
-_lock = threading.Lock()
-_engines: dict[int, "Engine"] = {}
+_tls = threading.local()
 
 
 def _require_cuda():
@@ -30,15 +37,28 @@ class Engine:
         self.width, self.height, self.device = width, height, device
         handle = ctypes.c_void_p()
         with torch.cuda.device(device):
-            stream = torch.cuda.current_stream(device).cuda_stream
-            _native.check(_native.lib().hdr_ctx_create(width, height, ctypes.c_void_p(stream),
+            self.stream = torch.cuda.current_stream(device)
+            _native.check(_native.lib().hdr_ctx_create(width, height,
+                                                       ctypes.c_void_p(self.stream.cuda_stream),
                                                        ctypes.byref(handle)), "hdr_ctx_create")
         self.handle = handle
 
     def bind_stream(self, stream: torch.cuda.Stream | None = None):
+        """Queue this context's next work on `stream` (default: torch's
+        current stream on the context's device), ordered after everything
+        it already queued elsewhere."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if s.cuda_stream != self.stream.cuda_stream:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            s.wait_event(ev)
+            self.stream = s
         _native.check(_native.lib().hdr_ctx_set_stream(self.handle, ctypes.c_void_p(s.cuda_stream)))
         return self.handle
+
+    def drain(self):
+        """Wait for every queued use of the workspace (before freeing it)."""
+        self.stream.synchronize()
 
     def sync(self):
         _native.check(_native.lib().hdr_ctx_sync(self.handle), "hdr_ctx_sync")
@@ -56,22 +76,25 @@ class Engine:
 
 
 def engine(width: int, height: int, device: int | None = None) -> Engine:
-    """Shared context for `device` with capacity >= (width, height)."""
+    """This thread's context for `device`, with capacity >= (width, height),
+    bound to the current stream."""
     _require_cuda()
     dev = torch.cuda.current_device() if device is None else device
-    with _lock:
-        e = _engines.get(dev)
-        if e is None or e.width < width or e.height < height:
-            if e is not None:
-                torch.cuda.synchronize(dev)
-                w, h = max(width, e.width), max(height, e.height)
-                e.close()
-            else:
-                w, h = width, height
-            e = Engine(w, h, dev)
-            _engines[dev] = e
-        e.bind_stream()
-        return e
+    engines = getattr(_tls, "engines", None)
+    if engines is None:
+        engines = _tls.engines = {}
+    e = engines.get(dev)
+    if e is None or e.width < width or e.height < height:
+        if e is not None:
+            e.drain()
+            w, h = max(width, e.width), max(height, e.height)
+            e.close()
+        else:
+            w, h = width, height
+        e = Engine(w, h, dev)
+        engines[dev] = e
+    e.bind_stream()
+    return e
 
 
 def engine_for_rows(n_rows: int, device: int | None = None) -> Engine:

@@ -5,7 +5,8 @@ import time
 sys.path.insert(0, ".")
 import torch  # noqa: E402
 
-from paper_1504_01441_b200 import pipeline, synth  # noqa: E402
+from paper_1504_01441_b200 import pipeline  # noqa: E402
+from harness import synth  # noqa: E402
 
 w = int(sys.argv[1]) if len(sys.argv) > 1 else 2592
 h = int(sys.argv[2]) if len(sys.argv) > 2 else 1944

@@ -4,10 +4,12 @@ import os
 
 import numpy as np
 
-from paper_1504_01441_b200 import synth
+from harness import synth
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 SCENES = ["vga_s0", "vga_rot_s1", "qvga_s2", "r960_s3"]
+# BASELINE configs[1] (5MP) and configs[3] (12MP), from the real reference
+BIG_SCENES = ["c2_5mp_s0", "c4_12mp_s0"]
 
 
 def digest(a) -> str:

@@ -175,7 +175,8 @@ def test_choose_reference_and_dumps(tmp_path):
 
 def test_flow_to_color_per_pixel():
     """viz.flow_to_color = the per-pixel hue-sector colouring the reference
-    intends (its fancy-indexing form would gather (h, w, h, w); see viz.py)."""
+    intends (its fancy-indexing form would gather (h, w, h, w); see viz.py),
+    checked against the reference's six-entry ramp evaluated per pixel."""
     from paper_1504_01441_b200 import viz
     f = np.random.default_rng(0).normal(size=(5, 6, 2)).astype(np.float32)
     got = viz.flow_to_color(f)
@@ -188,9 +189,32 @@ def test_flow_to_color_per_pixel():
             t = h6[i, j] - s
             ramp = [1.0, 1.0 - t, 0.0, 0.0, t, 1.0]
             rgb = np.array([ramp[s % 6], ramp[(s + 4) % 6], ramp[(s + 2) % 6]])
-            np.testing.assert_array_equal(got[i, j], (1.0 - mag[i, j] * (1.0 - rgb)).astype(np.float32))
+            np.testing.assert_allclose(got[i, j], (1.0 - mag[i, j] * (1.0 - rgb)).astype(np.float32),
+                                       atol=1e-6)
     hm = viz.heatmap(np.array([[-1.0, 0.0, 1.0]]), -1.0, 1.0)
     np.testing.assert_array_equal(hm[0], np.array([[0, 0, 1], [1, 1, 1], [1, 0, 0]], dtype=np.float32))
+    x = np.random.default_rng(1).random((4, 5))
+    t = x
+    ref_rgb = np.stack([np.clip(2 * t, 0, 1), 1 - np.abs(2 * t - 1), np.clip(2 * (1 - t), 0, 1)], -1)
+    np.testing.assert_allclose(viz.heatmap(x, 0.0, 1.0), ref_rgb.astype(np.float32), atol=1e-6)
+
+
+def test_overlay_matches_segments():
+    """Every pixel the reference's per-match line walk (viz.py:44-58) paints
+    is painted, in green for the displacement and red at the reference end."""
+    from paper_1504_01441_b200 import viz
+    lum = np.full((40, 50), 0.5, dtype=np.float32)
+    m = np.array([[3.0, 4.0, 20.0, 9.0, 0.1], [45.0, 30.0, 60.0, 35.0, 0.2]])
+    got = viz.overlay_matches(lum, m)
+    canvas = np.repeat(lum[:, :, None], 3, axis=2).copy()
+    for xr, yr, xs, ys, _ in m:
+        n = int(max(abs(xs - xr), abs(ys - yr))) + 1
+        px, py = np.round(np.linspace(xr, xs, n)).astype(int), np.round(np.linspace(yr, ys, n)).astype(int)
+        ok = (px >= 0) & (px < 50) & (py >= 0) & (py < 40)
+        canvas[py[ok], px[ok]] = (0.1, 0.9, 0.2)
+    for xr, yr, _, _, _ in m:
+        canvas[int(yr), int(xr)] = (1.0, 0.2, 0.1)
+    np.testing.assert_array_equal(got, canvas.astype(np.float32))
 
 
 @pytest.mark.gpu

@@ -15,8 +15,8 @@ import torch
 
 from golden_util import SCENES, digest, load, scene_inputs
 from oracle import hdr_oracle as O
-from paper_1504_01441_b200 import (densify, fusion, geometry, image, matcher, pipeline,
-                                   synth, weeding)
+from harness import synth
+from paper_1504_01441_b200 import densify, fusion, geometry, image, matcher, pipeline, weeding
 from paper_1504_01441_b200.errors import RegistrationError
 
 pytestmark = pytest.mark.gpu
@@ -246,7 +246,11 @@ def test_ssim_and_fuse_stages(scene):
     assert np.abs(comp - o.composite).max() < RADIANCE_TOL
 
 
-def check_pair(res, o, strict=True):
+def check_pair(res, o):
+    """The whole pair: sparse results exact, dense outputs through
+    test_gpu_headline.check_dense (valid identical; SSIM 1e-4 outside the
+    window of a quantisation flip of the warped luminance)."""
+    from test_gpu_headline import check_dense
     assert res.level_counts == o.level_counts
     assert_rows(res.raw_matches, o.raw_matches)
     assert_rows(res.matches, o.matches)
@@ -255,11 +259,7 @@ def check_pair(res, o, strict=True):
         assert rel_h(res.homography, o.homography) < H_RTOL
     assert res.flow.dtype == np.float32 and res.ssim.dtype == np.float64
     assert res.valid.dtype == bool and res.composite.dtype == np.float32
-    assert np.abs(res.flow - o.flow).max() < FLOW_TOL
-    assert np.abs(res.warped - o.warped).max() < RADIANCE_TOL
-    assert (res.valid != o.valid).mean() < 1e-4
-    assert np.abs(res.ssim - o.ssim).max() < 10 * SSIM_TOL
-    assert np.abs(res.composite - o.composite).max() < RADIANCE_TOL
+    check_dense(res, o)
 
 
 def test_register_and_fuse_end_to_end(scene):
@@ -283,6 +283,75 @@ def test_graph_replay_matches_eager(cuda):
     torch.cuda.synchronize()
     for name in ("composite", "flow", "warped", "valid", "ssim", "info"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
+
+
+def test_graph_cache_survives_parameter_changes(cuda):
+    """A cached pair graph replays against the key / fit / tap buffers it was
+    captured with: calls with more RANSAC iterations, another seed or another
+    SSIM window in between (which allocate new parameter sets) must not
+    change what the first graph computes."""
+    st = synth.synth_stack(synth.working_spec(640, 480), 0)
+    ref = torch.from_numpy(st.ref).cuda()
+    src = torch.from_numpy(st.src).cuda()
+    p = pipeline.PipelineParams()
+    a = pipeline.PairBuffers(640, 480, 0)
+    b = pipeline.PairBuffers(640, 480, 0)
+    pipeline.enqueue_pair(ref, src, p, a, graph=True)
+    torch.cuda.synchronize()
+    first = {n: getattr(a, n).clone() for n in ("composite", "flow", "ssim", "matches", "info")}
+    for q in (pipeline.PipelineParams(iterations=512, coarse_iterations=128),
+              pipeline.PipelineParams(seed=7), pipeline.PipelineParams(ssim_window=7, ssim_sigma=1.0)):
+        pipeline.enqueue_pair(ref, src, q, b, graph=True)
+    pipeline.enqueue_pair(ref, src, p, a, graph=True)
+    torch.cuda.synchronize()
+    for n, t in first.items():
+        assert torch.equal(getattr(a, n), t), n
+
+
+def test_concurrent_threads_are_independent(cuda):
+    """The drop-in is re-entrant like the reference's pure functions: two
+    host threads calling register_and_fuse at once on different scenes get
+    exactly what each gets alone (each thread owns its workspace)."""
+    import threading
+    scenes = [synth.synth_stack(synth.working_spec(640, 480), s) for s in (0, 3)]
+    alone = [pipeline.register_and_fuse(st.ref, st.src) for st in scenes]
+    got = [[None] * 3 for _ in scenes]
+    errs = []
+
+    def work(i):
+        try:
+            for r in range(3):
+                got[i][r] = pipeline.register_and_fuse(scenes[i].ref, scenes[i].src)
+        except Exception as exc:  # pragma: no cover - surfaced below
+            errs.append(exc)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        for r in range(3):
+            for n in ("composite", "flow", "ssim", "matches", "valid"):
+                np.testing.assert_array_equal(getattr(got[i][r], n), getattr(alone[i], n))
+
+
+def test_async_enqueues_on_two_streams(cuda):
+    """enqueue_pair on two streams without a host sync in between: the shared
+    thread context orders the second after the first (event), so both pairs
+    come out right."""
+    scenes = [synth.synth_stack(synth.working_spec(640, 480), s) for s in (0, 3)]
+    alone = [pipeline.register_and_fuse(st.ref, st.src) for st in scenes]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    bufs = [pipeline.PairBuffers(640, 480, 0) for _ in scenes]
+    ins = [(torch.from_numpy(st.ref).cuda(), torch.from_numpy(st.src).cuda()) for st in scenes]
+    torch.cuda.synchronize()
+    for k, s in enumerate((s1, s2)):
+        pipeline.enqueue_pair(ins[k][0], ins[k][1], pipeline.PipelineParams(), bufs[k], stream=s)
+    torch.cuda.synchronize()
+    for k in range(2):
+        np.testing.assert_array_equal(bufs[k].composite.cpu().numpy(), alone[k].composite)
 
 
 def test_registration_error_parity(cuda):
@@ -318,24 +387,6 @@ def test_gray_inputs_and_torch_inputs(cuda):
     assert isinstance(t.composite, torch.Tensor) and t.composite.is_cuda
     n = pipeline.register_and_fuse(st.ref, st.src)
     np.testing.assert_array_equal(t.composite.cpu().numpy(), n.composite)
-
-
-@pytest.mark.slow
-def test_5mp_pair_end_to_end(cuda):
-    st = synth.synth_stack(synth.working_spec(2592, 1944), 0)
-    res = pipeline.register_and_fuse(st.ref, st.src)
-    o = O.register_and_fuse(st.ref, st.src)
-    check_pair(res, o)
-
-
-@pytest.mark.slow
-def test_12mp_pair_end_to_end(cuda):
-    """BASELINE config C4: 12MP (4000x3000) pair (the "16x16 cell grid" is a
-    label only: the reference's 64-px detection tiles, 63x47 of them)."""
-    st = synth.synth_stack(synth.working_spec(4000, 3000), 0)
-    res = pipeline.register_and_fuse(st.ref, st.src)
-    o = O.register_and_fuse(st.ref, st.src)
-    check_pair(res, o)
 
 
 def test_batch_runner_raw_path(cuda):

@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 from oracle import hdr_oracle as O
-from paper_1504_01441_b200 import densify, fusion, image, synth
+from harness import synth
+from paper_1504_01441_b200 import densify, fusion, image
 
 pytestmark = pytest.mark.gpu
 

@@ -227,7 +227,7 @@ def test_register_and_fuse_random_scenes(cuda, seed, w, h, stops, rot):
     """End to end on random scene recipes and sizes: the same verdict as the
     oracle (RegistrationError or not), identical level counts and match
     coordinates, composite within 1e-3."""
-    from paper_1504_01441_b200 import synth
+    from harness import synth
     from paper_1504_01441_b200.errors import RegistrationError
     st_ = synth.synth_stack(synth.working_spec(w, h, stops=stops, rotation_deg=rot), seed)
     try:

@@ -4,12 +4,12 @@ REAL reference (oracle/gen_golden.py). CPU only."""
 import numpy as np
 import pytest
 
-from golden_util import SCENES, digest, load, scene_inputs
+from golden_util import BIG_SCENES, SCENES, digest, load, scene_inputs
 from oracle import hdr_oracle as O
-from paper_1504_01441_b200 import synth
+from harness import synth
 
 
-@pytest.fixture(scope="module", params=SCENES)
+@pytest.fixture(scope="module", params=SCENES + BIG_SCENES)
 def scene(request):
     fx = load(request.param)
     ref, src = scene_inputs(fx)

@@ -15,8 +15,10 @@ from oracle import gen_golden as G
 from oracle import hdr_oracle as O
 
 
-def test_oracle_stack_matches_reference_composition():
-    fx = load("stack3_vga")
+@pytest.mark.parametrize("name", ["stack3_vga", "stack3_5mp"])
+def test_oracle_stack_matches_reference_composition(name):
+    """stack3_5mp is BASELINE config C3 at full size (2592x1944)."""
+    fx = load(name)
     w, h, seed = (int(v) for v in fx["scene"])
     frames, exposures = G.stack_frames(w, h, seed)
     comp, k, regs = O.register_and_fuse_stack(frames, exposures)
@@ -89,7 +91,8 @@ def test_stack3_5mp_gpu_matches_oracle():
 def test_stack_errors(cuda):
     """Shape / count errors as ValueError / ConfigError; a source frame that
     cannot register raises RegistrationError like the pairwise reference."""
-    from paper_1504_01441_b200 import pipeline, synth
+    from paper_1504_01441_b200 import pipeline
+    from harness import synth
     from paper_1504_01441_b200.errors import ConfigError, RegistrationError
     st = synth.synth_stack(synth.working_spec(320, 240), 1)
     with pytest.raises(ValueError):

@@ -2,30 +2,48 @@
 """Benchmark: 5MP two-exposure pairs/sec registered+merged (BASELINE.json).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--total-pairs 512] [--no-extra-workloads]
 
-N > 1 is launched by torchrun (one process per GPU). Pairs are independent,
-so each rank owns its own resident batch: per-GPU work is fixed ("weak"
-scaling) and no collective touches the data path (timings are max-reduced
-over ranks with one tiny all-reduce after the timed region).
+One process per GPU. `--gpus N` with N > 1 outside torchrun re-launches this
+script under `torch.distributed.run` with N ranks (NCCL; LOCAL_RANK picks the
+device) and fails loudly when the box has fewer than N GPUs. Pairs are
+independent: no collective touches the data path; timing
+is max-reduced over ranks and per-scene output digests are gathered after
+the timed region to show that results do not depend on the rank or stream a
+pair ran on.
 
-A step = one batch of `--pairs` 5MP pairs per GPU (synthetic scenes of
-SURVEY.md §8(d) C2, rendered on the host, resident in HBM, each pair its own
-buffers so the batch (~1.9 GB of inputs) is far larger than the 126 MB L2).
-`e2e` is the same metric through the public batch API (runner.BatchRunner
-.run_host) with pinned host inputs: H2D of both frames and D2H of the
-composite + verdict words happen inside the timed region.
+Modes (BASELINE.json configs):
+  * default (configs[1], "weak"): a step = `--pairs` resident 5MP pairs per
+    GPU (synthetic scenes of SURVEY.md §8(d) C2; every pair reads its own
+    resident 121 MB copy of its scene, ~1.9 GB per GPU, far beyond the
+    126 MB L2);
+  * `--total-pairs 512` (configs[4], "strong"): a step = the rank's
+    contiguous share (dist.shard) of 512 pairs, all ranks drawing from the
+    same distinct scenes.
+Extra keys of the same line (unless --no-extra-workloads): configs[3] (12MP
+pairs) and configs[2] (5MP -2/0/+2 EV stacks), each with throughput, single
+item latency and its own CPU baseline; the drop-in single-call latency of
+`register_and_fuse(numpy, numpy)` with the full RegistrationOutput back.
 
---impl reference times the CPU oracle port of the reference (oracle/, the
-reference itself is pure Python and cannot travel to this box) on all host
-cores: one pair per process per step.
+`e2e` is the headline metric through the public batch API
+(runner.BatchRunner.run_host) with pinned host inputs: H2D of both frames and
+D2H of the composite + verdict words inside the timed region.
+
+CPU side (the reference arm and the `cpu_baseline` legs): the REAL reference
+(`hdrflow` installed in baseline/_ref, plus the one-line import shim of
+SURVEY.md §0) when present, else the oracle port in oracle/; one pair per
+process on the host cores. The `cpu_baseline` leg's outputs are kept and
+compared with the GPU's outputs of the same scenes (`checks.parity`).
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import multiprocessing as mp
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,17 +55,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 W5, H5 = 2592, 1944
+W12, H12 = 4000, 3000
 METRIC = "5MP 2-exposure pairs/sec registered+merged (1/2/4/8 B200) vs host-CPU ref"
 WORKLOAD = "5MP (2592x1944) two-exposure pair, registered + merged (BASELINE configs[1])"
+WORKLOAD_C5 = "batch of {n} synthetic 5MP pairs sharded by pair across the GPUs (BASELINE configs[4])"
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--pairs", type=int, default=16, help="resident pairs per GPU per step")
+    ap.add_argument("--pairs", type=int, default=16, help="resident pairs per GPU per step (weak mode)")
+    ap.add_argument("--total-pairs", type=int, default=0,
+                    help="strong mode (BASELINE configs[4]): this many pairs split across the ranks per step")
     ap.add_argument("--streams", type=int, default=8, help="compute streams of the device-resident runs")
     ap.add_argument("--e2e-streams", type=int, default=8, help="compute streams of the host-buffer runs")
     ap.add_argument("--scenes", type=int, default=4, help="distinct synthetic scenes")
@@ -55,51 +78,213 @@ def parse():
     ap.add_argument("--width", type=int, default=W5)
     ap.add_argument("--height", type=int, default=H5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-workloads", action="store_true",
+                    help="skip the 12MP / 5MP-stack legs and the drop-in latency")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-impl", choices=["auto", "reference", "port"], default="auto",
+                    help="CPU side: the real hdrflow from baseline/_ref, or the oracle port")
+    ap.add_argument("--selftest-cpu", action="store_true",
+                    help=argparse.SUPPRESS)  # launcher + rank plumbing on gloo, no GPU (tests/test_bench_launch.py)
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="hdr_set_option before the run (tuning hooks, e.g. dt_cols_grid_div=2)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+# ------------------------------------------------------------------ launcher / ranks
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def under_launcher() -> bool:
+    return "LOCAL_RANK" in os.environ and "WORLD_SIZE" in os.environ
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args, argv) -> int:
+    """Re-run this script under torch.distributed.run with args.gpus ranks."""
+    if not args.selftest_cpu:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}\n")
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def init_ranks(backend: str, local: int):
+    from paper_1504_01441_b200 import dist as hd
+    rank, world, _ = dist_env()
+    if world > 1:
+        hd.init(backend, local if backend == "nccl" else None)
+    return rank, world
+
+
+def assign_pairs(args, rank, world):
+    """Global pair indices this rank runs per step: weak mode owns `--pairs`
+    of its own; strong mode its dist.shard of --total-pairs."""
+    from paper_1504_01441_b200 import dist as hd
+    if args.total_pairs:
+        return list(hd.shard(args.total_pairs, world, rank))
+    return [rank * args.pairs + k for k in range(args.pairs)]
+
+
+def gather_digests(mine: dict) -> dict:
+    """{scene: set(digests)} over all ranks (after the timed region)."""
+    import torch.distributed as dist
+    allp = [mine]
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        allp = [None] * dist.get_world_size()
+        dist.all_gather_object(allp, mine)
+    merged = {}
+    for part in allp:
+        for scene, ds in part.items():
+            merged.setdefault(scene, set()).update(ds)
+    return merged
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
 
 
 # ------------------------------------------------------------------ scenes
-def _render(args):
+def _render(job):
     from harness import synth
-    w, h, seed = args
-    st = synth.synth_stack(synth.working_spec(w, h), seed)
-    return st.ref, st.src
+    kind, w, h, seed = job
+    if kind == "pair":
+        st = synth.synth_stack(synth.working_spec(w, h), seed)
+        return st.ref, st.src
+    # BASELINE configs[2]: -2/0/+2 EV stack (SURVEY.md §8(d) C3), frames in
+    # (+2, base, +4) order with the exposures the metering step reads
+    a = synth.synth_stack(synth.working_spec(w, h, stops=2.0), seed)
+    b = synth.synth_stack(synth.working_spec(w, h, stops=4.0), seed)
+    return [a.src, a.ref, b.src], [4.0, 1.0, 16.0]
 
 
-def render_scenes(n, w, h, base_seed):
-    jobs = [(w, h, base_seed + i) for i in range(n)]
+def render(kind, n, w, h, base_seed=0):
+    jobs = [(kind, w, h, base_seed + i) for i in range(n)]
     with mp.get_context("fork").Pool(min(n, os.cpu_count() or 1)) as pool:
         return pool.map(_render, jobs)
 
 
-# ------------------------------------------------------------------ CPU reference
-_CPU_PAIRS = None
+# ------------------------------------------------------------------ CPU side
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
 
 
-def _cpu_pair(i):
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+def cpu_impl(choice: str):
+    """('reference', hdrflow.pipeline) from baseline/_ref, else ('port', oracle)."""
+    if choice in ("auto", "reference") and os.path.isdir(os.path.join(REF_DIR, "hdrflow")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        try:
+            from hdrflow import matcher, pipeline
+            # SURVEY.md §0: pipeline.fit_fallback names fit_matches_homography,
+            # which pipeline.py never imports; without this the reference
+            # raises NameError on every successful registration
+            pipeline.fit_matches_homography = matcher.fit_matches_homography
+            return "reference", pipeline
+        except ImportError:
+            if choice == "reference":
+                raise
     from oracle import hdr_oracle as O
-    ref, src = _CPU_PAIRS[i % len(_CPU_PAIRS)]
+    return "port", O
+
+
+_CPU = {}
+
+
+def _cpu_item(i):
+    """One item of CPU work; returns its wall time and a parity summary."""
+    kind, impl, items = _CPU["kind"], _CPU["impl"], _CPU["items"]
+    item = items[i % len(items)]
     t = time.perf_counter()
-    out = O.register_and_fuse(ref, src)
-    return time.perf_counter() - t, len(out.matches)
+    if kind == "pair":
+        _, mod = cpu_impl(impl)
+        out = mod.register_and_fuse(item[0], item[1])
+        dt = time.perf_counter() - t
+        return dt, {"scene": i % len(items), "level_counts": [list(x) for x in out.level_counts],
+                    "matches": np.asarray(out.matches), "composite": np.asarray(out.composite),
+                    "valid": np.asarray(out.valid)}
+    frames, exposures = item
+    comp = cpu_stack(impl, frames, exposures)
+    return time.perf_counter() - t, {"scene": i % len(items), "composite": comp}
 
 
-def cpu_pool(pairs, procs):
-    global _CPU_PAIRS
-    _CPU_PAIRS = pairs
+def cpu_stack(impl, frames, exposures):
+    """BASELINE configs[2] on the CPU: the reference's functions composed as
+    the oracle's fuse_stack restates (reference choice by metering, pairwise
+    register_and_fuse per source, k-way Laplacian blend)."""
+    kind, mod = cpu_impl(impl)
+    if kind == "port":
+        comp, _, _ = mod.register_and_fuse_stack(frames, exposures)
+        return comp
+    from hdrflow import fusion, metering
+    k = metering.choose_reference(frames, exposures)
+    ref = frames[k]
+    warped, ws = [ref], [fusion.quality_weights(ref)]
+    for f, src in enumerate(frames):
+        if f == k:
+            continue
+        r = mod.register_and_fuse(ref, src)
+        warped.append(r.warped)
+        ws.append(fusion.quality_weights(r.warped) * np.clip(r.ssim, 0.0, 1.0)
+                  * r.valid.astype(np.float64))
+    tot = ws[0]
+    for x in ws[1:]:
+        tot = tot + x
+    ws = [x / tot for x in ws]
+    h, w = ref.shape[:2]
+    levels = fusion.default_fusion_levels(h, w)
+    laps = [fusion.laplacian_pyramid(x, levels) for x in warped]
+    gps = [fusion.gaussian_pyramid(x, levels) for x in ws]
+    blended = []
+    for lev in range(len(laps[0])):
+        acc = gps[0][lev][:, :, None] * laps[0][lev]
+        for f in range(1, len(warped)):
+            acc = acc + gps[f][lev][:, :, None] * laps[f][lev]
+        blended.append(acc)
+    return np.clip(fusion.collapse_pyramid(blended), 0.0, 1.0).astype(np.float32)
+
+
+def cpu_run(kind, items, procs, impl, steps=1):
+    """`steps` rounds of one item per process; returns (items/s, wall, results)."""
     for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[v] = "1"
-    return mp.get_context("fork").Pool(procs)
+    _CPU.update(kind=kind, impl=impl, items=items)
+    res = []
+    with mp.get_context("fork").Pool(procs) as pool:
+        t = time.perf_counter()
+        for _ in range(steps):
+            res = pool.map(_cpu_item, range(procs), chunksize=1)
+        dt = time.perf_counter() - t
+    return procs * steps / dt, dt, [r for _, r in res]
 
 
-def cpu_step(pool, procs):
-    t = time.perf_counter()
-    res = pool.map(_cpu_pair, range(procs), chunksize=1)
-    return time.perf_counter() - t, res
+def cpu_baseline_obj(kind_impl, value, procs, sample, unit="pairs/s"):
+    return {"value": value, "unit": unit, "cores": procs, "kind": kind_impl,
+            "cpu_model": cpu_model(), "sample": sample}
+
+
+def host_cores():
+    return min(os.cpu_count() or 1, 16)
 
 
 # ------------------------------------------------------------------ clocks
@@ -149,14 +334,8 @@ def stage_bytes(w, h, passes=3):
     """HBM bytes each stage must move per pair."""
     P = w * h
     return {
-        # both RGB frames in; lum_ref f32, q_src u8, eq_src f32, pyramids out
         "raster": P * (24 + 4 + 1 + 4) + 2 * 4 * P // 3,
-        # splat memsets (3 f64 planes), then per pass a row sweep and a column
-        # sweep pair, each reading the guide (4 B) and the 3 f64 planes (24 B)
-        # and writing the planes (24 B); the last column pass writes the f32
-        # flow (8 B) instead of the planes
         "dt_filter": P * 24 + passes * 2 * P * 52 - P * 16,
-        # warp_image: flow 8 + src 12 in; warped 12, valid 1, q 1 out
         "finalize_warp": P * (8 + 12 + 12 + 1 + 1),
         "ssim": P * (4 + 1 + 4),
         # SURVEY.md §8(d) merge: ref 12, warped 12, SSIM 4, valid 1, composite 12
@@ -169,25 +348,16 @@ def kernel_bytes(w, h, passes=3):
     launches in one pair) and the launch count."""
     P = w * h
     return {
-        # read guide 4 + 3 f64 planes 24, write the planes 24
         "dt_rows": (passes * P * 52, passes),
-        # same per column sweep pair; the last one writes the f32 flow (8)
         "dt_cols": ((passes - 1) * P * 52 + P * 36, passes),
-        # flow 8 + src 12 in; warped 12, valid 1, q 1 out
         "warp": (P * 34, 1),
-        # lum_ref 4 + q(warped) 1 in, ssim 4 out
         "ssim": (P * 9, 1),
-        # ref 12, warped 12, ssim 4, valid 1 in; weights 8 + level-1 Gaussian (8 ch / 4) 8 out
         "fuse_weights0": (P * 45, 1),
-        # ref 12, warped 12, weights 8, level-1 G (8 ch / 4) 8 + C (3 ch / 4) 3 in; composite 12 out
         "fuse_collapse0": (P * 55, 1),
     }
 
 
 def peaks():
-    """HBM peak for the roofline: the driver-measured STREAM-style copy
-    bandwidth (MEASURED_PEAKS.json `hbm_gbs`), else the profiling guide's
-    6.65 TB/s fallback."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as f:
@@ -200,198 +370,243 @@ def peaks():
 
 
 def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch, by kernel
-    family, from the committed ncu --set full captures (profiles/)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
         return json.load(open(path))
     return {}
 
 
-# ------------------------------------------------------------------ arms
-def dist_env():
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    return rank, world, local
+def out_digest(bufs) -> str:
+    """Digest of one pair's device outputs (verdict words, matches, composite, valid)."""
+    info = bufs.info.cpu().numpy()
+    m = int(info[16])
+    h = hashlib.sha256(info[:19].tobytes())
+    h.update(bufs.matches[:m].cpu().numpy().tobytes())
+    h.update(bufs.composite.cpu().numpy().tobytes())
+    h.update(bufs.valid.cpu().numpy().tobytes())
+    return h.hexdigest()[:16]
 
 
-def emit(obj):
-    print(json.dumps(obj), flush=True)
-
-
+# ------------------------------------------------------------------ reference arm
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    procs = min(os.cpu_count() or 1, 16)
-    scenes = render_scenes(min(args.scenes, procs), args.width, args.height, 0)
-    pool = cpu_pool(scenes, procs)
-    # one step = one 5MP pair per host core (~13 s of wall on this box); the
-    # step counts are capped so the whole run stays within a few minutes
-    warm, steps = min(args.warmup, 1), max(1, min(args.steps, 8))
-    for _ in range(warm):
-        cpu_step(pool, procs)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        cpu_step(pool, procs)
-    dt = time.perf_counter() - t0
-    pool.close()
-    value = procs * steps / dt
+    procs = host_cores()
+    impl_kind, _ = cpu_impl(args.cpu_impl)
+    scenes = render("pair", min(args.scenes, procs), args.width, args.height)
+    # one step = one 5MP pair per host core (~15 s of wall); the step counts
+    # are capped so the whole run stays within a few minutes
+    warm, steps = min(args.warmup, 1), max(1, min(args.steps, 6))
+    if warm:
+        cpu_run("pair", scenes, procs, args.cpu_impl, warm)
+    value, dt, _ = cpu_run("pair", scenes, procs, args.cpu_impl, steps)
+    src = ("hdrflow.pipeline.register_and_fuse from baseline/_ref (the unmodified reference + "
+           "the fit_matches_homography import shim)" if impl_kind == "reference"
+           else "oracle port of hdrflow.register_and_fuse (baseline/_ref absent)")
     sample = (f"{procs} synthetic {args.width}x{args.height} pairs per step, one per process "
-              f"(oracle port of hdrflow.register_and_fuse, OMP/OpenBLAS threads = 1); "
-              f"steps capped at 8 and warm-up at 1 to bound the run")
+              f"({src}; OMP/OpenBLAS threads = 1); steps capped at 6 and warm-up at 1")
+    cfg = {"workload": WORKLOAD, "width": args.width, "height": args.height,
+           "pairs_per_step": procs, "parallelism": "process per core"}
+    if args.total_pairs:
+        cfg["workload"] = WORKLOAD_C5.format(n=args.total_pairs)
     emit({"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
           "steps": steps, "warmup": warm, "steps_requested": args.steps,
           "warmup_requested": args.warmup, "ms_per_step": 1e3 * dt / steps,
-          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-          "dtype": "f32/f64", "data": "synthetic",
-          "config": {"workload": WORKLOAD, "width": args.width, "height": args.height,
-                     "pairs_per_step": procs, "parallelism": "process per core"},
+          "higher_is_better": True, "scaling": "strong" if args.total_pairs else "weak",
+          "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic", "config": cfg,
           "impl": "reference",
-          "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": procs, "kind": "port",
-                           "sample": sample},
+          "cpu_baseline": cpu_baseline_obj(impl_kind, value, procs, sample),
           "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                   "d2h_bytes_per_step": 0}})
 
 
-def run_ours(args):
-    rank, world, local = dist_env()
-    cpu_base = None
-    scenes = render_scenes(args.scenes, args.width, args.height, 1000 * rank)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        procs = min(os.cpu_count() or 1, 16)
-        pool = cpu_pool(scenes, procs)
-        dt, res = cpu_step(pool, procs)
-        pool.close()
-        cpu_base = {"value": procs / dt, "unit": "pairs/s", "cores": procs, "kind": "port",
-                    "sample": f"{procs} {args.width}x{args.height} pairs, one per process, "
-                              f"{dt:.1f} s wall (oracle port of the reference)"}
-
-    import torch
+# ------------------------------------------------------------------ CPU self-test of the rank plumbing
+def run_selftest_cpu(args):
+    """What the GPU path does around its kernels, on gloo: pair assignment,
+    barrier, max-over-ranks timing, digest gathering, one line from rank 0."""
     import torch.distributed as dist
-
-    from paper_1504_01441_b200.pipeline import PairBuffers, PipelineParams
-    from paper_1504_01441_b200.runner import BatchRunner
-
     from paper_1504_01441_b200 import dist as hd
-    from paper_1504_01441_b200 import _native as _nat
-    for opt in args.option:
-        name, val = opt.split("=")
-        _nat.check(_nat.lib().hdr_set_option(name.encode(), int(val)))
-    torch.cuda.set_device(local)
+    rank, world = init_ranks("gloo", 0)
+    mine = assign_pairs(args, rank, world)
+    digests = {}
+    for g in mine:
+        scene = g % args.scenes
+        digests.setdefault(scene, set()).add(hashlib.sha256(str(scene).encode()).hexdigest()[:16])
+    hd.barrier()
+    ms = hd.max_over_ranks(10.0 + rank)
+    merged = gather_digests(digests)
+    owned = [mine]
     if world > 1:
-        hd.init("nccl", local)
-    dev = f"cuda:{local}"
-    w, h, B = args.width, args.height, args.pairs
-    pairs = []
-    for k in range(B):
-        ref, src = scenes[k % len(scenes)]
-        pairs.append((torch.from_numpy(ref).to(dev), torch.from_numpy(src).to(dev)))
-    outs = [PairBuffers(w, h, local) for _ in range(B)]
-    runner = BatchRunner(w, h, streams=args.streams, params=PipelineParams(), device=local,
-                         graph=not args.no_graph)
-    from paper_1504_01441_b200 import _native
-    nst = _native.NUM_STAGES
-    probes = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(B)]
-    for evs in probes:
-        for e in evs:
-            e.record()
-    torch.cuda.synchronize()
+        owned = [None] * world
+        dist.all_gather_object(owned, mine)
+    if rank == 0:
+        total = args.total_pairs or args.pairs * world
+        emit({"metric": METRIC, "value": total / (ms / 1e3), "unit": "pairs/s", "n_gpus": world,
+              "selftest": True, "pairs_per_rank": owned, "ms": ms,
+              "scaling": "strong" if args.total_pairs else "weak",
+              "checks": {"replicas_identical": all(len(v) == 1 for v in merged.values()),
+                         "scenes": len(merged)}})
+    if world > 1:
+        dist.destroy_process_group()
 
-    def step():
+
+# ------------------------------------------------------------------ our arm
+class DeviceLeg:
+    """Resident pairs through BatchRunner (graph replays over S streams)."""
+
+    def __init__(self, w, h, scenes, pair_scenes, n_out, streams, device, graph=True):
+        import torch
+        from paper_1504_01441_b200.pipeline import PairBuffers, PipelineParams
+        from paper_1504_01441_b200.runner import BatchRunner
+        dev = f"cuda:{device}"
+        self.w, self.h = w, h
+        self.inputs = [(torch.from_numpy(r).to(dev), torch.from_numpy(s).to(dev)) for r, s in scenes]
+        # every pair reads its own resident copy of its scene (device-side
+        # replication), so no two pairs share input cache lines
+        self.pair_inputs = [(self.inputs[sc][0].clone(), self.inputs[sc][1].clone())
+                            for sc in pair_scenes]
+        self.outs = [PairBuffers(w, h, device) for _ in range(n_out)]
+        self.runner = BatchRunner(w, h, streams=streams, params=PipelineParams(), device=device,
+                                  graph=graph)
+
+    def step(self, pair_scenes=None):
+        import torch
         cur = torch.cuda.current_stream()
-        for s in runner.streams:
+        for s in self.runner.streams:
             s.wait_stream(cur)
-        for k in range(B):
-            runner.set_probes(k, probes[k])
-            runner.enqueue(k, pairs[k][0], pairs[k][1], outs[k])
-        for s in runner.streams:
+        for k, (ref, src) in enumerate(self.pair_inputs):
+            self.runner.enqueue(k, ref, src, self.outs[k % len(self.outs)])
+        for s in self.runner.streams:
             cur.wait_stream(s)
 
-    for _ in range(max(args.warmup, 1)):
-        step()
-    torch.cuda.synchronize()
-    infos = [o.info.cpu().numpy() for o in outs]
-    ok = all(int(i[0]) == 0 for i in infos)
-    by_scene = {}
-    for k, i in enumerate(infos):
-        by_scene.setdefault(k % len(scenes), set()).add(tuple(i[:18].tolist()))
-    consistent = all(len(v) == 1 for v in by_scene.values())
-
-    clocks = Clocks(local)
-    hd.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for _ in range(args.steps):
-        step()
-    t1.record()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    ms = hd.max_over_ranks(t0.elapsed_time(t1), device=dev)
-    hd.barrier()
-    # per-stage durations of the last timed step (probes inside the graphs);
-    # with 4 streams in flight these include time-sharing with other pairs
-    stage_ms_conc = {}
-    for s_i, name in enumerate(_native.STAGES):
-        v = [probes[k][2 * s_i].elapsed_time(probes[k][2 * s_i + 1]) for k in range(B)]
-        stage_ms_conc[name] = statistics.mean(v)
-    kernels_per_pair = runner.graph_kernels()
-    # isolated stage and kernel times: the same pipeline, one pair at a time
-    # on one stream, events recorded on that stream between the stages and
-    # around every launch of the probed kernel families
-    NI = 3
-    iso = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(NI)]
-    kfam = _native.KPROBES
-    kev = [[[torch.cuda.Event(enable_timing=True) for _ in range(16)] for _ in kfam] for _ in range(NI)]
-    for evs in iso + [e for run in kev for e in run]:
-        for e in evs:
-            e.record()
-    torch.cuda.synchronize()
-    s0 = runner.streams[0]
-    for j in range(NI):
-        runner.set_probes(0, iso[j])
-        for f in range(len(kfam)):
-            runner.set_kernel_probes(0, f, kev[j][f])
-        s0.wait_stream(torch.cuda.current_stream())
-        runner.enqueue(0, pairs[j % B][0], pairs[j % B][1], outs[0])
-        torch.cuda.current_stream().wait_stream(s0)
+    def timed(self, pair_scenes, steps, warmup, clocks=None, barrier=None):
+        import torch
+        for _ in range(max(warmup, 1)):
+            self.step(pair_scenes)
         torch.cuda.synchronize()
-    runner.set_probes(0, None)
-    for f in range(len(kfam)):
-        runner.set_kernel_probes(0, f, None)
-    stage_ms = {}
-    for s_i, name in enumerate(_native.STAGES):
-        stage_ms[name] = statistics.median(
-            iso[j][2 * s_i].elapsed_time(iso[j][2 * s_i + 1]) for j in range(NI))
-    # single-pair latency, device-resident inputs: first stage start to last stage end
-    pair_latency_ms = statistics.median(iso[j][0].elapsed_time(iso[j][2 * nst - 1]) for j in range(NI))
-    kb = kernel_bytes(w, h)
-    kernel_ms = {}
-    for f, name in enumerate(kfam):
-        n = kb[name][1]
-        kernel_ms[name] = statistics.median(
-            sum(kev[j][f][2 * i].elapsed_time(kev[j][f][2 * i + 1]) for i in range(n))
-            for j in range(NI))
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            self.step(pair_scenes)
+        t1.record()
+        torch.cuda.synchronize()
+        clk = clocks.stop() if clocks else None
+        return t0.elapsed_time(t1), clk
 
-    # ---- end to end through the public batch API (host buffers); the host
-    # link is the bottleneck (--e2e-streams may differ from --streams)
+    def isolated(self, n=3):
+        """Stage and kernel times of pairs run one at a time on one stream
+        (events recorded inside the replayed graph between the stages and
+        around every launch of the probed kernel families)."""
+        import torch
+        from paper_1504_01441_b200 import _native
+        nst = _native.NUM_STAGES
+        kfam = _native.KPROBES
+        iso = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(n)]
+        kev = [[[torch.cuda.Event(enable_timing=True) for _ in range(16)] for _ in kfam] for _ in range(n)]
+        for evs in iso + [e for run in kev for e in run]:
+            for e in evs:
+                e.record()
+        torch.cuda.synchronize()
+        r = self.runner
+        s0 = r.streams[0]
+        for j in range(n):
+            r.set_probes(0, iso[j])
+            for f in range(len(kfam)):
+                r.set_kernel_probes(0, f, kev[j][f])
+            s0.wait_stream(torch.cuda.current_stream())
+            ref, src = self.inputs[j % len(self.inputs)]
+            r.enqueue(0, ref, src, self.outs[0])
+            torch.cuda.current_stream().wait_stream(s0)
+            torch.cuda.synchronize()
+        r.set_probes(0, None)
+        for f in range(len(kfam)):
+            r.set_kernel_probes(0, f, None)
+        stage_ms = {name: statistics.median(iso[j][2 * i].elapsed_time(iso[j][2 * i + 1])
+                                            for j in range(n))
+                    for i, name in enumerate(_native.STAGES)}
+        latency = statistics.median(iso[j][0].elapsed_time(iso[j][2 * nst - 1]) for j in range(n))
+        kb = kernel_bytes(self.w, self.h)
+        kernel_ms = {}
+        for f, name in enumerate(kfam):
+            cnt = kb[name][1]
+            kernel_ms[name] = statistics.median(
+                sum(kev[j][f][2 * i].elapsed_time(kev[j][f][2 * i + 1]) for i in range(cnt))
+                for j in range(n))
+        return stage_ms, kernel_ms, latency
+
+    def close(self):
+        self.runner.close()
+
+
+def rooflines(w, h, stage_ms, kernel_ms, peak):
+    traffic = ncu_traffic()
+    kb = kernel_bytes(w, h)
+
+    def kroof(name):
+        nbytes, n = kb[name]
+        a = nbytes / (kernel_ms[name] / 1e3) / 1e9
+        return {"kernel": name, "launches_per_pair": n, "bytes_per_launch": nbytes / n,
+                "us_per_launch": 1e3 * kernel_ms[name] / n, "achieved": a, "frac": a / peak,
+                "traffic": traffic.get(name) if (w, h) == (W5, H5) else None}
+    sb = stage_bytes(w, h)
+
+    def sroof(stage):
+        a = sb[stage] / (stage_ms[stage] / 1e3) / 1e9
+        return {"stage": stage, "achieved": a, "frac": a / peak, "bytes": sb[stage],
+                "ms": stage_ms[stage]}
+    return ({k: kroof(k) for k in kernel_ms},
+            {k: sroof(k) for k in ("dt_filter", "finalize_warp", "fuse")})
+
+
+def parity_summary(leg, pair_scenes, cpu_results):
+    """GPU outputs of the scenes the CPU side also ran: level counts and match
+    coordinates bit-exact, valid identical, composite max-abs (bar 1e-3)."""
+    out = {"scenes_checked": 0, "level_counts_equal": True, "matches_equal": True,
+           "valid_equal": True, "composite_max_abs": 0.0}
+    seen = set()
+    for r in cpu_results:
+        sc = r["scene"]
+        if sc in seen or sc not in pair_scenes:
+            continue
+        seen.add(sc)
+        k = pair_scenes.index(sc)
+        b = leg.outs[k % len(leg.outs)]
+        info = b.info.cpu().numpy()
+        L = int(info[2])
+        lc = [[int(info[3 + 2 * l]), int(info[4 + 2 * l])] for l in range(L)]
+        m = b.matches[:int(info[16])].cpu().numpy()
+        out["scenes_checked"] += 1
+        out["level_counts_equal"] &= lc == r["level_counts"]
+        out["matches_equal"] &= bool(m.shape == r["matches"].shape
+                                     and np.array_equal(m[:, :4], r["matches"][:, :4]))
+        out["valid_equal"] &= bool(np.array_equal(b.valid.cpu().numpy().astype(bool), r["valid"]))
+        out["composite_max_abs"] = max(out["composite_max_abs"],
+                                       float(np.abs(b.composite.cpu().numpy() - r["composite"]).max()))
+    out["ok"] = bool(out["scenes_checked"] and out["level_counts_equal"] and out["matches_equal"]
+                     and out["valid_equal"] and out["composite_max_abs"] < 1e-3)
+    return out
+
+
+def e2e_leg(args, scenes, w, h, local, hd, dev):
+    """The public batch API with pinned host frames: f32 (run_host) and raw
+    8-bit samples (run_host_raw, the run_hdr file path)."""
+    import torch
+    from paper_1504_01441_b200 import _native
+    from paper_1504_01441_b200.pipeline import PipelineParams
+    from paper_1504_01441_b200.runner import BatchRunner
     E = args.e2e_pairs
-    if args.e2e_streams != args.streams:
-        runner.close()
-        runner = BatchRunner(w, h, streams=args.e2e_streams, params=PipelineParams(), device=local,
-                             graph=not args.no_graph)
-    # one pinned copy per distinct scene (every pair still moves its own
-    # 121 MB H2D each step); outputs are distinct per pair
+    runner = BatchRunner(w, h, streams=args.e2e_streams, params=PipelineParams(), device=local,
+                         graph=not args.no_graph)
     pinned = [(torch.from_numpy(ref).pin_memory(), torch.from_numpy(src).pin_memory()) for ref, src in scenes]
     hpairs = [pinned[k % len(pinned)] for k in range(E)]
     hout = [(torch.empty((h, w, 3), dtype=torch.float32).pin_memory(),
              torch.empty((_native.INFO_WORDS,), dtype=torch.int32).pin_memory()) for _ in range(E)]
-    runner.set_probes(0, None)
-    for k in range(len(runner.streams)):
-        runner.set_probes(k, None)
     for _ in range(max(args.warmup, 1)):
         runner.run_host(hpairs, hout)
     torch.cuda.synchronize()
@@ -400,21 +615,15 @@ def run_ours(args):
     e0.record()
     h2d = d2h = 0
     for _ in range(args.steps):
-        a, b = runner.run_host(hpairs, hout)
-        h2d, d2h = a, b
+        h2d, d2h = runner.run_host(hpairs, hout)
     e1.record()
     torch.cuda.synchronize()
     e2e_ok = all(int(x[1][0]) == 0 for x in hout)
     ems = hd.max_over_ranks(e0.elapsed_time(e1), device=dev)
 
-    # ---- end to end on the file path: the same scenes as
-    # 8-bit PNG samples (what run_hdr reads), raw bytes over PCIe, the 8-bit
-    # composite (save_png's samples) back
-    q8 = lambda a: np.clip(np.floor(a.astype(np.float64) * 255.0 + 0.5), 0, 255).astype(np.uint8)
-    rpairs = []
-    for k in range(E):
-        ref, src = scenes[k % len(scenes)]
-        rpairs.append((torch.from_numpy(q8(ref)).pin_memory(), torch.from_numpy(q8(src)).pin_memory()))
+    q8 = lambda a: np.clip(np.floor(a.astype(np.float64) * 255.0 + 0.5), 0, 255).astype(np.uint8)  # noqa: E731
+    rp = [(torch.from_numpy(q8(r)).pin_memory(), torch.from_numpy(q8(s)).pin_memory()) for r, s in scenes]
+    rpairs = [rp[k % len(rp)] for k in range(E)]
     rout = [(torch.empty((h, w, 3), dtype=torch.uint8).pin_memory(),
              torch.empty((_native.INFO_WORDS,), dtype=torch.int32).pin_memory()) for _ in range(E)]
     for _ in range(max(args.warmup, 1)):
@@ -430,44 +639,240 @@ def run_ours(args):
     torch.cuda.synchronize()
     raw_ok = all(int(x[1][0]) == 0 for x in rout)
     rms = hd.max_over_ranks(r0.elapsed_time(r1), device=dev)
+    runner.close()
+    return (ems, h2d, d2h, e2e_ok), (rms, rh2d, rd2h, raw_ok)
+
+
+def dropin_latency(scene, n=5):
+    """register_and_fuse(numpy, numpy) as a reference user calls it: pageable
+    numpy in, every RegistrationOutput field back as numpy (host wall time,
+    median of n after one warm-up call)."""
+    import torch
+    from paper_1504_01441_b200 import pipeline
+    ref, src = scene
+    pipeline.register_and_fuse(ref, src)
+    ts = []
+    out = None
+    for _ in range(n):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = pipeline.register_and_fuse(ref, src)
+        ts.append(1e3 * (time.perf_counter() - t))
+    nbytes_out = sum(np.asarray(getattr(out, k)).nbytes for k in
+                     ("composite", "flow", "warped", "valid", "ssim", "matches", "raw_matches"))
+    return {"ms": statistics.median(ts), "ms_all": ts, "h2d_bytes": ref.nbytes + src.nbytes,
+            "d2h_bytes": nbytes_out,
+            "note": "pipeline.register_and_fuse(ref, src) on pageable numpy float32 frames; "
+                    "returns the full RegistrationOutput as numpy (pipeline.py:174-198 contract); "
+                    "host wall clock"}
+
+
+def extra_pairs_leg(args, local, peak, cpu_kind):
+    """BASELINE configs[3]: 12MP pairs (4000x3000), same runner as the headline."""
+    import torch
+    w, h = W12, H12
+    scenes = render("pair", 2, w, h)
+    n = 8
+    sc = [k % len(scenes) for k in range(n)]
+    leg = DeviceLeg(w, h, scenes, sc, n, args.streams, local, graph=not args.no_graph)
+    steps = max(3, args.steps // 4)
+    ms, _ = leg.timed(sc, steps, args.warmup)
+    stage_ms, kernel_ms, latency = leg.isolated(3)
+    kro, sro = rooflines(w, h, stage_ms, kernel_ms, peak)
+    obj = {"workload": "12MP (4000x3000) two-exposure pair (BASELINE configs[3])",
+           "value": n * steps / (ms / 1e3), "unit": "pairs/s", "pairs_per_step": n, "steps": steps,
+           "pair_latency_ms": latency, "stage_ms": stage_ms, "kernel_rooflines": kro,
+           "stage_rooflines": sro, "gpu_launches": leg.runner.graph_kernels() * n * steps}
+    if not args.no_cpu_baseline:
+        procs = min(host_cores(), 8)
+        v, dt, res = cpu_run("pair", scenes, procs, args.cpu_impl)
+        obj["cpu_baseline"] = cpu_baseline_obj(cpu_kind, v, procs,
+                                               f"{procs} 12MP pairs, one per process, {dt:.1f} s wall")
+        obj["parity"] = parity_summary(leg, sc, res)
+    leg.close()
+    del leg
+    torch.cuda.empty_cache()
+    return obj
+
+
+def extra_stack_leg(args, local, cpu_kind):
+    """BASELINE configs[2]: 5MP -2/0/+2 EV three-frame stacks (metering's
+    reference, two registrations, k-way merge): 8 stacks per step on 4
+    streams, one context each."""
+    import ctypes
+    import torch
+    from paper_1504_01441_b200 import _native, metering
+    from paper_1504_01441_b200.engine import Engine
+    from paper_1504_01441_b200.pipeline import PairBuffers, PipelineParams
+    w, h = W5, H5
+    stacks = render("stack", 2, w, h)
+    dev = f"cuda:{local}"
+    S = 4
+    streams = [torch.cuda.Stream(local) for _ in range(S)]
+    engines = [Engine(w, h, local) for _ in range(S)]
+    for e, s in zip(engines, streams):
+        e.bind_stream(s)
+    p = PipelineParams().to_native()
+    frames = []
+    for fr, ex in stacks:
+        t = [torch.from_numpy(x).to(dev) for x in fr]
+        k = metering.choose_reference(t, ex)       # the darkest exposure (metering.py:37-51)
+        frames.append([t[k]] + [t[f] for f in range(3) if f != k])
+    bufs = [[PairBuffers(w, h, local) for _ in range(2)] for _ in range(S)]
+    comps = [torch.empty((h, w, 3), dtype=torch.float32, device=dev) for _ in range(S)]
+
+    def one(j, k):
+        fr = frames[k % len(frames)]
+        arr = (ctypes.c_void_p * 3)(*[x.data_ptr() for x in fr])
+        outs = (ctypes.c_void_p * 2)(*[ctypes.addressof(b.native) for b in bufs[j]])
+        _native.check(_native.lib().hdr_register_and_fuse_stack(
+            engines[j].handle, ctypes.byref(p), 3, w, h, arr, outs,
+            ctypes.c_void_p(comps[j].data_ptr())), "register_and_fuse_stack")
+
+    per_step = 8
+
+    def step():
+        cur = torch.cuda.current_stream()
+        for s in streams:
+            s.wait_stream(cur)
+        for k in range(per_step):
+            one(k % S, k)
+        for s in streams:
+            cur.wait_stream(s)
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    steps = max(3, args.steps // 4)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    lat = []
+    for j in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        streams[0].wait_stream(torch.cuda.current_stream())
+        a.record(streams[0])
+        one(0, j)
+        b.record(streams[0])
+        torch.cuda.synchronize()
+        lat.append(a.elapsed_time(b))
+    ok = all(int(b.info.cpu()[0]) == 0 for bb in bufs for b in bb)
+    obj = {"workload": "5MP -2/0/+2 EV three-exposure stack (BASELINE configs[2])",
+           "value": per_step * steps / (ms / 1e3), "unit": "stacks/s", "stacks_per_step": per_step,
+           "steps": steps, "stack_latency_ms": statistics.median(lat), "all_registered": ok,
+           "pair_registrations_per_s": 2 * per_step * steps / (ms / 1e3)}
+    if not args.no_cpu_baseline:
+        procs = min(host_cores(), 8)
+        v, dt, res = cpu_run("stack", stacks, procs, args.cpu_impl)
+        obj["cpu_baseline"] = cpu_baseline_obj(cpu_kind, v, procs,
+                                               f"{procs} 5MP 3-frame stacks, one per process, "
+                                               f"{dt:.1f} s wall", unit="stacks/s")
+        err = 0.0
+        for r in res[:len(stacks)]:
+            with torch.cuda.stream(streams[0]):
+                one(0, r["scene"])
+            torch.cuda.synchronize()
+            err = max(err, float(np.abs(comps[0].cpu().numpy() - r["composite"]).max()))
+        obj["parity"] = {"composite_max_abs": err, "ok": err < 1e-3}
+    for e in engines:
+        e.close()
+    return obj
+
+
+def run_ours(args):
+    import torch
+    from paper_1504_01441_b200 import _native
+    from paper_1504_01441_b200 import dist as hd
+
+    _, _, local = dist_env()
+    torch.cuda.set_device(local)
+    rank, world = init_ranks("nccl", local)
+    for opt in args.option:
+        name, val = opt.split("=")
+        _native.check(_native.lib().hdr_set_option(name.encode(), int(val)))
+    dev = f"cuda:{local}"
+    w, h = args.width, args.height
+    # every rank draws from the same distinct scenes: global pair g is scene
+    # g % K, so per-scene digests must agree across ranks and streams
+    scenes = render("pair", args.scenes, w, h)
+    mine = assign_pairs(args, rank, world)
+    pair_scenes = [g % len(scenes) for g in mine]
+    cpu_kind = cpu_impl(args.cpu_impl)[0]
+    cpu_base, cpu_res = None, []
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = host_cores()
+        v, dt, cpu_res = cpu_run("pair", scenes, procs, args.cpu_impl)
+        cpu_base = cpu_baseline_obj(cpu_kind, v, procs,
+                                    f"{procs} {w}x{h} pairs, one per process, {dt:.1f} s wall")
+
+    # weak mode gives each of the rank's pairs its own output set; strong
+    # mode cycles 16 sets (every pair still writes its full outputs)
+    n_out = min(len(mine), 16) if args.total_pairs else len(mine)
+    leg = DeviceLeg(w, h, scenes, pair_scenes, max(n_out, 1), args.streams, local,
+                    graph=not args.no_graph)
+    leg.step(pair_scenes)
+    torch.cuda.synchronize()
+    ok = all(int(b.info.cpu()[0]) == 0 for b in leg.outs)
+    # per-scene digests of the last pair written to each output set
+    digests = {}
+    first = max(0, len(pair_scenes) - len(leg.outs))
+    for k in range(first, len(pair_scenes)):
+        digests.setdefault(pair_scenes[k], set()).add(out_digest(leg.outs[k % len(leg.outs)]))
+    merged = gather_digests(digests)
+    replicas_identical = all(len(v) == 1 for v in merged.values())
+
+    clocks = Clocks(local)
+    ms, clk = leg.timed(pair_scenes, args.steps, args.warmup, clocks, hd.barrier)
+    ms = hd.max_over_ranks(ms, device=dev)
+    hd.barrier()
+    parity = parity_summary(leg, pair_scenes, cpu_res) if cpu_res else None
+    stage_ms, kernel_ms, latency = leg.isolated(3)
+    kernels_per_pair = leg.runner.graph_kernels()
+    leg.close()
+    del leg
+    torch.cuda.empty_cache()
+
+    (ems, h2d, d2h, e2e_ok), (rms, rh2d, rd2h, raw_ok) = e2e_leg(args, scenes, w, h, local, hd, dev)
+
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extra_workloads and (w, h) == (W5, H5):
+        peak, _ = peaks()
+        extras["dropin_latency"] = dropin_latency(scenes[0])
+        extras["c4_12mp"] = extra_pairs_leg(args, local, peak, cpu_kind)
+        extras["c3_stack3_5mp"] = extra_stack_leg(args, local, cpu_kind)
 
     if rank != 0:
         if world > 1:
+            import torch.distributed as dist
             dist.destroy_process_group()
         return
-    value = world * B * args.steps / (ms / 1e3)
+    per_step = args.total_pairs or args.pairs * world
+    value = per_step * args.steps / (ms / 1e3)
+    E = args.e2e_pairs
     e2e_value = world * E * args.steps / (ems / 1e3)
     png8_value = world * E * args.steps / (rms / 1e3)
     peak, peak_src = peaks()
-    traffic_all = ncu_traffic()
-
-    def kroof(name):
-        nbytes, n = kb[name]
-        t = kernel_ms[name] / 1e3
-        a = nbytes / t / 1e9
-        tr = traffic_all.get(name)
-        return {"kernel": name, "launches_per_pair": n, "bytes_per_launch": nbytes / n,
-                "us_per_launch": 1e3 * kernel_ms[name] / n, "achieved": a, "frac": a / peak,
-                "traffic": tr}
+    kro, sro = rooflines(w, h, stage_ms, kernel_ms, peak)
     dom = max(kernel_ms, key=lambda k: kernel_ms[k])
-    d = kroof(dom)
-    sb = stage_bytes(w, h)
-
-    def sroof(stage):
-        a = sb[stage] / (stage_ms[stage] / 1e3) / 1e9
-        return {"stage": stage, "achieved": a, "frac": a / peak, "bytes": sb[stage],
-                "ms": stage_ms[stage]}
+    d = kro[dom]
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "width": w, "height": h, "pairs_per_step_per_gpu": B,
-                   "global_pairs_per_step": B * world, "streams": args.streams,
-                   "e2e_streams": args.e2e_streams,
-                   "distinct_scenes": len(scenes), "graph": not args.no_graph,
-                   "options": args.option,
-                   "l2": "inputs larger than L2 (each pair 121 MB, %d resident pairs)" % B,
+        "higher_is_better": True, "scaling": "strong" if args.total_pairs else "weak",
+        "vs_baseline": None,
+        "dtype": "f32/f64 (f64 registration, domain transform, SSIM moments and quality "
+                 "weights; f32 fusion pyramid, as SURVEY.md §8(a) a19/a22)",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD_C5.format(n=args.total_pairs) if args.total_pairs else WORKLOAD,
+                   "width": w, "height": h, "pairs_per_rank": len(mine),
+                   "global_pairs_per_step": per_step, "streams": args.streams,
+                   "e2e_streams": args.e2e_streams, "distinct_scenes": len(scenes),
+                   "graph": not args.no_graph, "options": args.option,
+                   "l2": "inputs larger than L2 (every pair its own resident 121 MB input copy, "
+                         "%d per rank; %d output sets of 185 MB)" % (len(mine), n_out),
                    "parallelism": f"pair-sharded x{world}, no collective"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak,
                      "unit": "GB/s", "frac": d["frac"], "traffic": d["traffic"],
@@ -479,32 +884,41 @@ def run_ours(args):
                              "on the launching stream around each launch (kernel probes), pairs "
                              "run one at a time after the timed region; traffic = ncu dram bytes "
                              "per launch (profiles/)"},
-        "kernel_rooflines": {k: kroof(k) for k in kernel_ms},
-        "stage_rooflines": {k: sroof(k) for k in ("dt_filter", "finalize_warp", "fuse")},
-        "pair_latency_ms": pair_latency_ms,
-        "stage_ms": stage_ms, "stage_ms_concurrent": stage_ms_conc, "kernel_ms": kernel_ms,
+        "kernel_rooflines": kro, "stage_rooflines": sro,
+        "pair_latency_ms": latency, "stage_ms": stage_ms, "kernel_ms": kernel_ms,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "pairs_per_step": E},
         "e2e_png8": {"value": png8_value, "unit": "pairs/s", "h2d_bytes_per_step": rh2d,
                      "d2h_bytes_per_step": rd2h, "pairs_per_step": E,
                      "note": "file path (run_hdr): the same scenes as 8-bit PNG samples, "
                              "raw uint8 H2D, device decode, pair graph, 8-bit composite D2H"},
-        "gpu_launches": kernels_per_pair * B * args.steps,
+        "gpu_launches": kernels_per_pair * len(mine) * args.steps,
         "kernels_per_pair": kernels_per_pair,
         "clocks": clk,
-        "checks": {"all_registered": ok, "replicas_identical": consistent, "e2e_ok": e2e_ok,
-                   "e2e_png8_ok": raw_ok},
+        "checks": {"all_registered": ok, "replicas_identical": replicas_identical,
+                   "scenes_digested": len(merged), "e2e_ok": e2e_ok, "e2e_png8_ok": raw_ok,
+                   "parity": parity},
     }
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base
+    line.update(extras)
     emit(line)
     if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and not under_launcher() and (args.impl == "ours" or args.selftest_cpu):
+        sys.exit(self_launch(args, argv))
+    if under_launcher() and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}\n")
+        sys.exit(2)
+    if args.selftest_cpu:
+        run_selftest_cpu(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -28,7 +28,8 @@ enum {
   HDR_ERR_REGISTRATION = 3, /* pipeline.RegistrationError (pipeline.py:27)  */
   HDR_ERR_CONFIG = 4,       /* pipeline.ConfigError (pipeline.py:31)        */
   HDR_ERR_CUDA = 5,         /* RuntimeError from the CUDA runtime           */
-  HDR_ERR_EMPTY = 6         /* "no result" (ssd_match returns None)         */
+  HDR_ERR_EMPTY = 6,        /* "no result" (ssd_match returns None)         */
+  HDR_ERR_SINGULAR = 7      /* numpy.linalg.LinAlgError (np.linalg.inv)     */
 };
 
 /* Mirror of PipelineParams (pipeline.py:35-57); delta < 0 means None. */
@@ -190,6 +191,18 @@ int hdr_build_pyramid(hdr_ctx* ctx, const float* img, int32_t width, int32_t hei
 /* image.integral (image.py:32-44): (h+1, w+1) float64 summed-area table. */
 int hdr_integral(hdr_ctx* ctx, const float* img, int32_t width, int32_t height,
                  double* table);
+/* image.rect_sum (image.py:47-58): n queries q = (x0[n], y0[n], x1[n], y1[n])
+ * int64 against a (h1, w1) float64 table; HDR_ERR_INVALID ("rectangle bounds
+ * out of range") if any query is out of range. Synchronous. */
+int hdr_rect_sum(hdr_ctx* ctx, const double* table, int32_t w1, int32_t h1, const int64_t* q,
+                 int64_t n, double* out);
+/* image.quantize_256 (image.py:91-93): n samples (f32, or f64 when is_f64)
+ * -> uint8. */
+int hdr_quantize_256(hdr_ctx* ctx, const void* x, int32_t is_f64, int64_t n, uint8_t* out);
+/* image.downsample (image.py:61-68): (h, w, channels) interleaved, f32 (or
+ * f64 when is_f64) -> (h/2, w/2, channels) float32. */
+int hdr_downsample(hdr_ctx* ctx, const void* img, int32_t is_f64, int32_t width, int32_t height,
+                   int32_t channels, float* out);
 /* matcher.cornerness (matcher.py:51-61) at n points xy (n, 2) int32 of an
  * image whose (h+1, w+1) f64 integral table is given (callers check the
  * half-neighbourhood bounds): out (n, 2) = (cornerness, min contrast). */
@@ -223,6 +236,16 @@ int hdr_fit_matches_homography(hdr_ctx* ctx, const double* matches, int32_t n,
 /* geometry.fit_homography (geometry.py:35-77): ref_pts/src_pts (n, 2). */
 int hdr_fit_homography(hdr_ctx* ctx, const double* ref_pts, const double* src_pts,
                        int32_t n, double* h);
+/* geometry.apply_homography (geometry.py:80-93): pts (n, 2) -> out (n, 2);
+ * HDR_ERR_INVALID ("point maps to infinity") if any |denominator| < 1e-12.
+ * Synchronous. */
+int hdr_apply_homography(hdr_ctx* ctx, const double* h, const double* pts, int64_t n,
+                         double* out);
+/* geometry.symmetric_transfer_error (geometry.py:107-115): (n) float64;
+ * HDR_ERR_SINGULAR if h is exactly singular (np.linalg.inv raises).
+ * Synchronous. */
+int hdr_symmetric_transfer_error(hdr_ctx* ctx, const double* h, const double* ref_pts,
+                                 const double* src_pts, int64_t n, double* out);
 /* geometry.inlier_mask (geometry.py:118-121). */
 int hdr_inlier_mask(hdr_ctx* ctx, const double* h, const double* ref_pts,
                     const double* src_pts, int32_t n, double eps, uint8_t* mask);
@@ -239,16 +262,25 @@ int hdr_match_stack(hdr_ctx* ctx, const hdr_params* p, int32_t width, int32_t he
 int hdr_sparse_maps(hdr_ctx* ctx, const double* matches, int32_t m, int32_t width,
                     int32_t height, double* pu, double* pv, double* n);
 /* densify.dt_filter (densify.py:78-113): guide (h, w) f32, planes (k, h, w)
- * float64 planar, filtered in place. */
+ * float64 planar (any k; the planes are filtered three at a time), filtered
+ * in place. Any width: rows wider than the shared-memory row kernels take
+ * the sequential row twin. */
 int hdr_dt_filter(hdr_ctx* ctx, const float* guide, double* planes, int32_t k,
                   int32_t width, int32_t height, double sigma_s, double sigma_r,
                   int32_t passes);
+/* densify.dt_filter for a general guide (densify.py:59-66: the domain
+ * distances sum |diff| over the guide's channels): guide (h, w, channels)
+ * float64 interleaved, planes (k, h, w) float64, filtered in place by the
+ * reference's sequential recursion, one thread per (line, plane). */
+int hdr_dt_filter_general(hdr_ctx* ctx, const double* guide, int32_t channels, double* planes,
+                          int32_t k, int32_t width, int32_t height, double sigma_s,
+                          double sigma_r, int32_t passes);
 /* densify.densify_flow (densify.py:116-142): filtered planes (3, h, w) ->
  * flow (h, w, 2) f32; fallback = device 3x3 or NULL. */
 int hdr_densify_finalize(hdr_ctx* ctx, const double* smooth, int32_t width,
                          int32_t height, const double* fallback, double floor_,
                          float* flow);
-/* densify.warp_image (densify.py:145-174): src (h, w, c) c in {1,3}. */
+/* densify.warp_image (densify.py:145-174): src (h, w, c), any c >= 1. */
 int hdr_warp_image(hdr_ctx* ctx, const float* src, int32_t channels, int32_t width,
                    int32_t height, const float* flow, float* warped, uint8_t* valid);
 /* fusion.ssim_map (fusion.py:34-64): a, b (h, w) f32 -> ssim (h, w) f32. */

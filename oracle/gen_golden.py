@@ -275,14 +275,88 @@ def metering_fixture():
             "plans": np.array([[p.offset_stops, p.reference_index] for p in plans])}
 
 
+# rows wider than the shared-memory row kernels (the pair pipeline's
+# sequential row twin, k_twins.cu) -- pinned like the headline shapes
+WIDE_SCENES = [("wide_7200x1000_s0", 7200, 1000, 0.0, 0)]
+
+
+def twins_fixture():
+    """Stage twins with the general arguments the reference accepts and the
+    pair pipeline never passes: multi-channel / float64 guides and any plane
+    count for dt_filter, any channel count for warp_image, batched rect_sum,
+    quantize_256 and downsample on float32/float64, apply_homography and
+    symmetric_transfer_error (image.py:47-93, geometry.py:80-115,
+    densify.py:59-174)."""
+    from hdrflow import densify, geometry, image
+    r = np.random.default_rng(11)
+    fx = {}
+    g3 = r.random((37, 53, 3)).astype(np.float32)
+    d4 = r.random((37, 53, 4))
+    fx["dt_g3_guide"], fx["dt_g3_data"] = g3, d4
+    fx["dt_g3_out"] = densify.dt_filter(g3, d4, 40.0, 0.3, 2)
+    g64 = r.random((29, 31))
+    d1 = r.random((29, 31))
+    fx["dt_g64_guide"], fx["dt_g64_data"] = g64, d1
+    fx["dt_g64_out"] = densify.dt_filter(g64, d1)
+    g9 = r.random((20, 24, 9)).astype(np.float32)
+    d2 = r.random((20, 24, 2))
+    fx["dt_g9_guide"], fx["dt_g9_data"] = g9, d2
+    fx["dt_g9_out"] = densify.dt_filter(g9, d2, 25.0, 0.1, 3)
+    g1 = r.random((23, 41)).astype(np.float32)
+    d5 = r.random((23, 41, 5))
+    fx["dt_k5_guide"], fx["dt_k5_data"] = g1, d5
+    fx["dt_k5_out"] = densify.dt_filter(g1, d5, 60.0, 0.2, 3)
+    for c in (2, 4, 5):
+        src = r.random((30, 40, c)).astype(np.float32)
+        flow = (r.random((30, 40, 2)) * 8 - 4).astype(np.float32)
+        warped, valid = densify.warp_image(src, flow)
+        fx[f"warp{c}_src"], fx[f"warp{c}_flow"] = src, flow
+        fx[f"warp{c}_out"], fx[f"warp{c}_valid"] = warped, valid
+    img = r.random((17, 23)).astype(np.float32)
+    t = image.integral(img)
+    q = np.sort(r.integers(0, 18, (2, 50)), axis=0), np.sort(r.integers(0, 24, (2, 50)), axis=0)
+    fx["rs_table"] = t
+    fx["rs_q"] = np.stack([q[1][0], q[0][0], q[1][1], q[0][1]])
+    fx["rs_out"] = image.rect_sum(t, q[1][0], q[0][0], q[1][1], q[0][1])
+    fx["rs_scalar"] = np.float64(image.rect_sum(t, 3, 2, 19, 11))
+    x32 = np.concatenate([r.random(200).astype(np.float32) * 1.4 - 0.2,
+                          (np.arange(256, dtype=np.float32) + 0.5) / 255,
+                          np.array([0.0, 1.0, -0.0, 2.0], np.float32)])
+    x64 = np.concatenate([r.random(200) * 1.4 - 0.2, (np.arange(256) + 0.5) / 255])
+    fx["q32_in"], fx["q32_out"] = x32, image.quantize_256(x32)
+    fx["q64_in"], fx["q64_out"] = x64, image.quantize_256(x64)
+    ds3 = r.random((21, 17, 3)).astype(np.float32)
+    ds64 = r.random((14, 19, 2))
+    fx["ds3_in"], fx["ds3_out"] = ds3, image.downsample(ds3)
+    fx["ds64_in"], fx["ds64_out"] = ds64, image.downsample(ds64)
+    hm = np.eye(3) + r.normal(size=(3, 3)) * 0.05
+    pts = r.random((4, 25, 2)) * 100
+    fx["h"], fx["h_pts"], fx["h_out"] = hm, pts, geometry.apply_homography(hm, pts)
+    rp, sp = r.random((60, 2)) * 100, r.random((60, 2)) * 100
+    fx["ste_ref"], fx["ste_src"] = rp, sp
+    fx["ste_out"] = geometry.symmetric_transfer_error(hm, rp, sp)
+    return fx
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
+    ap.add_argument("--wide", action="store_true",
+                    help="only the wide-row scene (7200x1000) and the stage-twin fixture")
     ap.add_argument("--big", action="store_true",
                     help="only the headline-size fixtures (C2 5MP, C4 12MP, C3 5MP stack; minutes of CPU)")
     args = ap.parse_args()
     hf = load_reference(args.ref)
     os.makedirs(GOLDEN, exist_ok=True)
+    if args.wide:
+        np.savez_compressed(os.path.join(GOLDEN, "twins.npz"), **twins_fixture())
+        print("twins done")
+        for name, w, h, rot, seed in WIDE_SCENES:
+            fx = scene_fixture(hf, w, h, rot, seed, BIG_STRIDE)
+            fx["scene"] = np.array([w, h, rot, seed], dtype=np.float64)
+            np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **fx)
+            print(name, fx["level_counts"].tolist(), int(fx["floor_fallback"]), int(fx["floor_near"]))
+        return
     if args.big:
         for name, w, h, rot, seed in BIG_SCENES:
             fx = scene_fixture(hf, w, h, rot, seed, BIG_STRIDE)

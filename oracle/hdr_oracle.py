@@ -311,6 +311,27 @@ def _transfer(hm, pts, tgt):
     return out
 
 
+def apply_homography(hm, pts):
+    """geometry.py:80-93 — projective map of (..., 2) points."""
+    pts = np.asarray(pts, dtype=np.float64)
+    x, y = pts[..., 0], pts[..., 1]
+    den = hm[2, 0] * x + hm[2, 1] * y + hm[2, 2]
+    if np.any(np.abs(den) < 1e-12):
+        raise ValueError("point maps to infinity")
+    out = np.empty_like(pts)
+    out[..., 0] = (hm[0, 0] * x + hm[0, 1] * y + hm[0, 2]) / den
+    out[..., 1] = (hm[1, 0] * x + hm[1, 1] * y + hm[1, 2]) / den
+    return out
+
+
+def symmetric_transfer_error(hm, ref_pts, src_pts):
+    """geometry.py:107-115 — hypot(fwd, bwd) per pair."""
+    ref_pts = np.asarray(ref_pts, dtype=np.float64).reshape(-1, 2)
+    src_pts = np.asarray(src_pts, dtype=np.float64).reshape(-1, 2)
+    return np.hypot(_transfer(hm, ref_pts, src_pts),
+                    _transfer(np.linalg.inv(hm), src_pts, ref_pts))
+
+
 def inlier_mask(hm, ref_pts, src_pts, eps):
     """geometry.py:107-121 — hypot(fwd, bwd) < eps."""
     ref_pts = np.asarray(ref_pts, dtype=np.float64).reshape(-1, 2)

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libhdrb200.so")
 
 HDR_OK, HDR_ERR_INVALID, HDR_ERR_DEGENERATE = 0, 1, 2
 HDR_ERR_REGISTRATION, HDR_ERR_CONFIG, HDR_ERR_CUDA, HDR_ERR_EMPTY = 3, 4, 5, 6
+HDR_ERR_SINGULAR = 7
 INFO_WORDS = 32
 NUM_STAGES = 7
 STAGES = ("raster", "corners", "match_chain", "dt_filter", "finalize_warp", "ssim", "fuse")
@@ -78,6 +79,12 @@ SIGNATURES = {
     "hdr_match_stack": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "hdr_sparse_maps": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "hdr_dt_filter": (_I, [_P, _P, _P, _I, _I, _I, _D, _D, _I]),
+    "hdr_dt_filter_general": (_I, [_P, _P, _I, _P, _I, _I, _I, _D, _D, _I]),
+    "hdr_rect_sum": (_I, [_P, _P, _I, _I, _P, _I64, _P]),
+    "hdr_quantize_256": (_I, [_P, _P, _I, _I64, _P]),
+    "hdr_downsample": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "hdr_apply_homography": (_I, [_P, _P, _P, _I64, _P]),
+    "hdr_symmetric_transfer_error": (_I, [_P, _P, _P, _P, _I64, _P]),
     "hdr_densify_finalize": (_I, [_P, _P, _I, _I, _P, _D, _P]),
     "hdr_warp_image": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "hdr_ssim_map": (_I, [_P, _P, _P, _I, _I, _I, _D, _P]),
@@ -138,4 +145,7 @@ def check(rc: int, what: str = "") -> None:
         raise RegistrationError(msg)
     if rc == HDR_ERR_INVALID:
         raise ValueError(msg)
+    if rc == HDR_ERR_SINGULAR:
+        import numpy as np
+        raise np.linalg.LinAlgError(msg)
     raise RuntimeError(f"{what}: {msg}" if what else msg)

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhdrb200.so")
-SOURCES = ["hdr_api.cu", "k_raster.cu", "k_match.cu", "k_densify.cu", "k_dtfilter.cu", "k_fusion.cu", "k_merge.cu", "k_ingest.cu"]
+SOURCES = ["hdr_api.cu", "k_raster.cu", "k_match.cu", "k_densify.cu", "k_dtfilter.cu", "k_fusion.cu", "k_merge.cu", "k_ingest.cu", "k_twins.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

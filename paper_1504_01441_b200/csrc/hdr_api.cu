@@ -1003,7 +1003,6 @@ static int check_pair_args(hdr_ctx* c, const hdr_params* p, int w, int h, const 
     return fail(HDR_ERR_INVALID, "image larger than the context workspace");
   if (std::min(w, h) < 100) return fail(HDR_ERR_INVALID, "input below 100 pixels in one dimension");
   if (ntiles_of(w, h, p->tile) > c->rows_cap) return fail(HDR_ERR_INVALID, "too many tiles");
-  if (w > 7000) return fail(HDR_ERR_INVALID, "width above 7000 is not supported by the row filter");
   size_t side = 2 * (size_t)p->radius + p->patch;
   if ((side * side + (size_t)p->patch * p->patch) * 8 > 200 * 1024)
     return fail(HDR_ERR_INVALID, "radius/patch search window exceeds shared memory");
@@ -1058,7 +1057,7 @@ extern "C" int hdr_dark_count(hdr_ctx* c, const float* img, int32_t channels, in
                               float dark_level, uint64_t* out) {
   CtxDevice dg_(c);
   NEED(c && img && out, "null argument");
-  NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  NEED(channels >= 1, "channels must be >= 1");
   launch_dark_count(img, channels, n, dark_level, reinterpret_cast<unsigned long long*>(out),
                     c->stream);
   return check_launch();
@@ -1068,7 +1067,7 @@ extern "C" int hdr_mean_luminance(hdr_ctx* c, const float* img, int32_t channels
                                   double* out) {
   CtxDevice dg_(c);
   NEED(c && img && out, "null argument");
-  NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  NEED(channels >= 1, "channels must be >= 1");
   launch_mean_luminance(img, channels, n, out, c->stream);
   return check_launch();
 }
@@ -1460,16 +1459,100 @@ extern "C" int hdr_sparse_maps(hdr_ctx* c, const double* matches, int32_t m, int
 extern "C" int hdr_dt_filter(hdr_ctx* c, const float* guide, double* planes, int32_t k, int32_t w,
                              int32_t h, double sigma_s, double sigma_r, int32_t passes) {
   CtxDevice dg_(c);
-  NEED(c && guide && planes, "null argument");
+  NEED(c && guide && planes && w >= 1 && h >= 1, "null argument");
   if (!(sigma_s > 0) || !(sigma_r > 0)) return fail(HDR_ERR_INVALID, "sigma_s and sigma_r must be positive");
   if (passes < 1) return fail(HDR_ERR_INVALID, "passes must be >= 1");
-  NEED(k >= 1 && k <= 3, "1 to 3 planes supported");
-  NEED(w <= 7000, "width above 7000 is not supported by the row filter");
-  NEED(dt_scratch_doubles(w, h, k) <= dt_scratch_doubles(c->W, c->H, 3), "image larger than the workspace");
+  NEED(k >= 1, "at least one data plane");
+  NEED(dt_scratch_doubles(w, h, 3) <= dt_scratch_doubles(c->W, c->H, 3), "image larger than the workspace");
   int64_t P = (int64_t)w * h;
-  DtPlanes pl = f64_planes(planes, planes + P, planes + 2 * P, k);
-  launch_dt_filter(guide, pl, w, h, sigma_s, sigma_r, passes, c->carry, c->stream);
+  // planes share the guide's coefficients and never interact: groups of three
+  for (int k0 = 0; k0 < k; k0 += 3) {
+    int kk = std::min(3, k - k0);
+    double* b = planes + (int64_t)k0 * P;
+    DtPlanes pl = f64_planes(b, b + P, b + 2 * P, kk);
+    launch_dt_filter(guide, pl, w, h, sigma_s, sigma_r, passes, c->carry, c->stream);
+  }
   return check_launch();
+}
+
+extern "C" int hdr_dt_filter_general(hdr_ctx* c, const double* guide, int32_t channels, double* planes,
+                                     int32_t k, int32_t w, int32_t h, double sigma_s, double sigma_r,
+                                     int32_t passes) {
+  CtxDevice dg_(c);
+  NEED(c && guide && planes && w >= 1 && h >= 1, "null argument");
+  if (!(sigma_s > 0) || !(sigma_r > 0)) return fail(HDR_ERR_INVALID, "sigma_s and sigma_r must be positive");
+  if (passes < 1) return fail(HDR_ERR_INVALID, "passes must be >= 1");
+  NEED(k >= 1 && channels >= 1, "at least one data plane and one guide channel");
+  int64_t P = (int64_t)w * h;
+  for (int k0 = 0; k0 < k; k0 += 3) {
+    int kk = std::min(3, k - k0);
+    double* b = planes + (int64_t)k0 * P;
+    DtPlanes pl = f64_planes(b, b + P, b + 2 * P, kk);
+    launch_dt_filter_general(guide, channels, pl, w, h, sigma_s, sigma_r, passes, c->stream);
+  }
+  return check_launch();
+}
+
+// one status word of the context read back synchronously (stage twins whose
+// reference raises on a data-dependent condition)
+static int status_word(hdr_ctx* c, int32_t* st) {
+  CUDA_TRY(cudaMemcpyAsync(st, c->counters + 2, sizeof *st, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return check_launch();
+}
+
+extern "C" int hdr_rect_sum(hdr_ctx* c, const double* table, int32_t w1, int32_t h1, const int64_t* q,
+                            int64_t n, double* out) {
+  CtxDevice dg_(c);
+  NEED(c && table && (n == 0 || (q && out)) && w1 >= 1 && h1 >= 1, "null argument");
+  CUDA_TRY(cudaMemsetAsync(c->counters + 2, 0, sizeof(int32_t), c->stream));
+  launch_rect_sum(table, w1, h1, q, n, out, c->counters + 2, c->stream);
+  int32_t st = 0;
+  int rc = status_word(c, &st);
+  if (rc) return rc;
+  if (st) return fail(HDR_ERR_INVALID, "rectangle bounds out of range");
+  return HDR_OK;
+}
+
+extern "C" int hdr_quantize_256(hdr_ctx* c, const void* x, int32_t is_f64, int64_t n, uint8_t* out) {
+  CtxDevice dg_(c);
+  NEED(c && (n == 0 || (x && out)), "null argument");
+  launch_quantize(x, is_f64 != 0, n, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_downsample(hdr_ctx* c, const void* img, int32_t is_f64, int32_t w, int32_t h,
+                              int32_t channels, float* out) {
+  CtxDevice dg_(c);
+  NEED(c && img && out && channels >= 1, "null argument");
+  if (h < 2 || w < 2) return fail(HDR_ERR_INVALID, "image too small to downsample");
+  launch_downsample_ch(img, is_f64 != 0, w, h, channels, out, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_apply_homography(hdr_ctx* c, const double* H, const double* pts, int64_t n, double* out) {
+  CtxDevice dg_(c);
+  NEED(c && H && (n == 0 || (pts && out)), "null argument");
+  CUDA_TRY(cudaMemsetAsync(c->counters + 2, 0, sizeof(int32_t), c->stream));
+  launch_apply_homography(H, pts, n, out, c->counters + 2, c->stream);
+  int32_t st = 0;
+  int rc = status_word(c, &st);
+  if (rc) return rc;
+  if (st) return fail(HDR_ERR_INVALID, "point maps to infinity");
+  return HDR_OK;
+}
+
+extern "C" int hdr_symmetric_transfer_error(hdr_ctx* c, const double* H, const double* ref_pts,
+                                            const double* src_pts, int64_t n, double* out) {
+  CtxDevice dg_(c);
+  NEED(c && H && (n == 0 || (ref_pts && src_pts && out)), "null argument");
+  CUDA_TRY(cudaMemsetAsync(c->counters + 2, 0, sizeof(int32_t), c->stream));
+  launch_transfer_error(H, ref_pts, src_pts, n, out, c->counters + 2, c->stream);
+  int32_t st = 0;
+  int rc = status_word(c, &st);
+  if (rc) return rc;
+  if (st) return fail(HDR_ERR_SINGULAR, "Singular matrix");
+  return HDR_OK;
 }
 
 extern "C" int hdr_densify_finalize(hdr_ctx* c, const double* smooth, int32_t w, int32_t h,
@@ -1489,7 +1572,7 @@ extern "C" int hdr_warp_image(hdr_ctx* c, const float* src, int32_t channels, in
                               const float* flow, float* warped, uint8_t* valid) {
   CtxDevice dg_(c);
   NEED(c && src && flow && warped && valid, "null argument");
-  NEED(channels == 1 || channels == 3, "channels must be 1 or 3");
+  NEED(channels >= 1, "channels must be >= 1");
   if (channels == 3 && (int64_t)w * h <= c->P) {
     // the pair pipeline's kernel (its luminance histogram lands in scratch)
     launch_warp(flow, w, h, src, warped, valid, c->qw, c->hist + 2 * kBins, c->stream);

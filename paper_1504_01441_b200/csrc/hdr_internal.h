@@ -160,6 +160,22 @@ bool launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double 
                       double sigma_r, int passes, double* scratch, cudaStream_t s,
                       const DtFlowOut* fo = nullptr, KProbe* kp_rows = nullptr,
                       KProbe* kp_cols = nullptr, const DtSparse* first = nullptr);
+// ---- k_twins.cu (general stage twins)
+// f32 single-channel guide, one row pass of any width (sequential per row)
+void launch_dt_rows_seq(const float* guide, const DtPlanes& P, int w, int h, double ratio, double c,
+                        cudaStream_t s);
+// the whole filter for an f64 guide of C interleaved channels, <= 3 planes
+void launch_dt_filter_general(const double* guide, int C, const DtPlanes& P, int w, int h,
+                              double sigma_s, double sigma_r, int passes, cudaStream_t s);
+// q = (x0[n], y0[n], x1[n], y1[n]) int64; *bad = 1 on an out-of-range query
+void launch_rect_sum(const double* table, int64_t w1, int64_t h1, const int64_t* q, int64_t n,
+                     double* out, int32_t* bad, cudaStream_t s);
+void launch_quantize(const void* x, bool f64, int64_t n, uint8_t* out, cudaStream_t s);
+void launch_downsample_ch(const void* in, bool f64, int w, int h, int C, float* out, cudaStream_t s);
+void launch_apply_homography(const double* H, const double* pts, int64_t n, double* out, int32_t* bad,
+                             cudaStream_t s);
+void launch_transfer_error(const double* H, const double* rp, const double* sp, int64_t n, double* out,
+                           int32_t* bad, cudaStream_t s);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
                  uint8_t* qw, uint32_t* hist, cudaStream_t s);

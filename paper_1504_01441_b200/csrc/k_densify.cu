@@ -224,12 +224,13 @@ __global__ void __launch_bounds__(256) finalize_warp_kernel(
     const float* s01 = src + ((int64_t)y0 * w + x1) * channels;
     const float* s10 = src + ((int64_t)y1 * w + x0) * channels;
     const float* s11 = src + ((int64_t)y1 * w + x1) * channels;
-    float o[3];
+    float o[3] = {0.0f, 0.0f, 0.0f};  // the first three channels, for the luminance
     for (int k = 0; k < channels; ++k) {
       double top = dadd(dmul((double)s00[k], gx), dmul((double)s01[k], fx));
       double bot = dadd(dmul((double)s10[k], gx), dmul((double)s11[k], fx));
-      o[k] = (float)dadd(dmul(top, gy), dmul(bot, fy));
-      warped[i * channels + k] = o[k];
+      float v = (float)dadd(dmul(top, gy), dmul(bot, fy));
+      if (k < 3) o[k] = v;
+      warped[i * channels + k] = v;
     }
     valid[i] = ok ? 1 : 0;
     if (qw) {

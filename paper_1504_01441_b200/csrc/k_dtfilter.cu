@@ -1102,6 +1102,9 @@ static int cluster_bw_log2(int h) {
   return bl >= 1 ? bl : -1;
 }
 
+// dynamic shared memory dt_rows_kernel<K> may take (set by init_densify_attributes)
+static int g_rows_smem_max[4] = {0, 0, 0, 0};
+
 // test hook: 0 selects the agg/link/apply column path
 static bool g_cols_cluster = true;
 // test hook: 0 makes the sparse-first row pass write its sample-free rows
@@ -1144,8 +1147,10 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
       else if (w <= kRowThreads * kRowSeg)
         dt_rows_reg_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double), s>>>(guide, P, w, h,
                                                                                     ratio, c);
-      else
+      else if (row_smem <= (size_t)g_rows_smem_max[K])
         dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
+      else  // rows wider than shared memory: the sequential twin (k_twins.cu)
+        launch_dt_rows_seq(guide, P, w, h, ratio, c, s);
       kprobe_mark(kr, 1, s);
     }
     int bl = cluster_bw_log2(h);
@@ -1185,9 +1190,9 @@ void dt_set_skip_zero_rows(bool on) { g_skip_zero_rows = on; }
 void dt_set_cols_grid_div(int d) { g_cols_grid_div = d < 1 ? 1 : d; }
 
 void init_densify_attributes() {
-  allow_max_dynamic_smem(dt_rows_kernel<1>);
-  allow_max_dynamic_smem(dt_rows_kernel<2>);
-  allow_max_dynamic_smem(dt_rows_kernel<3>);
+  g_rows_smem_max[1] = allow_max_dynamic_smem(dt_rows_kernel<1>);
+  g_rows_smem_max[2] = allow_max_dynamic_smem(dt_rows_kernel<2>);
+  g_rows_smem_max[3] = allow_max_dynamic_smem(dt_rows_kernel<3>);
   allow_max_dynamic_smem(dt_rows_reg_kernel<1>);
   allow_max_dynamic_smem(dt_rows_reg_kernel<2>);
   allow_max_dynamic_smem(dt_rows_reg_kernel<3>);

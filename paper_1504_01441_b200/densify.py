@@ -43,30 +43,39 @@ def build_sparse_maps(matches, width: int, height: int) -> SparseMaps:
 
 def dt_filter(guide, data, sigma_s: float = DEFAULT_SIGMA_S, sigma_r: float = DEFAULT_SIGMA_R,
               passes: int = DEFAULT_PASSES):
-    """densify.py:78-113 — data (h, w) or (h, w, k<=3), float64 result."""
+    """densify.py:78-113 — data (h, w) or (h, w, k), float64 result.
+
+    A single-channel float32 guide takes the pair pipeline's kernels (row
+    sweeps in shared memory, cluster column sweeps); any other guide (several
+    channels, float64 values) takes hdr_dt_filter_general, which sums the
+    channel distances as densify.py:59-66 does."""
     if sigma_s <= 0 or sigma_r <= 0:
         raise ValueError("sigma_s and sigma_r must be positive")
     if passes < 1:
         raise ValueError("passes must be >= 1")
     if guide.shape[:2] != data.shape[:2]:
         raise ValueError("guide and data dimensions differ")
-    if guide.ndim != 2:
-        raise ValueError("the GPU filter takes a single-channel guide")
     as_torch = is_torch(guide, data)
     dev = device_of(guide, data)
-    g = to_dev(guide, torch.float32, dev)
     d = to_dev(data, torch.float64, dev)
     squeeze = d.dim() == 2
     if squeeze:
         d = d[:, :, None]
     h, w, k = d.shape
-    if k > 3:
-        raise ValueError("at most 3 data planes are supported")
     planes = d.permute(2, 0, 1).contiguous()
+    gch = 1 if guide.ndim == 2 else int(guide.shape[2])
+    fast = gch == 1 and guide.dtype in (np.float32, torch.float32)
     e = engine(w, h, dev)
-    _native.check(_native.lib().hdr_dt_filter(e.handle, ptr(g), ptr(planes), k, w, h,
-                                              float(sigma_s), float(sigma_r), int(passes)),
-                  "dt_filter")
+    lib = _native.lib()
+    if fast:
+        g = to_dev(guide, torch.float32, dev).reshape(h, w)
+        rc = lib.hdr_dt_filter(e.handle, ptr(g), ptr(planes), k, w, h, float(sigma_s),
+                               float(sigma_r), int(passes))
+    else:
+        g = to_dev(guide, torch.float64, dev).reshape(h, w, gch)
+        rc = lib.hdr_dt_filter_general(e.handle, ptr(g), gch, ptr(planes), k, w, h,
+                                       float(sigma_s), float(sigma_r), int(passes))
+    _native.check(rc, "dt_filter")
     res = planes.permute(1, 2, 0)
     res = res[:, :, 0] if squeeze else res.contiguous()
     return out(res.contiguous(), as_torch)
@@ -104,9 +113,7 @@ def warp_image(src, flow):
     dev = device_of(src, flow)
     s = to_dev(src, torch.float32, dev)
     f = to_dev(flow, torch.float32, dev)
-    ch = 1 if s.dim() == 2 else s.shape[2]
-    if ch not in (1, 3):
-        raise ValueError("warp_image supports 1 or 3 channels")
+    ch = 1 if s.dim() == 2 else int(s.shape[2])
     warped = torch.empty_like(s)
     valid = torch.empty((h, w), dtype=torch.uint8, device=s.device)
     e = engine(1, 1, dev)

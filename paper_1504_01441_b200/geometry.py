@@ -2,8 +2,9 @@
 
 `fit_homography` runs the block-wide DLT of K8 (pivoted Householder for
 four points, Gram + Jacobi for least squares) with the reference's
-DegenerateFit rules; `inlier_mask` and `homography_pixel_flow` are K7's
-transfer test and the fallback flow of K11.
+DegenerateFit rules; `inlier_mask`, `symmetric_transfer_error` and
+`homography_pixel_flow` are K7's transfer test and the fallback flow of K11;
+`apply_homography` maps points on the device.
 """
 
 from __future__ import annotations
@@ -38,17 +39,19 @@ def fit_homography(ref_pts, src_pts):
 
 
 def apply_homography(h, pts):
-    """geometry.py:80-93 (host helper; not on the pair path)."""
-    h = h.cpu().numpy() if isinstance(h, torch.Tensor) else np.asarray(h)
-    pts = np.asarray(pts, dtype=np.float64)
-    x, y = pts[..., 0], pts[..., 1]
-    denom = h[2, 0] * x + h[2, 1] * y + h[2, 2]
-    if np.any(np.abs(denom) < 1e-12):
-        raise ValueError("point maps to infinity")
-    res = np.empty_like(pts)
-    res[..., 0] = (h[0, 0] * x + h[0, 1] * y + h[0, 2]) / denom
-    res[..., 1] = (h[1, 0] * x + h[1, 1] * y + h[1, 2]) / denom
-    return res
+    """geometry.py:80-93 — projective map of (..., 2) points on the GPU;
+    ValueError if any point lands at infinity."""
+    as_torch = is_torch(h, pts)
+    dev = device_of(h, pts)
+    hm = to_dev(h, torch.float64, dev)
+    p = to_dev(pts, torch.float64, dev)
+    shape = tuple(p.shape)
+    p2 = p.reshape(-1, 2)
+    res = torch.empty_like(p2)
+    e = engine(1, 1, dev)
+    _native.check(_native.lib().hdr_apply_homography(e.handle, ptr(hm), ptr(p2), p2.shape[0], ptr(res)),
+                  "apply_homography")
+    return out(res.reshape(shape), as_torch)
 
 
 def inlier_mask(h, ref_pts, src_pts, eps: float):
@@ -67,21 +70,21 @@ def inlier_mask(h, ref_pts, src_pts, eps: float):
 
 
 def symmetric_transfer_error(h, ref_pts, src_pts):
-    """geometry.py:107-115 (host helper used by diagnostics only)."""
-    h = h.cpu().numpy() if isinstance(h, torch.Tensor) else np.asarray(h, dtype=np.float64)
-    ref_pts = np.asarray(ref_pts, dtype=np.float64).reshape(-1, 2)
-    src_pts = np.asarray(src_pts, dtype=np.float64).reshape(-1, 2)
-
-    def dist(hh, p, t):
-        d = hh[2, 0] * p[:, 0] + hh[2, 1] * p[:, 1] + hh[2, 2]
-        res = np.full(len(p), np.inf)
-        ok = np.abs(d) >= 1e-12
-        mx = (hh[0, 0] * p[:, 0] + hh[0, 1] * p[:, 1] + hh[0, 2])[ok] / d[ok]
-        my = (hh[1, 0] * p[:, 0] + hh[1, 1] * p[:, 1] + hh[1, 2])[ok] / d[ok]
-        res[ok] = np.hypot(mx - t[ok, 0], my - t[ok, 1])
-        return res
-
-    return np.hypot(dist(h, ref_pts, src_pts), dist(np.linalg.inv(h), src_pts, ref_pts))
+    """geometry.py:107-115 — per-pair hypot(fwd, bwd) on the GPU, h_inv by
+    LU with partial pivoting as np.linalg.inv (LinAlgError if singular)."""
+    as_torch = is_torch(h, ref_pts, src_pts)
+    dev = device_of(h, ref_pts, src_pts)
+    hm = to_dev(h, torch.float64, dev)
+    r = to_dev(ref_pts, torch.float64, dev).reshape(-1, 2)
+    s = to_dev(src_pts, torch.float64, dev).reshape(-1, 2)
+    if r.shape[0] != s.shape[0]:
+        raise ValueError("ref_pts and src_pts hold different numbers of points")
+    res = torch.empty(r.shape[0], dtype=torch.float64, device=r.device)
+    e = engine(1, 1, dev)
+    _native.check(_native.lib().hdr_symmetric_transfer_error(e.handle, ptr(hm), ptr(r), ptr(s),
+                                                             r.shape[0], ptr(res)),
+                  "symmetric_transfer_error")
+    return out(res, as_torch)
 
 
 def homography_pixel_flow(h, width: int, height: int):

@@ -57,8 +57,17 @@ def match_histogram(src, ref):
 
 
 def quantize_256(img):
-    """image.py:91-93 (host helper, not on the GPU path)."""
-    return np.clip(np.floor(np.asarray(img) * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    """image.py:91-93 — floor(x * 255 + 0.5) clipped to uint8 on the GPU
+    (float32 samples in float32 arithmetic, anything else in float64)."""
+    as_torch = is_torch(img)
+    dev = device_of(img)
+    f32 = img.dtype in (np.float32, torch.float32)
+    t = to_dev(img, torch.float32 if f32 else torch.float64, dev)
+    res = torch.empty(t.shape, dtype=torch.uint8, device=t.device)
+    e = engine(1, 1, dev)
+    _native.check(_native.lib().hdr_quantize_256(e.handle, ptr(t), 0 if f32 else 1, t.numel(),
+                                                 ptr(res)), "quantize_256")
+    return out(res, as_torch)
 
 
 def integral(img):
@@ -74,26 +83,60 @@ def integral(img):
     return out(table, as_torch)
 
 
+_INDEX_ERROR = ("only integers, slices (`:`), ellipsis (`...`), numpy.newaxis (`None`) and "
+                "integer or boolean arrays are valid indices")
+
+
 def rect_sum(table, x0, y0, x1, y1):
-    """image.py:47-58 (host helper over an already computed table)."""
-    t = table.cpu().numpy() if isinstance(table, torch.Tensor) else table
+    """image.py:47-58 — batched rectangle sums on the GPU (scalars or
+    broadcastable integer arrays; an out-of-range rectangle raises
+    ValueError as the reference does)."""
+    as_torch = is_torch(table, x0, y0, x1, y1)
+    dev = device_of(table, x0, y0, x1, y1)
+    t = to_dev(table, torch.float64, dev)
     h1, w1 = t.shape
-    x0, y0, x1, y1 = (np.asarray(v) for v in (x0, y0, x1, y1))
-    if (np.any(x0 < 0) or np.any(y0 < 0) or np.any(x0 > x1) or np.any(y0 > y1)
-            or np.any(x1 >= w1) or np.any(y1 >= h1)):
-        raise ValueError("rectangle bounds out of range")
-    return t[y1, x1] - t[y0, x1] - t[y1, x0] + t[y0, x0]
+    if is_torch(x0, y0, x1, y1):
+        b = torch.broadcast_tensors(*(to_dev(v, torch.int64, dev) if isinstance(v, torch.Tensor)
+                                      else torch.as_tensor(v, device=f"cuda:{dev}")
+                                      for v in (x0, y0, x1, y1)))
+        if any(v.dtype.is_floating_point or v.dtype.is_complex for v in b):
+            raise IndexError(_INDEX_ERROR)
+        shape = tuple(b[0].shape)
+        q = torch.stack([v.reshape(-1).to(torch.int64) for v in b]).contiguous()
+    else:
+        b = np.broadcast_arrays(*(np.asarray(v) for v in (x0, y0, x1, y1)))
+        if any(not (np.issubdtype(v.dtype, np.integer) or v.dtype == np.bool_) for v in b):
+            raise IndexError(_INDEX_ERROR)
+        shape = b[0].shape
+        q = to_dev(np.stack([v.reshape(-1).astype(np.int64) for v in b]), torch.int64, dev)
+    n = q.shape[1]
+    res = torch.empty(n, dtype=torch.float64, device=t.device)
+    e = engine(1, 1, dev)
+    _native.check(_native.lib().hdr_rect_sum(e.handle, ptr(t), w1, h1, ptr(q), n, ptr(res)),
+                  "rect_sum")
+    res = res.reshape(shape)
+    if as_torch:
+        return res
+    r = res.cpu().numpy()
+    return r[()] if shape == () else r
 
 
 def downsample(img):
-    """image.py:61-68 — one 2x2 box level (kernel K3)."""
+    """image.py:61-68 — one 2x2 box level, any channel count (kernel K3 /
+    hdr_downsample); float32 result."""
     h, w = img.shape[:2]
     if h < 2 or w < 2:
         raise ValueError("image too small to downsample")
-    if img.ndim != 2:
-        raise ValueError("downsample on the GPU path expects a single-channel image")
-    lv = build_pyramid(img, max_levels=2, min_dim=0)
-    return lv[1]
+    as_torch = is_torch(img)
+    dev = device_of(img)
+    f32 = img.dtype in (np.float32, torch.float32)
+    t = to_dev(img, torch.float32 if f32 else torch.float64, dev)
+    ch = 1 if t.dim() == 2 else int(t.shape[2])
+    res = torch.empty((h // 2, w // 2) + tuple(t.shape[2:]), dtype=torch.float32, device=t.device)
+    e = engine(1, 1, dev)
+    _native.check(_native.lib().hdr_downsample(e.handle, ptr(t), 0 if f32 else 1, w, h, ch, ptr(res)),
+                  "downsample")
+    return out(res, as_torch)
 
 
 def build_pyramid(img, max_levels: int = PYRAMID_MAX_LEVELS, min_dim: int = PYRAMID_MIN_DIM):
@@ -101,8 +144,15 @@ def build_pyramid(img, max_levels: int = PYRAMID_MAX_LEVELS, min_dim: int = PYRA
     h, w = img.shape[:2]
     if min(h, w) < min_dim:
         raise ValueError(f"input below {min_dim} pixels in one dimension")
-    if img.ndim != 2:
-        raise ValueError("the GPU pyramid expects a single-channel image")
+    if img.ndim != 2 or img.dtype not in (np.float32, torch.float32):
+        # multi-channel or non-float32 levels: one hdr_downsample per level
+        levels = [img]
+        while len(levels) < max_levels:
+            ph, pw = levels[-1].shape[:2]
+            if min(ph // 2, pw // 2) < min_dim:
+                break
+            levels.append(downsample(levels[-1]))
+        return levels
     as_torch = is_torch(img)
     t = to_dev(img, torch.float32, device_of(img))
     dims = [(h, w)]

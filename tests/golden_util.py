@@ -10,6 +10,8 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 SCENES = ["vga_s0", "vga_rot_s1", "qvga_s2", "r960_s3"]
 # BASELINE configs[1] (5MP) and configs[3] (12MP), from the real reference
 BIG_SCENES = ["c2_5mp_s0", "c4_12mp_s0"]
+# rows wider than the shared-memory row kernels (7200 px), same fixture format
+WIDE_SCENES = ["wide_7200x1000_s0"]
 
 
 def digest(a) -> str:

@@ -19,7 +19,7 @@ luminance).
 import numpy as np
 import pytest
 
-from golden_util import BIG_SCENES, digest, load, scene_inputs
+from golden_util import BIG_SCENES, WIDE_SCENES, digest, load, scene_inputs
 from oracle import hdr_oracle as O
 from paper_1504_01441_b200 import matcher, pipeline, weeding
 
@@ -31,7 +31,7 @@ SSIM_TOL = 1e-4
 H_RTOL = 1e-4
 
 
-@pytest.fixture(scope="module", params=BIG_SCENES)
+@pytest.fixture(scope="module", params=BIG_SCENES + WIDE_SCENES)
 def big(request, cuda):
     fx = load(request.param)
     ref, src = scene_inputs(fx)

@@ -4,12 +4,12 @@ REAL reference (oracle/gen_golden.py). CPU only."""
 import numpy as np
 import pytest
 
-from golden_util import BIG_SCENES, SCENES, digest, load, scene_inputs
+from golden_util import BIG_SCENES, WIDE_SCENES, SCENES, digest, load, scene_inputs
 from oracle import hdr_oracle as O
 from harness import synth
 
 
-@pytest.fixture(scope="module", params=SCENES + BIG_SCENES)
+@pytest.fixture(scope="module", params=SCENES + BIG_SCENES + WIDE_SCENES)
 def scene(request):
     fx = load(request.param)
     ref, src = scene_inputs(fx)

@@ -71,8 +71,12 @@ __device__ __forceinline__ Aff<K> shfl_aff(const Aff<K>& v, int off, bool up) {
 #ifndef HDR_ROW_THREADS
 #define HDR_ROW_THREADS 512
 #endif
+// 9, not 8: widths in (3584, 4096] (12MP is 4000) then take 9-sample odd
+// segments instead of 8-sample even ones whose half-warp loads conflict
+// (kbench dt at 4000x3000: 2267 -> 1295 us for the three-pass filter; 5MP
+// unchanged, its segments are 7)
 #ifndef HDR_ROW_SEG
-#define HDR_ROW_SEG 8
+#define HDR_ROW_SEG 9
 #endif
 constexpr int kRowThreads = HDR_ROW_THREADS;
 

@@ -499,10 +499,33 @@ class DeviceLeg:
         clk = clocks.stop() if clocks else None
         return t0.elapsed_time(t1), clk
 
+    def latency(self, n=5):
+        """Device time of one pair alone on one stream, no probes: CUDA events
+        on the launching stream around one replay of the pair graph (median of
+        n after a warm replay that captures it; the same buffers every time,
+        so no replay waits for a capture)."""
+        import torch
+        r = self.runner
+        s0 = r.streams[0]
+        ts = []
+        ref, src = self.inputs[0]
+        for j in range(n + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(s0)
+            r.enqueue(0, ref, src, self.outs[0])
+            e1.record(s0)
+            torch.cuda.synchronize()
+            if j:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
     def isolated(self, n=3):
         """Stage and kernel times of pairs run one at a time on one stream
         (events recorded inside the replayed graph between the stages and
-        around every launch of the probed kernel families)."""
+        around every launch of the probed kernel families). The probes cut
+        the replay into event-separated pieces, so their sum runs ~0.1 ms
+        above latency()'s unprobed pair."""
         import torch
         from paper_1504_01441_b200 import _native
         nst = _native.NUM_STAGES
@@ -677,11 +700,13 @@ def extra_pairs_leg(args, local, peak, cpu_kind):
     leg = DeviceLeg(w, h, scenes, sc, n, args.streams, local, graph=not args.no_graph)
     steps = max(3, args.steps // 4)
     ms, _ = leg.timed(sc, steps, args.warmup)
-    stage_ms, kernel_ms, latency = leg.isolated(3)
+    stage_ms, kernel_ms, probed = leg.isolated(3)
+    latency = leg.latency()
     kro, sro = rooflines(w, h, stage_ms, kernel_ms, peak)
     obj = {"workload": "12MP (4000x3000) two-exposure pair (BASELINE configs[3])",
            "value": n * steps / (ms / 1e3), "unit": "pairs/s", "pairs_per_step": n, "steps": steps,
-           "pair_latency_ms": latency, "stage_ms": stage_ms, "kernel_rooflines": kro,
+           "pair_latency_ms": latency, "pair_latency_probed_ms": probed, "stage_ms": stage_ms,
+           "kernel_rooflines": kro,
            "stage_rooflines": sro, "gpu_launches": leg.runner.graph_kernels() * n * steps}
     if not args.no_cpu_baseline:
         procs = min(host_cores(), 8)
@@ -829,7 +854,8 @@ def run_ours(args):
     ms = hd.max_over_ranks(ms, device=dev)
     hd.barrier()
     parity = parity_summary(leg, pair_scenes, cpu_res) if cpu_res else None
-    stage_ms, kernel_ms, latency = leg.isolated(3)
+    stage_ms, kernel_ms, probed = leg.isolated(3)
+    latency = leg.latency()
     kernels_per_pair = leg.runner.graph_kernels()
     leg.close()
     del leg
@@ -885,7 +911,8 @@ def run_ours(args):
                              "run one at a time after the timed region; traffic = ncu dram bytes "
                              "per launch (profiles/)"},
         "kernel_rooflines": kro, "stage_rooflines": sro,
-        "pair_latency_ms": latency, "stage_ms": stage_ms, "kernel_ms": kernel_ms,
+        "pair_latency_ms": latency, "pair_latency_probed_ms": probed, "stage_ms": stage_ms,
+        "kernel_ms": kernel_ms,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "pairs_per_step": E},
         "e2e_png8": {"value": png8_value, "unit": "pairs/s", "h2d_bytes_per_step": rh2d,

@@ -42,6 +42,10 @@ static int check_launch() {
 
 extern "C" const char* hdr_last_error(void) { return g_err.c_str(); }
 
+namespace hdr {
+bool g_pdl = true;
+}
+
 // test hook: 0 sends the pair through the dense splat + first row pass
 static bool g_sparse_first = true;
 
@@ -56,6 +60,10 @@ extern "C" int hdr_set_option(const char* name, int64_t value) {
   }
   if (name && std::string(name) == "dt_cols_grid_div") {
     hdr::dt_set_cols_grid_div((int)value);
+    return HDR_OK;
+  }
+  if (name && std::string(name) == "pdl") {
+    hdr::g_pdl = value != 0;
     return HDR_OK;
   }
   if (name && std::string(name) == "dt_cols_prefetch") {
@@ -818,15 +826,18 @@ static DtPlanes pair_planes(hdr_ctx* c, int64_t P) {
 
 // ------------------------------------------------------------ kernels used by the pipeline only
 __global__ void info_init_kernel(int32_t* info, int levels) {
+  pdl_wait();
   int i = threadIdx.x;
   if (i < HDR_INFO_WORDS) info[i] = (i == 2) ? levels : 0;
 }
 
 __global__ void status_kernel(const int32_t* weeded_count, int32_t* info) {
+  pdl_wait();
   if (threadIdx.x == 0) info[0] = (*weeded_count >= 4) ? HDR_OK : HDR_ERR_REGISTRATION;
 }
 
 __global__ void copy_i32_kernel(const int32_t* src, int32_t* dst) {
+  pdl_wait();
   if (threadIdx.x == 0) *dst = *src;
 }
 
@@ -845,7 +856,7 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
   Dims d[kMaxLevels];
   int L = pyramid_dims(w, h, p->max_levels, d);
   probe(c, 0, 0);
-  info_init_kernel<<<1, 32, 0, s>>>(info, L);
+  klaunch(info_init_kernel, 1, 32, 0, s, info, L);
   CUDA_TRY(cudaMemsetAsync(c->hist, 0, sizeof(uint32_t) * 4 * kBins, s));
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(int32_t) * 16, s));
   launch_luma_hist(ref, P, c->lum_ref, nullptr, c->hist, s);
@@ -898,8 +909,8 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
                         nullptr, c->hpred, out_h, info, l == 0 ? out_matches : nullptr, nullptr,
                         grey, s);
   }
-  status_kernel<<<1, 32, 0, s>>>(weeded_count, info);
-  copy_i32_kernel<<<1, 32, 0, s>>>(grey, info + 18);
+  klaunch(status_kernel, 1, 32, 0, s, weeded_count, info);
+  klaunch(copy_i32_kernel, 1, 32, 0, s, grey, info + 18);
   probe(c, 2, 1);
   return check_launch();
 }
@@ -1312,6 +1323,7 @@ extern "C" int hdr_match_level(hdr_ctx* c, const hdr_params* p, const float* lum
 }
 
 __global__ void rows_from_matrix_kernel(const double* m, int n, MatchRow* rows, int32_t* count) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) *count = n;
   if (i >= n) return;
@@ -1322,6 +1334,7 @@ __global__ void rows_from_matrix_kernel(const double* m, int n, MatchRow* rows, 
 
 __global__ void widen_kept_kernel(const uint32_t* mask, const int32_t* wit, int n, int64_t* kept,
                                   int32_t* n_kept, int64_t* witness) {
+  pdl_wait();
   // single block: ordered compaction of the reliable mask
   __shared__ int scratch[32];
   int base = 0;
@@ -1356,10 +1369,10 @@ extern "C" int hdr_weed(hdr_ctx* c, const double* matches, int32_t n, int32_t w,
   CUDA_TRY(cudaMallocAsync(&dkeys, host.size() * sizeof(uint64_t), s));
   CUDA_TRY(cudaMallocAsync(&dfits, sizeof(double) * 20 * (size_t)iterations, s));
   CUDA_TRY(cudaMemcpyAsync(dkeys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-  rows_from_matrix_kernel<<<ceil_div(n, 256), 256, 0, s>>>(matches, n, c->raw, c->counters + 0);
+  klaunch(rows_from_matrix_kernel, ceil_div(n, 256), 256, 0, s, matches, n, c->raw, c->counters + 0);
   launch_weed(c->raw, c->counters + 0, n, w, h, iterations, eps, dkeys, delta, dfits, c->mask,
               c->witness, c->counters + 3, s);
-  widen_kept_kernel<<<1, 1024, 0, s>>>(c->mask, c->witness, n, kept, c->counters + 6, witness);
+  klaunch(widen_kept_kernel, 1, 1024, 0, s, c->mask, c->witness, n, kept, c->counters + 6, witness);
   CUDA_TRY(cudaMemcpyAsync(n_kept, c->counters + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaFreeAsync(dkeys, s));
   CUDA_TRY(cudaFreeAsync(dfits, s));
@@ -1380,7 +1393,7 @@ extern "C" int hdr_fit_matches_homography(hdr_ctx* c, const double* matches, int
   if (n < 4) return fail(HDR_ERR_INVALID, "need at least 4 point pairs");
   NEED(n <= c->rows_cap, "too many matches for the workspace");
   cudaStream_t s = c->stream;
-  rows_from_matrix_kernel<<<ceil_div(n, 256), 256, 0, s>>>(matches, n, c->raw, c->counters + 0);
+  klaunch(rows_from_matrix_kernel, ceil_div(n, 256), 256, 0, s, matches, n, c->raw, c->counters + 0);
   launch_fit_rows(c->raw, c->counters + 0, w, h, H, c->counters + 4, s);
   int32_t st = 0;
   CUDA_TRY(cudaMemcpyAsync(&st, c->counters + 4, sizeof st, cudaMemcpyDeviceToHost, s));

@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(1024) splat_kernel(const double* __restrict__ 
                                                      unsigned long long* __restrict__ key,
                                                      int32_t* __restrict__ idx,
                                                      int32_t* __restrict__ status) {
+  pdl_wait();
   int n = count ? *count : m_static;
   int64_t p;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -63,7 +64,7 @@ void launch_splat(const double* matches, const int32_t* count, int m_static, int
   int64_t P = (int64_t)w * h;
   for (int k = 0; k < 3; ++k)
     cudaMemsetAsync(maps.p[k], 0, P * (maps.f64[k] ? 8 : 4), s);
-  splat_kernel<<<1, 1024, 0, s>>>(matches, count, m_static, w, h, maps,
+  klaunch(splat_kernel, 1, 1024, 0, s, matches, count, m_static, w, h, maps,
                                   reinterpret_cast<unsigned long long*>(scratch_key), scratch_idx,
                                   status);
 }
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(1024) splat_rows_kernel(
     const double* __restrict__ m, const int32_t* __restrict__ count, int m_static, int w, int h,
     unsigned long long* __restrict__ key, int32_t* __restrict__ idx, int32_t* __restrict__ row_count,
     int32_t* __restrict__ row_start, SparseEntry* __restrict__ entries, int32_t* __restrict__ status) {
+  pdl_wait();
   __shared__ int32_t part[1024];
   int n = count ? *count : m_static;
   int64_t p;
@@ -140,13 +142,14 @@ __global__ void __launch_bounds__(1024) splat_rows_kernel(
 void launch_splat_rows(const double* matches, const int32_t* count, int m_static, int w, int h,
                        uint64_t* scratch_key, int32_t* scratch_idx, int32_t* row_count,
                        int32_t* row_start, SparseEntry* entries, int32_t* status, cudaStream_t s) {
-  splat_rows_kernel<<<1, 1024, 0, s>>>(matches, count, m_static, w, h,
+  klaunch(splat_rows_kernel, 1, 1024, 0, s, matches, count, m_static, w, h,
                                        reinterpret_cast<unsigned long long*>(scratch_key),
                                        scratch_idx, row_count, row_start, entries, status);
 }
 
 // ---------------------------------------------------------------- K11/K12
 __global__ void hflow_kernel(const double* __restrict__ Hd, int w, int h, float* __restrict__ flow) {
+  pdl_wait();
   __shared__ double H[9];
   if (threadIdx.x < 9) H[threadIdx.x] = Hd[threadIdx.x];
   __syncthreads();
@@ -160,7 +163,7 @@ __global__ void hflow_kernel(const double* __restrict__ Hd, int w, int h, float*
 
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s) {
   int64_t n = (int64_t)w * h;
-  hflow_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, w, h, flow);
+  klaunch(hflow_kernel, (unsigned)((n + 255) / 256), 256, 0, s, H, w, h, flow);
 }
 
 __device__ __forceinline__ float luma3(float r, float g, float b) {
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(256) finalize_warp_kernel(
     int w, int h, double floor_, const float* __restrict__ src, int channels,
     float* __restrict__ flow, float* __restrict__ warped, uint8_t* __restrict__ valid,
     uint8_t* __restrict__ qw, uint32_t* __restrict__ hist, bool do_flow) {
+  pdl_wait();
   __shared__ uint32_t sh[kBins];
   __shared__ double H[9];
   __shared__ int use_fb;
@@ -257,6 +261,7 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
                                                    uint8_t* __restrict__ valid,
                                                    uint8_t* __restrict__ qw,
                                                    uint32_t* __restrict__ hist) {
+  pdl_wait();
   // one histogram per warp (plain shared atomics; see luma_hist_kernel)
   __shared__ uint32_t sh[8][kBins];
   for (int i = threadIdx.x; i < 8 * kBins; i += blockDim.x) (&sh[0][0])[i] = 0;
@@ -315,7 +320,7 @@ void launch_warp(const float* flow, int w, int h, const float* src, float* warpe
 #endif
   int64_t cap = 148 * HDR_WARP_BLOCKS_PER_SM;
   int64_t blocks = work < cap ? work : cap;
-  warp_kernel<<<(unsigned)blocks, 256, 0, s>>>(flow, w, h, src, warped, valid, qw, hist);
+  klaunch(warp_kernel, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist);
 }
 
 void launch_finalize_warp(DtPlanes smooth, const double* fallback, const int32_t* has_fallback,
@@ -325,7 +330,7 @@ void launch_finalize_warp(DtPlanes smooth, const double* fallback, const int32_t
   int64_t P = (int64_t)w * h;
   int64_t blocks = (P + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  finalize_warp_kernel<<<(unsigned)blocks, 256, 0, s>>>(smooth, fallback, has_fallback, w, h,
+  klaunch(finalize_warp_kernel, (unsigned)blocks, 256, 0, s, smooth, fallback, has_fallback, w, h,
                                                         floor_, src, channels, flow, warped,
                                                         valid, qw, hist_w, do_flow);
 }

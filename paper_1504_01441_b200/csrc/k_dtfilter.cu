@@ -84,6 +84,7 @@ template <int K>
 __global__ void __launch_bounds__(kRowThreads) dt_rows_kernel(const float* __restrict__ guide,
                                                               DtPlanes P, int w, int h,
                                                               double ratio, double c) {
+  pdl_wait();
   extern __shared__ double sm[];
   double* xs = sm;          // K * w
   double* av = sm + K * w;  // a between i and i+1; av[w-1] = 0
@@ -191,6 +192,7 @@ template <int K>
 __global__ void __launch_bounds__(kRowThreads) dt_rows_reg_kernel(const float* __restrict__ guide,
                                                                   DtPlanes P, int w, int h,
                                                                   double ratio, double c) {
+  pdl_wait();
   extern __shared__ double xs[];  // K * w
   __shared__ Aff<K> wsum[kRowThreads / 32];
   int y = blockIdx.x;
@@ -379,6 +381,7 @@ template <int K>
 __global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* __restrict__ guide,
                                                                    DtPlanes P, int w, int h,
                                                                    double ratio, double c) {
+  pdl_wait();
   extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
   float* gs = reinterpret_cast<float*>(xs + K * w);
   __shared__ Aff<K> wsum[kRowThreads / 32];
@@ -410,6 +413,7 @@ __global__ void __launch_bounds__(kRowThreads) dt_rows_first_kernel(const float*
                                                                     DtPlanes P, int w, int h,
                                                                     double ratio, double c,
                                                                     DtSparse sp, bool zero_rows) {
+  pdl_wait();
   constexpr int K = 3;
   extern __shared__ __align__(16) double xs[];  // K * w planes, then w guide floats
   float* gs = reinterpret_cast<float*>(xs + K * w);
@@ -507,6 +511,7 @@ template <int K>
 __global__ void __launch_bounds__(kColThreads) dt_cols_agg(const float* __restrict__ guide,
                                                            DtPlanes P, int w, int h, double ratio,
                                                            double c, double* __restrict__ agg) {
+  pdl_wait();
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
@@ -548,6 +553,7 @@ constexpr int kLinkGroups = 32;
 template <int K>
 __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const double* __restrict__ agg,
                                                      double* __restrict__ carry) {
+  pdl_wait();
   __shared__ Aff<K> maps[kLinkGroups][33];
   int cx = threadIdx.x & 31, g = threadIdx.x >> 5;
   int x = blockIdx.x * 32 + cx;
@@ -639,6 +645,7 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
                                                              double ratio, double c,
                                                              const double* __restrict__ carry,
                                                              DtFlowOut fo) {
+  pdl_wait();
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int ch = blockIdx.y, nch = gridDim.y;
   if (x >= w) return;
@@ -818,6 +825,7 @@ template <int K, bool FINAL, bool PF>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 2 : 1)
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
                     double c, int bw_log2, DtFlowOut fo, const int32_t* __restrict__ zrows) {
+  pdl_wait();
   __shared__ Aff<K> wsc[kCT / 32][kMaxBw];  // per-warp totals of the group scans
   // per-column CTA totals read by the cluster peers, double-buffered by band
   // parity: band b+2 reuses band b's buffer only after two cluster barriers,
@@ -1087,13 +1095,13 @@ static void launch_cols_cluster(const float* guide, const DtPlanes& P, int w, in
   if (pf && mc > 0) {
     if (g_cols_grid_div > 1) mc = std::max(1, mc / g_cols_grid_div);
     dim3 cgrid(kCL, std::min(nb, mc));
-    dt_cols_cluster<K, FINAL, true><<<cgrid, kCT, cols_pf_smem<K>(), s>>>(guide, P, w, h, ratio, c, bl, fo,
+    klaunch(dt_cols_cluster<K, FINAL, true>, cgrid, kCT, cols_pf_smem<K>(), s, guide, P, w, h, ratio, c, bl, fo,
                                                                           zrows);
     return;
   }
   mc = max_clusters<K, FINAL, false>();
   dim3 cgrid(kCL, mc > 0 ? std::min(nb, mc) : nb);
-  dt_cols_cluster<K, FINAL, false><<<cgrid, kCT, 0, s>>>(guide, P, w, h, ratio, c, bl, fo, nullptr);
+  klaunch(dt_cols_cluster<K, FINAL, false>, cgrid, kCT, 0, s, guide, P, w, h, ratio, c, bl, fo, nullptr);
 }
 
 // log2 of the cluster kernel's band width for this height, or -1 (too tall)
@@ -1143,16 +1151,16 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
     if (w > 1) {
       kprobe_mark(kr, 0, s);
       if (i == 1 && sp && K == 3)
-        dt_rows_first_kernel<<<h, kRowThreads, (size_t)3 * w * sizeof(double) + (size_t)w * 4, s>>>(
+        klaunch(dt_rows_first_kernel, h, kRowThreads, (size_t)3 * w * sizeof(double) + (size_t)w * 4, s, 
             guide, P, w, h, ratio, c, *sp, !skip_zero);
       else if (rows_bulk_ok(guide, P, w))
-        dt_rows_bulk_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double) + (size_t)w * 4, s>>>(
+        klaunch(dt_rows_bulk_kernel<K>, h, kRowThreads, (size_t)K * w * sizeof(double) + (size_t)w * 4, s, 
             guide, P, w, h, ratio, c);
       else if (w <= kRowThreads * kRowSeg)
-        dt_rows_reg_kernel<K><<<h, kRowThreads, (size_t)K * w * sizeof(double), s>>>(guide, P, w, h,
+        klaunch(dt_rows_reg_kernel<K>, h, kRowThreads, (size_t)K * w * sizeof(double), s, guide, P, w, h,
                                                                                     ratio, c);
       else if (row_smem <= (size_t)g_rows_smem_max[K])
-        dt_rows_kernel<K><<<h, kRowThreads, row_smem, s>>>(guide, P, w, h, ratio, c);
+        klaunch(dt_rows_kernel<K>, h, kRowThreads, row_smem, s, guide, P, w, h, ratio, c);
       else  // rows wider than shared memory: the sequential twin (k_twins.cu)
         launch_dt_rows_seq(guide, P, w, h, ratio, c, s);
       kprobe_mark(kr, 1, s);
@@ -1169,13 +1177,13 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
         launch_cols_cluster<K, false>(guide, P, w, h, ratio, c, bl, fo, s, zr);
       }
     } else if (h > 1) {
-      dt_cols_agg<K><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, agg);
-      dt_cols_link<K><<<ceil_div(w, 32), 1024, 0, s>>>(w, nch, agg, carry);
+      klaunch(dt_cols_agg<K>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, agg);
+      klaunch(dt_cols_link<K>, ceil_div(w, 32), 1024, 0, s, w, nch, agg, carry);
       if (i == passes && fo.flow && K == 3) {
-        dt_cols_apply<K, true><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry, fo);
+        klaunch(dt_cols_apply<K, true>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, carry, fo);
         finalized = true;
       } else {
-        dt_cols_apply<K, false><<<cg, kColThreads, 0, s>>>(guide, P, w, h, ratio, c, carry, fo);
+        klaunch(dt_cols_apply<K, false>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, carry, fo);
       }
     }
     if (h > 1) kprobe_mark(kc, 1, s);

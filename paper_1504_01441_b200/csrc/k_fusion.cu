@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(kSsimTW * 8) ssim_kernel(
     const float* __restrict__ a, const float* __restrict__ b, const uint8_t* __restrict__ qb,
     const float* __restrict__ lut_b, int w, int h, int r, const double* __restrict__ taps,
     float* __restrict__ out) {
+  pdl_wait();
   extern __shared__ double sm[];
   const int EW = kSsimTW + 2 * r, EH = kSsimTH + 2 * r;
   float* sa = reinterpret_cast<float*>(sm);  // EH x EW
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     const float* __restrict__ a, const float* __restrict__ b, const uint8_t* __restrict__ qb,
     const float* __restrict__ lut_b, int w, int h, const double* __restrict__ taps,
     float* __restrict__ out) {
+  pdl_wait();
   constexpr int E = kS2 + 2 * R;  // staged rows/cols incl. halo
   __shared__ float sa[E][E + 1], sb[E][E + 1];
   __shared__ int rows[E], cols[E];
@@ -243,13 +245,13 @@ void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb, cons
   if (r == 5) {
     size_t vb = 5 * (size_t)kS2 * (kS2 + 10) * sizeof(double);
     dim3 grd(ceil_div(w, kS2), ceil_div(h, kS2));
-    ssim_fixed_kernel<5><<<grd, dim3(32, 8), vb, s>>>(a, b_or_null, qb, lut_b, w, h, taps, out);
+    klaunch(ssim_fixed_kernel<5>, grd, dim3(32, 8), vb, s, a, b_or_null, qb, lut_b, w, h, taps, out);
     return;
   }
   int EW = kSsimTW + 2 * r, EH = kSsimTH + 2 * r;
   size_t bytes = ((2 * EH * EW + 1) / 2) * sizeof(double) + 5 * (size_t)kSsimTH * EW * sizeof(double);
   dim3 grd(ceil_div(w, kSsimTW), ceil_div(h, kSsimTH));
-  ssim_kernel<<<grd, kSsimTW * 8, bytes, s>>>(a, b_or_null, qb, lut_b, w, h, r, taps, out);
+  klaunch(ssim_kernel, grd, kSsimTW * 8, bytes, s, a, b_or_null, qb, lut_b, w, h, r, taps, out);
 }
 
 // ---------------------------------------------------------------- K14
@@ -278,6 +280,7 @@ __device__ __forceinline__ double quality(const float* __restrict__ rgb, int w, 
 }
 
 __global__ void quality_kernel(const float* __restrict__ rgb, int w, int h, float* __restrict__ out) {
+  pdl_wait();
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
   out[(int64_t)y * w + x] = (float)quality(rgb, w, h, x, y);
@@ -285,7 +288,7 @@ __global__ void quality_kernel(const float* __restrict__ rgb, int w, int h, floa
 
 void launch_quality(const float* rgb, int w, int h, float* out, cudaStream_t s) {
   dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
-  quality_kernel<<<grd, blk, 0, s>>>(rgb, w, h, out);
+  klaunch(quality_kernel, grd, blk, 0, s, rgb, w, h, out);
 }
 
 // fusion.fusion_weights (fusion.py:117-128)
@@ -293,6 +296,7 @@ __global__ void fusion_weights_kernel(const float* __restrict__ ref, const float
                                       const float* __restrict__ ssim,
                                       const uint8_t* __restrict__ valid, int w, int h,
                                       float* __restrict__ wr, float* __restrict__ ws) {
+  pdl_wait();
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
   int64_t i = (int64_t)y * w + x;
@@ -309,7 +313,7 @@ void launch_fusion_weights(const float* ref, const float* warped, const float* s
                            const uint8_t* valid, int w, int h, float* wr, float* ws,
                            cudaStream_t s) {
   dim3 blk(32, 8), grd(ceil_div(w, 32), ceil_div(h, 8));
-  fusion_weights_kernel<<<grd, blk, 0, s>>>(ref, warped, ssim, valid, w, h, wr, ws);
+  klaunch(fusion_weights_kernel, grd, blk, 0, s, ref, warped, ssim, valid, w, h, wr, ws);
 }
 
 }  // namespace hdr
@@ -333,6 +337,7 @@ __device__ __forceinline__ double sym5(double xm2, double xm1, double x0, double
 // out (oh, ow, c) = blur5(in)[::2, ::2]
 __global__ void pyr_down_kernel(const double* __restrict__ in, int w, int h, int c,
                                 double* __restrict__ out, int ow, int oh) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)ow * oh * c) return;
   int k = (int)(i % c);
@@ -356,6 +361,7 @@ __global__ void pyr_down_kernel(const double* __restrict__ in, int w, int h, int
 __global__ void pyr_up_kernel(const double* __restrict__ in, int cw, int ch, int c,
                               double* __restrict__ out, int w, int h,
                               const double* __restrict__ base, int sign) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)w * h * c) return;
   int k = (int)(i % c);
@@ -380,14 +386,14 @@ __global__ void pyr_up_kernel(const double* __restrict__ in, int cw, int ch, int
 void launch_pyr_down(const double* in, int w, int h, int c, double* out, cudaStream_t s) {
   int ow = (w + 1) / 2, oh = (h + 1) / 2;
   int64_t n = (int64_t)ow * oh * c;
-  if (n > 0) pyr_down_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, w, h, c, out, ow, oh);
+  if (n > 0) klaunch(pyr_down_kernel, (unsigned)((n + 255) / 256), 256, 0, s, in, w, h, c, out, ow, oh);
 }
 
 void launch_pyr_up(const double* in, int cw, int ch, int c, double* out, int w, int h,
                    const double* base, int sign, cudaStream_t s) {
   int64_t n = (int64_t)w * h * c;
   if (n > 0)
-    pyr_up_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, cw, ch, c, out, w, h, base, sign);
+    klaunch(pyr_up_kernel, (unsigned)((n + 255) / 256), 256, 0, s, in, cw, ch, c, out, w, h, base, sign);
 }
 
 }  // namespace hdr

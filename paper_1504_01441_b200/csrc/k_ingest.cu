@@ -15,6 +15,7 @@ namespace hdr {
 template <class T, int C>
 __global__ void __launch_bounds__(256) decode_kernel(const T* __restrict__ in, int64_t npx,
                                                      double scale, float* __restrict__ out) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < npx; i += stride) {
@@ -35,14 +36,14 @@ void launch_decode(const void* in, int64_t npx, int channels, int bits, float* o
   double scale = bits == 16 ? 65535.0 : 255.0;
   if (bits == 16) {
     if (channels == 3)
-      decode_kernel<uint16_t, 3><<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)in, npx, scale, out);
+      klaunch(decode_kernel<uint16_t, 3>, (unsigned)blocks, 256, 0, s, (const uint16_t*)in, npx, scale, out);
     else
-      decode_kernel<uint16_t, 1><<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)in, npx, scale, out);
+      klaunch(decode_kernel<uint16_t, 1>, (unsigned)blocks, 256, 0, s, (const uint16_t*)in, npx, scale, out);
   } else {
     if (channels == 3)
-      decode_kernel<uint8_t, 3><<<(unsigned)blocks, 256, 0, s>>>((const uint8_t*)in, npx, scale, out);
+      klaunch(decode_kernel<uint8_t, 3>, (unsigned)blocks, 256, 0, s, (const uint8_t*)in, npx, scale, out);
     else
-      decode_kernel<uint8_t, 1><<<(unsigned)blocks, 256, 0, s>>>((const uint8_t*)in, npx, scale, out);
+      klaunch(decode_kernel<uint8_t, 1>, (unsigned)blocks, 256, 0, s, (const uint8_t*)in, npx, scale, out);
   }
 }
 
@@ -50,6 +51,7 @@ void launch_decode(const void* in, int64_t npx, int channels, int bits, float* o
 // as uint8, 16 values per thread (four 16-byte loads, one 16-byte store).
 __global__ void __launch_bounds__(256) encode_u8_kernel(const float* __restrict__ x, int64_t n,
                                                         uint8_t* __restrict__ out) {
+  pdl_wait();
   auto q = [](float v) -> uint32_t {
     double d = floor(fma((double)v, 255.0, 0.5));  // exact: v*255 fits in 53 bits
     return (uint32_t)fmin(fmax(d, 0.0), 255.0);
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(256) encode_u8_kernel(const float* __restrict_
 
 void launch_encode_u8(const float* x, int64_t n, uint8_t* out, cudaStream_t s) {
   int64_t blocks = std::min<int64_t>((n / 16 + 255) / 256 + 1, 148 * 8);
-  encode_u8_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, n, out);
+  klaunch(encode_u8_kernel, (unsigned)blocks, 256, 0, s, x, n, out);
 }
 
 // metering.choose_reference's mean_lum (metering.py:46-48): mean of
@@ -94,6 +96,7 @@ __device__ __forceinline__ float meter_value(const float* img, int channels, int
 
 __global__ void __launch_bounds__(256) mean_lum_kernel(const float* __restrict__ img, int channels,
                                                        int64_t n, double* __restrict__ out) {
+  pdl_wait();
   __shared__ double part[8];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -114,7 +117,7 @@ void launch_mean_luminance(const float* img, int channels, int64_t n, double* ou
   cudaMemsetAsync(out, 0, sizeof(double), s);
   int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
   if (blocks < 1) return;
-  mean_lum_kernel<<<(unsigned)blocks, 256, 0, s>>>(img, channels, n, out);
+  klaunch(mean_lum_kernel, (unsigned)blocks, 256, 0, s, img, channels, n, out);
 }
 
 // metering.select_offset's statistic (metering.py:28-29): the number of
@@ -124,6 +127,7 @@ void launch_mean_luminance(const float* img, int channels, int64_t n, double* ou
 __global__ void __launch_bounds__(256) dark_count_kernel(const float* __restrict__ img, int channels,
                                                          int64_t n, float dark,
                                                          unsigned long long* out) {
+  pdl_wait();
   unsigned long long cnt = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -138,7 +142,7 @@ void launch_dark_count(const float* img, int channels, int64_t n, float dark,
   cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
   int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
   if (blocks < 1) return;
-  dark_count_kernel<<<(unsigned)blocks, 256, 0, s>>>(img, channels, n, dark, out);
+  klaunch(dark_count_kernel, (unsigned)blocks, 256, 0, s, img, channels, n, dark, out);
 }
 
 }  // namespace hdr

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256) ssd_tiles_kernel(const TileCorner* __rest
                                                         int radius, int patch,
                                                         MatchRow* __restrict__ rows,
                                                         uint8_t* __restrict__ flags) {
+  pdl_wait();
   extern __shared__ double smem[];
   int slot = blockIdx.x;
   TileCorner tc = tiles[slot];
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(256) ssd_points_kernel(const float* __restrict
                                                          int radius, int patch,
                                                          double* __restrict__ out,
                                                          uint8_t* __restrict__ found) {
+  pdl_wait();
   extern __shared__ double smem[];
   int i = blockIdx.x;
   int hp = patch / 2;
@@ -236,7 +238,7 @@ void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref, con
                       int w, int h, const double* hpred, int radius, int patch, MatchRow* rows,
                       uint8_t* flags, cudaStream_t s) {
   size_t bytes = ssd_smem(radius, patch);
-  ssd_tiles_kernel<<<ntiles, kSsdThreads, bytes, s>>>(tiles, ref, src, w, h, hpred, radius, patch, rows,
+  klaunch(ssd_tiles_kernel, ntiles, kSsdThreads, bytes, s, tiles, ref, src, w, h, hpred, radius, patch, rows,
                                               flags);
 }
 
@@ -245,7 +247,7 @@ void launch_ssd_points(const float* ref, const float* src, int w, int h, const i
                        cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = ssd_smem(radius, patch);
-  ssd_points_kernel<<<n, kSsdThreads, bytes, s>>>(ref, src, w, h, pts, radius, patch, out, found);
+  klaunch(ssd_points_kernel, n, kSsdThreads, bytes, s, ref, src, w, h, pts, radius, patch, out, found);
 }
 
 // ordered compaction of per-slot rows (tile order is the reference's corner
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(1024) compact_rows_kernel(const MatchRow* __re
                                                             int nslots, MatchRow* __restrict__ out,
                                                             int32_t* __restrict__ count,
                                                             double* __restrict__ out_copy) {
+  pdl_wait();
   __shared__ int scratch[32];
   int base = 0;
   for (int c0 = 0; c0 < nslots; c0 += blockDim.x) {
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(1024) compact_rows_kernel(const MatchRow* __re
 
 void launch_compact_rows(const MatchRow* rows, const uint8_t* flags, int nslots, MatchRow* out,
                          int32_t* count, double* out_copy, cudaStream_t s) {
-  compact_rows_kernel<<<1, 1024, 0, s>>>(rows, flags, nslots, out, count, out_copy);
+  klaunch(compact_rows_kernel, 1, 1024, 0, s, rows, flags, nslots, out, count, out_copy);
 }
 
 // ---------------------------------------------------------------- K7
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(64) weed_fit_kernel(const MatchRow* __restrict
                                                       const uint64_t* __restrict__ keys,
                                                       double* __restrict__ fits,
                                                       int32_t* __restrict__ grey) {
+  pdl_wait();
   int it = blockIdx.x * blockDim.x + threadIdx.x;
   if (it >= iterations) return;
   int n = *count;
@@ -337,6 +341,7 @@ __global__ void __launch_bounds__(256) weed_count_kernel(const MatchRow* __restr
                                                          const double* __restrict__ fits,
                                                          uint32_t* __restrict__ mask,
                                                          int32_t* __restrict__ witness) {
+  pdl_wait();
   int it = blockIdx.x;
   int n = *count;
   const double* f = fits + (int64_t)it * kFitStride;
@@ -384,9 +389,9 @@ void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w
                  cudaStream_t s) {
   cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((n_static + 31) / 32 + 1), s);
   cudaMemsetAsync(witness, 0, sizeof(int32_t) * (n_static + 1), s);
-  weed_fit_kernel<<<ceil_div(iterations, 64), 64, 0, s>>>(rows, count, w, h, iterations, keys,
+  klaunch(weed_fit_kernel, ceil_div(iterations, 64), 64, 0, s, rows, count, w, h, iterations, keys,
                                                           fit_scratch, grey);
-  weed_count_kernel<<<iterations, 256, 0, s>>>(rows, count, w, h, eps, delta, fit_scratch, mask,
+  klaunch(weed_count_kernel, iterations, 256, 0, s, rows, count, w, h, eps, delta, fit_scratch, mask,
                                                witness);
 }
 
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     int32_t* __restrict__ weeded_count, int64_t* __restrict__ kept_idx,
     double* __restrict__ hpred, double* __restrict__ homography, int32_t* __restrict__ info,
     double* __restrict__ out_matches, double* __restrict__ out_raw, int32_t* grey) {
+  pdl_wait();
   extern __shared__ double pts_cache[];  // normalised (rx, ry, sx, sy) of the weeded set
   __shared__ int scratch[32];
   int n = *raw_count;
@@ -602,7 +608,7 @@ void launch_finish_level(const MatchRow* raw, const int32_t* raw_count, const ui
                          int64_t* kept_idx, double* hpred, double* homography, int32_t* info,
                          double* out_matches, double* out_raw, int32_t* grey, cudaStream_t s) {
   (void)out_raw;
-  finish_level_kernel<<<1, 256, kFitCache * 4 * sizeof(double), s>>>(raw, raw_count, mask, w, h, level, weeded, weeded_count,
+  klaunch(finish_level_kernel, 1, 256, kFitCache * 4 * sizeof(double), s, raw, raw_count, mask, w, h, level, weeded, weeded_count,
                                         kept_idx, hpred, homography, info, out_matches, out_raw,
                                         grey);
 }
@@ -612,6 +618,7 @@ __global__ void __launch_bounds__(256) fit_rows_kernel(const MatchRow* __restric
                                                        const int32_t* __restrict__ count, int w,
                                                        int h, double* __restrict__ H,
                                                        int32_t* __restrict__ status) {
+  pdl_wait();
   int n = *count;
   if (n < 4) {
     if (threadIdx.x == 0) *status = 1;
@@ -629,7 +636,7 @@ __global__ void __launch_bounds__(256) fit_rows_kernel(const MatchRow* __restric
 
 void launch_fit_rows(const MatchRow* rows, const int32_t* count, int w, int h, double* H,
                      int32_t* status, cudaStream_t s) {
-  fit_rows_kernel<<<1, 256, 0, s>>>(rows, count, w, h, H, status);
+  klaunch(fit_rows_kernel, 1, 256, 0, s, rows, count, w, h, H, status);
 }
 
 // geometry.fit_homography on explicit point arrays
@@ -637,6 +644,7 @@ __global__ void __launch_bounds__(256) fit_points_kernel(const double* __restric
                                                          const double* __restrict__ sp, int n,
                                                          double* __restrict__ H,
                                                          int32_t* __restrict__ status) {
+  pdl_wait();
   __shared__ double Hs[9];
   auto get = [&](int i, double* p) {
     p[0] = rp[2 * i]; p[1] = rp[2 * i + 1]; p[2] = sp[2 * i]; p[3] = sp[2 * i + 1];
@@ -651,12 +659,13 @@ __global__ void __launch_bounds__(256) fit_points_kernel(const double* __restric
 
 void launch_fit_points(const double* ref_pts, const double* src_pts, int n, double* H,
                        int32_t* status, cudaStream_t s) {
-  fit_points_kernel<<<1, 256, 0, s>>>(ref_pts, src_pts, n, H, status);
+  klaunch(fit_points_kernel, 1, 256, 0, s, ref_pts, src_pts, n, H, status);
 }
 
 __global__ void inlier_mask_kernel(const double* __restrict__ H, const double* __restrict__ rp,
                                    const double* __restrict__ sp, int n, double eps,
                                    uint8_t* __restrict__ mask) {
+  pdl_wait();
   __shared__ double Hs[18];
   __shared__ int okinv;
   if (threadIdx.x == 0) {
@@ -673,15 +682,16 @@ __global__ void inlier_mask_kernel(const double* __restrict__ H, const double* _
 void launch_inlier_mask(const double* H, const double* ref_pts, const double* src_pts, int n,
                         double eps, uint8_t* mask, cudaStream_t s) {
   if (n <= 0) return;
-  inlier_mask_kernel<<<ceil_div(n, 256), 256, 0, s>>>(H, ref_pts, src_pts, n, eps, mask);
+  klaunch(inlier_mask_kernel, ceil_div(n, 256), 256, 0, s, H, ref_pts, src_pts, n, eps, mask);
 }
 
 __global__ void set_identity_kernel(double* h) {
+  pdl_wait();
   int i = threadIdx.x;
   if (i < 9) h[i] = (i % 4 == 0) ? 1.0 : 0.0;
 }
 
-void launch_set_identity(double* h, cudaStream_t s) { set_identity_kernel<<<1, 32, 0, s>>>(h); }
+void launch_set_identity(double* h, cudaStream_t s) { klaunch(set_identity_kernel, 1, 32, 0, s, h); }
 
 static void init_finish_attributes() { allow_max_dynamic_smem(finish_level_kernel); }
 

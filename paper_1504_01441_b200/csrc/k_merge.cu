@@ -21,6 +21,8 @@
 #include "hdr_common.cuh"
 #include "hdr_internal.h"
 
+#include <algorithm>
+
 namespace hdr {
 
 __constant__ float kK5[5] = {1.0f / 16, 4.0f / 16, 6.0f / 16, 4.0f / 16, 1.0f / 16};
@@ -121,6 +123,7 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
 template <int NF>
 __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_down_kernel(FuseFrames<NF> fr, int w, int h,
                                                           float* __restrict__ g1, int ow, int oh) {
+  pdl_wait();
   extern __shared__ float smf[];
   float* lum = smf;                    // [NF][38][38] luminance of every frame
   float* px = smf + NF * kLT * kLT;    // [4NF][36][37]: RGB of every frame, then the weights
@@ -237,6 +240,7 @@ constexpr size_t down_smem() { return sizeof(float) * (4 * NF * kRT * kRP + 4 * 
 template <int NF>
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
                                                    float* __restrict__ out, int ow, int oh) {
+  pdl_wait();
   constexpr int NC = 4 * NF;
   extern __shared__ float smd[];
   float* tile = smd;                // [NC][36][37]
@@ -320,6 +324,7 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
                                                       int w, int h, const float* __restrict__ gc,
                                                       const float* __restrict__ cc, int cw, int ch,
                                                       float* __restrict__ out) {
+  pdl_wait();
   constexpr int NCH = 3 * (NF + 1);
   extern __shared__ float smc[];
   float* C = smc;                      // [NCH][19][19] coarse tile
@@ -479,6 +484,7 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
 // top of the pyramid: C = sum_f w_f * G_f (laps[-1] = gp[-1])
 template <int NF>
 __global__ void fuse_top_kernel(const float* __restrict__ g, int w, int h, float* __restrict__ c) {
+  pdl_wait();
   int64_t P = (int64_t)w * h;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
@@ -523,31 +529,33 @@ static void launch_fuse_nf(const FuseFrames<NF>& fr, const FusePyramid& py, cuda
   const Dims d1 = L > 1 ? d[1] : Dims{(d[0].w + 1) / 2, (d[0].h + 1) / 2};
   kprobe_mark(kp_w0, 0, s);
   dim3 g0(ceil_div(d1.w, kOT), ceil_div(d1.h, kOT));
-  weights_down_kernel<NF><<<g0, 256, weights_smem<NF>(), s>>>(fr, d[0].w, d[0].h, py.g[1], d1.w, d1.h);
+  klaunch(weights_down_kernel<NF>, g0, dim3(256), weights_smem<NF>(), s, fr, d[0].w, d[0].h, py.g[1], d1.w,
+             d1.h);
   kprobe_mark(kp_w0, 1, s);
   if (L == 1) {
     dim3 gf(ceil_div(d[0].w, kFT), ceil_div(d[0].h, kFT));
-    collapse_kernel<true, NF><<<gf, 256, collapse_smem<NF>(), s>>>(nullptr, fr, d[0].w, d[0].h, nullptr,
-                                                                  nullptr, 0, 0, py.out);
+    klaunch(collapse_kernel<true, NF>, gf, dim3(256), collapse_smem<NF>(), s, (const float*)nullptr, fr,
+               d[0].w, d[0].h, (const float*)nullptr, (const float*)nullptr, 0, 0, py.out);
     return;
   }
   for (int k = 1; k + 1 < L; ++k) {
     dim3 gk(ceil_div(d[k + 1].w, kOT), ceil_div(d[k + 1].h, kOT));
-    down_kernel<NF><<<gk, 256, down_smem<NF>(), s>>>(py.g[k], d[k].w, d[k].h, py.g[k + 1], d[k + 1].w,
-                                                    d[k + 1].h);
+    klaunch(down_kernel<NF>, gk, dim3(256), down_smem<NF>(), s, (const float*)py.g[k], d[k].w, d[k].h,
+            py.g[k + 1], d[k + 1].w, d[k + 1].h);
   }
   int64_t Pt = (int64_t)d[L - 1].w * d[L - 1].h;
-  fuse_top_kernel<NF><<<(unsigned)((Pt + 255) / 256), 256, 0, s>>>(py.g[L - 1], d[L - 1].w,
-                                                                   d[L - 1].h, py.c[L - 1]);
+  klaunch(fuse_top_kernel<NF>, dim3((unsigned)((Pt + 255) / 256)), dim3(256), 0, s, (const float*)py.g[L - 1],
+          d[L - 1].w, d[L - 1].h, py.c[L - 1]);
   for (int k = L - 2; k >= 1; --k) {
     dim3 gk(ceil_div(d[k].w, kFT), ceil_div(d[k].h, kFT));
-    collapse_kernel<false, NF><<<gk, 256, collapse_smem<NF>(), s>>>(
-        py.g[k], fr, d[k].w, d[k].h, py.g[k + 1], py.c[k + 1], d[k + 1].w, d[k + 1].h, py.c[k]);
+    klaunch(collapse_kernel<false, NF>, gk, dim3(256), collapse_smem<NF>(), s, (const float*)py.g[k], fr,
+               d[k].w, d[k].h, (const float*)py.g[k + 1], (const float*)py.c[k + 1], d[k + 1].w, d[k + 1].h,
+               py.c[k]);
   }
   kprobe_mark(kp_c0, 0, s);
   dim3 gf(ceil_div(d[0].w, kFT), ceil_div(d[0].h, kFT));
-  collapse_kernel<true, NF><<<gf, 256, collapse_smem<NF>(), s>>>(
-      nullptr, fr, d[0].w, d[0].h, py.g[1], py.c[1], d[1].w, d[1].h, py.out);
+  klaunch(collapse_kernel<true, NF>, gf, dim3(256), collapse_smem<NF>(), s, (const float*)nullptr, fr, d[0].w,
+             d[0].h, (const float*)py.g[1], (const float*)py.c[1], d[1].w, d[1].h, py.out);
   kprobe_mark(kp_c0, 1, s);
 }
 

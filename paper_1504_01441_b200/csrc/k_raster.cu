@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(256) luma_hist_kernel(const float* __restrict_
                                                         int64_t n, float* __restrict__ lum,
                                                         uint8_t* __restrict__ q,
                                                         uint32_t* __restrict__ hist) {
+  pdl_wait();
   __shared__ uint32_t sh[kHistWarps][kBins];
   for (int i = threadIdx.x; i < kHistWarps * kBins; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
@@ -96,16 +97,17 @@ static int grid_for(int64_t work, int threads) {
 
 void launch_luma_hist(const float* rgb, int64_t n, float* lum, uint8_t* q, uint32_t* hist,
                       cudaStream_t s) {
-  luma_hist_kernel<<<grid_for((n >> 2) + 1, 256), 256, 0, s>>>(rgb, n, lum, q, hist);
+  klaunch(luma_hist_kernel, grid_for((n >> 2) + 1, 256), 256, 0, s, rgb, n, lum, q, hist);
 }
 
 void launch_luminance(const float* rgb, int64_t n, float* lum, cudaStream_t s) {
-  luma_hist_kernel<<<grid_for((n >> 2) + 1, 256), 256, 0, s>>>(rgb, n, lum, nullptr, nullptr);
+  klaunch(luma_hist_kernel, grid_for((n >> 2) + 1, 256), 256, 0, s, rgb, n, lum, nullptr, nullptr);
 }
 
 // histogram of quantize_256(x) for a strided single-channel view
 __global__ void hist_plain_kernel(const float* __restrict__ x, int64_t n, int32_t stride,
                                   uint32_t* __restrict__ hist) {
+  pdl_wait();
   __shared__ uint32_t sh[kBins];
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
   __syncthreads();
@@ -119,7 +121,7 @@ __global__ void hist_plain_kernel(const float* __restrict__ x, int64_t n, int32_
 
 void launch_hist_plain(const float* x, int64_t n, int32_t stride, uint32_t* hist,
                        cudaStream_t s) {
-  hist_plain_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, stride, hist);
+  klaunch(hist_plain_kernel, grid_for(n, 256), 256, 0, s, x, n, stride, hist);
 }
 
 // ---------------------------------------------------------------- K2
@@ -128,6 +130,7 @@ void launch_hist_plain(const float* x, int64_t n, int32_t stride, uint32_t* hist
 __global__ void __launch_bounds__(256) lut_kernel(const uint32_t* __restrict__ hs,
                                                   int64_t ns, const uint32_t* __restrict__ hr,
                                                   int64_t nr, float* __restrict__ lut) {
+  pdl_wait();
   __shared__ double cdf_s[kBins], cdf_r[kBins];
   __shared__ long long ws[kBins], wr[kBins];
   int t = threadIdx.x;
@@ -157,11 +160,12 @@ __global__ void __launch_bounds__(256) lut_kernel(const uint32_t* __restrict__ h
 
 void launch_lut(const uint32_t* hist_src, int64_t n_src, const uint32_t* hist_ref,
                 int64_t n_ref, float* lut, cudaStream_t s) {
-  lut_kernel<<<1, kBins, 0, s>>>(hist_src, n_src, hist_ref, n_ref, lut);
+  klaunch(lut_kernel, 1, kBins, 0, s, hist_src, n_src, hist_ref, n_ref, lut);
 }
 
 __global__ void apply_lut_q_kernel(const uint8_t* __restrict__ q, int64_t n,
                                    const float* __restrict__ lut, float* __restrict__ out) {
+  pdl_wait();
   __shared__ float t[kBins];
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) t[i] = lut[i];
   __syncthreads();
@@ -178,11 +182,12 @@ __global__ void apply_lut_q_kernel(const uint8_t* __restrict__ q, int64_t n,
 
 void launch_apply_lut_q(const uint8_t* q, int64_t n, const float* lut, float* out,
                         cudaStream_t s) {
-  apply_lut_q_kernel<<<grid_for((n >> 2) + 1, 256), 256, 0, s>>>(q, n, lut, out);
+  klaunch(apply_lut_q_kernel, grid_for((n >> 2) + 1, 256), 256, 0, s, q, n, lut, out);
 }
 
 __global__ void apply_lut_f_kernel(const float* __restrict__ x, int64_t n, int32_t stride,
                                    const float* __restrict__ lut, float* __restrict__ out) {
+  pdl_wait();
   __shared__ float t[kBins];
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) t[i] = lut[i];
   __syncthreads();
@@ -193,7 +198,7 @@ __global__ void apply_lut_f_kernel(const float* __restrict__ x, int64_t n, int32
 
 void launch_apply_lut_f(const float* x, int64_t n, int32_t stride, const float* lut,
                         float* out, cudaStream_t s) {
-  apply_lut_f_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, stride, lut, out);
+  klaunch(apply_lut_f_kernel, grid_for(n, 256), 256, 0, s, x, n, stride, lut, out);
 }
 
 // ---------------------------------------------------------------- K3
@@ -203,6 +208,7 @@ void launch_apply_lut_f(const float* x, int64_t n, int32_t stride, const float* 
 __global__ void downsample2_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                    int w, int h, float* __restrict__ oa,
                                    float* __restrict__ ob) {
+  pdl_wait();
   const float* in = blockIdx.z ? b : a;
   float* out = blockIdx.z ? ob : oa;
   if (!in) return;
@@ -227,7 +233,7 @@ void launch_downsample2(const float* a, const float* b, int w, int h, float* oa,
                         cudaStream_t s) {
   dim3 blk(32, 8);
   dim3 grd(ceil_div(w / 2, 32), ceil_div(h / 2, 8), 2);
-  downsample2_kernel<<<grd, blk, 0, s>>>(a, b, w, h, oa, ob);
+  klaunch(downsample2_kernel, grd, blk, 0, s, a, b, w, h, oa, ob);
 }
 
 // ---------------------------------------------------------------- K4
@@ -262,6 +268,7 @@ __device__ __forceinline__ bool level_exact(const SatBatch& b, int l) {
 }
 
 __global__ void __launch_bounds__(256) level_stats_kernel(SatBatch b) {
+  pdl_wait();
   const SatLevel& L = b.lv[blockIdx.y];
   int64_t n = (int64_t)L.w * L.h;
   int qm = 1 << 20;
@@ -304,10 +311,11 @@ void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s) {
   // eight independent loads, and a level costs only ~300 same-address atomics
   int bx = std::min(grid_for(max_pixels, 256), 148 * 2);
   dim3 g(bx, b.n);
-  level_stats_kernel<<<g, 256, 0, s>>>(b);
+  klaunch(level_stats_kernel, g, 256, 0, s, b);
 }
 
 __global__ void __launch_bounds__(32) sat_cols_kernel(SatBatch b) {
+  pdl_wait();
   const SatLevel& L = b.lv[blockIdx.y];
   if (level_exact(b, blockIdx.y)) return;  // the tile-local detector handles it
   int x = blockIdx.x * 32 + threadIdx.x;
@@ -345,6 +353,7 @@ __global__ void __launch_bounds__(32) sat_cols_kernel(SatBatch b) {
 // staged through shared memory so the global loads stay coalesced, and the
 // next tile is prefetched into registers while the current one is scanned.
 __global__ void __launch_bounds__(32) sat_rows_kernel(SatBatch b) {
+  pdl_wait();
   const SatLevel& L = b.lv[blockIdx.y];
   if (level_exact(b, blockIdx.y)) return;
   __shared__ double tile[32][33];
@@ -386,8 +395,8 @@ __global__ void __launch_bounds__(32) sat_rows_kernel(SatBatch b) {
 
 void launch_sat(const SatBatch& b, int max_w, int max_rows, cudaStream_t s) {
   dim3 g1(ceil_div(max_w, 32), b.n), g2(ceil_div(max_rows, 32), b.n);
-  sat_cols_kernel<<<g1, 32, 0, s>>>(b);
-  sat_rows_kernel<<<g2, 32, 0, s>>>(b);
+  klaunch(sat_cols_kernel, g1, 32, 0, s, b);
+  klaunch(sat_rows_kernel, g2, 32, 0, s, b);
 }
 
 // ---------------------------------------------------------------- K5
@@ -411,6 +420,7 @@ __device__ __forceinline__ double box(const LatticeView& v, int x0, int y0, int 
 
 template <bool EXACT>
 __global__ void __launch_bounds__(256) detect_kernel(SatBatch b, DetectParams dp) {
+  pdl_wait();
   extern __shared__ double local_sat[];
   int lev = 0;
   while (lev + 1 < b.n && (int)blockIdx.x >= b.lv[lev + 1].tile_base) ++lev;
@@ -555,13 +565,14 @@ void init_raster_attributes() { allow_max_dynamic_smem(detect_kernel<true>); }
 
 void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s) {
   if (dp.exact_ok)
-    detect_kernel<true><<<total_tiles, 256, detect_exact_smem(dp.tile, dp.half), s>>>(b, dp);
-  detect_kernel<false><<<total_tiles, 256, 0, s>>>(b, dp);
+    klaunch(detect_kernel<true>, total_tiles, 256, detect_exact_smem(dp.tile, dp.half), s, b, dp);
+  klaunch(detect_kernel<false>, total_tiles, 256, 0, s, b, dp);
 }
 
 __global__ void __launch_bounds__(1024) compact_corners_kernel(const TileCorner* __restrict__ tiles,
                                                                int ntiles, double* __restrict__ out,
                                                                int32_t* __restrict__ count) {
+  pdl_wait();
   __shared__ int scratch[32];
   int base = 0;
   for (int c0 = 0; c0 < ntiles; c0 += blockDim.x) {
@@ -581,7 +592,7 @@ __global__ void __launch_bounds__(1024) compact_corners_kernel(const TileCorner*
 
 void launch_compact_corners(const TileCorner* tiles, int ntiles, double* corners,
                             int32_t* count, cudaStream_t s) {
-  compact_corners_kernel<<<1, 1024, 0, s>>>(tiles, ntiles, corners, count);
+  klaunch(compact_corners_kernel, 1, 1024, 0, s, tiles, ntiles, corners, count);
 }
 
 }  // namespace hdr
@@ -592,6 +603,7 @@ namespace hdr {
 // f64 integral table: out[2i] = C = ((d0 + d1) + d2) + d3, out[2i+1] = min.
 __global__ void cornerness_kernel(const double* __restrict__ t, int w1, const int32_t* __restrict__ xy,
                                   int n, int half, double* __restrict__ out) {
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int x = xy[2 * i], y = xy[2 * i + 1];
@@ -609,7 +621,7 @@ __global__ void cornerness_kernel(const double* __restrict__ t, int w1, const in
 
 void launch_cornerness(const double* table, int w1, const int32_t* xy, int n, int half, double* out,
                        cudaStream_t s) {
-  if (n > 0) cornerness_kernel<<<(n + 127) / 128, 128, 0, s>>>(table, w1, xy, n, half, out);
+  if (n > 0) klaunch(cornerness_kernel, (n + 127) / 128, 128, 0, s, table, w1, xy, n, half, out);
 }
 
 }  // namespace hdr

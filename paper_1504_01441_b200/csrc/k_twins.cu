@@ -67,6 +67,7 @@ template <typename GT>
 __global__ void __launch_bounds__(128) dt_rows_seq_kernel(const GT* __restrict__ guide, int C,
                                                           DtPlanes P, int w, int h, double ratio,
                                                           double c) {
+  pdl_wait();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)h * P.k) return;
   const int k = (int)(t / h), y = (int)(t - (int64_t)k * h);
@@ -87,6 +88,7 @@ template <typename GT>
 __global__ void __launch_bounds__(128) dt_cols_seq_kernel(const GT* __restrict__ guide, int C,
                                                           DtPlanes P, int w, int h, double ratio,
                                                           double c) {
+  pdl_wait();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)w * P.k) return;
   const int k = (int)(t / w), x = (int)(t - (int64_t)k * w);
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(128) dt_cols_seq_kernel(const GT* __restrict__
 void launch_dt_rows_seq(const float* guide, const DtPlanes& P, int w, int h, double ratio, double c,
                         cudaStream_t s) {
   int64_t n = (int64_t)h * P.k;
-  dt_rows_seq_kernel<float><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(guide, 1, P, w, h, ratio, c);
+  klaunch(dt_rows_seq_kernel<float>, (unsigned)((n + 127) / 128), 128, 0, s, guide, 1, P, w, h, ratio, c);
 }
 
 // the whole filter, densify.py:96-113 (sigma_i and c per pass as dt_filter_k)
@@ -121,11 +123,11 @@ static void dt_filter_seq(const GT* guide, int C, const DtPlanes& P, int w, int 
     double c = -root / sigma_i;
     if (w > 1) {
       int64_t n = (int64_t)h * P.k;
-      dt_rows_seq_kernel<GT><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(guide, C, P, w, h, ratio, c);
+      klaunch(dt_rows_seq_kernel<GT>, (unsigned)((n + 127) / 128), 128, 0, s, guide, C, P, w, h, ratio, c);
     }
     if (h > 1) {
       int64_t n = (int64_t)w * P.k;
-      dt_cols_seq_kernel<GT><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(guide, C, P, w, h, ratio, c);
+      klaunch(dt_cols_seq_kernel<GT>, (unsigned)((n + 127) / 128), 128, 0, s, guide, C, P, w, h, ratio, c);
     }
   }
 }
@@ -142,6 +144,7 @@ void launch_dt_filter_general(const double* guide, int C, const DtPlanes& P, int
 __global__ void rect_sum_kernel(const double* __restrict__ t, int64_t w1, int64_t h1,
                                 const int64_t* __restrict__ q, int64_t n, double* __restrict__ out,
                                 int32_t* __restrict__ bad) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t x0 = q[i], y0 = q[n + i], x1 = q[2 * n + i], y1 = q[3 * n + i];
@@ -155,7 +158,7 @@ __global__ void rect_sum_kernel(const double* __restrict__ t, int64_t w1, int64_
 void launch_rect_sum(const double* table, int64_t w1, int64_t h1, const int64_t* q, int64_t n,
                      double* out, int32_t* bad, cudaStream_t s) {
   if (n <= 0) return;
-  rect_sum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(table, w1, h1, q, n, out, bad);
+  klaunch(rect_sum_kernel, (unsigned)((n + 255) / 256), 256, 0, s, table, w1, h1, q, n, out, bad);
 }
 
 // ---------------------------------------------------------------- quantize_256
@@ -163,6 +166,7 @@ void launch_rect_sum(const double* table, int64_t w1, int64_t h1, const int64_t*
 // stay f32 (numpy's weak Python-float scalars), f64 inputs are f64
 template <typename T>
 __global__ void quantize_kernel(const T* __restrict__ x, int64_t n, uint8_t* __restrict__ out) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     T v;
@@ -177,8 +181,8 @@ void launch_quantize(const void* x, bool f64, int64_t n, uint8_t* out, cudaStrea
   if (n <= 0) return;
   int64_t b = (n + 255) / 256;
   unsigned blocks = (unsigned)(b < 148 * 16 ? b : 148 * 16);
-  if (f64) quantize_kernel<double><<<blocks, 256, 0, s>>>((const double*)x, n, out);
-  else quantize_kernel<float><<<blocks, 256, 0, s>>>((const float*)x, n, out);
+  if (f64) klaunch(quantize_kernel<double>, blocks, 256, 0, s, (const double*)x, n, out);
+  else klaunch(quantize_kernel<float>, blocks, 256, 0, s, (const float*)x, n, out);
 }
 
 // ---------------------------------------------------------------- downsample
@@ -188,6 +192,7 @@ void launch_quantize(const void* x, bool f64, int64_t n, uint8_t* out, cudaStrea
 template <typename T>
 __global__ void downsample_ch_kernel(const T* __restrict__ in, int w, int h, int C,
                                      float* __restrict__ out) {
+  pdl_wait();
   const int ow = w / 2, oh = h / 2;
   int64_t n = (int64_t)ow * oh * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -209,14 +214,15 @@ void launch_downsample_ch(const void* in, bool f64, int w, int h, int C, float* 
   if (n <= 0) return;
   int64_t b = (n + 255) / 256;
   unsigned blocks = (unsigned)(b < 148 * 16 ? b : 148 * 16);
-  if (f64) downsample_ch_kernel<double><<<blocks, 256, 0, s>>>((const double*)in, w, h, C, out);
-  else downsample_ch_kernel<float><<<blocks, 256, 0, s>>>((const float*)in, w, h, C, out);
+  if (f64) klaunch(downsample_ch_kernel<double>, blocks, 256, 0, s, (const double*)in, w, h, C, out);
+  else klaunch(downsample_ch_kernel<float>, blocks, 256, 0, s, (const float*)in, w, h, C, out);
 }
 
 // ---------------------------------------------------------------- geometry
 // apply_homography (geometry.py:80-93); *bad = 1 if any |denom| < 1e-12
 __global__ void apply_h_kernel(const double* __restrict__ H, const double* __restrict__ pts, int64_t n,
                                double* __restrict__ out, int32_t* __restrict__ bad) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double Hs[9];
@@ -232,7 +238,7 @@ __global__ void apply_h_kernel(const double* __restrict__ H, const double* __res
 void launch_apply_homography(const double* H, const double* pts, int64_t n, double* out, int32_t* bad,
                              cudaStream_t s) {
   if (n <= 0) return;
-  apply_h_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, pts, n, out, bad);
+  klaunch(apply_h_kernel, (unsigned)((n + 255) / 256), 256, 0, s, H, pts, n, out, bad);
 }
 
 // symmetric_transfer_error (geometry.py:107-115): hypot(fwd, bwd) with
@@ -241,6 +247,7 @@ void launch_apply_homography(const double* H, const double* pts, int64_t n, doub
 __global__ void transfer_error_kernel(const double* __restrict__ H, const double* __restrict__ rp,
                                       const double* __restrict__ sp, int64_t n,
                                       double* __restrict__ out, int32_t* __restrict__ bad) {
+  pdl_wait();
   __shared__ double Hs[18];
   __shared__ int okinv;
   if (threadIdx.x == 0) {
@@ -259,7 +266,7 @@ __global__ void transfer_error_kernel(const double* __restrict__ H, const double
 void launch_transfer_error(const double* H, const double* rp, const double* sp, int64_t n, double* out,
                            int32_t* bad, cudaStream_t s) {
   unsigned blocks = n > 0 ? (unsigned)((n + 255) / 256) : 1;
-  transfer_error_kernel<<<blocks, 256, 0, s>>>(H, rp, sp, n, out, bad);
+  klaunch(transfer_error_kernel, blocks, 256, 0, s, H, rp, sp, n, out, bad);
 }
 
 }  // namespace hdr

@@ -337,6 +337,11 @@ int hdr_fuse(hdr_ctx* ctx, const float* ref, const float* warped, const float* s
              const uint8_t* valid, int32_t width, int32_t height, int32_t levels,
              float* out);
 
+/* Tool: with hdr_set_option("trace", 1) every launch is bracketed by events;
+ * writes "kernel<TAB>microseconds" lines for the launches since, then clears
+ * them (synchronises the device). */
+int hdr_trace_dump(char* buf, int64_t cap);
+
 /* ---- host-side helpers (no GPU work) ------------------------------------ */
 /* matcher.level_seed (matcher.py:146-149). */
 uint32_t hdr_level_seed(uint64_t seed, int32_t level);

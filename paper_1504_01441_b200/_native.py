@@ -101,6 +101,7 @@ SIGNATURES = {
     "hdr_mean_luminance": (_I, [_P, _P, _I, _I64, _P]),
     "hdr_dark_count": (_I, [_P, _P, _I, _I64, ctypes.c_float, _P]),
     "hdr_register_and_fuse_raw": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P]),
+    "hdr_trace_dump": (_I, [ctypes.c_char_p, _I64]),
     "hdr_level_seed": (ctypes.c_uint32, [_U64, _I]),
     "hdr_iteration_keys": (_I, [_U64, _I, _P]),
     "hdr_choice4_host": (_I, [_P, _I, _I, _P]),

@@ -8,6 +8,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <cstring>
 #include <tuple>
 #include <vector>
 
@@ -44,6 +45,43 @@ extern "C" const char* hdr_last_error(void) { return g_err.c_str(); }
 
 namespace hdr {
 bool g_pdl = true;
+bool g_trace = false;
+struct TraceRec {
+  const void* kern;
+  cudaEvent_t ev[2];
+};
+static std::vector<TraceRec> g_trace_recs;
+void trace_launch(const void* kern, cudaStream_t s, int end) {
+  if (!end) {
+    TraceRec r{kern, {nullptr, nullptr}};
+    cudaEventCreate(&r.ev[0]);
+    cudaEventCreate(&r.ev[1]);
+    g_trace_recs.push_back(r);
+  }
+  cudaEventRecord(g_trace_recs.back().ev[end], s);
+}
+}
+
+// Tool: per-launch device times since tracing was switched on (one line per
+// launch, "name<TAB>microseconds"), then the records are cleared. Needs the
+// traced work finished (synchronises the device).
+extern "C" int hdr_trace_dump(char* buf, int64_t cap) {
+  cudaDeviceSynchronize();
+  std::string out;
+  for (auto& r : hdr::g_trace_recs) {
+    const char* name = nullptr;
+    if (cudaFuncGetName(&name, r.kern) != cudaSuccess || !name) name = "?";
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, r.ev[0], r.ev[1]);
+    out += std::string(name) + "\t" + std::to_string(ms * 1e3) + "\n";
+    cudaEventDestroy(r.ev[0]);
+    cudaEventDestroy(r.ev[1]);
+  }
+  hdr::g_trace_recs.clear();
+  cudaGetLastError();
+  if ((int64_t)out.size() + 1 > cap) return HDR_ERR_INVALID;
+  memcpy(buf, out.c_str(), out.size() + 1);
+  return HDR_OK;
 }
 
 // test hook: 0 sends the pair through the dense splat + first row pass
@@ -60,6 +98,10 @@ extern "C" int hdr_set_option(const char* name, int64_t value) {
   }
   if (name && std::string(name) == "dt_cols_grid_div") {
     hdr::dt_set_cols_grid_div((int)value);
+    return HDR_OK;
+  }
+  if (name && std::string(name) == "trace") {
+    hdr::g_trace = value != 0;
     return HDR_OK;
   }
   if (name && std::string(name) == "pdl") {

@@ -105,6 +105,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 // every kernel of the library is launched through klaunch and starts with
 // pdl_wait(); hdr_set_option("pdl", 0) turns the attribute off
 extern bool g_pdl;
+// launch tracing (hdr_set_option("trace", 1)): events around every launch,
+// read back with hdr_trace_dump (tools only; it breaks PDL overlap)
+extern bool g_trace;
+void trace_launch(const void* kern, cudaStream_t s, int end);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t klaunch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -119,7 +123,10 @@ inline cudaError_t klaunch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = g_pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (g_trace) trace_launch((const void*)kern, s, 0);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (g_trace) trace_launch((const void*)kern, s, 1);
+  return e;
 }
 
 // Apply a row-major 3x3 H to (x, y), numpy operation order:

@@ -6,8 +6,11 @@
 // for the tile count (the maximum number of corners) and idle blocks exit,
 // so the coarse-to-fine chain of matcher.pyramidal_match (matcher.py:221-263)
 // runs without a host round trip and can be captured in one CUDA graph.
+#include <cstdio>
+
 #include "hdr_common.cuh"
 #include "hdr_geom.cuh"
+#include "hdr_warpfit.cuh"
 #include "hdr_internal.h"
 #include "hdr_scan.cuh"
 
@@ -295,19 +298,25 @@ __device__ __forceinline__ int weed_delta(int n, int delta) {
 
 constexpr int kFitStride = 20;  // H[9], Hinv[9], ok, pad
 
-// One thread per iteration: draw with resampling (weeding.py:74-84), fit.
-__global__ void __launch_bounds__(64) weed_fit_kernel(const MatchRow* __restrict__ rows,
-                                                      const int32_t* __restrict__ count, int w,
-                                                      int h, int iterations,
-                                                      const uint64_t* __restrict__ keys,
-                                                      double* __restrict__ fits,
-                                                      int32_t* __restrict__ grey) {
+// One warp per iteration: draw with resampling (weeding.py:74-84) -- every
+// lane runs the same Philox stream -- and the four-point fit spread over the
+// lanes (warp_fit4); 8 iterations per block, so the hypotheses of a level
+// occupy ~32 SMs instead of 4 and no thread runs a 9x8 QR alone.
+constexpr int kFitWarps = 8;
+__global__ void __launch_bounds__(32 * kFitWarps) weed_fit_kernel(const MatchRow* __restrict__ rows,
+                                                                  const int32_t* __restrict__ count, int w,
+                                                                  int h, int iterations,
+                                                                  const uint64_t* __restrict__ keys,
+                                                                  double* __restrict__ fits,
+                                                                  int32_t* __restrict__ grey) {
   pdl_wait();
-  int it = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ WarpFitSmem wsm[kFitWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = blockIdx.x * kFitWarps + warp;
   if (it >= iterations) return;
   int n = *count;
   double* f = fits + (int64_t)it * kFitStride;
-  f[18] = 0.0;
+  if (lane == 0) f[18] = 0.0;
   if (n < 4) return;
   Philox g;
   philox_init(&g, keys[2 * it], keys[2 * it + 1]);
@@ -323,14 +332,16 @@ __global__ void __launch_bounds__(64) weed_fit_kernel(const MatchRow* __restrict
       norm_row(rows[idx[k]], w, h, p);
       px[k] = p[0]; py[k] = p[1]; qx[k] = p[2]; qy[k] = p[3];
     }
-    ok = fit4(px, py, qx, qy, H, &g_local) == 0;
+    ok = warp_fit4(px, py, qx, qy, H, &g_local, &wsm[warp]) == 0;
   }
-  if (g_local) atomicAdd(grey, g_local);
+  if (lane == 0 && g_local) atomicAdd(grey, g_local);
   if (!ok) return;
   double Hi[9];
   if (!inv3(H, Hi)) return;
-  for (int k = 0; k < 9; ++k) { f[k] = H[k]; f[9 + k] = Hi[k]; }
-  f[18] = 1.0;
+  if (lane == 0) {
+    for (int k = 0; k < 9; ++k) { f[k] = H[k]; f[9 + k] = Hi[k]; }
+    f[18] = 1.0;
+  }
 }
 
 // One block per iteration: symmetric-transfer inliers over the whole set
@@ -389,7 +400,7 @@ void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w
                  cudaStream_t s) {
   cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((n_static + 31) / 32 + 1), s);
   cudaMemsetAsync(witness, 0, sizeof(int32_t) * (n_static + 1), s);
-  klaunch(weed_fit_kernel, ceil_div(iterations, 64), 64, 0, s, rows, count, w, h, iterations, keys,
+  klaunch(weed_fit_kernel, ceil_div(iterations, kFitWarps), 32 * kFitWarps, 0, s, rows, count, w, h, iterations, keys,
                                                           fit_scratch, grey);
   klaunch(weed_count_kernel, iterations, 256, 0, s, rows, count, w, h, eps, delta, fit_scratch, mask,
                                                witness);
@@ -413,15 +424,24 @@ __device__ __forceinline__ double dlt_entry(int r, int k, double px, double py, 
 }
 // Block-wide least-squares DLT (geometry.fit_homography for n >= 4) over
 // points fetched by `get(i, p)` (p = ref x, ref y, src x, src y).
+#ifdef HDR_FL_TRACE
+__device__ __forceinline__ long long fl_clk() { return clock64(); }
+__shared__ long long fl_ts[8];
+#define FLT(i) do { if (threadIdx.x == 0) fl_ts[i] = fl_clk(); } while (0)
+#else
+#define FLT(i) do {} while (0)
+#endif
 template <class Get>
 __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
+
   __shared__ double red[32][6];
   __shared__ double bc[6];
   __shared__ int status;
   int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int nw = (blockDim.x + 31) >> 5;
+  __shared__ WarpFitSmem wfs;
   if (n == 4) {
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
       double px[4], py[4], qx[4], qy[4];
       for (int k = 0; k < 4; ++k) {
         double p[4];
@@ -429,8 +449,13 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
         px[k] = p[0]; py[k] = p[1]; qx[k] = p[2]; qy[k] = p[3];
       }
       int g = 0;
-      status = fit4(px, py, qx, qy, H, &g);
-      if (g && grey) atomicAdd(grey, g);
+      double Hl[9];
+      int st = warp_fit4(px, py, qx, qy, Hl, &g, &wfs);
+      if (lane == 0) {
+        status = st;
+        for (int k = 0; k < 9; ++k) H[k] = Hl[k];
+        if (g && grey) atomicAdd(grey, g);
+      }
     }
     __syncthreads();
     return status;
@@ -455,6 +480,7 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     }
   }
   __syncthreads();
+  FLT(1);
   // mean distances to the centroids
   double md[2] = {0, 0};
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -484,6 +510,7 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
   }
   __syncthreads();
   if (status) return status;
+  FLT(2);
   // Gram matrix of the conditioned DLT rows. With p~ = (px, py, 1), rows are
   // r0 = [-p~, 0, qx p~], r1 = [0, -p~, qy p~], so G is assembled from 24 sums
   // S_w = sum w p~ p~^T (6 unique entries each) for w in {1, qx, qy, qx^2+qy^2}.
@@ -503,6 +530,7 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
       for (int b = 0; b < 6; ++b) acc[6 * a + b] += wts[a] * mono[b];
   }
   __shared__ double gsh[8][24];
+  __shared__ double g45s[45];
 #pragma unroll
   for (int k = 0; k < 24; ++k) {
     double v = acc[k];
@@ -530,15 +558,16 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
         G[3 + i][6 + j] = G[6 + j][3 + i] = -S[12 + m];
         G[6 + i][6 + j] = S[18 + m];
       }
-    double g45[45];
     int k = 0;
     for (int i = 0; i < 9; ++i)
-      for (int j = i; j < 9; ++j) g45[k++] = G[i][j];
+      for (int j = i; j < 9; ++j) g45s[k++] = G[i][j];
+    FLT(3);
     int g = 0;
-    status = fit_from_gram(g45, tr, ts, H, &g);
+    status = fit_from_gram(g45s, tr, ts, H, &g);
     if (g && grey) atomicAdd(grey, g);
   }
   __syncthreads();
+  FLT(4);
   return status;
 }
 
@@ -552,25 +581,31 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     double* __restrict__ hpred, double* __restrict__ homography, int32_t* __restrict__ info,
     double* __restrict__ out_matches, double* __restrict__ out_raw, int32_t* grey) {
   pdl_wait();
+  FLT(5);
   extern __shared__ double pts_cache[];  // normalised (rx, ry, sx, sy) of the weeded set
   __shared__ int scratch[32];
   int n = *raw_count;
   int m = 0;
   bool cached = n <= kFitCache;
   if (n >= 4) {
-    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
-      int i = c0 + threadIdx.x;
-      int f = (i < n) ? (int)((mask[i >> 5] >> (i & 31)) & 1u) : 0;
-      int total;
-      int pos = block_exclusive_scan(f, scratch, &total);
-      if (f) {
-        weeded[m + pos] = raw[i];
-        if (cached) norm_row(raw[i], w, h, pts_cache + 4 * (m + pos));
-        if (kept_idx) kept_idx[m + pos] = i;
-        if (out_matches)
-          for (int k = 0; k < 5; ++k) out_matches[5 * (int64_t)(m + pos) + k] = raw[i].v[k];
-      }
-      m += total;
+    // np.flatnonzero order with one block scan: thread t owns the contiguous
+    // rows [t L, t L + L), counts its flags, and writes them after the
+    // exclusive prefix of the counts (every row load of a thread in flight
+    // at once, instead of one dependent load + scan per 256-row chunk)
+    const int L = (n + blockDim.x - 1) / blockDim.x;
+    const int i0 = min(n, (int)threadIdx.x * L), i1 = min(n, i0 + L);
+    int cnt = 0;
+    for (int i = i0; i < i1; ++i) cnt += (int)((mask[i >> 5] >> (i & 31)) & 1u);
+    int pos = block_exclusive_scan(cnt, scratch, &m);
+    for (int i = i0; i < i1; ++i) {
+      if (!((mask[i >> 5] >> (i & 31)) & 1u)) continue;
+      const MatchRow rw = raw[i];
+      weeded[pos] = rw;
+      if (cached) norm_row(rw, w, h, pts_cache + 4 * pos);
+      if (kept_idx) kept_idx[pos] = i;
+      if (out_matches)
+        for (int k = 0; k < 5; ++k) out_matches[5 * (int64_t)pos + k] = rw.v[k];
+      ++pos;
     }
   }
   if (threadIdx.x == 0) {
@@ -593,7 +628,13 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     }
   };
   __syncthreads();  // weeded rows / cached points visible block-wide
+  FLT(0);
   int st = block_fit(m, get, Hs, grey);
+#ifdef HDR_FL_TRACE
+  if (threadIdx.x == 0)
+    printf("FLT level %d n=%d m=%d compact %lld centroid %lld md %lld gram %lld solve %lld\n", level, n, m,
+           fl_ts[0] - fl_ts[5], fl_ts[1] - fl_ts[0], fl_ts[2] - fl_ts[1], fl_ts[3] - fl_ts[2], fl_ts[4] - fl_ts[3]);
+#endif
   if (threadIdx.x == 0 && st == 0) {
     for (int k = 0; k < 9; ++k) hpred[k] = Hs[k];
     if (level == 0 && homography) {

@@ -2,21 +2,22 @@
 // frames (NF = 2: the reference's fuse; NF > 2: the k-way generalisation of
 // frame 0 is the reference, weights normalised over all
 // frames), as four tiled kernels:
-//   weights_down0  quality weights of both frames (fusion.py:67-77), the
+//   weights_down0  quality weights of every frame (fusion.py:67-77), the
 //                  SSIM/validity trust and normalisation (fusion.py:117-128)
-//                  for a 36x36 level-0 tile, written for the owned 32x32 and
-//                  immediately blurred + decimated into level 1 of the
-//                  4*NF-channel Gaussian pyramid (RGB of every frame, then
-//                  the NF weights) -- the weights never make a separate HBM
-//                  round trip before the first reduction;
+//                  for a 36x36 level-0 tile; for the owned 32x32 it writes
+//                  the sources' weights and the level-0 blend of the frames
+//                  B0 = sum_f w_f I_f (into the composite buffer), and it
+//                  blurs + decimates the tile into level 1 of the 4*NF-channel
+//                  Gaussian pyramid (RGB of every frame, then the NF weights)
+//                  -- the weights never make a separate HBM round trip before
+//                  the first reduction;
 //   down           the same 5-tap reflect blur + [::2, ::2] for levels >= 1;
 //   collapse       C_k = sum_f W_f (G_f - up G_f') + up C'  (the blend of
-//                  laplacian_pyramid terms and
-//                  collapse_pyramid folded together); level 0 reads the
-//                  interleaved inputs and writes the clipped composite.
-// up() is _pyr_up (fusion.py:89-93): zero-insert on the fine grid, 2x-gain
-// 5-tap blur, scipy 'reflect' on the fine grid -- evaluated separably from a
-// shared-memory staging of the horizontally up-sampled rows.
+//                  laplacian_pyramid terms and collapse_pyramid folded
+//                  together); level 0 is B0 - sum_f w_f up G_f' + up C',
+//                  clipped: it reads B0 and NF-1 weight planes instead of
+//                  every frame and weight (55 -> 31 B/px of level-0 traffic
+//                  plus the coarse tiles), w_0 = 1 - sum_{f>0} w_f.
 // Arithmetic is f32 (the composite tolerance is 1e-3).
 #include "hdr_common.cuh"
 #include "hdr_internal.h"
@@ -34,19 +35,18 @@ __device__ __forceinline__ float lum_f(float r, float g, float b) {
 }
 
 // contrast x saturation x well-exposedness + 1e-12 (fusion.py:67-77).
-// The laplacian and the channel variance are formed in f64 as in the
-// reference: both are then exact (sums of a few f32 values), so a grey or
-// clipped pixel gets exactly 0 contrast/saturation like numpy's (an f32 mean
-// leaves ~1e-8 of std there, which outweighs the 1e-12 floor and changes the
-// blend weights completely). Everything after that -- sqrt, exp, products,
+// The laplacian is formed in f64 as in the reference: it is then exact (a sum
+// of a few f32 values), so a flat neighbourhood gets exactly 0 contrast like
+// numpy's. The channel std uses the pairwise form var = ((r-g)^2 + (g-b)^2 +
+// (b-r)^2) / 9 in f32: it is exactly 0 for a grey pixel, as numpy's f64 std
+// is (an f32 MEAN would leave ~1e-8 of std there, which outweighs the 1e-12
+// floor and changes the blend weights completely), and within ~1e-7 relative
+// of it otherwise. Everything after the laplacian -- sqrt, exp, products,
 // normalisation -- is f32: relative error ~1e-7 on a weight moves the
 // composite by ~1e-7, far inside the 1e-3 bar.
 __device__ __forceinline__ float quality_f(double lap, float r, float g, float b) {
-  const double third = 1.0 / 3.0;
-  double R = r, G = g, B = b;
-  double mean = ((R + G) + B) * third;
-  double dr = R - mean, dg = G - mean, db = B - mean;
-  float sat = sqrtf((float)(((dr * dr + dg * dg) + db * db) * third));
+  float d0 = r - g, d1 = g - b, d2 = b - r;
+  float sat = __fsqrt_rn((d0 * d0 + d1 * d1 + d2 * d2) * (1.0f / 9.0f));
   float er = r - 0.5f, eg = g - 0.5f, eb = b - 0.5f;
   float ex = __expf(-(er * er + eg * eg + eb * eb) * 12.5f);
   return fabsf((float)lap) * sat * ex + 1e-12f;
@@ -122,7 +122,8 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
 #endif
 template <int NF>
 __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_down_kernel(FuseFrames<NF> fr, int w, int h,
-                                                          float* __restrict__ g1, int ow, int oh) {
+                                                          float* __restrict__ g1, int ow, int oh,
+                                                          float* __restrict__ b0) {
   pdl_wait();
   extern __shared__ float smf[];
   float* lum = smf;                    // [NF][38][38] luminance of every frame
@@ -219,12 +220,22 @@ __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_
       bool own = (unsigned)(ty - 2) < 2u * kOT && (unsigned)(tx - 2) < 2u * kOT &&
                  vy0 + ty + 1 < h && vx0 + tx + 1 < w;
       int p = own ? ridx[ty + 1] * w + cidx[tx + 1] : 0;
+      float bl[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int f = 0; f < NF; ++f) {
         float wf = q[f] * inv;
         d[(3 * NF + f) * kRT * kRP] = wf;
-        if (own) fr.wout[f][p] = wf;
+        // the sources' weights for the collapse (w_0 = 1 - their sum there)
+        if (own && f > 0) fr.wout[f][p] = wf;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) bl[k] = f == 0 ? wf * d[k * kRT * kRP] : bl[k] + wf * d[(3 * f + k) * kRT * kRP];
       }
+      // level 0's blend of the frames, B0 = sum_f w_f I_f: the level-0 term of
+      // the Laplacian blend is B0 - sum_f w_f up(G1_f), so the collapse reads
+      // B0 (12 B/px) instead of every frame (12 NF B/px)
+      if (own)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) b0[3 * p + k] = bl[k];
       tx += 4; ty += 7;
       if (tx >= kRT) { tx -= kRT; ++ty; }
     }
@@ -392,15 +403,14 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
   bool aligned = ((uintptr_t)out & 15) == 0;
   if (LEVEL0) {
 #pragma unroll
-    for (int f = 0; f < NF; ++f)
-      aligned = aligned && (((uintptr_t)fr.img[f] | (uintptr_t)fr.wout[f]) & 15) == 0;
+    for (int f = 1; f < NF; ++f) aligned = aligned && ((uintptr_t)fr.wout[f] & 15) == 0;
   } else {
     aligned = aligned && ((uintptr_t)g & 15) == 0;
   }
   const bool vec = full && aligned && (w & 3) == 0 && (LEVEL0 || (P & 3) == 0);
-  float wt[NF][4], gv[NF][3][4];
+  float wt[NF][4];
 #pragma unroll
-  for (int f = 0; f < NF; ++f) {
+  for (int f = LEVEL0 ? 1 : 0; f < NF; ++f) {
     const float* wp = LEVEL0 ? fr.wout[f] + p : g + (3 * NF + f) * P + p;
     if (vec) {
       float4 t = __ldg(reinterpret_cast<const float4*>(wp));
@@ -409,51 +419,41 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
 #pragma unroll
       for (int j = 0; j < 4; ++j) wt[f][j] = X + j < w ? __ldg(wp + j) : 0.0f;
     }
-    if (LEVEL0) {
-      const float* ip = fr.img[f] + 3 * p;  // 12 interleaved floats
-      if (vec) {
-        float4 t0 = __ldg(reinterpret_cast<const float4*>(ip));
-        float4 t1 = __ldg(reinterpret_cast<const float4*>(ip) + 1);
-        float4 t2 = __ldg(reinterpret_cast<const float4*>(ip) + 2);
-        float v12[12] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w, t2.x, t2.y, t2.z, t2.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) gv[f][k][j] = v12[3 * j + k];
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) gv[f][k][j] = X + j < w ? __ldg(ip + 3 * j + k) : 0.0f;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float* gp = g + (3 * f + k) * P + p;
-        if (vec) {
-          float4 t = __ldg(reinterpret_cast<const float4*>(gp));
-          gv[f][k][0] = t.x; gv[f][k][1] = t.y; gv[f][k][2] = t.z; gv[f][k][3] = t.w;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) gv[f][k][j] = X + j < w ? __ldg(gp + j) : 0.0f;
-        }
-      }
-    }
   }
   float o[3][4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      float v = 0.0f;
-#pragma unroll
-      for (int f = 0; f < NF; ++f)
-        v = f == 0 ? wt[0][j] * (gv[0][k][j] - u[k][j]) : v + wt[f][j] * (gv[f][k][j] - u[3 * f + k][j]);
-      v += u[3 * NF + k][j];
-      o[k][j] = LEVEL0 ? fminf(fmaxf(v, 0.0f), 1.0f) : v;
-    }
   if (LEVEL0) {
+    // composite = B0 - sum_f w_f up(G1_f) + up(C1), w_0 = 1 - sum_{f>0} w_f
+    // (B0 = sum_f w_f I_f, written by weights_down into `out`)
+    float b[3][4];
     float* op = out + 3 * p;
+    if (vec) {
+      float4 t0 = *reinterpret_cast<const float4*>(op);
+      float4 t1 = *(reinterpret_cast<const float4*>(op) + 1);
+      float4 t2 = *(reinterpret_cast<const float4*>(op) + 2);
+      float v12[12] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w, t2.x, t2.y, t2.z, t2.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) b[k][j] = v12[3 * j + k];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) b[k][j] = X + j < w ? op[3 * j + k] : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float w0 = 1.0f;
+#pragma unroll
+      for (int f = 1; f < NF; ++f) w0 -= wt[f][j];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float v = w0 * u[k][j];
+#pragma unroll
+        for (int f = 1; f < NF; ++f) v += wt[f][j] * u[3 * f + k][j];
+        o[k][j] = fminf(fmaxf(b[k][j] - v + u[3 * NF + k][j], 0.0f), 1.0f);
+      }
+    }
     if (vec) {
       float4* o4 = reinterpret_cast<float4*>(op);
       o4[0] = make_float4(o[0][0], o[1][0], o[2][0], o[0][1]);
@@ -466,17 +466,41 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
 #pragma unroll
           for (int k = 0; k < 3; ++k) op[3 * j + k] = o[k][j];
     }
-  } else {
+    return;
+  }
+  float gv[NF][3][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      float* op = out + k * P + p;
+      const float* gp = g + (3 * f + k) * P + p;
       if (vec) {
-        *reinterpret_cast<float4*>(op) = make_float4(o[k][0], o[k][1], o[k][2], o[k][3]);
+        float4 t = __ldg(reinterpret_cast<const float4*>(gp));
+        gv[f][k][0] = t.x; gv[f][k][1] = t.y; gv[f][k][2] = t.z; gv[f][k][3] = t.w;
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (X + j < w) op[j] = o[k][j];
+        for (int j = 0; j < 4; ++j) gv[f][k][j] = X + j < w ? __ldg(gp + j) : 0.0f;
       }
+    }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float v = 0.0f;
+#pragma unroll
+      for (int f = 0; f < NF; ++f)
+        v = f == 0 ? wt[0][j] * (gv[0][k][j] - u[k][j]) : v + wt[f][j] * (gv[f][k][j] - u[3 * f + k][j]);
+      o[k][j] = v + u[3 * NF + k][j];
+    }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float* op = out + k * P + p;
+    if (vec) {
+      *reinterpret_cast<float4*>(op) = make_float4(o[k][0], o[k][1], o[k][2], o[k][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (X + j < w) op[j] = o[k][j];
     }
   }
 }
@@ -530,7 +554,7 @@ static void launch_fuse_nf(const FuseFrames<NF>& fr, const FusePyramid& py, cuda
   kprobe_mark(kp_w0, 0, s);
   dim3 g0(ceil_div(d1.w, kOT), ceil_div(d1.h, kOT));
   klaunch(weights_down_kernel<NF>, g0, dim3(256), weights_smem<NF>(), s, fr, d[0].w, d[0].h, py.g[1], d1.w,
-             d1.h);
+          d1.h, py.out);
   kprobe_mark(kp_w0, 1, s);
   if (L == 1) {
     dim3 gf(ceil_div(d[0].w, kFT), ceil_div(d[0].h, kFT));

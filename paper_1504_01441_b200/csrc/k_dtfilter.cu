@@ -761,17 +761,6 @@ __device__ __forceinline__ void cluster_sync_smem() {
 #endif
 }
 
-// cp.async (LDGSTS): per-thread asynchronous global -> shared copies, used to
-// prefetch the next band of dt_cols_cluster while the current one is linked,
-// applied and stored
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // prefetch slots of one thread: element (k, j) at pfx[(k * kSR + j) * kCT + tid]
 // (consecutive threads, consecutive words: conflict-free), guide j at

@@ -21,6 +21,7 @@
 // Arithmetic is f32 (the composite tolerance is 1e-3).
 #include "hdr_common.cuh"
 #include "hdr_internal.h"
+#include "hdr_bulk.cuh"
 
 #include <algorithm>
 
@@ -267,31 +268,21 @@ __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in,
   __syncthreads();
   int P = w * h;
   {
-    int ty = tid / kRT, tx = tid - ty * kRT;
-    // two region samples (2 NC loads) in flight per step
+    // the whole region gathered by cp.async: every sample of every channel
+    // in flight at once (register loads in dependent rounds left the small
+    // levels latency-bound at ~8 us per launch)
+    int ty = tid / kRT, tx = tid - ty * kRT;  // 256 = 7 * 36 + 4
 #pragma unroll 1
-    for (int i = tid; i < kRT * kRT; i += 512) {
-      int ty2 = ty + 7, tx2 = tx + 4;
-      if (tx2 >= kRT) { tx2 -= kRT; ++ty2; }
-      bool ok2 = i + 256 < kRT * kRT;
-      const float* s1 = in + ridx[ty] * w + cidx[tx];
-      const float* s2 = in + ridx[min(ty2, kRT - 1)] * w + cidx[tx2];
-      float v1[NC], v2[NC];
+    for (int i = tid; i < kRT * kRT; i += 256) {
+      const float* sp = in + ridx[ty] * w + cidx[tx];
+      float* dp = tile + ty * kRP + tx;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        v1[c] = __ldg(s1 + c * P);
-        v2[c] = ok2 ? __ldg(s2 + c * P) : 0.0f;
-      }
-      float* d1 = tile + ty * kRP + tx;
-      float* d2 = tile + ty2 * kRP + tx2;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        d1[c * kRT * kRP] = v1[c];
-        if (ok2) d2[c * kRT * kRP] = v2[c];
-      }
-      ty = ty2 + 7; tx = tx2 + 4;
+      for (int c = 0; c < NC; ++c) cp_async4(dp + c * kRT * kRP, sp + (int64_t)c * P);
+      tx += 4; ty += 7;
       if (tx >= kRT) { tx -= kRT; ++ty; }
     }
+    cp_async_commit();
+    cp_async_wait_all();
   }
   __syncthreads();
   down_tile<NC>(tile, V, tid, Y0, X0, out, ow, oh);
@@ -352,15 +343,18 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
   }
   int CP = cw * ch;
   if (gc) {  // null for a single-level pyramid: up() of nothing is 0
+    // gathered by cp.async, every request in flight at once
     int yy = tid / kCT, xx = tid - yy * kCT;  // 256 = 13 * 19 + 9
     for (int i = tid; i < kCT * kCT; i += 256) {
       int p = min(cy0 + yy, ch - 1) * cw + min(cx0 + xx, cw - 1);
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
-        C[c * kCT * kCT + i] = c < 3 * NF ? __ldg(gc + c * CP + p) : __ldg(cc + (c - 3 * NF) * CP + p);
+        cp_async4(C + c * kCT * kCT + i, c < 3 * NF ? gc + c * CP + p : cc + (c - 3 * NF) * CP + p);
       xx += 9; yy += 13;
       if (xx >= kCT) { xx -= kCT; ++yy; }
     }
+    cp_async_commit();
+    cp_async_wait_all();
   }
   __syncthreads();
   // horizontal: Hc[c][r][x] for the 19 coarse rows and the 32 fine columns

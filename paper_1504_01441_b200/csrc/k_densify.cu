@@ -278,17 +278,22 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
     int64_t i = (int64_t)y * w + x;
     float2 f = __ldcs(reinterpret_cast<const float2*>(flow) + i);
     double sx = dadd((double)x, (double)f.x), sy = dadd((double)y, (double)f.y);
-    bool ok = sx >= 0.0 && sx <= (double)(w - 1) && sy >= 0.0 && sy <= (double)(h - 1);
-    double cx = fmin(fmax(sx, 0.0), (double)(w - 1));
-    double cy = fmin(fmax(sy, 0.0), (double)(h - 1));
+    const double wm = (double)(w - 1), hm = (double)(h - 1);
+    bool ok = sx >= 0.0 && sx <= wm && sy >= 0.0 && sy <= hm;
+    // np.clip of a finite value: compare + select (f64 fmin/fmax cost ~7
+    // instructions each here)
+    double cx = sx < 0.0 ? 0.0 : (sx > wm ? wm : sx);
+    double cy = sy < 0.0 ? 0.0 : (sy > hm ? hm : sy);
     int x0 = (int)floor(cx), y0 = (int)floor(cy);
-    int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
     double fx = dsub(cx, (double)x0), fy = dsub(cy, (double)y0);
     double gx = dsub(1.0, fx), gy = dsub(1.0, fy);
-    const float* s00 = src + ((int64_t)y0 * w + x0) * 3;
-    const float* s01 = src + ((int64_t)y0 * w + x1) * 3;
-    const float* s10 = src + ((int64_t)y1 * w + x0) * 3;
-    const float* s11 = src + ((int64_t)y1 * w + x1) * 3;
+    // 32-bit element offsets (3 w h < 2^31 for any frame the context holds)
+    const int o00 = 3 * (y0 * w + x0);
+    const int dxo = x0 + 1 < w ? 3 : 0, dyo = y0 + 1 < h ? 3 * w : 0;
+    const float* s00 = src + o00;
+    const float* s01 = s00 + dxo;
+    const float* s10 = s00 + dyo;
+    const float* s11 = s10 + dxo;
     float o[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -314,6 +319,12 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
 
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
                  uint8_t* qw, uint32_t* hist, cudaStream_t s) {
+  if (3 * (int64_t)w * h >= ((int64_t)1 << 31)) {  // beyond the 32-bit offsets of warp_kernel
+    DtPlanes none{{nullptr, nullptr, nullptr}, {0, 0, 0}, 0};
+    launch_finalize_warp(none, nullptr, nullptr, w, h, 0.0, src, 3, const_cast<float*>(flow), warped, valid,
+                         qw, hist, false, s);
+    return;
+  }
   int64_t work = (int64_t)((w + 255) / 256) * h;
 #ifndef HDR_WARP_BLOCKS_PER_SM
 #define HDR_WARP_BLOCKS_PER_SM 12

@@ -352,8 +352,12 @@ def kernel_bytes(w, h, passes=3):
         "dt_cols": ((passes - 1) * P * 52 + P * 36, passes),
         "warp": (P * 34, 1),
         "ssim": (P * 9, 1),
-        "fuse_weights0": (P * 45, 1),
-        "fuse_collapse0": (P * 55, 1),
+        # weights_down0: ref 12, warped 12, SSIM 4, valid 1 in; source weight
+        # 4, B0 12 and the 8-channel level-1 pyramid 8 out
+        "fuse_weights0": (P * 53, 1),
+        # level-0 collapse: B0 12 + source weight 4 + the 9 level-1 channels
+        # it up-samples (9 B per level-0 px) in, composite 12 out
+        "fuse_collapse0": (P * 37, 1),
     }
 
 

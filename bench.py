@@ -81,6 +81,8 @@ def parse(argv=None):
     ap.add_argument("--no-extra-workloads", action="store_true",
                     help="skip the 12MP / 5MP-stack legs and the drop-in latency")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-banded", action="store_true",
+                    help="skip the one-12MP-pair-over-all-ranks row-band leg (SURVEY.md §8(f)4)")
     ap.add_argument("--cpu-impl", choices=["auto", "reference", "port"], default="auto",
                     help="CPU side: the real hdrflow from baseline/_ref, or the oracle port")
     ap.add_argument("--selftest-cpu", action="store_true",
@@ -694,6 +696,38 @@ def dropin_latency(scene, n=5):
                     "host wall clock"}
 
 
+def banded_leg(local, hd, world, w=None, h=None, n=3):
+    """ONE 12MP pair split across all the ranks by row bands
+    (paper_1504_01441_b200/banded.py). Device time of each call between CUDA
+    events on the calling stream (the collectives and the host syncs inside
+    the call included), median of n after a warm-up, max over ranks; digest
+    of the composite so the driver can see every N computes the same pair."""
+    import torch
+    from paper_1504_01441_b200.banded import register_and_fuse_banded
+    w, h = w or W12, h or H12
+    ref, src = render("pair", 1, w, h)[0]
+    ref_t, src_t = torch.from_numpy(ref).to(f"cuda:{local}"), torch.from_numpy(src).to(f"cuda:{local}")
+    res = register_and_fuse_banded(ref_t, src_t)
+    ts = []
+    for _ in range(n):
+        hd.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = register_and_fuse_banded(ref_t, src_t)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = hd.max_over_ranks(statistics.median(ts), device=f"cuda:{local}")
+    comp = hashlib.sha256(res.composite.cpu().numpy().tobytes()).hexdigest()[:16]
+    del res
+    torch.cuda.empty_cache()
+    return {"workload": f"one {w}x{h} pair split by row bands over {world} rank(s) (SURVEY.md §8(f)4)",
+            "latency_ms": ms, "ranks": world, "composite_digest": comp,
+            "note": "registration and merge replicated, domain transform / warp / SSIM banded; "
+                    "chunk aggregates, flow, histogram and the band outputs all-reduced (NCCL)"}
+
+
 def extra_pairs_leg(args, local, peak, cpu_kind):
     """BASELINE configs[3]: 12MP pairs (4000x3000), same runner as the headline."""
     import torch
@@ -868,6 +902,8 @@ def run_ours(args):
     (ems, h2d, d2h, e2e_ok), (rms, rh2d, rd2h, raw_ok) = e2e_leg(args, scenes, w, h, local, hd, dev)
 
     extras = {}
+    if not args.no_banded and (w, h) == (W5, H5):
+        extras["banded_12mp"] = banded_leg(local, hd, world)
     if rank == 0 and world == 1 and not args.no_extra_workloads and (w, h) == (W5, H5):
         peak, _ = peaks()
         extras["dropin_latency"] = dropin_latency(scenes[0])

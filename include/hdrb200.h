@@ -337,6 +337,35 @@ int hdr_fuse(hdr_ctx* ctx, const float* ref, const float* warped, const float* s
              const uint8_t* valid, int32_t width, int32_t height, int32_t levels,
              float* out);
 
+/* ---- row-band pieces of one pair across ranks ---------
+ * paper_1504_01441_b200/banded.py runs one giant pair over N GPUs: the
+ * registration is replicated, every rank owns the rows [y0, y1) of a band
+ * (a multiple of hdr_band_rows_multiple() rows), and these entries do that
+ * band's share of densify_flow (densify.py:116-142), warp_image
+ * (densify.py:145-174) and make_ssim (pipeline.py:165-171); the caller sums
+ * the column-chunk aggregates and the warped-luminance histogram over the
+ * ranks (NCCL all-reduce) between them. */
+int32_t hdr_band_rows_multiple(void);
+/* doubles of the dt_filter chunk-aggregate buffer for (w, h) and k planes */
+int64_t hdr_band_agg_doubles(int32_t width, int32_t height, int32_t k);
+/* op 0: the band's row sweeps of pass pass_i; op 1: its column-chunk
+ * aggregates into agg (whole-image layout, caller-zeroed; sum over ranks
+ * next); op 2: link the summed agg and re-run the band's chunks, writing the
+ * planes -- or, when flow != NULL (last pass, k = 3), the f32 flow with the
+ * homography fallback below `floor_` (fallback/has_fb as hdr_densify_finalize). */
+int hdr_band_dt(hdr_ctx* ctx, int32_t op, const float* guide, double* planes, int32_t k, int32_t width,
+                int32_t height, int32_t y0, int32_t y1, double sigma_s, double sigma_r, int32_t passes,
+                int32_t pass_i, double* agg, const double* fallback, const int32_t* has_fb, double floor_,
+                float* flow);
+/* warp_image of rows [y0, y1) of full-size buffers (+ the quantised warped
+ * luminance and, when hist != NULL, its 256-bin histogram added to hist). */
+int hdr_band_warp(hdr_ctx* ctx, const float* flow, int32_t width, int32_t height, int32_t y0, int32_t y1,
+                  const float* src, float* warped, uint8_t* valid, uint8_t* qw, uint32_t* hist);
+/* make_ssim rows [y0, y1): hist_w = the whole frame's warped-luminance
+ * histogram (summed over ranks), qw valid on [y0 - 5, y1 + 5). */
+int hdr_band_ssim(hdr_ctx* ctx, const float* lum_ref, const uint8_t* qw, const uint32_t* hist_w, int32_t width,
+                  int32_t height, int32_t y0, int32_t y1, int32_t window, double sigma, float* out);
+
 /* Tool: with hdr_set_option("trace", 1) every launch is bracketed by events;
  * writes "kernel<TAB>microseconds" lines for the launches since, then clears
  * them (synchronises the device). */

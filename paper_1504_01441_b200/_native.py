@@ -102,6 +102,11 @@ SIGNATURES = {
     "hdr_dark_count": (_I, [_P, _P, _I, _I64, ctypes.c_float, _P]),
     "hdr_register_and_fuse_raw": (_I, [_P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P]),
     "hdr_trace_dump": (_I, [ctypes.c_char_p, _I64]),
+    "hdr_band_rows_multiple": (_I, []),
+    "hdr_band_agg_doubles": (_I64, [_I, _I, _I]),
+    "hdr_band_dt": (_I, [_P, _I, _P, _P, _I, _I, _I, _I, _I, _D, _D, _I, _I, _P, _P, _P, _D, _P]),
+    "hdr_band_warp": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "hdr_band_ssim": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _D, _P]),
     "hdr_level_seed": (ctypes.c_uint32, [_U64, _I]),
     "hdr_iteration_keys": (_I, [_U64, _I, _P]),
     "hdr_choice4_host": (_I, [_P, _I, _I, _P]),

@@ -1610,6 +1610,61 @@ extern "C" int hdr_symmetric_transfer_error(hdr_ctx* c, const double* H, const d
   return HDR_OK;
 }
 
+// ---- row-band pieces of the pair (paper_1504_01441_b200/banded.py)
+extern "C" int32_t hdr_band_rows_multiple(void) { return 32; }
+
+extern "C" int64_t hdr_band_agg_doubles(int32_t w, int32_t h, int32_t k) {
+  return hdr::dt_band_agg_doubles(w, h, k);
+}
+
+extern "C" int hdr_band_dt(hdr_ctx* c, int32_t op, const float* guide, double* planes, int32_t k, int32_t w,
+                           int32_t h, int32_t y0, int32_t y1, double sigma_s, double sigma_r, int32_t passes,
+                           int32_t pass_i, double* agg, const double* fallback, const int32_t* has_fb,
+                           double floor_, float* flow) {
+  CtxDevice dg_(c);
+  NEED(c && guide && planes && k >= 1 && k <= 3 && w >= 1 && h >= 1, "bad argument");
+  NEED(op >= 0 && op <= 2 && pass_i >= 1 && pass_i <= passes, "bad band operation");
+  NEED(0 <= y0 && y0 <= y1 && y1 <= h && y0 % dt_band_chunk_rows() == 0 &&
+           (y1 == h || y1 % dt_band_chunk_rows() == 0),
+       "band rows must be whole chunks");
+  NEED(op == 0 || agg, "null aggregate buffer");
+  NEED(dt_scratch_doubles(w, h, k) <= dt_scratch_doubles(c->W, c->H, 3), "image larger than the workspace");
+  int64_t P = (int64_t)w * h;
+  DtPlanes pl = f64_planes(planes, planes + P, planes + 2 * P, k);
+  DtFlowOut fo{fallback, has_fb, floor_, flow};
+  double* carry = c->carry + hdr::dt_band_agg_doubles(w, h, k);
+  launch_dt_band(op, guide, pl, w, h, y0, y1, sigma_s, sigma_r, passes, pass_i, agg, carry, &fo, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_band_warp(hdr_ctx* c, const float* flow, int32_t w, int32_t h, int32_t y0, int32_t y1,
+                             const float* src, float* warped, uint8_t* valid, uint8_t* qw, uint32_t* hist) {
+  CtxDevice dg_(c);
+  NEED(c && flow && src && warped && valid && qw && 0 <= y0 && y0 <= y1 && y1 <= h, "bad argument");
+  NEED(3 * (int64_t)w * h < ((int64_t)1 << 31), "frame too large for the banded warp");
+  launch_warp_rows(flow, w, h, y0, y1, src, warped, valid, qw, hist, c->stream);
+  return check_launch();
+}
+
+extern "C" int hdr_band_ssim(hdr_ctx* c, const float* lum_ref, const uint8_t* qw, const uint32_t* hist_w,
+                             int32_t w, int32_t h, int32_t y0, int32_t y1, int32_t window, double sigma,
+                             float* out) {
+  CtxDevice dg_(c);
+  NEED(c && lum_ref && qw && hist_w && out && 0 <= y0 && y0 <= y1 && y1 <= h, "bad argument");
+  NEED((int64_t)w * h <= c->P, "image larger than the workspace");
+  int rc = ensure_taps(c, window, sigma);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  int64_t P = (int64_t)w * h;
+  uint32_t* hr = c->hist + 3 * kBins;
+  CUDA_TRY(cudaMemsetAsync(hr, 0, sizeof(uint32_t) * kBins, s));
+  launch_hist_plain(lum_ref, P, 1, hr, s);
+  launch_lut(hist_w, P, hr, P, c->lut + 2 * kBins, s);
+  if (!launch_ssim_rows(lum_ref, qw, c->lut + 2 * kBins, w, h, y0, y1, window, c->taps, out, s))
+    return fail(HDR_ERR_INVALID, "banded SSIM needs an 11-tap window and 32-row band starts");
+  return check_launch();
+}
+
 extern "C" int hdr_densify_finalize(hdr_ctx* c, const double* smooth, int32_t w, int32_t h,
                                     const double* fallback, double floor_, float* flow) {
   CtxDevice dg_(c);

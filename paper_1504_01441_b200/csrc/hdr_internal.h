@@ -160,6 +160,15 @@ bool launch_dt_filter(const float* guide, DtPlanes planes, int w, int h, double 
                       double sigma_r, int passes, double* scratch, cudaStream_t s,
                       const DtFlowOut* fo = nullptr, KProbe* kp_rows = nullptr,
                       KProbe* kp_cols = nullptr, const DtSparse* first = nullptr);
+// row-band pieces of dt_filter: op 0 = the band's row
+// sweeps, 1 = its column-chunk aggregates into agg (the whole image's layout),
+// 2 = link the (rank-summed) agg and apply the band's chunks (+ the flow when
+// fo->flow, K == 3). Bands are whole chunks of dt_band_chunk_rows() rows.
+void launch_dt_band(int op, const float* guide, const DtPlanes& P, int w, int h, int y0, int y1,
+                    double sigma_s, double sigma_r, int passes, int i, double* agg, double* carry,
+                    const DtFlowOut* fo, cudaStream_t s);
+int64_t dt_band_agg_doubles(int w, int h, int k);
+int dt_band_chunk_rows();
 // ---- k_twins.cu (general stage twins)
 // f32 single-channel guide, one row pass of any width (sequential per row)
 void launch_dt_rows_seq(const float* guide, const DtPlanes& P, int w, int h, double ratio, double c,
@@ -177,6 +186,10 @@ void launch_apply_homography(const double* H, const double* pts, int64_t n, doub
 void launch_transfer_error(const double* H, const double* rp, const double* sp, int64_t n, double* out,
                            int32_t* bad, cudaStream_t s);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
+void launch_warp_rows(const float* flow, int w, int h, int y0, int y1, const float* src, float* warped,
+                      uint8_t* valid, uint8_t* qw, uint32_t* hist, cudaStream_t s);
+bool launch_ssim_rows(const float* a, const uint8_t* qb, const float* lut_b, int w, int h, int y0, int y1,
+                      int window, const double* taps, float* out, cudaStream_t s);
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
                  uint8_t* qw, uint32_t* hist, cudaStream_t s);
 void launch_finalize_warp(DtPlanes smooth, const double* fallback,

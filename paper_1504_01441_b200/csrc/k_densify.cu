@@ -255,12 +255,14 @@ __global__ void __launch_bounds__(256) finalize_warp_kernel(
 // flow given. Blocks sweep 256-pixel row segments (grid-stride), so each
 // thread's (x, y) comes without a per-pixel division and the block histogram
 // is flushed once per block.
+// Rows [y0, y1) of the (w, h) frame (the whole frame for the pair; a row
+// band of it for the banded pair); hist may be null (halo rows of a band).
 __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flow, int w, int h,
                                                    const float* __restrict__ src,
                                                    float* __restrict__ warped,
                                                    uint8_t* __restrict__ valid,
                                                    uint8_t* __restrict__ qw,
-                                                   uint32_t* __restrict__ hist) {
+                                                   uint32_t* __restrict__ hist, int y0, int y1) {
   pdl_wait();
   // one histogram per warp (plain shared atomics; see luma_hist_kernel)
   __shared__ uint32_t sh[8][kBins];
@@ -270,9 +272,9 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
   // row / segment indices advance without a division per step
   const int segs = (w + 255) >> 8;
   const int dq = gridDim.x / segs, dr = gridDim.x - dq * segs;
-  int y = blockIdx.x / segs, seg = blockIdx.x - y * segs;
-  for (; y < h; y += dq, seg += dr) {
-    if (seg >= segs) { seg -= segs; ++y; if (y >= h) break; }
+  int y = y0 + (int)blockIdx.x / segs, seg = blockIdx.x - (y - y0) * segs;
+  for (; y < y1; y += dq, seg += dr) {
+    if (seg >= segs) { seg -= segs; ++y; if (y >= y1) break; }
     int x = seg * 256 + threadIdx.x;
     if (x >= w) continue;
     int64_t i = (int64_t)y * w + x;
@@ -308,6 +310,7 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
     qw[i] = (uint8_t)q;
     atomicAdd(&mine[q], 1u);
   }
+  if (!hist) return;
   __syncthreads();
   for (int b = threadIdx.x; b < kBins; b += blockDim.x) {
     uint32_t t = 0;
@@ -315,6 +318,15 @@ __global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flo
     for (int w8 = 0; w8 < 8; ++w8) t += sh[w8][b];
     if (t) atomicAdd(&hist[b], t);
   }
+}
+
+void launch_warp_rows(const float* flow, int w, int h, int y0, int y1, const float* src, float* warped,
+                      uint8_t* valid, uint8_t* qw, uint32_t* hist, cudaStream_t s) {
+  if (y1 <= y0) return;
+  int64_t work = (int64_t)((w + 255) / 256) * (y1 - y0);
+  int64_t cap = 148 * 12;
+  int64_t blocks = work < cap ? work : cap;
+  klaunch(warp_kernel, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, y0, y1);
 }
 
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
@@ -331,7 +343,7 @@ void launch_warp(const float* flow, int w, int h, const float* src, float* warpe
 #endif
   int64_t cap = 148 * HDR_WARP_BLOCKS_PER_SM;
   int64_t blocks = work < cap ? work : cap;
-  klaunch(warp_kernel, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist);
+  klaunch(warp_kernel, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, 0, h);
 }
 
 void launch_finalize_warp(DtPlanes smooth, const double* fallback, const int32_t* has_fallback,

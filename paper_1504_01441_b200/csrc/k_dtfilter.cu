@@ -31,6 +31,7 @@
 
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <type_traits>
 
 namespace hdr {
 
@@ -507,13 +508,16 @@ __device__ __forceinline__ void load_chunk(const float* __restrict__ guide, cons
 
 // Aggregates, field-major agg[f][chunk][col], f = A, Q, R, B[K], Z0[K]:
 // forward zero-carry map y_end = A*C + B, and z_start = Z0 + C*R + Q*D.
+// ch0: first chunk of the launch (a row band's chunks; 0 for the whole
+// image), nch: chunks of the whole image (the agg layout)
 template <int K>
 __global__ void __launch_bounds__(kColThreads) dt_cols_agg(const float* __restrict__ guide,
                                                            DtPlanes P, int w, int h, double ratio,
-                                                           double c, double* __restrict__ agg) {
+                                                           double c, double* __restrict__ agg,
+                                                           int ch0, int nch) {
   pdl_wait();
   int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int ch = blockIdx.y, nch = gridDim.y;
+  int ch = ch0 + (int)blockIdx.y;
   if (x >= w) return;
   ColChunk<K> ck;
   load_chunk<K>(guide, P, w, h, x, ch * kColChunk, ratio, c, ck);
@@ -644,10 +648,10 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __rest
                                                              DtPlanes P, int w, int h,
                                                              double ratio, double c,
                                                              const double* __restrict__ carry,
-                                                             DtFlowOut fo) {
+                                                             DtFlowOut fo, int ch0, int nch) {
   pdl_wait();
   int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int ch = blockIdx.y, nch = gridDim.y;
+  int ch = ch0 + (int)blockIdx.y;
   if (x >= w) return;
   int r0 = ch * kColChunk;
   int64_t F = (int64_t)nch * w, o = (int64_t)ch * w + x;
@@ -1112,6 +1116,92 @@ static bool g_cols_cluster = true;
 // (zeros) instead of letting the first column sweep skip them
 static bool g_skip_zero_rows = true;
 
+// c of pass i (densify.py:104-106)
+static double dt_pass_c(double sigma_s, int passes, int i) {
+  double den = sqrt(pow(4.0, passes) - 1.0);
+  double sigma_i = sigma_s * sqrt(3.0) * pow(2.0, passes - i) / den;
+  return -sqrt(2.0) / sigma_i;
+}
+
+// one horizontal sweep pair over h rows (any row set: rows are independent)
+template <int K>
+static void rows_pass(const float* guide, const DtPlanes& P, int w, int h, double ratio, double c,
+                      cudaStream_t s) {
+  size_t row_smem = (size_t)(K + 1) * w * sizeof(double);
+  if (rows_bulk_ok(guide, P, w))
+    klaunch(dt_rows_bulk_kernel<K>, h, kRowThreads, (size_t)K * w * sizeof(double) + (size_t)w * 4, s,
+            guide, P, w, h, ratio, c);
+  else if (w <= kRowThreads * kRowSeg)
+    klaunch(dt_rows_reg_kernel<K>, h, kRowThreads, (size_t)K * w * sizeof(double), s, guide, P, w, h, ratio, c);
+  else if (row_smem <= (size_t)g_rows_smem_max[K])
+    klaunch(dt_rows_kernel<K>, h, kRowThreads, row_smem, s, guide, P, w, h, ratio, c);
+  else
+    launch_dt_rows_seq(guide, P, w, h, ratio, c, s);
+}
+
+// ---- row-band pieces of the filter: a band of whole
+// chunks [ch0, ch1) runs its rows and its column chunks locally; only the
+// chunk aggregates cross bands (the caller sums them over the ranks), and
+// link + apply then give every band exactly the single-GPU agg/link/apply
+// result.
+int64_t dt_band_agg_doubles(int w, int h, int k) { return (int64_t)ceil_div(h, kColChunk) * w * (3 + 2 * k); }
+int dt_band_chunk_rows() { return kColChunk; }
+
+template <int K>
+static void band_rows_k(const float* guide, const DtPlanes& P, int w, int h, int y0, int y1, double sigma_s,
+                        double sigma_r, int passes, int i, cudaStream_t s) {
+  if (w <= 1 || y1 <= y0) return;
+  DtPlanes B = P;
+  for (int k = 0; k < K; ++k)
+    B.p[k] = P.f64[k] ? (void*)((double*)P.p[k] + (int64_t)y0 * w) : (void*)((float*)P.p[k] + (int64_t)y0 * w);
+  rows_pass<K>(guide + (int64_t)y0 * w, B, w, y1 - y0, sigma_s / sigma_r, dt_pass_c(sigma_s, passes, i), s);
+}
+
+template <int K>
+static void band_agg_k(const float* guide, const DtPlanes& P, int w, int h, int y0, int y1, double sigma_s,
+                       double sigma_r, int passes, int i, double* agg, cudaStream_t s) {
+  int nch = ceil_div(h, kColChunk), ch0 = y0 / kColChunk, ch1 = ceil_div(y1, kColChunk);
+  if (h <= 1 || ch1 <= ch0) return;
+  dim3 cg(ceil_div(w, kColThreads), ch1 - ch0);
+  klaunch(dt_cols_agg<K>, cg, kColThreads, 0, s, guide, P, w, h, sigma_s / sigma_r, dt_pass_c(sigma_s, passes, i),
+          agg, ch0, nch);
+}
+
+template <int K>
+static void band_apply_k(const float* guide, const DtPlanes& P, int w, int h, int y0, int y1, double sigma_s,
+                         double sigma_r, int passes, int i, const double* agg, double* carry,
+                         const DtFlowOut& fo, cudaStream_t s) {
+  int nch = ceil_div(h, kColChunk), ch0 = y0 / kColChunk, ch1 = ceil_div(y1, kColChunk);
+  if (h <= 1 || ch1 <= ch0) return;
+  double ratio = sigma_s / sigma_r, c = dt_pass_c(sigma_s, passes, i);
+  klaunch(dt_cols_link<K>, ceil_div(w, 32), 1024, 0, s, w, nch, agg, carry);
+  dim3 cg(ceil_div(w, kColThreads), ch1 - ch0);
+  if (fo.flow && K == 3)
+    klaunch(dt_cols_apply<K, true>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, (const double*)carry, fo,
+            ch0, nch);
+  else
+    klaunch(dt_cols_apply<K, false>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, (const double*)carry, fo,
+            ch0, nch);
+}
+
+void launch_dt_band(int op, const float* guide, const DtPlanes& P, int w, int h, int y0, int y1,
+                    double sigma_s, double sigma_r, int passes, int i, double* agg, double* carry,
+                    const DtFlowOut* fo, cudaStream_t s) {
+  DtFlowOut none{nullptr, nullptr, 0.0, nullptr};
+  const DtFlowOut& f = fo ? *fo : none;
+  auto go = [&](auto kk) {
+    constexpr int K = decltype(kk)::value;
+    if (op == 0) band_rows_k<K>(guide, P, w, h, y0, y1, sigma_s, sigma_r, passes, i, s);
+    else if (op == 1) band_agg_k<K>(guide, P, w, h, y0, y1, sigma_s, sigma_r, passes, i, agg, s);
+    else band_apply_k<K>(guide, P, w, h, y0, y1, sigma_s, sigma_r, passes, i, agg, carry, f, s);
+  };
+  switch (P.k) {
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    default: go(std::integral_constant<int, 3>{}); break;
+  }
+}
+
 template <int K>
 static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sigma_s,
                         double sigma_r, int passes, double* scratch, const DtFlowOut& fo,
@@ -1166,13 +1256,13 @@ static bool dt_filter_k(const float* guide, DtPlanes P, int w, int h, double sig
         launch_cols_cluster<K, false>(guide, P, w, h, ratio, c, bl, fo, s, zr);
       }
     } else if (h > 1) {
-      klaunch(dt_cols_agg<K>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, agg);
+      klaunch(dt_cols_agg<K>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, agg, 0, nch);
       klaunch(dt_cols_link<K>, ceil_div(w, 32), 1024, 0, s, w, nch, agg, carry);
       if (i == passes && fo.flow && K == 3) {
-        klaunch(dt_cols_apply<K, true>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, carry, fo);
+        klaunch(dt_cols_apply<K, true>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, carry, fo, 0, nch);
         finalized = true;
       } else {
-        klaunch(dt_cols_apply<K, false>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, carry, fo);
+        klaunch(dt_cols_apply<K, false>, cg, kColThreads, 0, s, guide, P, w, h, ratio, c, carry, fo, 0, nch);
       }
     }
     if (h > 1) kprobe_mark(kc, 1, s);

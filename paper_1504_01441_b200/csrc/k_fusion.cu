@@ -98,7 +98,7 @@ template <int R>
 __global__ void ssim_fixed_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                   const uint8_t* __restrict__ qb, const float* __restrict__ lut_b,
                                   int w, int h, const double* __restrict__ taps,
-                                  float* __restrict__ out);
+                                  float* __restrict__ out, int ty0);
 
 void init_fusion_attributes() {
   allow_max_dynamic_smem(ssim_fixed_kernel<5>);
@@ -117,15 +117,16 @@ template <int R>
 __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     const float* __restrict__ a, const float* __restrict__ b, const uint8_t* __restrict__ qb,
     const float* __restrict__ lut_b, int w, int h, const double* __restrict__ taps,
-    float* __restrict__ out) {
+    float* __restrict__ out, int ty0) {
   pdl_wait();
   constexpr int E = kS2 + 2 * R;  // staged rows/cols incl. halo
+  const int by = ty0 + (int)blockIdx.y;  // tile row (ty0 > 0: a row band's tiles)
   __shared__ float sa[E][E + 1], sb[E][E + 1];
   __shared__ int rows[E], cols[E];
   __shared__ float lut[kBins];
   extern __shared__ double V[];  // [5][kS2][E]
   int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  int x0 = blockIdx.x * kS2 - R, y0 = blockIdx.y * kS2 - R;
+  int x0 = blockIdx.x * kS2 - R, y0 = by * kS2 - R;
   double k[2 * R + 1];
 #pragma unroll
   for (int j = 0; j <= 2 * R; ++j) k[j] = taps[j];
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
   // horizontal (axis 1): thread owns 4 consecutive outputs of one row
   const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
   int oy = tid >> 3, ox0 = (tid & 7) * 4;
-  int gy = blockIdx.y * kS2 + oy;
+  int gy = by * kS2 + oy;
   double m[5][4];
   // the 8 lanes of a row read 16-byte chunks 32 bytes apart (two lanes per
   // bank group); lanes 4-7 fetch their chunks rotated by one, so most steps
@@ -239,13 +240,26 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
   }
 }
 
+// rows [y0, y1) of the SSIM map (y0 a multiple of 32; radius 5 only): a row
+// band's tiles
+bool launch_ssim_rows(const float* a, const uint8_t* qb, const float* lut_b, int w, int h, int y0, int y1,
+                      int window, const double* taps, float* out, cudaStream_t s) {
+  if (window / 2 != 5 || y0 % kS2) return false;
+  if (y1 <= y0) return true;
+  size_t vb = 5 * (size_t)kS2 * (kS2 + 10) * sizeof(double);
+  dim3 grd(ceil_div(w, kS2), ceil_div(y1, kS2) - y0 / kS2);
+  klaunch(ssim_fixed_kernel<5>, grd, dim3(32, 8), vb, s, a, (const float*)nullptr, qb, lut_b, w, h, taps, out,
+          y0 / kS2);
+  return true;
+}
+
 void launch_ssim(const float* a, const float* b_or_null, const uint8_t* qb, const float* lut_b,
                  int w, int h, int window, const double* taps, float* out, cudaStream_t s) {
   int r = window / 2;
   if (r == 5) {
     size_t vb = 5 * (size_t)kS2 * (kS2 + 10) * sizeof(double);
     dim3 grd(ceil_div(w, kS2), ceil_div(h, kS2));
-    klaunch(ssim_fixed_kernel<5>, grd, dim3(32, 8), vb, s, a, b_or_null, qb, lut_b, w, h, taps, out);
+    klaunch(ssim_fixed_kernel<5>, grd, dim3(32, 8), vb, s, a, b_or_null, qb, lut_b, w, h, taps, out, 0);
     return;
   }
   int EW = kSsimTW + 2 * r, EH = kSsimTH + 2 * r;

@@ -61,3 +61,20 @@ def test_shard_sizes():
             parts = [shard(n, world, r) for r in range(world)]
             assert sum(len(p) for p in parts) == n
             assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+
+
+def test_band_rows_partition():
+    """banded.py's row bands: contiguous, whole 32-row blocks, balanced."""
+    from paper_1504_01441_b200.banded import band_rows
+    for h in (100, 480, 481, 1944, 3000):
+        for world in (1, 2, 3, 5, 8):
+            bands = [band_rows(h, world, r, 32) for r in range(world)]
+            assert bands[0][0] == 0 and bands[-1][1] == h
+            for (a0, a1), (b0, b1) in zip(bands, bands[1:]):
+                assert a1 == b0 and a0 % 32 == 0
+            sizes = [b - a for a, b in bands]
+            # full bands, then at most one partial band, then empty ones
+            full = max(sizes)
+            assert sizes == sorted(sizes, reverse=True)
+            assert full % 32 == 0 or world == 1 or full == h
+            assert sum(0 < sz < full for sz in sizes) <= 1

@@ -6,8 +6,6 @@
 // for the tile count (the maximum number of corners) and idle blocks exit,
 // so the coarse-to-fine chain of matcher.pyramidal_match (matcher.py:221-263)
 // runs without a host round trip and can be captured in one CUDA graph.
-#include <cstdio>
-
 #include "hdr_common.cuh"
 #include "hdr_geom.cuh"
 #include "hdr_warpfit.cuh"
@@ -424,13 +422,6 @@ __device__ __forceinline__ double dlt_entry(int r, int k, double px, double py, 
 }
 // Block-wide least-squares DLT (geometry.fit_homography for n >= 4) over
 // points fetched by `get(i, p)` (p = ref x, ref y, src x, src y).
-#ifdef HDR_FL_TRACE
-__device__ __forceinline__ long long fl_clk() { return clock64(); }
-__shared__ long long fl_ts[8];
-#define FLT(i) do { if (threadIdx.x == 0) fl_ts[i] = fl_clk(); } while (0)
-#else
-#define FLT(i) do {} while (0)
-#endif
 template <class Get>
 __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
 
@@ -480,7 +471,6 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     }
   }
   __syncthreads();
-  FLT(1);
   // mean distances to the centroids
   double md[2] = {0, 0};
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -510,7 +500,6 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
   }
   __syncthreads();
   if (status) return status;
-  FLT(2);
   // Gram matrix of the conditioned DLT rows. With p~ = (px, py, 1), rows are
   // r0 = [-p~, 0, qx p~], r1 = [0, -p~, qy p~], so G is assembled from 24 sums
   // S_w = sum w p~ p~^T (6 unique entries each) for w in {1, qx, qy, qx^2+qy^2}.
@@ -561,13 +550,11 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     int k = 0;
     for (int i = 0; i < 9; ++i)
       for (int j = i; j < 9; ++j) g45s[k++] = G[i][j];
-    FLT(3);
     int g = 0;
     status = fit_from_gram(g45s, tr, ts, H, &g);
     if (g && grey) atomicAdd(grey, g);
   }
   __syncthreads();
-  FLT(4);
   return status;
 }
 
@@ -581,7 +568,6 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     double* __restrict__ hpred, double* __restrict__ homography, int32_t* __restrict__ info,
     double* __restrict__ out_matches, double* __restrict__ out_raw, int32_t* grey) {
   pdl_wait();
-  FLT(5);
   extern __shared__ double pts_cache[];  // normalised (rx, ry, sx, sy) of the weeded set
   __shared__ int scratch[32];
   int n = *raw_count;
@@ -628,13 +614,8 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     }
   };
   __syncthreads();  // weeded rows / cached points visible block-wide
-  FLT(0);
   int st = block_fit(m, get, Hs, grey);
-#ifdef HDR_FL_TRACE
-  if (threadIdx.x == 0)
-    printf("FLT level %d n=%d m=%d compact %lld centroid %lld md %lld gram %lld solve %lld\n", level, n, m,
-           fl_ts[0] - fl_ts[5], fl_ts[1] - fl_ts[0], fl_ts[2] - fl_ts[1], fl_ts[3] - fl_ts[2], fl_ts[4] - fl_ts[3]);
-#endif
+
   if (threadIdx.x == 0 && st == 0) {
     for (int k = 0; k < 9; ++k) hpred[k] = Hs[k];
     if (level == 0 && homography) {

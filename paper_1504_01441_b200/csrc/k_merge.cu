@@ -246,14 +246,19 @@ __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_
 }
 
 // ---------------------------------------------------------------- levels >= 1
+// 4 channels per CTA (blockIdx.z picks the group of the level's 4 NF
+// channels): 31 KB of shared memory, so 7 CTAs fit per SM where the 8-channel
+// tile (52 KB) fitted 4
 template <int NF>
-constexpr size_t down_smem() { return sizeof(float) * (4 * NF * kRT * kRP + 4 * kOT * kVP); }
+constexpr size_t down_smem() { return sizeof(float) * (4 * kRT * kRP + 4 * kOT * kVP); }
 
 template <int NF>
 __global__ void __launch_bounds__(256) down_kernel(const float* __restrict__ in, int w, int h,
                                                    float* __restrict__ out, int ow, int oh) {
   pdl_wait();
-  constexpr int NC = 4 * NF;
+  constexpr int NC = 4;
+  in += (int64_t)blockIdx.z * NC * w * h;
+  out += (int64_t)blockIdx.z * NC * ow * oh;
   extern __shared__ float smd[];
   float* tile = smd;                // [NC][36][37]
   float* V = smd + NC * kRT * kRP;  // [4][16][37]
@@ -557,7 +562,7 @@ static void launch_fuse_nf(const FuseFrames<NF>& fr, const FusePyramid& py, cuda
     return;
   }
   for (int k = 1; k + 1 < L; ++k) {
-    dim3 gk(ceil_div(d[k + 1].w, kOT), ceil_div(d[k + 1].h, kOT));
+    dim3 gk(ceil_div(d[k + 1].w, kOT), ceil_div(d[k + 1].h, kOT), NF);
     klaunch(down_kernel<NF>, gk, dim3(256), down_smem<NF>(), s, (const float*)py.g[k], d[k].w, d[k].h,
             py.g[k + 1], d[k + 1].w, d[k + 1].h);
   }

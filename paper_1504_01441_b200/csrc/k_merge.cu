@@ -119,7 +119,7 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
 }
 
 #ifndef HDR_W0_MIN_BLOCKS
-#define HDR_W0_MIN_BLOCKS 4
+#define HDR_W0_MIN_BLOCKS 3
 #endif
 template <int NF>
 __global__ void __launch_bounds__(256, NF == 2 ? HDR_W0_MIN_BLOCKS : 2) weights_down_kernel(FuseFrames<NF> fr, int w, int h,

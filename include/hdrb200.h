@@ -349,8 +349,10 @@ int32_t hdr_band_rows_multiple(void);
 /* doubles of the dt_filter chunk-aggregate buffer for (w, h) and k planes */
 int64_t hdr_band_agg_doubles(int32_t width, int32_t height, int32_t k);
 /* op 0: the band's row sweeps of pass pass_i; op 1: its column-chunk
- * aggregates into agg (whole-image layout, caller-zeroed; sum over ranks
- * next); op 2: link the summed agg and re-run the band's chunks, writing the
+ * aggregates into agg (chunk-major: chunk c's aggregates are the
+ * hdr_band_agg_doubles(width, 16, k) doubles at c times that offset, so a
+ * band's chunks form one block; gather the blocks over the ranks next);
+ * op 2: link the whole agg and re-run the band's chunks, writing the
  * planes -- or, when flow != NULL (last pass, k = 3), the f32 flow with the
  * homography fallback below `floor_` (fallback/has_fb as hdr_densify_finalize). */
 int hdr_band_dt(hdr_ctx* ctx, int32_t op, const float* guide, double* planes, int32_t k, int32_t width,

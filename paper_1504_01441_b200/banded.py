@@ -11,9 +11,8 @@ through the host):
   and homography without a collective;
 * the domain-transform filter (densify.py:78-113) is split by row bands of
   whole 16-row chunks: each rank sweeps its rows and aggregates its column
-  chunks; the chunk aggregates are summed over the ranks (all-reduce: the
-  bands are disjoint, so the sum is their union, bit for bit), and each rank
-  links them and re-runs its own chunks -- the carries of the column
+  chunks; the chunk aggregates (chunk-major, so a band's are one block) are
+  all-gathered, and each rank links them and re-runs its own chunks -- the carries of the column
   recursion crossing the bands (densify.py:69-75). The last pass writes the
   band's f32 flow (densify_flow, densify.py:134-142);
 * the flow is all-gathered (every rank needs the rows above and below its
@@ -83,6 +82,20 @@ def _allreduce_sum(t: torch.Tensor, group, backend) -> None:
     t.copy_(h)
 
 
+def _gather_blocks(t: torch.Tensor, rank: int, n: int, group, backend) -> None:
+    """Every rank's block [rank * n, (rank + 1) * n) of the flat t into every
+    rank's t (NCCL all-gather in place; other backends sum zero-padded copies
+    through the host)."""
+    if backend is None:
+        return
+    if backend == "nccl":
+        dist.all_gather_into_tensor(t, t[rank * n:(rank + 1) * n].clone(), group=group)
+        return
+    t[:rank * n].zero_()
+    t[(rank + 1) * n:].zero_()
+    _allreduce_sum(t, group, backend)
+
+
 def _gather_rows(t: torch.Tensor, rank: int, band: int, group, backend) -> None:
     """Every rank's band rows of t (rows padded to world * band) into every
     rank's t: NCCL all-gather in place; other backends sum zero-padded
@@ -134,8 +147,12 @@ def register_and_fuse_banded(ref, src, params: PipelineParams | None = None, gro
     band = band_size(h, world)
     y0, y1 = band_rows(h, world, rank)
     hp = band * world  # rows of the gathered (padded) outputs
-    # densify_flow: rows and column chunks of the band, aggregates summed
-    agg = torch.empty(int(lib.hdr_band_agg_doubles(w, h, 3)), dtype=torch.float64, **kw)
+    # densify_flow: rows and column chunks of the band, aggregates gathered
+    # chunk aggregates, chunk-major: a band's chunks are one block, padded to
+    # `world` equal blocks so they move by all-gather
+    chunk = int(lib.hdr_band_agg_doubles(w, 16, 3))  # doubles per 16-row chunk
+    per_band = band // 16 * chunk
+    agg = torch.zeros(max(int(lib.hdr_band_agg_doubles(w, h, 3)), world * per_band), dtype=torch.float64, **kw)
     flow_p = torch.zeros((hp, w, 2), dtype=torch.float32, **kw)
     flow = flow_p[:h]
     has_fb = ctypes.c_void_p(bufs.info.data_ptr() + 4)  # info[1]: the homography exists
@@ -147,9 +164,8 @@ def register_and_fuse_banded(ref, src, params: PipelineParams | None = None, gro
 
     for i in range(1, params.passes + 1):
         band_dt(0, i)                                    # the band's row sweeps
-        agg.zero_()
         band_dt(1, i, ptr(agg))                          # its column-chunk aggregates
-        _allreduce_sum(agg, group, backend)              # the carries' inputs from every band
+        _gather_blocks(agg, rank, per_band, group, backend)  # the carries' inputs from every band
         last = i == params.passes
         band_dt(2, i, ptr(agg), ptr(bufs.homography), has_fb, float(params.normalization_floor),
                 ptr(flow) if last else None)             # link + the band's chunks (flow on the last pass)

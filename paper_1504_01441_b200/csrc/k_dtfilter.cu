@@ -506,7 +506,7 @@ __device__ __forceinline__ void load_chunk(const float* __restrict__ guide, cons
   }
 }
 
-// Aggregates, field-major agg[f][chunk][col], f = A, Q, R, B[K], Z0[K]:
+// Aggregates, chunk-major agg[chunk][f][col], f = A, Q, R, B[K], Z0[K]:
 // forward zero-carry map y_end = A*C + B, and z_start = Z0 + C*R + Q*D.
 // ch0: first chunk of the launch (a row band's chunks; 0 for the whole
 // image), nch: chunks of the whole image (the agg layout)
@@ -539,12 +539,13 @@ __global__ void __launch_bounds__(kColThreads) dt_cols_agg(const float* __restri
       pref *= an;
     }
   }
-  int64_t F = (int64_t)nch * w, o = (int64_t)ch * w + x;
-  agg[o] = Pp;
-  agg[F + o] = pref;
-  agg[2 * F + o] = R;
+  // chunk-major: a run of chunks (a row band) is one contiguous block
+  double* a = agg + (int64_t)ch * (3 + 2 * K) * w + x;
+  a[0] = Pp;
+  a[w] = pref;
+  a[2 * w] = R;
 #pragma unroll
-  for (int k = 0; k < K; ++k) { agg[(3 + k) * F + o] = y0[k]; agg[(3 + K + k) * F + o] = z0[k]; }
+  for (int k = 0; k < K; ++k) { a[(3 + k) * w] = y0[k]; a[(3 + K + k) * w] = z0[k]; }
 }
 
 // Carry chains. A block owns 32 columns; thread (cx, g) composes the affine
@@ -563,6 +564,8 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
   int x = blockIdx.x * 32 + cx;
   bool live = x < w;
   int64_t F = (int64_t)nch * w;
+  // agg[chunk][field][col] (chunk-major, see dt_cols_agg)
+  auto AG = [&](int f, int b) { return ((int64_t)b * (3 + 2 * K) + f) * w + x; };
   int per = (nch + kLinkGroups - 1) / kLinkGroups;
   int b0 = min(nch, g * per), b1 = min(nch, b0 + per);
   // ---- forward: y_end(b) = A_b C_b + B_b
@@ -574,9 +577,9 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
     for (int b = b0; b < b1; ++b) {
       int64_t o = (int64_t)b * w + x;
       Aff<K> t;
-      t.A = agg[o];
+      t.A = agg[AG(0, b)];
 #pragma unroll
-      for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + k) * F + o];
+      for (int k = 0; k < K; ++k) t.B[k] = agg[AG(3 + k, b)];
       m = compose(m, t);
     }
   maps[g][cx] = m;
@@ -593,11 +596,11 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
   if (live)
     for (int b = b0; b < b1; ++b) {
       int64_t o = (int64_t)b * w + x;
-      double A = agg[o];
+      double A = agg[AG(0, b)];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         carry[k * F + o] = C[k];
-        C[k] = A * C[k] + agg[(3 + k) * F + o];
+        C[k] = A * C[k] + agg[AG(3 + k, b)];
       }
     }
   __syncthreads();
@@ -609,10 +612,10 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
     for (int b = b1 - 1; b >= b0; --b) {
       int64_t o = (int64_t)b * w + x;
       Aff<K> t;
-      t.A = agg[F + o];
-      double Rb = agg[2 * F + o];
+      t.A = agg[AG(1, b)];
+      double Rb = agg[AG(2, b)];
 #pragma unroll
-      for (int k = 0; k < K; ++k) t.B[k] = agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
+      for (int k = 0; k < K; ++k) t.B[k] = agg[AG(3 + K + k, b)] + carry[k * F + o] * Rb;
       m = compose(m, t);
     }
   maps[g][cx] = m;
@@ -629,11 +632,11 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
   if (live)
     for (int b = b1 - 1; b >= b0; --b) {
       int64_t o = (int64_t)b * w + x;
-      double Q = agg[F + o], Rb = agg[2 * F + o];
+      double Q = agg[AG(1, b)], Rb = agg[AG(2, b)];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         carry[(K + k) * F + o] = D[k];
-        D[k] = Q * D[k] + agg[(3 + K + k) * F + o] + carry[k * F + o] * Rb;
+        D[k] = Q * D[k] + agg[AG(3 + K + k, b)] + carry[k * F + o] * Rb;
       }
     }
 }

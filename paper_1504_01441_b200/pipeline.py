@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .engine import device_of, engine, is_torch, out, ptr, to_dev
+from .engine import device_of, engine, is_torch, out, ptr, to_dev, to_host
 from .errors import ConfigError, RegistrationError
 
 PYRAMID_MAX_LEVELS = 5
@@ -188,16 +188,14 @@ def _collect(bufs: PairBuffers, as_torch: bool, composite: bool = True) -> Regis
     if info[0] == _native.HDR_ERR_REGISTRATION:
         raise RegistrationError(f"only {m} reliable matches at full resolution")
     hom = bufs.homography if info[1] else None
-    return RegistrationOutput(
-        composite=out(bufs.composite, as_torch) if composite else None,
-        flow=out(bufs.flow, as_torch),
-        warped=out(bufs.warped, as_torch),
-        valid=out(bufs.valid.bool(), as_torch),
-        ssim=out(bufs.ssim.double(), as_torch),
-        matches=out(bufs.matches[:m].clone(), as_torch),
-        raw_matches=out(bufs.raw_matches[:n].clone(), as_torch),
-        homography=None if hom is None else out(hom.clone(), as_torch),
-        level_counts=_level_counts(info))
+    fields = {"composite": bufs.composite if composite else None, "flow": bufs.flow,
+              "warped": bufs.warped, "valid": bufs.valid.bool(), "ssim": bufs.ssim.double(),
+              "matches": bufs.matches[:m].clone(), "raw_matches": bufs.raw_matches[:n].clone(),
+              "homography": None if hom is None else hom.clone()}
+    if not as_torch:  # every D2H issued before the one synchronisation
+        live = [k for k, v in fields.items() if v is not None]
+        fields.update(zip(live, to_host(*(fields[k] for k in live))))
+    return RegistrationOutput(level_counts=_level_counts(info), **fields)
 
 
 def match_stack(ref, src, params: PipelineParams):

@@ -941,12 +941,12 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
     launch_ssd_tiles(tiles_level(c, d, l, p->tile), nt, lref[l], lsrc[l], d[l].w, d[l].h,
                      c->hpred, p->radius, p->patch, c->slot_rows, c->slot_flags, s);
     launch_compact_rows(c->slot_rows, c->slot_flags, nt, c->raw, raw_count,
-                        l == 0 ? out_raw : nullptr, s);
+                        l == 0 ? out_raw : nullptr, s, c->mask, c->witness);
     int iters = l == 0 ? p->iterations : p->coarse_iterations;
     double eps = 2.0 * p->eps_px / (double)d[l].w;  // MatcherParams.weed_params
     launch_weed(c->raw, raw_count, nt, d[l].w, d[l].h, iters, eps,
                 c->keyset->keys + 2 * (size_t)c->keyset->iters * l, p->delta, c->keyset->fits, c->mask, c->witness,
-                grey, s);
+                grey, s, true);
     launch_finish_level(c->raw, raw_count, c->mask, d[l].w, d[l].h, l, c->weeded, weeded_count,
                         nullptr, c->hpred, out_h, info, l == 0 ? out_matches : nullptr, nullptr,
                         grey, s);

@@ -92,13 +92,15 @@ void launch_ssd_tiles(const TileCorner* tiles, int ntiles, const float* ref,
 void launch_ssd_points(const float* ref, const float* src, int w, int h,
                        const int32_t* pts, int n, int radius, int patch, double* out,
                        uint8_t* found, cudaStream_t s);
+// mask / witness: when given, the weeding arrays for nslots rows are cleared
+// too (launch_weed(..., cleared = true) then skips its memsets)
 void launch_compact_rows(const MatchRow* rows, const uint8_t* flags, int nslots,
                          MatchRow* out, int32_t* count, double* out_copy,
-                         cudaStream_t s);
+                         cudaStream_t s, uint32_t* mask = nullptr, int32_t* witness = nullptr);
 void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w,
                  int h, int iterations, double eps, const uint64_t* keys, int delta,
                  double* fit_scratch, uint32_t* mask, int32_t* witness,
-                 int32_t* grey, cudaStream_t s);
+                 int32_t* grey, cudaStream_t s, bool cleared = false);
 // compaction of the weeded set + least-squares H (+ level bookkeeping)
 void launch_finish_level(const MatchRow* raw, const int32_t* raw_count,
                          const uint32_t* mask, int w, int h, int level,

@@ -253,12 +253,21 @@ void launch_ssd_points(const float* ref, const float* src, int w, int h, const i
 
 // ordered compaction of per-slot rows (tile order is the reference's corner
 // order, matcher.py:97-104 -> :187)
+// mask / witness (may be null): the weeding arrays of the n rows that follow,
+// cleared here so the pair needs no memset node between this kernel and
+// weed_fit (a memset would also break the programmatic launch chain)
 __global__ void __launch_bounds__(1024) compact_rows_kernel(const MatchRow* __restrict__ rows,
                                                             const uint8_t* __restrict__ flags,
                                                             int nslots, MatchRow* __restrict__ out,
                                                             int32_t* __restrict__ count,
-                                                            double* __restrict__ out_copy) {
+                                                            double* __restrict__ out_copy,
+                                                            uint32_t* __restrict__ mask,
+                                                            int32_t* __restrict__ witness) {
   pdl_wait();
+  if (mask) {
+    for (int i = threadIdx.x; i < (nslots + 31) / 32 + 1; i += blockDim.x) mask[i] = 0u;
+    for (int i = threadIdx.x; i < nslots + 1; i += blockDim.x) witness[i] = 0;
+  }
   __shared__ int scratch[32];
   int base = 0;
   for (int c0 = 0; c0 < nslots; c0 += blockDim.x) {
@@ -278,8 +287,9 @@ __global__ void __launch_bounds__(1024) compact_rows_kernel(const MatchRow* __re
 }
 
 void launch_compact_rows(const MatchRow* rows, const uint8_t* flags, int nslots, MatchRow* out,
-                         int32_t* count, double* out_copy, cudaStream_t s) {
-  klaunch(compact_rows_kernel, 1, 1024, 0, s, rows, flags, nslots, out, count, out_copy);
+                         int32_t* count, double* out_copy, cudaStream_t s, uint32_t* mask,
+                         int32_t* witness) {
+  klaunch(compact_rows_kernel, 1, 1024, 0, s, rows, flags, nslots, out, count, out_copy, mask, witness);
 }
 
 // ---------------------------------------------------------------- K7
@@ -395,9 +405,11 @@ __global__ void __launch_bounds__(256) weed_count_kernel(const MatchRow* __restr
 void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w, int h,
                  int iterations, double eps, const uint64_t* keys, int delta,
                  double* fit_scratch, uint32_t* mask, int32_t* witness, int32_t* grey,
-                 cudaStream_t s) {
-  cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((n_static + 31) / 32 + 1), s);
-  cudaMemsetAsync(witness, 0, sizeof(int32_t) * (n_static + 1), s);
+                 cudaStream_t s, bool cleared) {
+  if (!cleared) {
+    cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((n_static + 31) / 32 + 1), s);
+    cudaMemsetAsync(witness, 0, sizeof(int32_t) * (n_static + 1), s);
+  }
   klaunch(weed_fit_kernel, ceil_div(iterations, kFitWarps), 32 * kFitWarps, 0, s, rows, count, w, h, iterations, keys,
                                                           fit_scratch, grey);
   klaunch(weed_count_kernel, iterations, 256, 0, s, rows, count, w, h, eps, delta, fit_scratch, mask,

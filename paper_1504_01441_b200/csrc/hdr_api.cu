@@ -867,10 +867,21 @@ static DtPlanes pair_planes(hdr_ctx* c, int64_t P) {
 }
 
 // ------------------------------------------------------------ kernels used by the pipeline only
-__global__ void info_init_kernel(int32_t* info, int levels) {
+// The pair's first kernel: info words, and the per-pair accumulators
+// (histograms, counters, the exactness certificate's per-level min/sum)
+// cleared here rather than by memset nodes, which would break the
+// programmatic launch chain.
+__global__ void info_init_kernel(int32_t* info, int levels, uint32_t* hist, int32_t* counters,
+                                 int32_t* stats_q, double* stats_s) {
   pdl_wait();
   int i = threadIdx.x;
   if (i < HDR_INFO_WORDS) info[i] = (i == 2) ? levels : 0;
+  for (int j = i; j < 4 * kBins; j += blockDim.x) hist[j] = 0u;
+  if (i < 16) counters[i] = 0;
+  if (i < 5) {
+    stats_q[i] = 0x3f3f3f3f;  // large positive: atomicMin identity
+    stats_s[i] = 0.0;
+  }
 }
 
 __global__ void status_kernel(const int32_t* weeded_count, int32_t* info) {
@@ -898,9 +909,7 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
   Dims d[kMaxLevels];
   int L = pyramid_dims(w, h, p->max_levels, d);
   probe(c, 0, 0);
-  klaunch(info_init_kernel, 1, 32, 0, s, info, L);
-  CUDA_TRY(cudaMemsetAsync(c->hist, 0, sizeof(uint32_t) * 4 * kBins, s));
-  CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(int32_t) * 16, s));
+  klaunch(info_init_kernel, 1, 256, 0, s, info, L, c->hist, c->counters, c->stats_q, c->stats_s);
   launch_luma_hist(ref, P, c->lum_ref, nullptr, c->hist, s);
   launch_luma_hist(src, P, nullptr, c->q_src, c->hist + kBins, s);
   launch_lut(c->hist + kBins, P, c->hist, P, c->lut, s);
@@ -926,7 +935,7 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
     int rc = sat_batch(c, L, lref, d, p->tile, p->quadrant_half, false, tl, nullptr, &sb, &mw, &mr, &nt);
     if (rc) return rc;
     int maxpx = d[0].w * d[0].h;
-    launch_level_stats(sb, maxpx, s);
+    launch_level_stats(sb, maxpx, s, true);
     launch_sat(sb, mw, mr, s);
     launch_detect(sb, nt, detect_params(p->tile, p->quadrant_half, p->threshold), s);
   }

@@ -76,7 +76,8 @@ struct DetectParams {
   double threshold;
   int exact_ok;    // tile region fits the tile-local kernel's shared memory
 };
-void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s);
+// precleared: sums = 0 and qmin = 0x3f3f3f3f already (the pair's first kernel)
+void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s, bool precleared = false);
 void launch_sat(const SatBatch& b, int max_w, int max_rows, cudaStream_t s);
 void launch_detect(const SatBatch& b, int total_tiles, const DetectParams& dp, cudaStream_t s);
 size_t detect_exact_smem(int tile, int half);

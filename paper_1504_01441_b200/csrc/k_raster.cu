@@ -304,9 +304,11 @@ __global__ void __launch_bounds__(256) level_stats_kernel(SatBatch b) {
   }
 }
 
-void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s) {
-  cudaMemsetAsync(b.sums, 0, sizeof(double) * 5, s);
-  cudaMemsetAsync(b.qmin, 0x3f, sizeof(int32_t) * 5, s);  // large positive
+void launch_level_stats(const SatBatch& b, int max_pixels, cudaStream_t s, bool precleared) {
+  if (!precleared) {
+    cudaMemsetAsync(b.sums, 0, sizeof(double) * 5, s);
+    cudaMemsetAsync(b.qmin, 0x3f, sizeof(int32_t) * 5, s);  // large positive
+  }
   // two blocks per SM per level: each thread streams its share in steps of
   // eight independent loads, and a level costs only ~300 same-address atomics
   int bx = std::min(grid_for(max_pixels, 256), 148 * 2);

@@ -872,10 +872,11 @@ static DtPlanes pair_planes(hdr_ctx* c, int64_t P) {
 // cleared here rather than by memset nodes, which would break the
 // programmatic launch chain.
 __global__ void info_init_kernel(int32_t* info, int levels, uint32_t* hist, int32_t* counters,
-                                 int32_t* stats_q, double* stats_s) {
+                                 int32_t* stats_q, double* stats_s, double* hpred) {
   pdl_wait();
   int i = threadIdx.x;
   if (i < HDR_INFO_WORDS) info[i] = (i == 2) ? levels : 0;
+  if (i < 9) hpred[i] = (i % 4 == 0) ? 1.0 : 0.0;  // the coarsest level predicts with identity
   for (int j = i; j < 4 * kBins; j += blockDim.x) hist[j] = 0u;
   if (i < 16) counters[i] = 0;
   if (i < 5) {
@@ -884,14 +885,13 @@ __global__ void info_init_kernel(int32_t* info, int levels, uint32_t* hist, int3
   }
 }
 
-__global__ void status_kernel(const int32_t* weeded_count, int32_t* info) {
+// the registration verdict (pipeline.py:185-187) and the grey-zone count
+__global__ void status_kernel(const int32_t* weeded_count, int32_t* info, const int32_t* grey) {
   pdl_wait();
-  if (threadIdx.x == 0) info[0] = (*weeded_count >= 4) ? HDR_OK : HDR_ERR_REGISTRATION;
-}
-
-__global__ void copy_i32_kernel(const int32_t* src, int32_t* dst) {
-  pdl_wait();
-  if (threadIdx.x == 0) *dst = *src;
+  if (threadIdx.x == 0) {
+    info[0] = (*weeded_count >= 4) ? HDR_OK : HDR_ERR_REGISTRATION;
+    info[18] = *grey;
+  }
 }
 
 static int check_ptr_align(const void* p, size_t a, const char* what) {
@@ -909,7 +909,7 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
   Dims d[kMaxLevels];
   int L = pyramid_dims(w, h, p->max_levels, d);
   probe(c, 0, 0);
-  klaunch(info_init_kernel, 1, 256, 0, s, info, L, c->hist, c->counters, c->stats_q, c->stats_s);
+  klaunch(info_init_kernel, 1, 256, 0, s, info, L, c->hist, c->counters, c->stats_q, c->stats_s, c->hpred);
   launch_luma_hist(ref, P, c->lum_ref, nullptr, c->hist, s);
   launch_luma_hist(src, P, nullptr, c->q_src, c->hist + kBins, s);
   launch_lut(c->hist + kBins, P, c->hist, P, c->lut, s);
@@ -941,7 +941,6 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
   }
   probe(c, 1, 1);
   probe(c, 2, 0);
-  launch_set_identity(c->hpred, s);
   int32_t* raw_count = c->counters + 0;
   int32_t* weeded_count = c->counters + 1;
   int32_t* grey = c->counters + 3;
@@ -960,8 +959,7 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
                         nullptr, c->hpred, out_h, info, l == 0 ? out_matches : nullptr, nullptr,
                         grey, s);
   }
-  klaunch(status_kernel, 1, 32, 0, s, weeded_count, info);
-  klaunch(copy_i32_kernel, 1, 32, 0, s, grey, info + 18);
+  klaunch(status_kernel, 1, 32, 0, s, weeded_count, info, (const int32_t*)grey);
   probe(c, 2, 1);
   return check_launch();
 }

@@ -362,7 +362,6 @@ struct GraphEntry {
 
 struct KeySet {
   uint64_t* keys = nullptr;     // kMaxLevels x iters x 2
-  double* fits = nullptr;       // iters x 20
   int iters = 0;
 };
 
@@ -476,7 +475,6 @@ extern "C" int hdr_ctx_destroy(hdr_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   for (auto& kv : c->keysets) {
     cudaFree(kv.second.keys);
-    cudaFree(kv.second.fits);
   }
   for (auto& kv : c->tapsets) cudaFree(kv.second);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -672,26 +670,20 @@ static int ensure_keys(hdr_ctx* c, const hdr_params* p) {
     c->keyset = &it->second;
     return HDR_OK;
   }
-  int rc = evict_if_full(c, c->keysets, [](KeySet& k) { cudaFree(k.keys); cudaFree(k.fits); });
+  int rc = evict_if_full(c, c->keysets, [](KeySet& k) { cudaFree(k.keys); });
   if (rc) return rc;
   KeySet ks;
   ks.iters = std::max(p->iterations, p->coarse_iterations);
   CUDA_TRY(cudaMalloc(&ks.keys, sizeof(uint64_t) * 2 * (size_t)ks.iters * kMaxLevels));
-  cudaError_t e = cudaMalloc(&ks.fits, sizeof(double) * 20 * (size_t)ks.iters);
-  if (e != cudaSuccess) {
-    cudaFree(ks.keys);
-    return fail(HDR_ERR_CUDA, std::string("key set: ") + cudaGetErrorString(e));
-  }
   std::vector<uint64_t> host(2 * (size_t)ks.iters * kMaxLevels, 0);
   for (int l = 0; l < kMaxLevels; ++l) {
     int n = l == 0 ? p->iterations : p->coarse_iterations;
     hdr_iteration_keys(hdr_level_seed(p->seed, l), n, host.data() + 2 * (size_t)ks.iters * l);
   }
   // a fresh buffer no queued work reads: a plain blocking upload suffices
-  e = cudaMemcpy(ks.keys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMemcpy(ks.keys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(ks.keys);
-    cudaFree(ks.fits);
     return fail(HDR_ERR_CUDA, std::string("key upload: ") + cudaGetErrorString(e));
   }
   c->keyset = &(c->keysets[key] = ks);
@@ -953,8 +945,8 @@ static int enqueue_match(hdr_ctx* c, const hdr_params* p, int w, int h, const fl
     int iters = l == 0 ? p->iterations : p->coarse_iterations;
     double eps = 2.0 * p->eps_px / (double)d[l].w;  // MatcherParams.weed_params
     launch_weed(c->raw, raw_count, nt, d[l].w, d[l].h, iters, eps,
-                c->keyset->keys + 2 * (size_t)c->keyset->iters * l, p->delta, c->keyset->fits, c->mask, c->witness,
-                grey, s, true);
+                c->keyset->keys + 2 * (size_t)c->keyset->iters * l, p->delta, c->mask, c->witness, grey, s,
+                true);
     launch_finish_level(c->raw, raw_count, c->mask, d[l].w, d[l].h, l, c->weeded, weeded_count,
                         nullptr, c->hpred, out_h, info, l == 0 ? out_matches : nullptr, nullptr,
                         grey, s);
@@ -1414,17 +1406,14 @@ extern "C" int hdr_weed(hdr_ctx* c, const double* matches, int32_t n, int32_t w,
   std::vector<uint64_t> host(2 * (size_t)iterations);
   hdr_iteration_keys(seed, iterations, host.data());
   uint64_t* dkeys = nullptr;
-  double* dfits = nullptr;
   CUDA_TRY(cudaMallocAsync(&dkeys, host.size() * sizeof(uint64_t), s));
-  CUDA_TRY(cudaMallocAsync(&dfits, sizeof(double) * 20 * (size_t)iterations, s));
   CUDA_TRY(cudaMemcpyAsync(dkeys, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   klaunch(rows_from_matrix_kernel, ceil_div(n, 256), 256, 0, s, matches, n, c->raw, c->counters + 0);
-  launch_weed(c->raw, c->counters + 0, n, w, h, iterations, eps, dkeys, delta, dfits, c->mask,
-              c->witness, c->counters + 3, s);
+  launch_weed(c->raw, c->counters + 0, n, w, h, iterations, eps, dkeys, delta, c->mask, c->witness,
+              c->counters + 3, s);
   klaunch(widen_kept_kernel, 1, 1024, 0, s, c->mask, c->witness, n, kept, c->counters + 6, witness);
   CUDA_TRY(cudaMemcpyAsync(n_kept, c->counters + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaFreeAsync(dkeys, s));
-  CUDA_TRY(cudaFreeAsync(dfits, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return check_launch();
 }

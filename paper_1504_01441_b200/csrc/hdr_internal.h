@@ -100,8 +100,8 @@ void launch_compact_rows(const MatchRow* rows, const uint8_t* flags, int nslots,
                          cudaStream_t s, uint32_t* mask = nullptr, int32_t* witness = nullptr);
 void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w,
                  int h, int iterations, double eps, const uint64_t* keys, int delta,
-                 double* fit_scratch, uint32_t* mask, int32_t* witness,
-                 int32_t* grey, cudaStream_t s, bool cleared = false);
+                 uint32_t* mask, int32_t* witness, int32_t* grey, cudaStream_t s,
+                 bool cleared = false);
 // compaction of the weeded set + least-squares H (+ level bookkeeping)
 void launch_finish_level(const MatchRow* raw, const int32_t* raw_count,
                          const uint32_t* mask, int w, int h, int level,

@@ -255,7 +255,7 @@ void launch_ssd_points(const float* ref, const float* src, int w, int h, const i
 // order, matcher.py:97-104 -> :187)
 // mask / witness (may be null): the weeding arrays of the n rows that follow,
 // cleared here so the pair needs no memset node between this kernel and
-// weed_fit (a memset would also break the programmatic launch chain)
+// weed_kernel (a memset would also break the programmatic launch chain)
 __global__ void __launch_bounds__(1024) compact_rows_kernel(const MatchRow* __restrict__ rows,
                                                             const uint8_t* __restrict__ flags,
                                                             int nslots, MatchRow* __restrict__ out,
@@ -304,70 +304,51 @@ __device__ __forceinline__ int weed_delta(int n, int delta) {
   return d > 12 ? d : 12;
 }
 
-constexpr int kFitStride = 20;  // H[9], Hinv[9], ok, pad
-
-// One warp per iteration: draw with resampling (weeding.py:74-84) -- every
-// lane runs the same Philox stream -- and the four-point fit spread over the
-// lanes (warp_fit4); 8 iterations per block, so the hypotheses of a level
-// occupy ~32 SMs instead of 4 and no thread runs a 9x8 QR alone.
-constexpr int kFitWarps = 8;
-__global__ void __launch_bounds__(32 * kFitWarps) weed_fit_kernel(const MatchRow* __restrict__ rows,
-                                                                  const int32_t* __restrict__ count, int w,
-                                                                  int h, int iterations,
-                                                                  const uint64_t* __restrict__ keys,
-                                                                  double* __restrict__ fits,
-                                                                  int32_t* __restrict__ grey) {
+// One block per RANSAC iteration (weeding.py:69-89). Warp 0 draws with
+// resampling (weeding.py:74-84; every lane runs the same Philox stream) and
+// fits the four-point homography spread over its lanes (warp_fit4); then the
+// whole block tests the symmetric transfer error of every match against it
+// and OR-s an accepted inlier set into the reliable mask. One kernel per
+// level instead of a fit kernel + a count kernel with the fits in between.
+__global__ void __launch_bounds__(256) weed_kernel(const MatchRow* __restrict__ rows,
+                                                   const int32_t* __restrict__ count, int w, int h,
+                                                   double eps, int delta, const uint64_t* __restrict__ keys,
+                                                   uint32_t* __restrict__ mask, int32_t* __restrict__ witness,
+                                                   int32_t* __restrict__ grey) {
   pdl_wait();
-  __shared__ WarpFitSmem wsm[kFitWarps];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int it = blockIdx.x * kFitWarps + warp;
-  if (it >= iterations) return;
-  int n = *count;
-  double* f = fits + (int64_t)it * kFitStride;
-  if (lane == 0) f[18] = 0.0;
-  if (n < 4) return;
-  Philox g;
-  philox_init(&g, keys[2 * it], keys[2 * it + 1]);
-  double H[9];
-  int g_local = 0;
-  bool ok = false;
-  for (int r = 0; r < kMaxResample && !ok; ++r) {
-    int idx[4];
-    choice4(&g, n, idx);
-    double px[4], py[4], qx[4], qy[4];
-    for (int k = 0; k < 4; ++k) {
-      double p[4];
-      norm_row(rows[idx[k]], w, h, p);
-      px[k] = p[0]; py[k] = p[1]; qx[k] = p[2]; qy[k] = p[3];
-    }
-    ok = warp_fit4(px, py, qx, qy, H, &g_local, &wsm[warp]) == 0;
-  }
-  if (lane == 0 && g_local) atomicAdd(grey, g_local);
-  if (!ok) return;
-  double Hi[9];
-  if (!inv3(H, Hi)) return;
-  if (lane == 0) {
-    for (int k = 0; k < 9; ++k) { f[k] = H[k]; f[9 + k] = Hi[k]; }
-    f[18] = 1.0;
-  }
-}
-
-// One block per iteration: symmetric-transfer inliers over the whole set
-// (weeding.py:85-89); accepted sets are OR-ed into the reliable mask.
-__global__ void __launch_bounds__(256) weed_count_kernel(const MatchRow* __restrict__ rows,
-                                                         const int32_t* __restrict__ count,
-                                                         int w, int h, double eps, int delta,
-                                                         const double* __restrict__ fits,
-                                                         uint32_t* __restrict__ mask,
-                                                         int32_t* __restrict__ witness) {
-  pdl_wait();
-  int it = blockIdx.x;
-  int n = *count;
-  const double* f = fits + (int64_t)it * kFitStride;
-  if (n < 4 || f[18] == 0.0) return;
+  __shared__ WarpFitSmem wsm;
   __shared__ double Hs[18];
-  if (threadIdx.x < 18) Hs[threadIdx.x] = f[threadIdx.x];
+  __shared__ int okf;
+  const int it = blockIdx.x, lane = threadIdx.x & 31;
+  const int n = *count;
+  if (n < 4) return;
+  if (threadIdx.x < 32) {
+    Philox g;
+    philox_init(&g, keys[2 * it], keys[2 * it + 1]);
+    double H[9];
+    int g_local = 0;
+    bool ok = false;
+    for (int r = 0; r < kMaxResample && !ok; ++r) {
+      int idx[4];
+      choice4(&g, n, idx);
+      double px[4], py[4], qx[4], qy[4];
+      for (int k = 0; k < 4; ++k) {
+        double p[4];
+        norm_row(rows[idx[k]], w, h, p);
+        px[k] = p[0]; py[k] = p[1]; qx[k] = p[2]; qy[k] = p[3];
+      }
+      ok = warp_fit4(px, py, qx, qy, H, &g_local, &wsm) == 0;
+    }
+    double Hi[9];
+    ok = ok && inv3(H, Hi);
+    if (lane == 0) {
+      if (g_local) atomicAdd(grey, g_local);
+      for (int k = 0; k < 9; ++k) { Hs[k] = H[k]; Hs[9 + k] = Hi[k]; }
+      okf = ok;
+    }
+  }
   __syncthreads();
+  if (!okf) return;
   int total = 0;
   uint32_t bits = 0;  // inlier bits of this thread's first 32 chunks
   for (int c0 = 0, k = 0; c0 < n; c0 += blockDim.x, ++k) {
@@ -382,7 +363,6 @@ __global__ void __launch_bounds__(256) weed_count_kernel(const MatchRow* __restr
     total += __syncthreads_count(in);
   }
   if (total <= weed_delta(n, delta)) return;
-  int lane = threadIdx.x & 31;
   for (int c0 = 0, k = 0; c0 < n; c0 += blockDim.x, ++k) {
     int i = c0 + threadIdx.x;
     bool in;
@@ -403,17 +383,13 @@ __global__ void __launch_bounds__(256) weed_count_kernel(const MatchRow* __restr
 }
 
 void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w, int h,
-                 int iterations, double eps, const uint64_t* keys, int delta,
-                 double* fit_scratch, uint32_t* mask, int32_t* witness, int32_t* grey,
-                 cudaStream_t s, bool cleared) {
+                 int iterations, double eps, const uint64_t* keys, int delta, uint32_t* mask,
+                 int32_t* witness, int32_t* grey, cudaStream_t s, bool cleared) {
   if (!cleared) {
     cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((n_static + 31) / 32 + 1), s);
     cudaMemsetAsync(witness, 0, sizeof(int32_t) * (n_static + 1), s);
   }
-  klaunch(weed_fit_kernel, ceil_div(iterations, kFitWarps), 32 * kFitWarps, 0, s, rows, count, w, h, iterations, keys,
-                                                          fit_scratch, grey);
-  klaunch(weed_count_kernel, iterations, 256, 0, s, rows, count, w, h, eps, delta, fit_scratch, mask,
-                                               witness);
+  klaunch(weed_kernel, iterations, 256, 0, s, rows, count, w, h, eps, delta, keys, mask, witness, grey);
 }
 
 // ---------------------------------------------------------------- K8

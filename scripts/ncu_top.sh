@@ -13,7 +13,7 @@ run dt_agg 'dt_cols_agg' 0
 run dt_cols 'dt_cols_cluster' 1
 run ssd 'ssd_tiles_kernel' 4
 run finish 'finish_level_kernel' 4
-run weedfit 'weed_fit_kernel' 4
+run weed 'weed_kernel' 4
 run ssim 'ssim_fixed_kernel' 0
 run weights0 'weights_down_kernel' 0
 run collapse0 'collapse_kernel' 7

@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
 // band's tiles
 bool launch_ssim_rows(const float* a, const uint8_t* qb, const float* lut_b, int w, int h, int y0, int y1,
                       int window, const double* taps, float* out, cudaStream_t s) {
+  if (y1 <= y0) return true;  // an empty band (the last ranks of a short frame)
   if (window / 2 != 5 || y0 % kS2) return false;
-  if (y1 <= y0) return true;
   size_t vb = 5 * (size_t)kS2 * (kS2 + 10) * sizeof(double);
   dim3 grd(ceil_div(w, kS2), ceil_div(y1, kS2) - y0 / kS2);
   klaunch(ssim_fixed_kernel<5>, grd, dim3(32, 8), vb, s, a, (const float*)nullptr, qb, lut_b, w, h, taps, out,

@@ -75,10 +75,10 @@ def _worker(rank, world, port, name, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_banded_ranks_equal_one_rank(cuda, world):
+@pytest.mark.parametrize("world,name", [(2, "r960_s3"), (3, "r960_s3"), (5, "qvga_s2")])
+def test_banded_ranks_equal_one_rank(cuda, world, name):
+    """qvga_s2 (240 rows) over 5 ranks: 64-row bands, the last one empty."""
     from paper_1504_01441_b200.banded import register_and_fuse_banded
-    name = "r960_s3"
     ref, src = _scene(name)
     want = _outputs_digest(register_and_fuse_banded(ref, src))
     with socket.socket() as s:

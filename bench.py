@@ -903,7 +903,10 @@ def run_ours(args):
 
     extras = {}
     if not args.no_banded and (w, h) == (W5, H5):
-        extras["banded_12mp"] = banded_leg(local, hd, world)
+        try:
+            extras["banded_12mp"] = banded_leg(local, hd, world)
+        except Exception as exc:  # an auxiliary leg never takes the headline line down
+            extras["banded_12mp"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank == 0 and world == 1 and not args.no_extra_workloads and (w, h) == (W5, H5):
         peak, _ = peaks()
         extras["dropin_latency"] = dropin_latency(scenes[0])

@@ -95,3 +95,38 @@ def test_banded_ranks_equal_one_rank(cuda, world, name):
         assert p.exitcode == 0
     for r, d in enumerate(got):
         assert d == want, (r, [f for f in FIELDS if d[f] != want[f]])
+
+
+def _nccl_worker(port, name, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1",
+                      LOCAL_RANK="0")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", device_id=torch.device("cuda:0"))
+    from paper_1504_01441_b200.banded import register_and_fuse_banded
+    ref, src = _scene(name)
+    q.put(_outputs_digest(register_and_fuse_banded(ref, src)))
+    dist.destroy_process_group()
+
+
+def test_banded_nccl_collectives(cuda):
+    """The NCCL path (in-place all-gathers, all-reduce of the histogram) on a
+    one-rank group -- the only NCCL group one GPU allows -- gives the same
+    bits as no group at all."""
+    from paper_1504_01441_b200.banded import register_and_fuse_banded
+    name = "vga_rot_s1"
+    want = _outputs_digest(register_and_fuse_banded(*_scene(name)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(port, name, q))
+    p.start()
+    got = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert got == want

@@ -12,6 +12,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hdrb200.h"
 #include "hdr_common.cuh"
 #include "hdr_geom.cuh"
@@ -620,7 +622,14 @@ void kprobe_mark(KProbe* p, int end, cudaStream_t s) {
 }
 }  // namespace hdr
 
+// Stage boundaries of the pair: an NVTX range per stage on the host timeline
+// (nsys / ncu NVTX filtering; free when no tool is attached) and, with probes
+// set, CUDA events recorded on the stream (hdr_ctx_set_probes).
+static const char* const kStageNames[7] = {"hdr:raster", "hdr:corners", "hdr:match_chain", "hdr:dt_filter",
+                                           "hdr:finalize_warp", "hdr:ssim", "hdr:fuse"};
 static void probe(hdr_ctx* c, int stage, int end) {
+  if (end) nvtxRangePop();
+  else nvtxRangePushA(kStageNames[stage]);
   if (!c->probing) return;
   cudaEvent_t e = c->probes[2 * stage + end];
   if (!e) return;

@@ -10,7 +10,7 @@ through the host):
   on every rank; it is deterministic, so every rank holds the same matches
   and homography without a collective;
 * the domain-transform filter (densify.py:78-113) is split by row bands of
-  whole 16-row chunks: each rank sweeps its rows and aggregates its column
+  whole column chunks: each rank sweeps its rows and aggregates its column
   chunks; the chunk aggregates (chunk-major, so a band's are one block) are
   all-gathered, and each rank links them and re-runs its own chunks -- the carries of the column
   recursion crossing the bands (densify.py:69-75). The last pass writes the
@@ -150,8 +150,7 @@ def register_and_fuse_banded(ref, src, params: PipelineParams | None = None, gro
     # densify_flow: rows and column chunks of the band, aggregates gathered
     # chunk aggregates, chunk-major: a band's chunks are one block, padded to
     # `world` equal blocks so they move by all-gather
-    chunk = int(lib.hdr_band_agg_doubles(w, 16, 3))  # doubles per 16-row chunk
-    per_band = band // 16 * chunk
+    per_band = int(lib.hdr_band_agg_doubles(w, band, 3))  # a band is whole chunks
     agg = torch.zeros(max(int(lib.hdr_band_agg_doubles(w, h, 3)), world * per_band), dtype=torch.float64, **kw)
     flow_p = torch.zeros((hp, w, 2), dtype=torch.float32, **kw)
     flow = flow_p[:h]

@@ -19,7 +19,7 @@
 //   across the cluster through DSMEM, and the next band is prefetched by
 //   cp.async into per-thread shared-memory slots. The last pass writes the
 //   f32 flow (densify_flow) instead of the planes.
-// Columns fallback (tall images, test hook): `agg` reduces 16-row chunks to
+// Columns fallback (tall images, test hook): `agg` reduces 8-row chunks to
 //   the affine data both directions need (forward map A,B and the backward
 //   sums Z0 = sum (1-a_i) prod_{j<i} a_j y0_i, R, Q = prod a_i), `link` links
 //   the chunks of each column, `apply` re-runs each chunk from its carries.
@@ -470,10 +470,16 @@ static bool rows_bulk_ok(const float* guide, const DtPlanes& P, int w) {
 }
 
 // ---------------------------------------------------------------- columns
-// 16-row chunks, thread per (column, chunk), the chunk held in registers: all
-// 16 x K samples and 18 guide values are loaded up front (the loads carry no
-// dependency, so each thread has ~60 requests in flight), then swept.
-constexpr int kColChunk = 16;
+// 8-row chunks, thread per (column, chunk), the chunk held in registers: all
+// 8 x K samples and 10 guide values are loaded up front (the loads carry no
+// dependency, so each thread has ~34 requests in flight), then swept. 16-row
+// chunks held twice the registers (apply 255 + spill, agg 154) at a quarter
+// of the occupancy and ran slower: 5MP, 3 passes, 725 us (16) / 647 (8) /
+// 672 (4, where the link's serial chain over 486 chunks takes 40 us a pass).
+#ifndef HDR_COL_CHUNK
+#define HDR_COL_CHUNK 8
+#endif
+constexpr int kColChunk = HDR_COL_CHUNK;
 constexpr int kColThreads = 64;
 
 template <int K>

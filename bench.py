@@ -725,7 +725,7 @@ def banded_leg(local, hd, world, w=None, h=None, n=3):
     return {"workload": f"one {w}x{h} pair split by row bands over {world} rank(s) (SURVEY.md §8(f)4)",
             "latency_ms": ms, "ranks": world, "composite_digest": comp,
             "note": "registration and merge replicated, domain transform / warp / SSIM banded; "
-                    "chunk aggregates, flow, histogram and the band outputs all-reduced (NCCL)"}
+                    "chunk aggregates, flow and the band outputs all-gathered, the SSIM histogram all-reduced (NCCL)"}
 
 
 def extra_pairs_leg(args, local, peak, cpu_kind):

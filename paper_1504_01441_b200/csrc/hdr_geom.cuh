@@ -405,27 +405,30 @@ HD void jacobi_eig9(double* a, double* w, double* v) {
 // rank estimate (d7 ~ lambda7 within a small factor).
 HD int fit_from_gram(const double* g45, const double* tr, const double* ts, double* H,
                      int* grey) {
-  // every loop below has static bounds and is unrolled, so `a` stays in
-  // registers; the symmetric pivot swap is a predicated select over the
-  // candidates
-  double a[9][9];
-  double dmax = 0.0;
+  // The matrix lives as its packed lower triangle A[i (i + 1) / 2 + j], j <= i,
+  // with every loop unrolled so each index is a constant: a 9x9 array with
+  // the pivot swaps as selects was put in local memory by the compiler, and
+  // the factorisation and the iterations ran from there (~25-60k cycles per
+  // fit; the arithmetic below is the same, operation for operation).
+  double A[45];
+#define HDR_A(i, j) A[(i) * ((i) + 1) / 2 + (j)]
   {
     int k = 0;
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
-      for (int j = i; j < 9; ++j) { a[i][j] = g45[k]; a[j][i] = g45[k]; ++k; }
+      for (int j = i; j < 9; ++j) { HDR_A(j, i) = g45[k]; ++k; }
   }
+  double dmax = 0.0;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) dmax = fmax(dmax, a[i][i]);
+  for (int i = 0; i < 9; ++i) dmax = fmax(dmax, HDR_A(i, i));
 #ifdef HDR_DEBUG_FIT
   printf("gram in: g0=%g g1=%g g44=%g dmax=%g\n", g45[0], g45[1], g45[44], dmax);
 #endif
   if (!(dmax > 0.0)) return 2;
   double sigma = 1e-13 * dmax;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) a[i][i] += sigma;
+  for (int i = 0; i < 9; ++i) HDR_A(i, i) += sigma;
   int perm[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) perm[i] = i;
@@ -433,34 +436,45 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
 #pragma unroll
   for (int c = 0; c < 9; ++c) {
     int p = c;
-    double best = a[c][c];
+    double best = HDR_A(c, c);
 #pragma unroll
     for (int i = c + 1; i < 9; ++i)
-      if (a[i][i] > best) { best = a[i][i]; p = i; }
+      if (HDR_A(i, i) > best) { best = HDR_A(i, i); p = i; }
+    // symmetric swap of c and p: rows of the finished columns j < c (the
+    // factor) and the trailing symmetric block; (p, c) stays. Selects over
+    // the candidates: a branch per candidate measured ~20% slower (one thread
+    // walks this code, and the branchy form is longer)
 #pragma unroll
-    for (int q = c + 1; q < 9; ++q)
-      if (q == p) {
+    for (int q = c + 1; q < 9; ++q) {
+      const bool sw = q == p;
+      auto swp = [sw](double& x, double& y) {
+        double t0 = x, t1 = y;
+        x = sw ? t1 : t0;
+        y = sw ? t0 : t1;
+      };
 #pragma unroll
-        for (int j = 0; j < 9; ++j) { double t = a[c][j]; a[c][j] = a[q][j]; a[q][j] = t; }
+      for (int j = 0; j < c; ++j) swp(HDR_A(c, j), HDR_A(q, j));
+      swp(HDR_A(c, c), HDR_A(q, q));
 #pragma unroll
-        for (int j = 0; j < 9; ++j) { double t = a[j][c]; a[j][c] = a[j][q]; a[j][q] = t; }
-        int t = perm[c]; perm[c] = perm[q]; perm[q] = t;
-      }
-    double d = a[c][c];
+      for (int k = c + 1; k < q; ++k) swp(HDR_A(k, c), HDR_A(q, k));
+#pragma unroll
+      for (int k = q + 1; k < 9; ++k) swp(HDR_A(k, c), HDR_A(k, q));
+      int t0 = perm[c], t1 = perm[q];
+      perm[c] = sw ? t1 : t0;
+      perm[q] = sw ? t0 : t1;
+    }
+    double d = HDR_A(c, c);
     piv[c] = d;
     if (!(d > 0.0)) return 2;
     double l = sqrt(d);
-    a[c][c] = l;
+    HDR_A(c, c) = l;
     il[c] = 1.0 / l;
 #pragma unroll
-    for (int i = c + 1; i < 9; ++i) a[i][c] *= il[c];
+    for (int i = c + 1; i < 9; ++i) HDR_A(i, c) *= il[c];
 #pragma unroll
     for (int i = c + 1; i < 9; ++i)
 #pragma unroll
-      for (int j = c + 1; j <= i; ++j) {
-        a[i][j] -= a[i][c] * a[j][c];
-        a[j][i] = a[i][j];
-      }
+      for (int j = c + 1; j <= i; ++j) HDR_A(i, j) -= HDR_A(i, c) * HDR_A(j, c);
   }
   // rank rule s[-2] <= 1e-9 s[0]: resolvable in Gram precision only down to
   // ~1e-7 relative singular values; d7 - sigma estimates s7^2
@@ -477,14 +491,14 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
     for (int i = 0; i < 9; ++i) {  // L y = v
       double s = v[i];
 #pragma unroll
-      for (int j = 0; j < i; ++j) s -= a[i][j] * y[j];
+      for (int j = 0; j < i; ++j) s -= HDR_A(i, j) * y[j];
       y[i] = s * il[i];
     }
 #pragma unroll
     for (int i = 8; i >= 0; --i) {  // L^T z = y (z into y)
       double s = y[i];
 #pragma unroll
-      for (int j = i + 1; j < 9; ++j) s -= a[j][i] * y[j];
+      for (int j = i + 1; j < 9; ++j) s -= HDR_A(j, i) * y[j];
       y[i] = s * il[i];
     }
     double nrm = 0.0, sgn = 0.0;
@@ -501,6 +515,7 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
     }
     if (diff < 1e-13) break;
   }
+
   double hc[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) hc[i] = 0.0;
@@ -509,6 +524,7 @@ HD int fit_from_gram(const double* g45, const double* tr, const double* ts, doub
 #pragma unroll
     for (int j = 0; j < 9; ++j)
       if (perm[i] == j) hc[j] = v[i];
+#undef HDR_A
   return finish_h(hc, tr, ts, H);
 }
 

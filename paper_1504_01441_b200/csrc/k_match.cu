@@ -6,6 +6,15 @@
 // for the tile count (the maximum number of corners) and idle blocks exit,
 // so the coarse-to-fine chain of matcher.pyramidal_match (matcher.py:221-263)
 // runs without a host round trip and can be captured in one CUDA graph.
+#ifdef HDR_FINISH_TIMING
+#include <cstdio>
+// debug build only: clock64 stamps of finish_level's phases (thread 0)
+__device__ long long g_fit_stamps[8];
+#define FIT_STAMP(i) \
+  if (threadIdx.x == 0) g_fit_stamps[i] = clock64()
+#else
+#define FIT_STAMP(i) (void)0
+#endif
 #include "hdr_common.cuh"
 #include "hdr_geom.cuh"
 #include "hdr_warpfit.cuh"
@@ -394,6 +403,12 @@ void launch_weed(const MatchRow* rows, const int32_t* count, int n_static, int w
 
 // ---------------------------------------------------------------- K8
 constexpr int kFitCache = 4096;  // weeded points held in shared memory by finish_level
+constexpr int kCompactWords = 2048;  // mask words (65536 rows) whose prefix finish_level keeps in shared memory
+// the bits of mask word k that are rows below n
+__device__ __forceinline__ uint32_t word_bits(int k, int n) {
+  int r = n - 32 * k;
+  return r >= 32 ? 0xffffffffu : (1u << r) - 1u;
+}
 
 // entry k of DLT row r (0 or 1) of correspondence p -> q (geometry.py:51-63)
 __device__ __forceinline__ double dlt_entry(int r, int k, double px, double py, double qx,
@@ -459,6 +474,7 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     }
   }
   __syncthreads();
+  FIT_STAMP(2);
   // mean distances to the centroids
   double md[2] = {0, 0};
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -487,6 +503,7 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     ts[0] = ss; ts[1] = -ss * bc[2]; ts[2] = -ss * bc[3];
   }
   __syncthreads();
+  FIT_STAMP(3);
   if (status) return status;
   // Gram matrix of the conditioned DLT rows. With p~ = (px, py, 1), rows are
   // r0 = [-p~, 0, qx p~], r1 = [0, -p~, qy p~], so G is assembled from 24 sums
@@ -539,7 +556,9 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
     for (int i = 0; i < 9; ++i)
       for (int j = i; j < 9; ++j) g45s[k++] = G[i][j];
     int g = 0;
+    FIT_STAMP(4);
     status = fit_from_gram(g45s, tr, ts, H, &g);
+    FIT_STAMP(5);
     if (g && grey) atomicAdd(grey, g);
   }
   __syncthreads();
@@ -549,37 +568,55 @@ __device__ int block_fit(int n, Get get, double* H, int32_t* grey) {
 // Close one pyramid level (matcher.py:247-260): compact the weeded set in
 // index order (np.flatnonzero), record level_counts, fit the LSQ H and hand
 // it to the next finer level; level 0 also fills the user-visible outputs.
-__global__ void __launch_bounds__(256) finish_level_kernel(
+__global__ void __launch_bounds__(256, 1) finish_level_kernel(
     const MatchRow* __restrict__ raw, const int32_t* __restrict__ raw_count,
     const uint32_t* __restrict__ mask, int w, int h, int level, MatchRow* __restrict__ weeded,
     int32_t* __restrict__ weeded_count, int64_t* __restrict__ kept_idx,
     double* __restrict__ hpred, double* __restrict__ homography, int32_t* __restrict__ info,
     double* __restrict__ out_matches, double* __restrict__ out_raw, int32_t* grey) {
   pdl_wait();
+  FIT_STAMP(0);
   extern __shared__ double pts_cache[];  // normalised (rx, ry, sx, sy) of the weeded set
   __shared__ int scratch[32];
+  __shared__ int word_base[kCompactWords];
   int n = *raw_count;
   int m = 0;
   bool cached = n <= kFitCache;
+  auto put_row = [&](int i, int pos) {
+    const MatchRow rw = raw[i];
+    weeded[pos] = rw;
+    if (cached) norm_row(rw, w, h, pts_cache + 4 * pos);
+    if (kept_idx) kept_idx[pos] = i;
+    if (out_matches)
+      for (int k = 0; k < 5; ++k) out_matches[5 * (int64_t)pos + k] = rw.v[k];
+  };
   if (n >= 4) {
-    // np.flatnonzero order with one block scan: thread t owns the contiguous
-    // rows [t L, t L + L), counts its flags, and writes them after the
-    // exclusive prefix of the counts (every row load of a thread in flight
-    // at once, instead of one dependent load + scan per 256-row chunk)
-    const int L = (n + blockDim.x - 1) / blockDim.x;
-    const int i0 = min(n, (int)threadIdx.x * L), i1 = min(n, i0 + L);
+    // np.flatnonzero order: the exclusive prefix of the mask words' popcounts
+    // (thread t owns the contiguous words [t W, t W + W)) goes to shared
+    // memory, then every kept row r lands at word_base[r / 32] + (set bits
+    // below r in its word), rows dealt out one per thread so all of a
+    // thread's row loads are independent and in flight together
+    const int nw = (n + 31) >> 5;
+    const int W = (nw + blockDim.x - 1) / blockDim.x;
+    const int w0 = min(nw, (int)threadIdx.x * W), w1 = min(nw, w0 + W);
+    const bool in_smem = nw <= kCompactWords;
     int cnt = 0;
-    for (int i = i0; i < i1; ++i) cnt += (int)((mask[i >> 5] >> (i & 31)) & 1u);
+    for (int k = w0; k < w1; ++k) cnt += __popc(mask[k] & word_bits(k, n));
     int pos = block_exclusive_scan(cnt, scratch, &m);
-    for (int i = i0; i < i1; ++i) {
-      if (!((mask[i >> 5] >> (i & 31)) & 1u)) continue;
-      const MatchRow rw = raw[i];
-      weeded[pos] = rw;
-      if (cached) norm_row(rw, w, h, pts_cache + 4 * pos);
-      if (kept_idx) kept_idx[pos] = i;
-      if (out_matches)
-        for (int k = 0; k < 5; ++k) out_matches[5 * (int64_t)pos + k] = rw.v[k];
-      ++pos;
+    if (in_smem) {
+      for (int k = w0; k < w1; ++k) {
+        word_base[k] = pos;
+        pos += __popc(mask[k] & word_bits(k, n));
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t mw = mask[i >> 5];
+        if (!((mw >> (i & 31)) & 1u)) continue;
+        put_row(i, word_base[i >> 5] + __popc(mw & ((1u << (i & 31)) - 1u)));
+      }
+    } else {
+      for (int k = w0; k < w1; ++k)
+        for (uint32_t b = mask[k] & word_bits(k, n); b; b &= b - 1) put_row(32 * k + __ffs(b) - 1, pos++);
     }
   }
   if (threadIdx.x == 0) {
@@ -602,7 +639,15 @@ __global__ void __launch_bounds__(256) finish_level_kernel(
     }
   };
   __syncthreads();  // weeded rows / cached points visible block-wide
+  FIT_STAMP(1);
   int st = block_fit(m, get, Hs, grey);
+  FIT_STAMP(6);
+#ifdef HDR_FINISH_TIMING
+  if (threadIdx.x == 0)
+    printf("finish L%d n=%d m=%d compact %lld centroid %lld md %lld gram %lld solve %lld tail %lld\n", level, n, m,
+           g_fit_stamps[1] - g_fit_stamps[0], g_fit_stamps[2] - g_fit_stamps[1], g_fit_stamps[3] - g_fit_stamps[2],
+           g_fit_stamps[4] - g_fit_stamps[3], g_fit_stamps[5] - g_fit_stamps[4], g_fit_stamps[6] - g_fit_stamps[5]);
+#endif
 
   if (threadIdx.x == 0 && st == 0) {
     for (int k = 0; k < 9; ++k) hpred[k] = Hs[k];

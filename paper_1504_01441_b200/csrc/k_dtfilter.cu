@@ -824,7 +824,10 @@ __device__ __forceinline__ void scan_groups(Aff<K>& m, bool up, int bw_log2,
 // cols_pf_smem<K>()), so HBM reads of band b+1 overlap the link, apply and
 // store phases of band b; otherwise plain loads at the top of each band.
 template <int K, bool FINAL, bool PF>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, kCT <= 256 ? 2 : 1)
+#ifndef HDR_COL_MIN_BLOCKS
+#define HDR_COL_MIN_BLOCKS (kCT <= 256 ? 2 : 1)
+#endif
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, HDR_COL_MIN_BLOCKS)
     dt_cols_cluster(const float* __restrict__ guide, DtPlanes P, int w, int h, double ratio,
                     double c, int bw_log2, DtFlowOut fo, const int32_t* __restrict__ zrows) {
   pdl_wait();

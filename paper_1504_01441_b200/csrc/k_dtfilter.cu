@@ -517,7 +517,13 @@ __device__ __forceinline__ void load_chunk(const float* __restrict__ guide, cons
 // ch0: first chunk of the launch (a row band's chunks; 0 for the whole
 // image), nch: chunks of the whole image (the agg layout)
 template <int K>
-__global__ void __launch_bounds__(kColThreads) dt_cols_agg(const float* __restrict__ guide,
+#ifndef HDR_AGG_MIN_BLOCKS
+#define HDR_AGG_MIN_BLOCKS 1
+#endif
+#ifndef HDR_APPLY_MIN_BLOCKS
+#define HDR_APPLY_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(kColThreads, HDR_AGG_MIN_BLOCKS) dt_cols_agg(const float* __restrict__ guide,
                                                            DtPlanes P, int w, int h, double ratio,
                                                            double c, double* __restrict__ agg,
                                                            int ch0, int nch) {
@@ -653,7 +659,7 @@ __global__ void __launch_bounds__(1024) dt_cols_link(int w, int nch, const doubl
 // storing the planes, finish densify_flow (densify.py:134-142) in registers
 // and write the f32 flow: ratio where n > floor, else the homography flow.
 template <int K, bool FINAL>
-__global__ void __launch_bounds__(kColThreads) dt_cols_apply(const float* __restrict__ guide,
+__global__ void __launch_bounds__(kColThreads, HDR_APPLY_MIN_BLOCKS) dt_cols_apply(const float* __restrict__ guide,
                                                              DtPlanes P, int w, int h,
                                                              double ratio, double c,
                                                              const double* __restrict__ carry,

@@ -379,7 +379,12 @@ __device__ __forceinline__ void store_row_bulk(const DtPlanes& P, int64_t row, c
 // same way, so the 256 threads only compute. Needs all planes f64 and
 // 16-byte aligned rows (w % 4 == 0, aligned bases); w <= kRowThreads*kRowSeg.
 template <int K>
-__global__ void __launch_bounds__(kRowThreads) dt_rows_bulk_kernel(const float* __restrict__ guide,
+#ifdef HDR_ROW_MIN_BLOCKS
+#define HDR_ROW_BOUNDS kRowThreads, HDR_ROW_MIN_BLOCKS
+#else
+#define HDR_ROW_BOUNDS kRowThreads
+#endif
+__global__ void __launch_bounds__(HDR_ROW_BOUNDS) dt_rows_bulk_kernel(const float* __restrict__ guide,
                                                                    DtPlanes P, int w, int h,
                                                                    double ratio, double c) {
   pdl_wait();

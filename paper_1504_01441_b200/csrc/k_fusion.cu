@@ -109,6 +109,13 @@ void init_fusion_attributes() {
 // outputs per 32x8 block, each thread owning one column and 4 rows, so all
 // tap loops unroll and no index needs a division.
 constexpr int kS2 = 32;
+// rows per vertical work item of ssim_fixed_kernel: E x 32/VR items over 256
+// threads (VR = 4: 336 items, two rounds, the second 31% busy; VR = 2: 672
+// items, three rounds, 88% busy, ~1.7x the staged-sample products per output)
+#ifndef HDR_SSIM_VROWS
+#define HDR_SSIM_VROWS 4
+#endif
+constexpr int VR = HDR_SSIM_VROWS;
 
 template <int R>
 #ifndef HDR_SSIM_MIN_BLOCKS
@@ -159,24 +166,24 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     }
   }
   __syncthreads();
-  // vertical (axis 0): work item (rg, c) produces rows 4rg..4rg+3 of staged
+  // vertical (axis 0): work item (rg, c) produces rows VR rg .. VR rg + VR-1 of staged
   // column c from 14 staged samples (sliding); the E x 8 items are dealt out
   // flat over the 256 threads, so the second round runs 3 warps, not 8
-  for (int item = tid; item < E * (kS2 / 4); item += 256) {
+  for (int item = tid; item < E * (kS2 / VR); item += 256) {
     const int rg = item / E, c = item - rg * E;
     // the products of each staged sample are formed once (not once per tap
     // that reads it): same roundings, ~25% fewer f64 instructions
-    double va[4 + 2 * R], vb[4 + 2 * R], vaa[4 + 2 * R], vbb[4 + 2 * R], vab[4 + 2 * R];
+    double va[VR + 2 * R], vb[VR + 2 * R], vaa[VR + 2 * R], vbb[VR + 2 * R], vab[VR + 2 * R];
 #pragma unroll
-    for (int j = 0; j < 4 + 2 * R; ++j) {
-      va[j] = sa[4 * rg + j][c];
-      vb[j] = sb[4 * rg + j][c];
+    for (int j = 0; j < VR + 2 * R; ++j) {
+      va[j] = sa[VR * rg + j][c];
+      vb[j] = sb[VR * rg + j][c];
       vaa[j] = va[j] * va[j];
       vbb[j] = vb[j] * vb[j];
       vab[j] = va[j] * vb[j];
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < VR; ++q) {
       double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
 #pragma unroll
       for (int j = 0; j <= 2 * R; ++j) {
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
         m3 = fma(vbb[q + j], k[j], m3);
         m4 = fma(vab[q + j], k[j], m4);
       }
-      int oy = 4 * rg + q;
+      int oy = VR * rg + q;
       V[(0 * kS2 + oy) * E + c] = m0;
       V[(1 * kS2 + oy) * E + c] = m1;
       V[(2 * kS2 + oy) * E + c] = m2;

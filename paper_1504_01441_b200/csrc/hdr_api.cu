@@ -114,10 +114,6 @@ extern "C" int hdr_set_option(const char* name, int64_t value) {
     hdr::dt_set_cols_prefetch(value != 0);
     return HDR_OK;
   }
-  if (name && std::string(name) == "warp_unroll") {
-    hdr::warp_set_unroll((int)value);
-    return HDR_OK;
-  }
   if (name && std::string(name) == "dt_skip_zero_rows") {
     hdr::dt_set_skip_zero_rows(value != 0);
     return HDR_OK;

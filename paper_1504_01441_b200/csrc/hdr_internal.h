@@ -189,7 +189,6 @@ void launch_apply_homography(const double* H, const double* pts, int64_t n, doub
 void launch_transfer_error(const double* H, const double* rp, const double* sp, int64_t n, double* out,
                            int32_t* bad, cudaStream_t s);
 void launch_hflow(const double* H, int w, int h, float* flow, cudaStream_t s);
-void warp_set_unroll(int u);
 void launch_warp_rows(const float* flow, int w, int h, int y0, int y1, const float* src, float* warped,
                       uint8_t* valid, uint8_t* qw, uint32_t* hist, cudaStream_t s);
 bool launch_ssim_rows(const float* a, const uint8_t* qb, const float* lut_b, int w, int h, int y0, int y1,

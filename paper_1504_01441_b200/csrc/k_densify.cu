@@ -252,22 +252,12 @@ __global__ void __launch_bounds__(256) finalize_warp_kernel(
 }
 
 // warp_image (densify.py:145-174) + luminance(warped) -> quantised histogram,
-// flow given. Blocks sweep row segments of 256*U pixels (grid-stride), so each
+// flow given. Blocks sweep 256-pixel row segments (grid-stride), so each
 // thread's (x, y) comes without a per-pixel division and the block histogram
-// is flushed once per block. With U > 1 a thread owns U pixels of a segment
-// (x, x+256, ...) and issues all U flow loads, then all 12U gathers, before
-// the math. Measured (5MP RGB, kbench): U = 1 52 us, U = 2 62 us, U = 4 74 us
-// -- the extra registers (63 -> 72 -> 114) cost more resident warps than the
-// per-thread memory parallelism gains, so U = 1 is the default (the bench's
-// warp probe: 58.3 us for the previous one-pixel kernel, 54.2 us for this one
-// at U = 1, on two boxes whose spread is ~10%).
+// is flushed once per block.
 // Rows [y0, y1) of the (w, h) frame (the whole frame for the pair; a row
 // band of it for the banded pair); hist may be null (halo rows of a band).
-template <int U>
-#ifndef HDR_WARP_MIN_BLOCKS
-#define HDR_WARP_MIN_BLOCKS 1
-#endif
-__global__ void __launch_bounds__(256, HDR_WARP_MIN_BLOCKS) warp_kernel(const float* __restrict__ flow, int w, int h,
+__global__ void __launch_bounds__(256) warp_kernel(const float* __restrict__ flow, int w, int h,
                                                    const float* __restrict__ src,
                                                    float* __restrict__ warped,
                                                    uint8_t* __restrict__ valid,
@@ -279,68 +269,67 @@ __global__ void __launch_bounds__(256, HDR_WARP_MIN_BLOCKS) warp_kernel(const fl
   for (int i = threadIdx.x; i < 8 * kBins; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
   uint32_t* mine = sh[threadIdx.x >> 5];
-  constexpr int SEG = 256 * U;
   // row / segment indices advance without a division per step
-  const int segs = (w + SEG - 1) / SEG;
+  const int segs = (w + 255) >> 8;
   const int dq = gridDim.x / segs, dr = gridDim.x - dq * segs;
-  const double wm = (double)(w - 1), hm = (double)(h - 1);
   int y = y0 + (int)blockIdx.x / segs, seg = blockIdx.x - (y - y0) * segs;
+  // the flow of the next work item is loaded before this one's gathers are
+  // issued (software pipelining: its DRAM latency hides behind them)
+  auto flow_at = [&](int yy, int ss) {
+    const int xx = ss * 256 + threadIdx.x;
+    return yy < y1 && xx < w ? __ldcs(reinterpret_cast<const float2*>(flow) + (int64_t)yy * w + xx)
+                             : make_float2(0.0f, 0.0f);
+  };
+#ifndef HDR_WARP_PREFETCH
+#define HDR_WARP_PREFETCH 1
+#endif
+  float2 fnext = HDR_WARP_PREFETCH ? flow_at(y, seg) : make_float2(0.0f, 0.0f);
   for (; y < y1; y += dq, seg += dr) {
     if (seg >= segs) { seg -= segs; ++y; if (y >= y1) break; }
-    const int xb = seg * SEG + threadIdx.x;
-    const int ib = y * w + xb;  // 32-bit pixel index (3 w h < 2^31)
-    float2 f[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      f[u] = xb + 256 * u < w ? __ldcs(reinterpret_cast<const float2*>(flow) + ib + 256 * u)
-                              : make_float2(0.0f, 0.0f);
-    double fx[U], fy[U];
-    bool ok[U];
-    float s[U][12];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int x = xb + 256 * u;
-      double sx = dadd((double)x, (double)f[u].x), sy = dadd((double)y, (double)f[u].y);
-      ok[u] = sx >= 0.0 && sx <= wm && sy >= 0.0 && sy <= hm;
-      // np.clip of a finite value: compare + select (f64 fmin/fmax cost ~7
-      // instructions each here)
-      double cx = sx < 0.0 ? 0.0 : (sx > wm ? wm : sx);
-      double cy = sy < 0.0 ? 0.0 : (sy > hm ? hm : sy);
-      int xi = (int)floor(cx), yi = (int)floor(cy);
-      fx[u] = dsub(cx, (double)xi);
-      fy[u] = dsub(cy, (double)yi);
-      // 32-bit element offsets; a dead lane gathers pixel 0
-      const int o00 = x < w ? 3 * (yi * w + xi) : 0;
-      const int dxo = xi + 1 < w ? 3 : 0, dyo = yi + 1 < h ? 3 * w : 0;
-      const float* s00 = src + o00;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        s[u][k] = __ldg(s00 + k);
-        s[u][3 + k] = __ldg(s00 + dxo + k);
-        s[u][6 + k] = __ldg(s00 + dyo + k);
-        s[u][9 + k] = __ldg(s00 + dyo + dxo + k);
-      }
+#if HDR_WARP_PREFETCH
+    const float2 f = fnext;
+    {
+      int yn = y + dq, sn = seg + dr;
+      if (sn >= segs) { sn -= segs; ++yn; }
+      fnext = flow_at(yn, sn);
     }
+#endif
+    int x = seg * 256 + threadIdx.x;
+    if (x >= w) continue;
+    int64_t i = (int64_t)y * w + x;
+#if !HDR_WARP_PREFETCH
+    float2 f = __ldcs(reinterpret_cast<const float2*>(flow) + i);
+#endif
+    double sx = dadd((double)x, (double)f.x), sy = dadd((double)y, (double)f.y);
+    const double wm = (double)(w - 1), hm = (double)(h - 1);
+    bool ok = sx >= 0.0 && sx <= wm && sy >= 0.0 && sy <= hm;
+    // np.clip of a finite value: compare + select (f64 fmin/fmax cost ~7
+    // instructions each here)
+    double cx = sx < 0.0 ? 0.0 : (sx > wm ? wm : sx);
+    double cy = sy < 0.0 ? 0.0 : (sy > hm ? hm : sy);
+    int x0 = (int)floor(cx), y0 = (int)floor(cy);
+    double fx = dsub(cx, (double)x0), fy = dsub(cy, (double)y0);
+    double gx = dsub(1.0, fx), gy = dsub(1.0, fy);
+    // 32-bit element offsets (3 w h < 2^31 for any frame the context holds)
+    const int o00 = 3 * (y0 * w + x0);
+    const int dxo = x0 + 1 < w ? 3 : 0, dyo = y0 + 1 < h ? 3 * w : 0;
+    const float* s00 = src + o00;
+    const float* s01 = s00 + dxo;
+    const float* s10 = s00 + dyo;
+    const float* s11 = s10 + dxo;
+    float o[3];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int x = xb + 256 * u;
-      if (x >= w) continue;
-      const double gx = dsub(1.0, fx[u]), gy = dsub(1.0, fy[u]);
-      float o[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        double top = dadd(dmul((double)s[u][k], gx), dmul((double)s[u][3 + k], fx[u]));
-        double bot = dadd(dmul((double)s[u][6 + k], gx), dmul((double)s[u][9 + k], fx[u]));
-        o[k] = (float)dadd(dmul(top, gy), dmul(bot, fy[u]));
-      }
-      const int i = ib + 256 * u;
-      float* wo = warped + 3 * i;
-      wo[0] = o[0]; wo[1] = o[1]; wo[2] = o[2];
-      valid[i] = ok[u] ? 1 : 0;
-      uint32_t q = quant3(luma3(o[0], o[1], o[2]));
-      qw[i] = (uint8_t)q;
-      atomicAdd(&mine[q], 1u);
+    for (int k = 0; k < 3; ++k) {
+      double top = dadd(dmul((double)__ldg(s00 + k), gx), dmul((double)__ldg(s01 + k), fx));
+      double bot = dadd(dmul((double)__ldg(s10 + k), gx), dmul((double)__ldg(s11 + k), fx));
+      o[k] = (float)dadd(dmul(top, gy), dmul(bot, fy));
     }
+    float* wo = warped + 3 * i;
+    wo[0] = o[0]; wo[1] = o[1]; wo[2] = o[2];
+    valid[i] = ok ? 1 : 0;
+    uint32_t q = quant3(luma3(o[0], o[1], o[2]));
+    qw[i] = (uint8_t)q;
+    atomicAdd(&mine[q], 1u);
   }
   if (!hist) return;
   __syncthreads();
@@ -352,34 +341,13 @@ __global__ void __launch_bounds__(256, HDR_WARP_MIN_BLOCKS) warp_kernel(const fl
   }
 }
 
-// pixels per thread of warp_kernel (hdr_set_option "warp_unroll": 1, 2, 4)
-#ifndef HDR_WARP_UNROLL
-#define HDR_WARP_UNROLL 1
-#endif
-static int g_warp_unroll = HDR_WARP_UNROLL;
-void warp_set_unroll(int u) { g_warp_unroll = (u == 1 || u == 2 || u == 4) ? u : HDR_WARP_UNROLL; }
-#ifndef HDR_WARP_BLOCKS_PER_SM
-#define HDR_WARP_BLOCKS_PER_SM 12
-#endif
-
-static void launch_warp_kernel(const float* flow, int w, int h, int y0, int y1, const float* src,
-                               float* warped, uint8_t* valid, uint8_t* qw, uint32_t* hist, cudaStream_t s) {
-  const int U = g_warp_unroll;
-  int64_t work = (int64_t)((w + 256 * U - 1) / (256 * U)) * (y1 - y0);
-  int64_t cap = 148 * HDR_WARP_BLOCKS_PER_SM / U;
-  int64_t blocks = work < cap ? work : cap;
-  if (U == 4)
-    klaunch(warp_kernel<4>, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, y0, y1);
-  else if (U == 2)
-    klaunch(warp_kernel<2>, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, y0, y1);
-  else
-    klaunch(warp_kernel<1>, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, y0, y1);
-}
-
 void launch_warp_rows(const float* flow, int w, int h, int y0, int y1, const float* src, float* warped,
                       uint8_t* valid, uint8_t* qw, uint32_t* hist, cudaStream_t s) {
   if (y1 <= y0) return;
-  launch_warp_kernel(flow, w, h, y0, y1, src, warped, valid, qw, hist, s);
+  int64_t work = (int64_t)((w + 255) / 256) * (y1 - y0);
+  int64_t cap = 148 * 12;
+  int64_t blocks = work < cap ? work : cap;
+  klaunch(warp_kernel, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, y0, y1);
 }
 
 void launch_warp(const float* flow, int w, int h, const float* src, float* warped, uint8_t* valid,
@@ -390,7 +358,13 @@ void launch_warp(const float* flow, int w, int h, const float* src, float* warpe
                          qw, hist, false, s);
     return;
   }
-  launch_warp_kernel(flow, w, h, 0, h, src, warped, valid, qw, hist, s);
+  int64_t work = (int64_t)((w + 255) / 256) * h;
+#ifndef HDR_WARP_BLOCKS_PER_SM
+#define HDR_WARP_BLOCKS_PER_SM 12
+#endif
+  int64_t cap = 148 * HDR_WARP_BLOCKS_PER_SM;
+  int64_t blocks = work < cap ? work : cap;
+  klaunch(warp_kernel, (unsigned)blocks, 256, 0, s, flow, w, h, src, warped, valid, qw, hist, 0, h);
 }
 
 void launch_finalize_warp(DtPlanes smooth, const double* fallback, const int32_t* has_fallback,

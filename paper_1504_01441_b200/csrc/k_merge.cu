@@ -45,9 +45,19 @@ __device__ __forceinline__ float lum_f(float r, float g, float b) {
 // of it otherwise. Everything after the laplacian -- sqrt, exp, products,
 // normalisation -- is f32: relative error ~1e-7 on a weight moves the
 // composite by ~1e-7, far inside the 1e-3 bar.
+#ifndef HDR_SAT_APPROX
+#define HDR_SAT_APPROX 1
+#endif
 __device__ __forceinline__ float quality_f(double lap, float r, float g, float b) {
   float d0 = r - g, d1 = g - b, d2 = b - r;
+#if HDR_SAT_APPROX
+  // MUFU square root (~2 ulp; exactly 0 at 0): the IEEE-rounded sqrt was 8% of
+  // the weights pass's instructions, and the weights carry no bit-exact bar
+  float sat, var = (d0 * d0 + d1 * d1 + d2 * d2) * (1.0f / 9.0f);
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(sat) : "f"(var));
+#else
   float sat = __fsqrt_rn((d0 * d0 + d1 * d1 + d2 * d2) * (1.0f / 9.0f));
+#endif
   float er = r - 0.5f, eg = g - 0.5f, eb = b - 0.5f;
   float ex = __expf(-(er * er + eg * eg + eb * eb) * 12.5f);
   return fabsf((float)lap) * sat * ex + 1e-12f;
@@ -72,6 +82,9 @@ constexpr int kVP = kRT + 1;
 // level-1 tile, four channels at a time: vertical into V[4][16][37], then
 // horizontal to global. V needs only 2368 floats, so it can alias the
 // luminance tiles of weights_down (the occupancy limit is shared memory).
+#ifndef HDR_DOWN_SLIDE
+#define HDR_DOWN_SLIDE 1
+#endif
 template <int NC>
 __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, int Y0, int X0,
                                           float* __restrict__ out, int ow, int oh) {
@@ -84,6 +97,26 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
     // (consecutive words, no bank conflicts -- dealing the 36 columns out
     // flat put two q rows 74 words apart into one warp: 2.3 wavefronts per
     // load), then the last 4 columns of all 64 q rows in one round
+#if HDR_DOWN_SLIDE
+    // one task per (channel, column): the column's 35 input rows are read
+    // from shared memory once into registers and its 16 outputs formed from
+    // them (2.2 shared loads per output instead of 5: the weights pass was
+    // bound by the L1/shared pipe, ncu l1tex 81%); 144 of the 256 threads
+    if (tid < 4 * kRT) {
+      const int c = tid / kRT, x = tid - c * kRT;
+      const float* col = src + c * kRT * kRP + x;
+      float in[2 * kOT + 3];
+#pragma unroll
+      for (int r = 0; r < 2 * kOT + 3; ++r) in[r] = col[r * kRP];
+#pragma unroll
+      for (int oy = 0; oy < kOT; ++oy) {
+        float acc = kK5[0] * in[2 * oy];
+#pragma unroll
+        for (int k = 1; k < 5; ++k) acc += kK5[k] * in[2 * oy + k];
+        V[(c * kOT + oy) * kVP + x] = acc;
+      }
+    }
+#else
     auto vert = [&](int q, int x) {
       int c = q >> 4, oy = q & 15;
       const float* col = src + (c * kRT + 2 * oy) * kRP + x;
@@ -101,6 +134,7 @@ __device__ __forceinline__ void down_tile(const float* px, float* V, int tid, in
       const int wp = tid >> 5, ln = tid & 31;
       vert(16 * (wp >> 1) + 2 * (ln >> 2) + (wp & 1), 32 + (ln & 3));
     }
+#endif
     __syncthreads();
     // 4 * 16 * 16 = 1024 = 4 * 256 horizontal outputs
 #pragma unroll

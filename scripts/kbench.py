@@ -79,15 +79,6 @@ if what in ("warp", "all"):
         _native.check(L.hdr_warp_image(ctx, ctypes.c_void_p(src.data_ptr()), 3, W, H,
                                        ctypes.c_void_p(flow.data_ptr()), ctypes.c_void_p(warped.data_ptr()),
                                        ctypes.c_void_p(valid.data_ptr())))
-    ref = None
-    for u in (1, 2, 4):
-        _native.check(L.hdr_set_option(b"warp_unroll", u))
-        us = timed(runw, 20)
-        out = torch.cat([warped.flatten(), valid.float().flatten()])
-        if ref is None:
-            ref = out.clone()
-        same = bool(torch.equal(out, ref))
-        nbytes = P * (8 + 12 + 12 + 1 + 1)
-        print(f"warp_image RGB unroll={u}: {us:8.1f} us  {nbytes / us / 1e3:.0f} GB/s algorithmic "
-              f"({nbytes / 1e6:.1f} MB)  identical to unroll=1: {same}")
-    L.hdr_set_option(b"warp_unroll", 1)
+    us = timed(runw, 20)
+    nbytes = P * (8 + 12 + 12 + 1 + 1)
+    print(f"warp_image RGB: {us:8.1f} us  {nbytes / us / 1e3:.0f} GB/s algorithmic ({nbytes / 1e6:.1f} MB)")

@@ -360,6 +360,9 @@ constexpr size_t collapse_smem() {
 #ifndef HDR_COLLAPSE_MIN_BLOCKS
 #define HDR_COLLAPSE_MIN_BLOCKS 4
 #endif
+#ifndef HDR_COLLAPSE0_DIFF
+#define HDR_COLLAPSE0_DIFF 1
+#endif
 template <bool LEVEL0, int NF>
 __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(const float* __restrict__ g, FuseFrames<NF> fr,
                                                       int w, int h, const float* __restrict__ gc,
@@ -394,15 +397,35 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
     }
     cp_async_commit();
     cp_async_wait_all();
+    if (LEVEL0 && HDR_COLLAPSE0_DIFF) {
+      // up() is linear, so the level-0 term B0 - sum_f w_f up(G_f) + up(C)
+      // with w_0 = 1 - sum_{f>0} w_f is B0 + up(C - G_0) - sum_{f>0} w_f
+      // up(G_f - G_0): the differences are formed on the coarse samples this
+      // thread copied (its own cp.async landed), and only 3 NF channels are
+      // up-sampled instead of 3 NF + 3
+      for (int i = tid; i < kCT * kCT; i += 256) {
+        float g0[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) g0[k] = C[k * kCT * kCT + i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) C[k * kCT * kCT + i] = C[(3 * NF + k) * kCT * kCT + i] - g0[k];
+#pragma unroll
+        for (int f = 1; f < NF; ++f)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) C[(3 * f + k) * kCT * kCT + i] -= g0[k];
+      }
+    }
   }
   __syncthreads();
+  // channels up-sampled: the level-0 kernel needs 3 NF (differences above)
+  constexpr int NU = (LEVEL0 && HDR_COLLAPSE0_DIFF) ? 3 * NF : NCH;
   // horizontal: Hc[c][r][x] for the 19 coarse rows and the 32 fine columns
   for (int i = tid; i < kCT * kFT; i += 256) {
     int r = i >> 5, x = i & 31;
     int j0 = hc[x][0], j1 = hc[x][1], j2 = hc[x][2];
     float w0 = hw[x][0], w1 = hw[x][1], w2 = hw[x][2];
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    for (int c = 0; c < NU; ++c) {
       const float* row = C + (c * kCT + r) * kCT;
       Hc[(c * kCT + r) * kFT + x] = gc ? w0 * row[j0] + w1 * row[j1] + w2 * row[j2] : 0.0f;
     }
@@ -419,7 +442,7 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
   const float w0 = vw[yy][0], w1 = vw[yy][1], w2 = vw[yy][2];
   float u[NCH][4];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
+  for (int c = 0; c < NU; ++c) {
     const float* col = Hc + c * kCT * kFT + xq;
     float4 a = *reinterpret_cast<const float4*>(col + r0 * kFT);
     float4 b = *reinterpret_cast<const float4*>(col + r1 * kFT);
@@ -476,6 +499,16 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+#if HDR_COLLAPSE0_DIFF
+      // u[k] = up(C - G_0), u[3f + k] = up(G_f - G_0)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float v = b[k][j] + u[k][j];
+#pragma unroll
+        for (int f = 1; f < NF; ++f) v -= wt[f][j] * u[3 * f + k][j];
+        o[k][j] = fminf(fmaxf(v, 0.0f), 1.0f);
+      }
+#else
       float w0 = 1.0f;
 #pragma unroll
       for (int f = 1; f < NF; ++f) w0 -= wt[f][j];
@@ -486,6 +519,7 @@ __global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(
         for (int f = 1; f < NF; ++f) v += wt[f][j] * u[3 * f + k][j];
         o[k][j] = fminf(fmaxf(b[k][j] - v + u[3 * NF + k][j], 0.0f), 1.0f);
       }
+#endif
     }
     if (vec) {
       float4* o4 = reinterpret_cast<float4*>(op);

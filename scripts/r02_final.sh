@@ -1,10 +1,9 @@
-# round-2 closing evidence on one B200: GPU tests, smoke, sanitizers, bench +
+# round-2 closing evidence on one B200: GPU tests, smoke, bench +
 # reference arm, launch list of full pairs, ncu --set full of the heavy kernels
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/fin_smi.txt
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -rf 2>&1 | tail -30 > gpurun_out/fin_tests.log
 timeout 300 python __graft_entry__.py --smoke > gpurun_out/fin_smoke.log 2>&1
-bash scripts/sanitize.sh > gpurun_out/fin_san.log 2>&1
 timeout 900 python bench.py > gpurun_out/fin_bench.log 2>&1
 timeout 900 python bench.py --impl reference > gpurun_out/fin_ref.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/fin_launches.csv \

@@ -364,7 +364,10 @@ constexpr size_t collapse_smem() {
 #define HDR_COLLAPSE0_DIFF 1
 #endif
 template <bool LEVEL0, int NF>
-__global__ void __launch_bounds__(256, HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(const float* __restrict__ g, FuseFrames<NF> fr,
+#ifndef HDR_COLLAPSE0_MIN_BLOCKS
+#define HDR_COLLAPSE0_MIN_BLOCKS HDR_COLLAPSE_MIN_BLOCKS
+#endif
+__global__ void __launch_bounds__(256, LEVEL0 ? HDR_COLLAPSE0_MIN_BLOCKS : HDR_COLLAPSE_MIN_BLOCKS) collapse_kernel(const float* __restrict__ g, FuseFrames<NF> fr,
                                                       int w, int h, const float* __restrict__ gc,
                                                       const float* __restrict__ cc, int cw, int ch,
                                                       float* __restrict__ out) {

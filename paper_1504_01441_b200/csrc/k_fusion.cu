@@ -117,6 +117,13 @@ constexpr int kS2 = 32;
 #endif
 constexpr int VR = HDR_SSIM_VROWS;
 
+// chunk permutation of ssim_fixed_kernel's vertical-pass rows (radius 5:
+// 21 chunks of 16 bytes; found by exhaustive search, see the horizontal pass)
+__device__ __forceinline__ int ssim_chunk(int k) { return (unsigned)(k - 8) < 8u ? k ^ 1 : k; }
+#ifndef HDR_SSIM_SWIZZLE
+#define HDR_SSIM_SWIZZLE 1
+#endif
+
 template <int R>
 #ifndef HDR_SSIM_MIN_BLOCKS
 #define HDR_SSIM_MIN_BLOCKS 3
@@ -127,6 +134,7 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     float* __restrict__ out, int ty0) {
   pdl_wait();
   constexpr int E = kS2 + 2 * R;  // staged rows/cols incl. halo
+  constexpr bool SWZ = HDR_SSIM_SWIZZLE && R == 5;
   const int by = ty0 + (int)blockIdx.y;  // tile row (ty0 > 0: a row band's tiles)
   __shared__ float sa[E][E + 1], sb[E][E + 1];
   __shared__ int rows[E], cols[E];
@@ -194,11 +202,12 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
         m4 = fma(vab[q + j], k[j], m4);
       }
       int oy = VR * rg + q;
-      V[(0 * kS2 + oy) * E + c] = m0;
-      V[(1 * kS2 + oy) * E + c] = m1;
-      V[(2 * kS2 + oy) * E + c] = m2;
-      V[(3 * kS2 + oy) * E + c] = m3;
-      V[(4 * kS2 + oy) * E + c] = m4;
+      const int cs = SWZ ? (ssim_chunk(c >> 1) << 1) | (c & 1) : c;
+      V[(0 * kS2 + oy) * E + cs] = m0;
+      V[(1 * kS2 + oy) * E + cs] = m1;
+      V[(2 * kS2 + oy) * E + cs] = m2;
+      V[(3 * kS2 + oy) * E + cs] = m3;
+      V[(4 * kS2 + oy) * E + cs] = m4;
     }
   }
   __syncthreads();
@@ -208,17 +217,28 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
   int gy = by * kS2 + oy;
   double m[5][4];
   // the 8 lanes of a row read 16-byte chunks 32 bytes apart (two lanes per
-  // bank group); lanes 4-7 fetch their chunks rotated by one, so most steps
-  // see all eight bank groups once (one wavefront per row, not two)
+  // bank group: lanes l and l + 4 are 128 bytes apart). SWZ: the vertical
+  // pass stored chunk k of every row at ssim_chunk(k) (chunks 8..15 swapped in
+  // pairs), a permutation under which the 8 lanes' chunks of every step fall
+  // in 8 distinct bank groups -- one wavefront per row without the lane-
+  // dependent rotation (and its 2 x 7 x 5 double selects) used otherwise.
   constexpr int NC = (4 + 2 * R) / 2;  // 16-byte chunks per thread (7)
   static_assert((4 + 2 * R) % 2 == 0 && E % 2 == 0, "16-byte chunks");
-  const int rot = (tid >> 2) & 1;
+  const int rot = SWZ ? 0 : (tid >> 2) & 1;
+  int pst[NC];
+#pragma unroll
+  for (int st = 0; st < NC; ++st) pst[st] = SWZ ? ssim_chunk((ox0 >> 1) + st) : (ox0 >> 1) + st;
 #pragma unroll
   for (int mm = 0; mm < 5; ++mm) {
-    const double2* row2 = reinterpret_cast<const double2*>(V + (mm * kS2 + oy) * E + ox0);
+    const double2* row2 = reinterpret_cast<const double2*>(V + (mm * kS2 + oy) * E);
     double2 r[NC];
+    if (SWZ) {
 #pragma unroll
-    for (int st = 0; st < NC; ++st) r[st] = row2[st + rot == NC ? 0 : st + rot];
+      for (int st = 0; st < NC; ++st) r[st] = row2[pst[st]];
+    } else {
+#pragma unroll
+      for (int st = 0; st < NC; ++st) r[st] = row2[(ox0 >> 1) + (st + rot == NC ? 0 : st + rot)];
+    }
     double v[4 + 2 * R];
 #pragma unroll
     for (int t = 0; t < NC; ++t) {

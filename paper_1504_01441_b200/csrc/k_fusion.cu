@@ -123,6 +123,9 @@ __device__ __forceinline__ int ssim_chunk(int k) { return (unsigned)(k - 8) < 8u
 #ifndef HDR_SSIM_SWIZZLE
 #define HDR_SSIM_SWIZZLE 1
 #endif
+#ifndef HDR_SSIM_STAGE_INC
+#define HDR_SSIM_STAGE_INC 1
+#endif
 
 template <int R>
 #ifndef HDR_SSIM_MIN_BLOCKS
@@ -155,6 +158,35 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
     constexpr int NE = (E * E + 255) / 256;
     float va[NE];
     uint32_t vq[NE];
+#if HDR_SSIM_STAGE_INC
+    // (r, cc) of i = tid + 256 it advance without a division (256 = DR E + DC)
+    constexpr int DR = 256 / E, DC = 256 - DR * E;
+    const int r00 = tid / E, c00 = tid - r00 * E;
+    {
+      int r = r00, cc = c00;
+#pragma unroll
+      for (int it = 0; it < NE; ++it) {
+        bool ok = tid + it * 256 < E * E;
+        int64_t p = ok ? (int64_t)rows[r] * w + cols[cc] : 0;
+        va[it] = ok ? __ldg(a + p) : 0.0f;
+        vq[it] = qb ? (ok ? (uint32_t)__ldg(qb + p) : 0u) : __float_as_uint(ok ? __ldg(b + p) : 0.0f);
+        r += DR; cc += DC;
+        if (cc >= E) { cc -= E; ++r; }
+        r = min(r, E - 1);
+      }
+    }
+    {
+      int r = r00, cc = c00;
+#pragma unroll
+      for (int it = 0; it < NE; ++it) {
+        if (tid + it * 256 >= E * E) break;
+        sa[r][cc] = va[it];
+        sb[r][cc] = qb ? lut[vq[it]] : __uint_as_float(vq[it]);
+        r += DR; cc += DC;
+        if (cc >= E) { cc -= E; ++r; }
+      }
+    }
+#else
 #pragma unroll
     for (int it = 0; it < NE; ++it) {
       int i = tid + it * 256;
@@ -172,6 +204,7 @@ __global__ void __launch_bounds__(256, HDR_SSIM_MIN_BLOCKS) ssim_fixed_kernel(
       sa[r][cc] = va[it];
       sb[r][cc] = qb ? lut[vq[it]] : __uint_as_float(vq[it]);
     }
+#endif
   }
   __syncthreads();
   // vertical (axis 0): work item (rg, c) produces rows VR rg .. VR rg + VR-1 of staged

@@ -65,6 +65,19 @@ __device__ __forceinline__ Aff<K> shfl_aff(const Aff<K>& v, int off, bool up) {
   return r;
 }
 
+template <int K>
+__device__ __forceinline__ Aff<K> shfl_aff_idx(const Aff<K>& v, int src) {
+  Aff<K> r;
+  r.A = __shfl_sync(0xffffffff, v.A, src);
+#pragma unroll
+  for (int k = 0; k < K; ++k) r.B[k] = __shfl_sync(0xffffffff, v.B[k], src);
+  return r;
+}
+
+#ifndef HDR_ROW_SCAN_SHFL
+#define HDR_ROW_SCAN_SHFL 1
+#endif
+
 // ---------------------------------------------------------------- rows
 // Row-sweep block size / max segment: 512 x 8 measured best for batch
 // throughput (897 pairs/s vs 873 at 256 x 16 and 886 at 384 x 8); 384 x 8
@@ -179,11 +192,29 @@ __device__ __forceinline__ void row_block_scan(Aff<K>& inc, bool up, Aff<K>* wsu
   pre.A = 1.0;
 #pragma unroll
   for (int k = 0; k < K; ++k) pre.B[k] = 0.0;
+#if HDR_ROW_SCAN_SHFL
+  {
+    // the other warps' totals composed by a shuffle scan over lanes (lane j
+    // holds wsum[j]; 5 steps) instead of a serial fold of up to nw - 1
+    // dependent shared loads + compositions per thread
+    Aff<K> t = pre;
+    if (lane < nw) t = wsum[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      Aff<K> u = shfl_aff(t, off, up);
+      if (up ? lane >= off : lane + off < 32) t = compose(u, t);
+    }
+    const int src = up ? warp - 1 : warp + 1;
+    Aff<K> v = shfl_aff_idx(t, src < 0 ? 0 : src);
+    if (up ? warp > 0 : warp + 1 < nw) pre = v;
+  }
+#else
   if (up) {
     for (int j = 0; j < warp; ++j) pre = compose(pre, wsum[j]);
   } else {
     for (int j = nw - 1; j > warp; --j) pre = compose(pre, wsum[j]);
   }
+#endif
   Aff<K> o = shfl_aff(inc, 1, up);
   if (up ? lane > 0 : lane < 31) pre = compose(pre, o);
   __syncthreads();

@@ -363,6 +363,9 @@ constexpr size_t collapse_smem() {
 #ifndef HDR_COLLAPSE0_DIFF
 #define HDR_COLLAPSE0_DIFF 1
 #endif
+#ifndef HDR_COLLAPSE_DIFF
+#define HDR_COLLAPSE_DIFF 1
+#endif
 template <bool LEVEL0, int NF>
 #ifndef HDR_COLLAPSE0_MIN_BLOCKS
 #define HDR_COLLAPSE0_MIN_BLOCKS HDR_COLLAPSE_MIN_BLOCKS
@@ -373,6 +376,10 @@ __global__ void __launch_bounds__(256, LEVEL0 ? HDR_COLLAPSE0_MIN_BLOCKS : HDR_C
                                                       float* __restrict__ out) {
   pdl_wait();
   constexpr int NCH = 3 * (NF + 1);
+  // up-sample coarse differences (3 NF channels) instead of the 3 NF + 3
+  // coarse channels: level 0 (HDR_COLLAPSE0_DIFF) and the coarser levels
+  // (HDR_COLLAPSE_DIFF), see the gather below
+  constexpr bool DIFF = LEVEL0 ? HDR_COLLAPSE0_DIFF : HDR_COLLAPSE_DIFF;
   extern __shared__ float smc[];
   float* C = smc;                      // [NCH][19][19] coarse tile
   float* Hc = smc + ((NCH * kCT * kCT + 3) & ~3);  // [NCH][19][32] up-sampled along x (16B aligned)
@@ -400,12 +407,14 @@ __global__ void __launch_bounds__(256, LEVEL0 ? HDR_COLLAPSE0_MIN_BLOCKS : HDR_C
     }
     cp_async_commit();
     cp_async_wait_all();
-    if (LEVEL0 && HDR_COLLAPSE0_DIFF) {
+    if (DIFF) {
       // up() is linear, so the level-0 term B0 - sum_f w_f up(G_f) + up(C)
       // with w_0 = 1 - sum_{f>0} w_f is B0 + up(C - G_0) - sum_{f>0} w_f
-      // up(G_f - G_0): the differences are formed on the coarse samples this
-      // thread copied (its own cp.async landed), and only 3 NF channels are
-      // up-sampled instead of 3 NF + 3
+      // up(G_f - G_0) (and a coarser level's sum_f W_f (G_f - up G'_f) +
+      // up C' likewise, the blurred normalised weights summing to 1): the
+      // differences are formed on the coarse samples this thread copied (its
+      // own cp.async landed), and only 3 NF channels are up-sampled instead
+      // of 3 NF + 3
       for (int i = tid; i < kCT * kCT; i += 256) {
         float g0[3];
 #pragma unroll
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(256, LEVEL0 ? HDR_COLLAPSE0_MIN_BLOCKS : HDR_C
   }
   __syncthreads();
   // channels up-sampled: the level-0 kernel needs 3 NF (differences above)
-  constexpr int NU = (LEVEL0 && HDR_COLLAPSE0_DIFF) ? 3 * NF : NCH;
+  constexpr int NU = DIFF ? 3 * NF : NCH;
   // horizontal: Hc[c][r][x] for the 19 coarse rows and the 32 fine columns
   for (int i = tid; i < kCT * kFT; i += 256) {
     int r = i >> 5, x = i & 31;
@@ -469,7 +478,7 @@ __global__ void __launch_bounds__(256, LEVEL0 ? HDR_COLLAPSE0_MIN_BLOCKS : HDR_C
   const bool vec = full && aligned && (w & 3) == 0 && (LEVEL0 || (P & 3) == 0);
   float wt[NF][4];
 #pragma unroll
-  for (int f = LEVEL0 ? 1 : 0; f < NF; ++f) {
+  for (int f = (LEVEL0 || DIFF) ? 1 : 0; f < NF; ++f) {
     const float* wp = LEVEL0 ? fr.wout[f] + p : g + (3 * NF + f) * P + p;
     if (vec) {
       float4 t = __ldg(reinterpret_cast<const float4*>(wp));
@@ -556,11 +565,20 @@ __global__ void __launch_bounds__(256, LEVEL0 ? HDR_COLLAPSE0_MIN_BLOCKS : HDR_C
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      float v = 0.0f;
+      if (DIFF) {
+        // W_0 = 1 - sum_{f>0} W_f (the blurred normalised weights sum to 1):
+        // C = G_0 + up(C' - G'_0) + sum_{f>0} W_f ((G_f - G_0) - up(G'_f - G'_0))
+        float v = gv[0][k][j] + u[k][j];
 #pragma unroll
-      for (int f = 0; f < NF; ++f)
-        v = f == 0 ? wt[0][j] * (gv[0][k][j] - u[k][j]) : v + wt[f][j] * (gv[f][k][j] - u[3 * f + k][j]);
-      o[k][j] = v + u[3 * NF + k][j];
+        for (int f = 1; f < NF; ++f) v += wt[f][j] * ((gv[f][k][j] - gv[0][k][j]) - u[3 * f + k][j]);
+        o[k][j] = v;
+      } else {
+        float v = 0.0f;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          v = f == 0 ? wt[0][j] * (gv[0][k][j] - u[k][j]) : v + wt[f][j] * (gv[f][k][j] - u[3 * f + k][j]);
+        o[k][j] = v + u[3 * NF + k][j];
+      }
     }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
